@@ -1,0 +1,135 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * etap_mla.h — C-ABI of the B200 (sm_100a) ETAP MLA decode path.
+ *
+ * This is the drop-in boundary under the reference's hot path
+ *   etaplab::run_etap(const AttentionProblem&, const TileConfig&, const BlockHook&,
+ *                     const EtapFaults&)          (reference: proj/include/etaplab/etap.hpp:47-48,
+ *                                                   proj/src/etap.cpp:102-148)
+ * The reference has no C-ABI and no device boundary; each entry point below
+ * names the reference interface whose work it takes over.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. "device" pointers are CUDA device pointers; "host"
+ *     pointers are host memory (pinned recommended). The caller owns every buffer.
+ *   - The device entry points allocate nothing and are stream-ordered on `stream`
+ *     (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *   - Return codes: 0 ok, ETAP_ERR_SHAPE for shape/argument problems (the reference throws
+ *     std::invalid_argument there: etap.cpp:24-32,104-106, attention.cpp:11-19), ETAP_ERR_CUDA
+ *     for CUDA failures. etap_mla_last_error() returns a thread-local message.
+ *   - There is no CPU fallback: without a usable sm_100 device every compute entry point
+ *     returns ETAP_ERR_CUDA.
+ *
+ * Layouts (MLA latent attention, DeepSeek shapes)
+ *   q          [batch][q_tokens=1][heads][576]  bf16, row-major (heads folded into n_q as in
+ *              the reference bench harness, cli.cpp:214)
+ *   kv_pool    [num_pages][64][576]             bf16, the latent KV cache; V is the first 512
+ *              columns of every row (MLA aliasing; the reference keeps V separate,
+ *              attention.cpp:38-40, and callers build V = K[:, :512] with col_block)
+ *   block_table[batch][max_pages]               int32 page ids
+ *   seqlens    [batch]                          int32 context lengths (varlen; 0 allowed)
+ *   out        [batch][q_tokens=1][heads][512]  fp32  O = softmax(scale * Q K^T) V
+ *   lse        [batch][q_tokens=1][heads]       fp32  L = m + log l, natural log (etap.cpp:144)
+ */
+#ifndef ETAP_MLA_H
+#define ETAP_MLA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ETAP_MLA_D_QK 576
+#define ETAP_MLA_D_V 512
+#define ETAP_MLA_PAGE_ROWS 64
+#define ETAP_MLA_TILE_ROWS 128     /* KV rows per UMMA tile (M of S^T = K Q^T) */
+#define ETAP_MLA_HEAD_GROUP 16     /* heads per CTA work unit (N of both UMMAs) */
+#define ETAP_MLA_SCHED_INTS 8      /* int32 per CTA in the schedule */
+
+#define ETAP_OK 0
+#define ETAP_ERR_SHAPE 1
+#define ETAP_ERR_CUDA 2
+
+/* flags for etap_mla_decode */
+#define ETAP_FLAG_NEGATE_RESCALE 1u /* fault injection, mirrors EtapFaults::negate_rescale
+                                       (etap.hpp:39-41, etap.cpp:62): flips the sign of the
+                                       accumulator rescale factor; implies EAGER_RESCALE */
+#define ETAP_FLAG_EAGER_RESCALE 2u  /* rescale O^T whenever the running max grows (the
+                                       reference's per-block order, etap.cpp:40-47,62-70)
+                                       instead of the default thresholded lazy rescale */
+
+/* Thread-local description of the last error. Never NULL. */
+const char* etap_mla_last_error(void);
+
+/* Library build identification (for the driver's "which .so was loaded" evidence). */
+const char* etap_mla_version(void);
+
+/* Number of persistent CTAs the decode kernel uses on `device` (= its SM count). */
+int etap_mla_num_sm_parts(int device, int* num_sm_parts);
+
+/* Sizes of the caller-owned scratch buffers.
+ *   sched     : num_sm_parts * ETAP_MLA_SCHED_INTS int32
+ *   split_off : batch * heads/16 + 1 int32
+ *   workspace : bytes for split-KV partial O / LSE */
+int etap_mla_sched_ints(int batch, int heads, int num_sm_parts, size_t* sched_ints,
+                        size_t* split_off_ints);
+int etap_mla_workspace_bytes(int batch, int heads, int num_sm_parts, size_t* bytes);
+
+/* K1 — split-KV work scheduler (no reference analog: run_etap streams every KV block in one
+ * serial loop, etap.cpp:122-129, kv_block_count tiled_standard.cpp:21-23). Integer partition
+ * of the (sequence, head-group, 128-row tile) space over num_sm_parts persistent CTAs. */
+int etap_mla_metadata(const int32_t* seqlens /*device [batch]*/, int batch, int heads,
+                      int num_sm_parts, int32_t* sched /*device*/, int32_t* split_off /*device*/,
+                      void* stream);
+
+/* Host restatement of K1 (same partition, computed serially on the CPU from host seqlens);
+ * sched / split_off are host arrays of the sizes given by etap_mla_sched_ints. */
+int etap_mla_metadata_host(const int32_t* seqlens /*host [batch]*/, int batch, int heads,
+                           int num_sm_parts, int32_t* sched, int32_t* split_off);
+
+/* K2 + K3 — the transposed pipeline (run_etap + block_update_impl, etap.cpp:15-148) on
+ * tcgen05/TMEM/TMA, followed by the log-sum-exp combine of split partials.
+ * All pointers are device pointers. q_tokens must be 1 (decode); `causal` is accepted and is
+ * a no-op for one query token. heads must be a multiple of 16. */
+int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
+                    const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,
+                    int batch, int q_tokens, int heads, float scale, int causal,
+                    const int32_t* sched, const int32_t* split_off, int num_sm_parts,
+                    void* workspace, float* out, float* lse, unsigned flags, void* stream);
+
+/* End-to-end call with HOST buffers (the reference-facing path: run_etap receives host
+ * matrices): host->device copies, K1, K2, K3, device->host copies, synchronize.
+ * A context caches the device buffers for one (batch, heads, pages) shape. */
+typedef struct etap_mla_host_ctx etap_mla_host_ctx;
+int etap_mla_host_ctx_create(int batch, int heads, int64_t num_pages, int max_pages_per_seq,
+                             etap_mla_host_ctx** ctx);
+int etap_mla_host_decode(etap_mla_host_ctx* ctx, const void* q_host, const void* kv_pool_host,
+                         const int32_t* block_table_host, const int32_t* seqlens_host,
+                         float scale, unsigned flags, float* out_host, float* lse_host);
+void etap_mla_host_ctx_destroy(etap_mla_host_ctx* ctx);
+
+/* Reference-shaped entry (binary64 row-major matrices, exactly the storage of
+ * etaplab::AttentionProblem, attention.hpp:15-25): rounds Q/K to bf16, checks the MLA
+ * aliasing V == K[:, :512], runs the GPU path, widens O and L back to binary64.
+ * d_qk must be 576 and d_v 512; n_q is padded to a multiple of 16 heads internally.
+ * b_r/b_c/stages mirror TileConfig (tiled_standard.hpp:11-15): validated (>= 1, as
+ * run_etap does at etap.cpp:104-106) and otherwise ignored — the GPU tiling is fixed and the
+ * result is partition invariant (acceptance.cpp:209-229). */
+int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t n_kv,
+                          int64_t d_qk, const double* v, int64_t d_v, double scale,
+                          int64_t b_r, int64_t b_c, int64_t stages, unsigned flags, double* o,
+                          double* l);
+
+/* UMMA descriptor self-test (one CTA, one tile): S^T = K Q^T and O^T = V^T P^T through the
+ * same smem layouts as the decode kernel. Device pointers: k [128][576] bf16, q [16][576]
+ * bf16, p [128][16] fp32; outputs s_t [128][16] fp32, o_t [512][16] fp32. */
+int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* s_t, float* o_t,
+                           void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ETAP_MLA_H */

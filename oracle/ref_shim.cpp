@@ -1,0 +1,135 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// TEST INFRASTRUCTURE — NOT PART OF THE PRODUCT PATH.
+// extern "C" shim over the UNMODIFIED reference library (etaplab, compiled from the sources
+// under /root/reference/proj/src by oracle/Makefile into oracle/_ref/libetaplab_ref.so).
+// It only marshals plain arrays into etaplab::Matrix / AttentionProblem and calls the
+// reference's own functions; no reference code is copied here.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <thread>
+#include <vector>
+
+#include "etaplab/attention.hpp"
+#include "etaplab/etap.hpp"
+#include "etaplab/matrix.hpp"
+#include "etaplab/tiled_standard.hpp"
+
+using namespace etaplab;
+
+namespace {
+
+Matrix from_ptr(const double* p, std::int64_t rows, std::int64_t cols) {
+    return Matrix(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols),
+                  std::vector<double>(p, p + rows * cols));
+}
+
+void to_ptr(const AttentionOutput& out, double* o, double* l) {
+    std::memcpy(o, out.o.data(), sizeof(double) * out.o.size());
+    std::memcpy(l, out.l.data(), sizeof(double) * out.l.size());
+}
+
+Precision prec_of(int p) {
+    return p == 1 ? Precision::fp32 : p == 2 ? Precision::fp16emu : Precision::exact64;
+}
+
+}  // namespace
+
+extern "C" {
+
+// matrix_from_seed (src/matrix.cpp:153-165)
+void ref_matrix_from_seed(std::int64_t rows, std::int64_t cols, std::uint64_t seed, int dist,
+                          double* out) {
+    const Matrix m = matrix_from_seed(rows, cols, seed, dist == 1 ? Dist::uniform : Dist::normal);
+    std::memcpy(out, m.data(), sizeof(double) * m.size());
+}
+
+double ref_round_half(double x) { return round_half(x); }
+
+// make_problem(seed, ...) (src/attention.cpp:33-42): returns the stored (rounded) operands
+int ref_make_problem_seeded(std::uint64_t seed, std::int64_t n_q, std::int64_t n_kv,
+                            std::int64_t d_qk, std::int64_t d_v, double scale, int precision,
+                            double* q, double* k, double* v, double* scale_out) {
+    try {
+        const AttentionProblem p = make_problem(seed, n_q, n_kv, d_qk, d_v, scale, prec_of(precision));
+        std::memcpy(q, p.q.data(), sizeof(double) * p.q.size());
+        std::memcpy(k, p.k.data(), sizeof(double) * p.k.size());
+        std::memcpy(v, p.v.data(), sizeof(double) * p.v.size());
+        *scale_out = p.scale;
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+// mode 0: attention_ref (attention.cpp:44-77); 1: run_etap (etap.cpp:102-148);
+// 2: run_standard (tiled_standard.cpp:32-101). Returns 1 on std::invalid_argument.
+int ref_run(int mode, const double* q, std::int64_t n_q, const double* k, std::int64_t n_kv,
+            std::int64_t d_qk, const double* v, std::int64_t d_v, double scale, int precision,
+            std::int64_t b_r, std::int64_t b_c, std::int64_t stages, int negate_rescale, double* o,
+            double* l) {
+    try {
+        const AttentionProblem p = make_problem(from_ptr(q, n_q, d_qk), from_ptr(k, n_kv, d_qk),
+                                                from_ptr(v, n_kv, d_v), scale, prec_of(precision));
+        const TileConfig tiles{static_cast<std::size_t>(b_r), static_cast<std::size_t>(b_c),
+                               static_cast<std::size_t>(stages)};
+        AttentionOutput out;
+        if (mode == 0) {
+            out = attention_ref(p);
+        } else if (mode == 1) {
+            EtapFaults f;
+            f.negate_rescale = negate_rescale != 0;
+            out = run_etap(p, tiles, {}, f);
+        } else {
+            out = run_standard(p, tiles);
+        }
+        to_ptr(out, o, l);
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+std::uint64_t ref_transpose_count() { return transpose_count(); }
+void ref_reset_transpose_count() { reset_transpose_count(); }
+
+// CPU baseline: run_etap (exact64) over B MLA problems (V = K[:, :512] via col_block), one
+// std::thread per worker over the batch. Problems are built outside the timed region, like
+// cmd_bench (cli.cpp:236-283). q [B][H][576], kv [B][ctx][576] as binary64.
+// Returns the wall time of the run_etap calls in seconds (or -1 on error).
+double ref_mla_run_etap_batch(const double* q, const double* kv, std::int64_t batch,
+                              std::int64_t heads, std::int64_t ctx, double scale, int nthreads,
+                              double* o, double* l) {
+    try {
+        std::vector<AttentionProblem> probs;
+        probs.reserve(batch);
+        for (std::int64_t b = 0; b < batch; ++b) {
+            Matrix k = from_ptr(kv + b * ctx * 576, ctx, 576);
+            Matrix v = k.col_block(0, 512);
+            probs.push_back(make_problem(from_ptr(q + b * heads * 576, heads, 576), std::move(k),
+                                         std::move(v), scale, Precision::exact64));
+        }
+        const TileConfig tiles{64, 64, 2};  // cmd_bench defaults (cli.hpp:30-63)
+        std::vector<AttentionOutput> outs(batch);
+        if (nthreads < 1) nthreads = 1;
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> th;
+        for (int w = 0; w < nthreads; ++w)
+            th.emplace_back([&, w] {
+                for (std::int64_t b = w; b < batch; b += nthreads) outs[b] = run_etap(probs[b], tiles);
+            });
+        for (auto& t : th) t.join();
+        const auto t1 = std::chrono::steady_clock::now();
+        for (std::int64_t b = 0; b < batch; ++b) {
+            std::memcpy(o + b * heads * 512, outs[b].o.data(), sizeof(double) * heads * 512);
+            std::memcpy(l + b * heads, outs[b].l.data(), sizeof(double) * heads);
+        }
+        return std::chrono::duration<double>(t1 - t0).count();
+    } catch (const std::exception&) {
+        return -1.0;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Build the sm_100a CUDA library (libetap_mla.so) in-tree with nvcc.
+
+The library is a plain C-ABI shared object (include/etap_mla.h); Python reaches it with
+ctypes, C++ callers link it directly. Built for sm_100a only:
+``-gencode arch=compute_100a,code=sm_100a`` (tcgen05 is rejected in a generic compute_100
+pass).
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIBDIR = PKG / "lib"
+LIB = LIBDIR / "libetap_mla.so"
+
+SOURCES = [CSRC / "etap_mla.cu", CSRC / "etap_mla_host.cpp"]
+DEPS = SOURCES + [CSRC / "sm100_ptx.cuh", CSRC / "etap_mla_kernels.cuh", ROOT / "include" / "etap_mla.h"]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC",
+    "-Xptxas", "-v",
+    "--expt-relaxed-constexpr",
+]
+
+
+def nvcc() -> str:
+    cand = os.environ.get("NVCC") or shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not Path(cand).exists():
+        raise RuntimeError("nvcc not found")
+    return cand
+
+
+def up_to_date() -> bool:
+    if not LIB.exists():
+        return False
+    t = LIB.stat().st_mtime
+    return all(p.stat().st_mtime <= t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and up_to_date():
+        return LIB
+    LIBDIR.mkdir(exist_ok=True)
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [nvcc(), *NVCC_FLAGS, "-shared", *map(str, SOURCES), "-o", str(tmp),
+           "-Xlinker", "--export-dynamic"]
+    # C-ABI symbols are exported through an explicit visibility attribute-free version script
+    vs = LIBDIR / "exports.map"
+    vs.write_text("{ global: etap_mla_*; local: *; };\n")
+    cmd += ["-Xlinker", f"--version-script={vs}"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    log = LIBDIR / "build.log"
+    log.write_text(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"nvcc failed (see {log})")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,985 @@
+// SPDX-License-Identifier: Apache-2.0
+// B200 (sm_100a) ETAP MLA decode: kernels K1 (split-KV scheduler), K2 (transposed tcgen05
+// pipeline), K3 (log-sum-exp combine), a UMMA layout self-test, and the C-ABI declared in
+// include/etap_mla.h.
+//
+// Reference path replaced: etaplab::run_etap (/root/reference/proj/src/etap.cpp:102-148)
+// with its per-block body block_update_impl (etap.cpp:15-79). See DESIGN.md for the data
+// layout in HBM, the smem ring, the TMEM map and the roofline.
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/etap_mla.h"
+#include "etap_mla_kernels.cuh"
+
+using namespace etap_b200;
+
+#ifndef ETAP_MLA_VERSION
+#define ETAP_MLA_VERSION "etap_mla sm_100a r1"
+#endif
+
+// =============================================================================================
+// K1: split-KV scheduler. One CTA of 1024 threads.
+//
+// Virtual sequences vb = b * groups + g (sequence x head group). Each owns
+// tiles(vb) = ceil(seqlen_b / 128) KV tiles and a cost of tiles + META_FIXED_COST (0 if empty).
+// The cost line [0, total) is cut into num_parts equal intervals; CTA k takes
+// [k*T, (k+1)*T) mapped back to (vb, tile) coordinates. Partials of one vb are numbered
+// contiguously in CTA order: split_off[vb] .. split_off[vb+1].
+// sched[k] = {vb_begin, tile_begin, vb_end, tile_end (exclusive), first_partial_idx, 0,0,0}
+// =============================================================================================
+namespace {
+
+constexpr int META_THREADS = 1024;
+constexpr int META_MAX_VB = 2048;
+
+__device__ int block_excl_scan(int v, int* warp_tot, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = (lane < (int)(blockDim.x >> 5)) ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        warp_tot[lane] = w;  // inclusive
+    }
+    __syncthreads();
+    const int before = (warp > 0 ? warp_tot[warp - 1] : 0) + x - v;
+    if (total) *total = warp_tot[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return before;
+}
+
+// exclusive prefix over n values held in a[0..n); writes prefix to out[0..n], out[n] = total
+__device__ void block_scan_array(const int* a, int* out, int n, int* warp_tot) {
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int lo = threadIdx.x * per, hi = min(n, lo + per);
+    int s = 0;
+    for (int i = lo; i < hi; ++i) s += a[i];
+    int total;
+    int run = block_excl_scan(s, warp_tot, &total);
+    for (int i = lo; i < hi; ++i) {
+        out[i] = run;
+        run += a[i];
+    }
+    if (threadIdx.x == 0) out[n] = total;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(META_THREADS, 1)
+    etap_mla_metadata_kernel(const int32_t* __restrict__ seqlens, int batch, int groups,
+                             int num_parts, int32_t* __restrict__ sched,
+                             int32_t* __restrict__ split_off) {
+    ptx::grid_dep_launch();
+    __shared__ int s_tiles[META_MAX_VB];
+    __shared__ int s_pref[META_MAX_VB + 1];
+    __shared__ int s_ns[META_MAX_VB];
+    __shared__ int s_first[META_MAX_VB];
+    __shared__ int warp_tot[32];
+    const int nvb = batch * groups;
+
+    for (int i = threadIdx.x; i < nvb; i += blockDim.x) {
+        const int len = max(0, seqlens[i / groups]);
+        s_tiles[i] = (len + TILE - 1) / TILE;
+        s_ns[i] = s_tiles[i] > 0 ? s_tiles[i] + META_FIXED_COST : 0;  // cost, reused below
+        s_first[i] = 0x7fffffff;
+    }
+    __syncthreads();
+    block_scan_array(s_ns, s_pref, nvb, warp_tot);
+    const int total = s_pref[nvb];
+    for (int i = threadIdx.x; i < nvb; i += blockDim.x) s_ns[i] = 0;
+    __syncthreads();
+
+    const int T = max(1, (total + num_parts - 1) / num_parts);
+    // map a cost coordinate x in [0, total) to (vb, tile)
+    auto map = [&](int x, int& vb, int& t) {
+        int lo = 0, hi = nvb - 1;  // largest vb with s_pref[vb] <= x and nonzero cost
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_pref[mid] <= x) lo = mid; else hi = mid - 1;
+        }
+        // skip zero-cost sequences that share the same prefix value
+        while (lo + 1 < nvb && s_pref[lo + 1] <= x) ++lo;
+        vb = lo;
+        t = min(max(0, x - s_pref[lo] - META_FIXED_COST), s_tiles[lo]);
+    };
+
+    int vb_b = 0, t_b = 0, vb_e = -1, t_e = 0;
+    const int k = threadIdx.x;
+    for (int kk = k; kk < num_parts; kk += blockDim.x) {
+        const int x0 = kk * T, x1 = min(total, (kk + 1) * T);
+        int b0 = 0, tb = 0, b1 = -1, te = 0;
+        if (x0 < total) {
+            map(x0, b0, tb);
+            if (x1 >= total) { b1 = nvb - 1; te = s_tiles[nvb - 1]; }
+            else map(x1, b1, te);
+            for (int vb = b0; vb <= b1; ++vb) {
+                const int t0 = vb == b0 ? tb : 0;
+                const int t1 = vb == b1 ? te : s_tiles[vb];
+                if (t0 < t1) {
+                    atomicAdd(&s_ns[vb], 1);
+                    atomicMin(&s_first[vb], kk);
+                }
+            }
+        }
+        if (kk == k) { vb_b = b0; t_b = tb; vb_e = b1; t_e = te; }
+    }
+    __syncthreads();
+    block_scan_array(s_ns, s_pref, nvb, warp_tot);  // s_pref now = split offsets
+    for (int i = threadIdx.x; i <= nvb; i += blockDim.x) split_off[i] = s_pref[i];
+    for (int kk = k; kk < num_parts; kk += blockDim.x) {
+        int b0 = vb_b, tb = t_b, b1 = vb_e, te = t_e;
+        if (kk != k) {  // only reachable when num_parts > blockDim (not in practice)
+            b0 = 0; tb = 0; b1 = -1; te = 0;
+        }
+        int first_idx = 0;
+        if (b1 >= b0 && b0 < nvb) first_idx = s_pref[b0] + (kk - min(s_first[b0], kk));
+        int32_t* s = sched + kk * SCHED_INTS;
+        s[0] = b0; s[1] = tb; s[2] = b1; s[3] = te; s[4] = first_idx;
+        s[5] = 0; s[6] = 0; s[7] = 0;
+    }
+}
+
+// =============================================================================================
+// K2: the transposed pipeline. One persistent CTA per SM, 192 threads:
+//   warp 0      TMA producer (paged latent-KV chunks into the ring, Q per split)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  softmax (thread = KV row = TMEM lane) and epilogue (thread = d row of O^T)
+// =============================================================================================
+struct SplitDesc {
+    int vb, b, g, seqlen, t0, t1;
+};
+
+__device__ __forceinline__ bool split_at(const int32_t* sch, const int32_t* seqlens, int groups,
+                                         int vb, SplitDesc& d) {
+    d.vb = vb;
+    d.b = vb / groups;
+    d.g = vb - d.b * groups;
+    d.seqlen = max(0, seqlens[d.b]);
+    const int n_tiles = (d.seqlen + TILE - 1) / TILE;
+    d.t0 = (vb == sch[0]) ? sch[1] : 0;
+    d.t1 = (vb == sch[2]) ? min(sch[3], n_tiles) : n_tiles;
+    return d.t0 < d.t1;
+}
+
+template <int P_LAYOUT>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    etap_mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv,
+                           const __grid_constant__ CUtensorMap tm_q, const DecodeParams prm) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    // ---- prologue (overlaps the scheduler kernel under PDL)
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tm_kv);
+        ptx::prefetch_tmap(&tm_q);
+        for (int i = 0; i < NSLOT; ++i) {
+            ptx::mbar_init(&bars[BAR_FULL + i], 1);
+            ptx::mbar_init(&bars[BAR_EMPTY + i], 1);
+        }
+        ptx::mbar_init(&bars[BAR_Q_FULL], 1);
+        ptx::mbar_init(&bars[BAR_Q_EMPTY], 1);
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&bars[BAR_S_FULL + i], 1);
+            ptx::mbar_init(&bars[BAR_S_FREE + i], 128);
+        }
+        ptx::mbar_init(&bars[BAR_P_FULL], 128);
+        ptx::mbar_init(&bars[BAR_O_DONE], 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    // zero the ring once: rows of a half-filled tile then always hold finite data
+    {
+        uint4* r = reinterpret_cast<uint4*>(smem + OFF_RING);
+        for (int i = threadIdx.x; i < NSLOT * SLOT_BYTES / 16; i += NUM_THREADS)
+            r[i] = make_uint4(0, 0, 0, 0);
+        ptx::fence_proxy_async_smem();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    ptx::grid_dep_wait();     // schedule written by K1
+    ptx::grid_dep_launch();   // let the combine kernel get scheduled
+
+    const int32_t* sch = prm.sched + blockIdx.x * SCHED_INTS;
+    const int vb_begin = sch[0], vb_end = sch[2];
+    const int G = prm.groups;
+    const uint32_t ring_addr = ptx::smem_u32(smem + OFF_RING);
+    const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q);
+    const uint32_t phi_addr = ptx::smem_u32(smem + OFF_P);
+    const uint32_t plo_addr = phi_addr + P_BYTES;
+
+    if (warp == 0) {
+        // ===================================================== TMA producer (whole warp)
+        const uint64_t pol_kv = ptx::policy_evict_first();
+        const uint64_t pol_q = ptx::policy_evict_last();
+        uint32_t slot = 0, ring_phase = 0, gt = 0, nsplit = 0;
+        for (int vb = vb_begin; vb <= vb_end; ++vb) {
+            SplitDesc sd;
+            if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
+            if (nsplit > 0) ptx::mbar_wait(&bars[BAR_Q_EMPTY], (nsplit - 1) & 1);
+            if (lane == 0) {
+                ptx::mbar_arrive_expect_tx(&bars[BAR_Q_FULL], Q_BYTES);
+                const int qrow = sd.b * prm.heads + sd.g * HG;
+#pragma unroll 1
+                for (int c = 0; c < NCHUNK; ++c)
+                    ptx::tma_load_2d(smem + OFF_Q + c * Q_CHUNK_BYTES, &tm_q, &bars[BAR_Q_FULL],
+                                     c * 64, qrow, pol_q);
+            }
+            ++nsplit;
+            const int32_t* bt = prm.block_table + static_cast<size_t>(sd.b) * prm.max_pages;
+            const int n_pages = (sd.seqlen + PAGE - 1) / PAGE;
+            int pg0 = 0, pg1 = -1, base = -64;
+            for (int t = sd.t0; t < sd.t1; ++t) {
+                if (t - base >= 32) {  // fetch page ids of the next 32 tiles, one per lane
+                    base = t;
+                    const int tt = base + lane;
+                    pg0 = (tt < sd.t1) ? __ldg(bt + 2 * tt) : 0;
+                    pg1 = (tt < sd.t1 && 2 * tt + 1 < n_pages) ? __ldg(bt + 2 * tt + 1) : -1;
+                }
+                const int p0 = __shfl_sync(0xffffffffu, pg0, t - base);
+                const int p1 = __shfl_sync(0xffffffffu, pg1, t - base);
+                const uint32_t bytes = p1 >= 0 ? 2 * HALF_SLOT : HALF_SLOT;
+#pragma unroll 1
+                for (int pos = 0; pos < NCHUNK; ++pos) {
+                    ptx::mbar_wait(&bars[BAR_EMPTY + slot], ring_phase ^ 1);
+                    if (lane == 0) {
+                        const int chunk = chunk_at(pos, gt);
+                        uint8_t* dst = smem + OFF_RING + slot * SLOT_BYTES;
+                        ptx::mbar_arrive_expect_tx(&bars[BAR_FULL + slot], bytes);
+                        ptx::tma_load_2d(dst, &tm_kv, &bars[BAR_FULL + slot], chunk * 64, p0 * PAGE,
+                                         pol_kv);
+                        if (p1 >= 0)
+                            ptx::tma_load_2d(dst + HALF_SLOT, &tm_kv, &bars[BAR_FULL + slot],
+                                             chunk * 64, p1 * PAGE, pol_kv);
+                    }
+                    __syncwarp();
+                    if (++slot == NSLOT) { slot = 0; ring_phase ^= 1; }
+                }
+                ++gt;
+            }
+        }
+    } else if (warp == 1) {
+        // ===================================================== MMA issuer (one thread)
+        if (lane == 0) {
+            uint32_t gt = 0, nsplit = 0;
+            // pending GEMM2 (the previous tile)
+            bool has_prev = false;
+            uint32_t prev_gt = 0;
+            int prev_nk = 8;
+            bool prev_first = false;
+            auto gemm2 = [&](uint32_t tg, int n_k, bool first_of_split) {
+                ptx::mbar_wait(&bars[BAR_P_FULL], tg & 1);
+                ptx::tc_fence_after();
+                const uint32_t pos0 = (tg * NCHUNK) % NSLOT;
+#pragma unroll 1
+                for (int blk = 0; blk < 4; ++blk) {
+                    const uint32_t sa = (pos0 + pos_of_chunk(2 * blk, tg)) % NSLOT;
+                    issue_gemm2_block<P_LAYOUT>(tmem_base + TCOL_O + 16 * blk,
+                                                ring_addr + sa * SLOT_BYTES, phi_addr, plo_addr,
+                                                n_k, first_of_split);
+                    ptx::umma_commit(&bars[BAR_EMPTY + sa]);
+                    ptx::umma_commit(&bars[BAR_EMPTY + (sa + 1) % NSLOT]);
+                }
+                ptx::umma_commit(&bars[BAR_O_DONE]);
+            };
+            for (int vb = vb_begin; vb <= vb_end; ++vb) {
+                SplitDesc sd;
+                if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
+                const int n_pages = (sd.seqlen + PAGE - 1) / PAGE;
+                for (int t = sd.t0; t < sd.t1; ++t) {
+                    if (has_prev) {
+                        gemm2(prev_gt, prev_nk, prev_first);
+                        has_prev = false;
+                    }
+                    if (t == sd.t0) {
+                        ptx::mbar_wait(&bars[BAR_Q_FULL], nsplit & 1);
+                        ptx::tc_fence_after();
+                    }
+                    const uint32_t buf = gt & 1;
+                    if (gt >= 2) {
+                        ptx::mbar_wait(&bars[BAR_S_FREE + buf], ((gt >> 1) - 1) & 1);
+                        ptx::tc_fence_after();
+                    }
+                    const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
+                    const uint32_t ring_round0 = (gt * NCHUNK) / NSLOT;
+#pragma unroll 1
+                    for (int pos = 0; pos < NCHUNK; ++pos) {
+                        const uint32_t abs_pos = gt * NCHUNK + pos;
+                        const uint32_t s = (pos0 + pos) % NSLOT;
+                        (void)ring_round0;
+                        ptx::mbar_wait(&bars[BAR_FULL + s], (abs_pos / NSLOT) & 1);
+                        ptx::tc_fence_after();
+                        const int chunk = chunk_at(pos, gt);
+                        issue_gemm1_chunk(tmem_base + TCOL_S + 16 * buf, ring_addr + s * SLOT_BYTES,
+                                          q_addr + chunk * Q_CHUNK_BYTES, pos == 0);
+                        if (chunk == 8) ptx::umma_commit(&bars[BAR_EMPTY + s]);
+                    }
+                    ptx::umma_commit(&bars[BAR_S_FULL + buf]);
+                    if (t == sd.t1 - 1) ptx::umma_commit(&bars[BAR_Q_EMPTY]);
+                    has_prev = true;
+                    prev_gt = gt;
+                    prev_nk = (2 * t + 1 < n_pages) ? 8 : 4;
+                    prev_first = (t == sd.t0);
+                    ++gt;
+                }
+                ++nsplit;
+            }
+            if (has_prev) gemm2(prev_gt, prev_nk, prev_first);
+        }
+        __syncwarp();
+    } else {
+        // ===================================================== softmax + epilogue (128 threads)
+        const int wq = warp & 3;           // TMEM lane quadrant accessible by this warp
+        const int row = wq * 32 + lane;    // KV row in the tile / d row within an O^T block
+        const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
+        float* red_max = reinterpret_cast<float*>(smem + OFF_RED);  // [2][4][16]
+        float* red_sum = red_max + 128;                               // [4][16]
+        uint8_t* p_hi = smem + OFF_P;
+        uint8_t* p_lo = p_hi + P_BYTES;
+        const bool negate = prm.flags & FLAG_NEGATE_RESCALE;
+        const bool eager = negate || (prm.flags & FLAG_EAGER_RESCALE);
+        uint32_t gt = 0;
+        for (int vb = vb_begin; vb <= vb_end; ++vb) {
+            SplitDesc sd;
+            if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
+            const int n_pages = (sd.seqlen + PAGE - 1) / PAGE;
+            float m_used[16], l_part[16];
+#pragma unroll
+            for (int h = 0; h < 16; ++h) { m_used[h] = -INFINITY; l_part[h] = 0.f; }
+
+            for (int t = sd.t0; t < sd.t1; ++t) {
+                const uint32_t buf = gt & 1;
+                ptx::mbar_wait(&bars[BAR_S_FULL + buf], (gt >> 1) & 1);
+                ptx::tc_fence_after();
+                uint32_t sr[16];
+                ptx::tmem_ld16(t_lane + TCOL_S + 16 * buf, sr);
+                ptx::tmem_wait_ld();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&bars[BAR_S_FREE + buf]);
+
+                const int grow = t * TILE + row;
+                const bool valid = grow < sd.seqlen;
+                float x[16];
+#pragma unroll
+                for (int h = 0; h < 16; ++h)
+                    x[h] = valid ? __uint_as_float(sr[h]) * prm.scale_log2 : -INFINITY;
+
+                // column max over the 128 rows of the tile
+                const float wm = warp_reduce16<true>(x, lane);
+                float* rm = red_max + (gt & 1) * 64;
+                if ((lane & 1) == 0) rm[wq * 16 + (lane >> 1)] = wm;
+                ptx::named_bar_sync(1, 128);
+                float mt[16];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const float4 a = reinterpret_cast<const float4*>(rm)[q4];
+                    const float4 b = reinterpret_cast<const float4*>(rm + 16)[q4];
+                    const float4 c = reinterpret_cast<const float4*>(rm + 32)[q4];
+                    const float4 d = reinterpret_cast<const float4*>(rm + 48)[q4];
+                    mt[4 * q4 + 0] = fmaxf(fmaxf(a.x, b.x), fmaxf(c.x, d.x));
+                    mt[4 * q4 + 1] = fmaxf(fmaxf(a.y, b.y), fmaxf(c.y, d.y));
+                    mt[4 * q4 + 2] = fmaxf(fmaxf(a.z, b.z), fmaxf(c.z, d.z));
+                    mt[4 * q4 + 3] = fmaxf(fmaxf(a.w, b.w), fmaxf(c.w, d.w));
+                }
+                const bool first = (t == sd.t0);
+                bool need_rescale = false;
+                float alpha[16];
+#pragma unroll
+                for (int h = 0; h < 16; ++h) {
+                    if (first) {
+                        m_used[h] = mt[h];
+                        alpha[h] = 0.f;
+                    } else {
+                        const float mn = fmaxf(m_used[h], mt[h]);
+                        const bool upd = eager ? (mn > m_used[h]) : (mn > m_used[h] + LAZY_RESCALE_LOG2);
+                        alpha[h] = upd ? exp2f(m_used[h] - mn) : 1.f;
+                        if (upd) { m_used[h] = mn; need_rescale = true; }
+                    }
+                }
+                if (negate && !first) need_rescale = true;
+                float p[16];
+#pragma unroll
+                for (int h = 0; h < 16; ++h) {
+                    p[h] = exp2f(x[h] - m_used[h]);
+                    l_part[h] = first ? p[h] : fmaf(l_part[h], alpha[h], p[h]);
+                }
+                // GEMM2 of the previous tile must be complete before O^T is rescaled and P
+                // is overwritten
+                if (gt > 0) {
+                    ptx::mbar_wait(&bars[BAR_O_DONE], (gt - 1) & 1);
+                    ptx::tc_fence_after();
+                }
+                if (need_rescale) {
+#pragma unroll 1
+                    for (int blk = 0; blk < 4; ++blk) {
+                        uint32_t o[16];
+                        const uint32_t ta = t_lane + TCOL_O + 16 * blk;
+                        ptx::tmem_ld16(ta, o);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int h = 0; h < 16; ++h) {
+                            const float a = negate ? -alpha[h] : alpha[h];
+                            o[h] = __float_as_uint(__uint_as_float(o[h]) * a);
+                        }
+                        ptx::tmem_st16(ta, o);
+                    }
+                    ptx::tmem_wait_st();
+                }
+                write_p_hilo<P_LAYOUT>(p_hi, p_lo, row, p);
+                // rows of the last page past seqlen were loaded from HBM and may hold
+                // non-finite garbage; zero them in the V chunks (0 * NaN = NaN in the MMA)
+                const bool page1 = 2 * t + 1 < n_pages;
+                if (!valid && (row < PAGE || page1)) {
+                    const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
+#pragma unroll 1
+                    for (int c = 0; c < NVCHUNK; ++c) {
+                        const uint32_t s = (pos0 + pos_of_chunk(c, gt)) % NSLOT;
+                        uint4* dst = reinterpret_cast<uint4*>(smem + OFF_RING + s * SLOT_BYTES + row * 128);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) dst[j] = make_uint4(0, 0, 0, 0);
+                    }
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&bars[BAR_P_FULL]);
+                ++gt;
+            }
+
+            // ---- epilogue: wait for the last GEMM2, reduce l, O = O^T / l (the single
+            // transpose of etap.cpp:140 is the TMEM lane->d mapping), L = m + log l
+            ptx::mbar_wait(&bars[BAR_O_DONE], (gt - 1) & 1);
+            ptx::tc_fence_after();
+            const float ws = warp_reduce16<false>(l_part, lane);
+            if ((lane & 1) == 0) red_sum[wq * 16 + (lane >> 1)] = ws;
+            ptx::named_bar_sync(1, 128);
+            float inv_l[16], l_tot[16];
+#pragma unroll
+            for (int h = 0; h < 16; ++h) {
+                l_tot[h] = red_sum[h] + red_sum[16 + h] + red_sum[32 + h] + red_sum[48 + h];
+                inv_l[h] = 1.f / l_tot[h];
+            }
+            const int ns = prm.split_off[vb + 1] - prm.split_off[vb];
+            float* dst;
+            float* dst_lse;
+            if (ns == 1) {
+                const size_t hrow = static_cast<size_t>(sd.b) * prm.heads + sd.g * HG;
+                dst = prm.out + hrow * D_V;
+                dst_lse = prm.lse + hrow;
+            } else {
+                const int idx = (vb == sch[0]) ? sch[4] : prm.split_off[vb];
+                dst = prm.ws_o + static_cast<size_t>(idx) * HG * D_V;
+                dst_lse = prm.ws_lse + static_cast<size_t>(idx) * HG;
+            }
+#pragma unroll 1
+            for (int blk = 0; blk < 4; ++blk) {
+                uint32_t o[16];
+                ptx::tmem_ld16(t_lane + TCOL_O + 16 * blk, o);
+                ptx::tmem_wait_ld();
+                const int d = blk * 128 + row;
+#pragma unroll
+                for (int h = 0; h < 16; ++h) dst[h * D_V + d] = __uint_as_float(o[h]) * inv_l[h];
+            }
+            if (row < 16) {
+                float v = 0.f;
+#pragma unroll
+                for (int h = 0; h < 16; ++h)
+                    if (h == row) v = (m_used[h] + log2f(l_tot[h])) * 0.69314718055994530942f;
+                dst_lse[row] = v;
+            }
+            ptx::tc_fence_before();
+            // red_sum is rewritten by the next split's epilogue only after many barriers
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    }
+}
+
+// =============================================================================================
+// K3: log-sum-exp combine of split partials (no reference analog: split-KV is a SPEC
+// non-goal; the math is pinned by L = m + log l, etap.cpp:144, and partition
+// invariance, acceptance.cpp:209-229). Grid: one CTA of 128 threads per (vb, head).
+// =============================================================================================
+constexpr int COMBINE_THREADS = 128;
+constexpr int COMBINE_MAX_SPLITS = 1024;
+
+__global__ void __launch_bounds__(COMBINE_THREADS)
+    etap_mla_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
+                            const int32_t* __restrict__ split_off, int groups, int heads,
+                            float* __restrict__ out, float* __restrict__ lse) {
+    __shared__ float w[COMBINE_MAX_SPLITS];
+    __shared__ float red[COMBINE_THREADS / 32];
+    __shared__ float s_scale;
+    ptx::grid_dep_wait();
+    const int vb = blockIdx.x / HG;
+    const int h = blockIdx.x - vb * HG;
+    const int b = vb / groups, g = vb - b * groups;
+    const int s0 = split_off[vb];
+    const int ns = split_off[vb + 1] - s0;
+    if (ns == 1) return;
+    const size_t hrow = static_cast<size_t>(b) * heads + g * HG + h;
+    float4* o4 = reinterpret_cast<float4*>(out + hrow * D_V);
+    if (ns <= 0) {  // empty context: O = 0, L = -inf
+        o4[threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (threadIdx.x == 0) lse[hrow] = -INFINITY;
+        return;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float mx = -INFINITY;
+    for (int s = threadIdx.x; s < ns; s += COMBINE_THREADS) {
+        const float v = ws_lse[static_cast<size_t>(s0 + s) * HG + h];
+        w[s] = v;
+        mx = fmaxf(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+    __syncthreads();
+    float sum = 0.f;
+    for (int s = threadIdx.x; s < ns; s += COMBINE_THREADS) {
+        const float e = expf(w[s] - mx);
+        w[s] = e;
+        sum += e;
+    }
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) red[warp] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const float tot = red[0] + red[1] + red[2] + red[3];
+        s_scale = 1.f / tot;
+        lse[hrow] = mx + logf(tot);
+    }
+    __syncthreads();
+    const float inv = s_scale;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < ns; ++s) {
+        const float ws = w[s] * inv;
+        const float4 v = reinterpret_cast<const float4*>(
+            ws_o + (static_cast<size_t>(s0 + s) * HG + h) * D_V)[threadIdx.x];
+        acc.x = fmaf(ws, v.x, acc.x);
+        acc.y = fmaf(ws, v.y, acc.y);
+        acc.z = fmaf(ws, v.z, acc.z);
+        acc.w = fmaf(ws, v.w, acc.w);
+    }
+    o4[threadIdx.x] = acc;
+}
+
+// =============================================================================================
+// UMMA layout self-test: one CTA runs GEMM1 and GEMM2 of a single tile through exactly the
+// descriptors / smem layouts of the decode kernel and dumps the TMEM accumulators.
+// =============================================================================================
+template <int P_LAYOUT>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    etap_mla_selftest_kernel(const __grid_constant__ CUtensorMap tm_k,
+                             const __grid_constant__ CUtensorMap tm_q, const float* p_in,
+                             float* s_out, float* o_out) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bars[0], 1);
+        ptx::mbar_init(&bars[1], 1);
+        ptx::mbar_init(&bars[2], 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t ring_addr = ptx::smem_u32(smem + OFF_RING);
+    const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q);
+    const uint32_t phi_addr = ptx::smem_u32(smem + OFF_P);
+
+    if (threadIdx.x == 0) {
+        const uint64_t pol = ptx::policy_evict_first();
+        ptx::mbar_arrive_expect_tx(&bars[0], NCHUNK * SLOT_BYTES + Q_BYTES);
+        for (int c = 0; c < NCHUNK; ++c) {
+            uint8_t* dst = smem + OFF_RING + c * SLOT_BYTES;  // chunk c in slot c
+            ptx::tma_load_2d(dst, &tm_k, &bars[0], c * 64, 0, pol);
+            ptx::tma_load_2d(dst + HALF_SLOT, &tm_k, &bars[0], c * 64, 64, pol);
+            ptx::tma_load_2d(smem + OFF_Q + c * Q_CHUNK_BYTES, &tm_q, &bars[0], c * 64, 0, pol);
+        }
+    }
+    // P (hi only, lo = 0) written by the softmax warps exactly as the decode kernel does
+    if (warp >= 2) {
+        const int row = (warp & 3) * 32 + lane;
+        float p[16];
+        for (int h = 0; h < 16; ++h) p[h] = p_in[row * 16 + h];
+        uint32_t hi[8];
+        for (int i = 0; i < 8; ++i) hi[i] = pack_bf16x2(p[2 * i], p[2 * i + 1]);
+        uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        PLayout<P_LAYOUT>::write_row(smem + OFF_P, row, hi);
+        PLayout<P_LAYOUT>::write_row(smem + OFF_P + P_BYTES, row, zero);
+        ptx::fence_proxy_async_smem();
+    }
+    __syncthreads();
+    if (threadIdx.x == 32) {
+        ptx::mbar_wait(&bars[0], 0);
+        ptx::tc_fence_after();
+        for (int c = 0; c < NCHUNK; ++c)
+            issue_gemm1_chunk(tmem_base + TCOL_S, ring_addr + c * SLOT_BYTES,
+                              q_addr + c * Q_CHUNK_BYTES, c == 0);
+        for (int blk = 0; blk < 4; ++blk)
+            issue_gemm2_block<P_LAYOUT>(tmem_base + TCOL_O + 16 * blk,
+                                        ring_addr + (2 * blk) * SLOT_BYTES, phi_addr,
+                                        phi_addr + P_BYTES, 8, true);
+        ptx::umma_commit(&bars[1]);
+    }
+    if (warp >= 2) {
+        ptx::mbar_wait(&bars[1], 0);
+        ptx::tc_fence_after();
+        const int wq = warp & 3;
+        const int row = wq * 32 + lane;
+        const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
+        uint32_t r[16];
+        ptx::tmem_ld16(t_lane + TCOL_S, r);
+        ptx::tmem_wait_ld();
+        for (int h = 0; h < 16; ++h) s_out[row * 16 + h] = __uint_as_float(r[h]);
+        for (int blk = 0; blk < 4; ++blk) {
+            ptx::tmem_ld16(t_lane + TCOL_O + 16 * blk, r);
+            ptx::tmem_wait_ld();
+            for (int h = 0; h < 16; ++h) o_out[(blk * 128 + row) * 16 + h] = __uint_as_float(r[h]);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    }
+}
+
+// =============================================================================================
+// host side
+// =============================================================================================
+thread_local std::string g_last_error = "ok";
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(ETAP_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define ETAP_CUDA(call)                                        \
+    do {                                                       \
+        cudaError_t _e = (call);                               \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call);    \
+    } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows][576] matrix, box {64 cols, box_rows}, SW128.
+int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_rows) {
+    auto enc = get_encode_fn();
+    if (!enc) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver)");
+    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
+        return fail(ETAP_ERR_SHAPE, "tensor base address must be 16-byte aligned");
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(D_QK), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(D_QK) * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return ETAP_OK;
+}
+
+int p_layout_choice() {
+    static int v = [] {
+        const char* e = std::getenv("ETAP_P_LAYOUT");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return v;
+}
+
+template <typename K>
+int ensure_smem_attr(K kernel, int bytes) {
+    ETAP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    return ETAP_OK;
+}
+
+int check_device() {
+    int dev = 0;
+    ETAP_CUDA(cudaGetDevice(&dev));
+    int major = 0, minor = 0;
+    ETAP_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    ETAP_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+    if (major != 10 || minor != 0)
+        return fail(ETAP_ERR_CUDA, "etap_mla requires an sm_100 (B200) device, found sm_" +
+                                       std::to_string(major) + std::to_string(minor));
+    return ETAP_OK;
+}
+
+size_t max_partials(int batch, int heads, int num_sm_parts) {
+    return static_cast<size_t>(num_sm_parts) + static_cast<size_t>(batch) * (heads / HG);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* etap_mla_last_error(void) { return g_last_error.c_str(); }
+
+const char* etap_mla_version(void) { return ETAP_MLA_VERSION; }
+
+int etap_mla_num_sm_parts(int device, int* num_sm_parts) {
+    if (!num_sm_parts) return fail(ETAP_ERR_SHAPE, "num_sm_parts is NULL");
+    int n = 0;
+    ETAP_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+    *num_sm_parts = n;
+    return ETAP_OK;
+}
+
+int etap_mla_sched_ints(int batch, int heads, int num_sm_parts, size_t* sched_ints,
+                        size_t* split_off_ints) {
+    if (batch < 1 || heads < HG || heads % HG != 0 || num_sm_parts < 1)
+        return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
+    if (sched_ints) *sched_ints = static_cast<size_t>(num_sm_parts) * SCHED_INTS;
+    if (split_off_ints) *split_off_ints = static_cast<size_t>(batch) * (heads / HG) + 1;
+    return ETAP_OK;
+}
+
+int etap_mla_workspace_bytes(int batch, int heads, int num_sm_parts, size_t* bytes) {
+    if (batch < 1 || heads < HG || heads % HG != 0 || num_sm_parts < 1 || !bytes)
+        return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
+    const size_t np = max_partials(batch, heads, num_sm_parts);
+    *bytes = np * HG * D_V * sizeof(float) + np * HG * sizeof(float);
+    return ETAP_OK;
+}
+
+int etap_mla_metadata_host(const int32_t* seqlens, int batch, int heads, int num_sm_parts,
+                           int32_t* sched, int32_t* split_off) {
+    // Serial host restatement of etap_mla_metadata_kernel (same cost line, same mapping);
+    // used by tests to pin the device schedule and by callers that plan on the host.
+    if (!seqlens || !sched || !split_off) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    if (batch < 1 || heads < HG || heads % HG != 0)
+        return fail(ETAP_ERR_SHAPE, "batch >= 1 and heads a multiple of 16 required");
+    const int groups = heads / HG;
+    const int nvb = batch * groups;
+    if (nvb > META_MAX_VB) return fail(ETAP_ERR_SHAPE, "batch * heads/16 too large");
+    if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
+        return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
+    std::vector<int> tiles(nvb), pref(nvb + 1, 0), ns(nvb, 0), first(nvb, 0x7fffffff);
+    for (int i = 0; i < nvb; ++i) {
+        const int len = std::max(0, seqlens[i / groups]);
+        tiles[i] = (len + TILE - 1) / TILE;
+        pref[i + 1] = pref[i] + (tiles[i] > 0 ? tiles[i] + META_FIXED_COST : 0);
+    }
+    const int total = pref[nvb];
+    const int T = std::max(1, (total + num_sm_parts - 1) / num_sm_parts);
+    auto map = [&](int x, int& vb, int& t) {
+        int lo = 0, hi = nvb - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pref[mid] <= x) lo = mid; else hi = mid - 1;
+        }
+        while (lo + 1 < nvb && pref[lo + 1] <= x) ++lo;
+        vb = lo;
+        t = std::min(std::max(0, x - pref[lo] - META_FIXED_COST), tiles[lo]);
+    };
+    std::vector<int> rb(num_sm_parts), rt(num_sm_parts), re(num_sm_parts), rte(num_sm_parts);
+    for (int k = 0; k < num_sm_parts; ++k) {
+        const int x0 = k * T, x1 = std::min(total, (k + 1) * T);
+        int b0 = 0, tb = 0, b1 = -1, te = 0;
+        if (x0 < total) {
+            map(x0, b0, tb);
+            if (x1 >= total) { b1 = nvb - 1; te = tiles[nvb - 1]; }
+            else map(x1, b1, te);
+            for (int vb = b0; vb <= b1; ++vb) {
+                const int t0 = vb == b0 ? tb : 0;
+                const int t1 = vb == b1 ? te : tiles[vb];
+                if (t0 < t1) { ++ns[vb]; first[vb] = std::min(first[vb], k); }
+            }
+        }
+        rb[k] = b0; rt[k] = tb; re[k] = b1; rte[k] = te;
+    }
+    split_off[0] = 0;
+    for (int i = 0; i < nvb; ++i) split_off[i + 1] = split_off[i] + ns[i];
+    for (int k = 0; k < num_sm_parts; ++k) {
+        int first_idx = 0;
+        if (re[k] >= rb[k] && rb[k] < nvb) first_idx = split_off[rb[k]] + (k - std::min(first[rb[k]], k));
+        int32_t* s = sched + k * SCHED_INTS;
+        s[0] = rb[k]; s[1] = rt[k]; s[2] = re[k]; s[3] = rte[k]; s[4] = first_idx;
+        s[5] = 0; s[6] = 0; s[7] = 0;
+    }
+    return ETAP_OK;
+}
+
+int etap_mla_metadata(const int32_t* seqlens, int batch, int heads, int num_sm_parts,
+                      int32_t* sched, int32_t* split_off, void* stream) {
+    if (!seqlens || !sched || !split_off) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    if (batch < 1 || heads < HG || heads % HG != 0)
+        return fail(ETAP_ERR_SHAPE, "batch >= 1 and heads a multiple of 16 required");
+    const int groups = heads / HG;
+    if (batch * groups > META_MAX_VB)
+        return fail(ETAP_ERR_SHAPE, "batch * heads/16 exceeds " + std::to_string(META_MAX_VB));
+    if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
+        return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(META_THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_metadata_kernel, seqlens, batch, groups,
+                                 num_sm_parts, sched, split_off));
+    return ETAP_OK;
+}
+
+int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
+                    const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,
+                    int batch, int q_tokens, int heads, float scale, int causal,
+                    const int32_t* sched, const int32_t* split_off, int num_sm_parts,
+                    void* workspace, float* out, float* lse, unsigned flags, void* stream) {
+    (void)causal;  // one query token: the causal mask is the full context
+    if (!q || !kv_pool || !block_table || !seqlens || !sched || !split_off || !workspace ||
+        !out || !lse)
+        return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    if (q_tokens != 1) return fail(ETAP_ERR_SHAPE, "q_tokens must be 1 (decode)");
+    if (batch < 1 || heads < HG || heads % HG != 0)
+        return fail(ETAP_ERR_SHAPE, "batch >= 1 and heads a multiple of 16 required");
+    if (num_pages < 1 || max_pages_per_seq < 1)
+        return fail(ETAP_ERR_SHAPE, "num_pages and max_pages_per_seq must be >= 1");
+    if (num_pages * PAGE > (int64_t)0x7fffffff)
+        return fail(ETAP_ERR_SHAPE, "kv pool exceeds 2^31 rows");
+    if (!(scale >= 0.f) || !std::isfinite(scale))
+        return fail(ETAP_ERR_SHAPE, "scale must be finite and >= 0");
+    if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
+        return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
+    if (int rc = check_device()) return rc;
+
+    CUtensorMap tm_kv, tm_q;
+    if (int rc = make_map(&tm_kv, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, PAGE)) return rc;
+    if (int rc = make_map(&tm_q, q, static_cast<uint64_t>(batch) * heads, HG)) return rc;
+
+    const int groups = heads / HG;
+    const size_t np = max_partials(batch, heads, num_sm_parts);
+    DecodeParams prm;
+    prm.block_table = block_table;
+    prm.seqlens = seqlens;
+    prm.sched = sched;
+    prm.split_off = split_off;
+    prm.out = out;
+    prm.lse = lse;
+    prm.ws_o = static_cast<float*>(workspace);
+    prm.ws_lse = prm.ws_o + np * HG * D_V;
+    prm.max_pages = max_pages_per_seq;
+    prm.heads = heads;
+    prm.groups = groups;
+    prm.scale_log2 = scale * 1.4426950408889634f;
+    prm.flags = flags;
+
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(num_sm_parts);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = SMEM_ALLOC;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (p_layout_choice() == 1) {
+        static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<1>, SMEM_ALLOC);
+        if (attr_rc) return attr_rc;
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel<1>, tm_kv, tm_q, prm));
+    } else {
+        static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<0>, SMEM_ALLOC);
+        if (attr_rc) return attr_rc;
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel<0>, tm_kv, tm_q, prm));
+    }
+
+    cudaLaunchConfig_t cfg2 = {};
+    cfg2.gridDim = dim3(batch * groups * HG);
+    cfg2.blockDim = dim3(COMBINE_THREADS);
+    cfg2.dynamicSmemBytes = 0;
+    cfg2.stream = st;
+    cfg2.attrs = attr;
+    cfg2.numAttrs = 1;
+    ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, prm.ws_o, prm.ws_lse, split_off,
+                                 groups, heads, out, lse));
+    return ETAP_OK;
+}
+
+int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* s_t, float* o_t,
+                           void* stream) {
+    if (int rc = check_device()) return rc;
+    CUtensorMap tm_k, tm_q;
+    if (int rc = make_map(&tm_k, k, TILE, PAGE)) return rc;
+    if (int rc = make_map(&tm_q, q, HG, HG)) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (p_layout_choice() == 1) {
+        static int attr_rc = ensure_smem_attr(etap_mla_selftest_kernel<1>, SMEM_ALLOC);
+        if (attr_rc) return attr_rc;
+        etap_mla_selftest_kernel<1><<<1, NUM_THREADS, SMEM_ALLOC, st>>>(tm_k, tm_q, p, s_t, o_t);
+    } else {
+        static int attr_rc = ensure_smem_attr(etap_mla_selftest_kernel<0>, SMEM_ALLOC);
+        if (attr_rc) return attr_rc;
+        etap_mla_selftest_kernel<0><<<1, NUM_THREADS, SMEM_ALLOC, st>>>(tm_k, tm_q, p, s_t, o_t);
+    }
+    ETAP_CUDA(cudaGetLastError());
+    return ETAP_OK;
+}
+
+}  // extern "C"

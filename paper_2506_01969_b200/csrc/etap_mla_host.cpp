@@ -1,0 +1,180 @@
+// SPDX-License-Identifier: Apache-2.0
+// Host-buffer entry points of the C-ABI (include/etap_mla.h):
+//   * etap_mla_host_ctx_* / etap_mla_host_decode — end-to-end call with host buffers
+//     (H2D copies, K1/K2/K3, D2H copies), the path the `e2e` bench number measures;
+//   * etap_mla_run_etap_f64 — binary64 row-major matrices exactly as stored in
+//     etaplab::AttentionProblem (/root/reference/proj/include/etaplab/attention.hpp:15-25),
+//     mirroring run_etap's argument meaning and error behaviour (etap.cpp:102-106).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/etap_mla.h"
+
+namespace {
+
+thread_local std::string g_host_error;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t alloc(size_t bytes) {
+        n = bytes;
+        return cudaMalloc(&p, bytes > 0 ? bytes : 16);
+    }
+};
+
+// Round a binary64 value to the nearest bfloat16 (ties to even) directly, without the
+// double -> float -> bf16 double rounding; returns the 16-bit pattern.
+uint16_t bf16_bits_rne(double x) {
+    if (std::isnan(x)) return 0x7FC0;
+    const double ax = std::fabs(x);
+    float f;
+    if (ax == 0.0) {
+        f = static_cast<float>(x);
+    } else {
+        int e = 0;
+        std::frexp(ax, &e);              // ax = m * 2^e, m in [0.5, 1)
+        int q = e - 8;                   // 8 significant bits
+        if (q < -133) q = -133;          // bf16 subnormal quantum
+        const double r = std::nearbyint(std::ldexp(ax, -q));  // ties-to-even
+        const double v = std::ldexp(r, q);
+        // largest finite bf16 = (2 - 2^-7) * 2^127
+        f = v > 3.3895313892515355e38 ? INFINITY : static_cast<float>(v);
+        if (x < 0) f = -f;
+    }
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return static_cast<uint16_t>(u >> 16);
+}
+
+}  // namespace
+
+struct etap_mla_host_ctx {
+    int batch = 0, heads = 0, max_pages = 0, num_sm_parts = 0;
+    int64_t num_pages = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf q, kv, bt, sl, out, lse, sched, split_off, ws;
+};
+
+extern "C" {
+
+int etap_mla_host_ctx_create(int batch, int heads, int64_t num_pages, int max_pages_per_seq,
+                             etap_mla_host_ctx** ctx) {
+    if (!ctx) return ETAP_ERR_SHAPE;
+    *ctx = nullptr;
+    if (batch < 1 || heads < ETAP_MLA_HEAD_GROUP || heads % ETAP_MLA_HEAD_GROUP != 0 ||
+        num_pages < 1 || max_pages_per_seq < 1)
+        return ETAP_ERR_SHAPE;
+    auto* c = new etap_mla_host_ctx();
+    c->batch = batch;
+    c->heads = heads;
+    c->num_pages = num_pages;
+    c->max_pages = max_pages_per_seq;
+    int dev = 0;
+    size_t sched_n = 0, so_n = 0, ws_n = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    int rc = e == cudaSuccess ? etap_mla_num_sm_parts(dev, &c->num_sm_parts) : ETAP_ERR_CUDA;
+    if (!rc) rc = etap_mla_sched_ints(batch, heads, c->num_sm_parts, &sched_n, &so_n);
+    if (!rc) rc = etap_mla_workspace_bytes(batch, heads, c->num_sm_parts, &ws_n);
+    if (!rc) {
+        const size_t rows = static_cast<size_t>(batch) * heads;
+        if (c->q.alloc(rows * ETAP_MLA_D_QK * 2) ||
+            c->kv.alloc(static_cast<size_t>(num_pages) * ETAP_MLA_PAGE_ROWS * ETAP_MLA_D_QK * 2) ||
+            c->bt.alloc(static_cast<size_t>(batch) * max_pages_per_seq * 4) ||
+            c->sl.alloc(static_cast<size_t>(batch) * 4) || c->out.alloc(rows * ETAP_MLA_D_V * 4) ||
+            c->lse.alloc(rows * 4) || c->sched.alloc(sched_n * 4) ||
+            c->split_off.alloc(so_n * 4) || c->ws.alloc(ws_n) ||
+            cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking))
+            rc = ETAP_ERR_CUDA;
+    }
+    if (rc) {
+        delete c;
+        return rc;
+    }
+    *ctx = c;
+    return ETAP_OK;
+}
+
+int etap_mla_host_decode(etap_mla_host_ctx* c, const void* q_host, const void* kv_pool_host,
+                         const int32_t* block_table_host, const int32_t* seqlens_host,
+                         float scale, unsigned flags, float* out_host, float* lse_host) {
+    if (!c || !q_host || !kv_pool_host || !block_table_host || !seqlens_host || !out_host ||
+        !lse_host)
+        return ETAP_ERR_SHAPE;
+    cudaStream_t s = c->stream;
+    if (cudaMemcpyAsync(c->q.p, q_host, c->q.n, cudaMemcpyHostToDevice, s) ||
+        cudaMemcpyAsync(c->kv.p, kv_pool_host, c->kv.n, cudaMemcpyHostToDevice, s) ||
+        cudaMemcpyAsync(c->bt.p, block_table_host, c->bt.n, cudaMemcpyHostToDevice, s) ||
+        cudaMemcpyAsync(c->sl.p, seqlens_host, c->sl.n, cudaMemcpyHostToDevice, s))
+        return ETAP_ERR_CUDA;
+    int rc = etap_mla_metadata(static_cast<int32_t*>(c->sl.p), c->batch, c->heads,
+                               c->num_sm_parts, static_cast<int32_t*>(c->sched.p),
+                               static_cast<int32_t*>(c->split_off.p), s);
+    if (rc) return rc;
+    rc = etap_mla_decode(c->q.p, c->kv.p, c->num_pages, static_cast<int32_t*>(c->bt.p),
+                         c->max_pages, static_cast<int32_t*>(c->sl.p), c->batch, 1, c->heads,
+                         scale, 1, static_cast<int32_t*>(c->sched.p),
+                         static_cast<int32_t*>(c->split_off.p), c->num_sm_parts, c->ws.p,
+                         static_cast<float*>(c->out.p), static_cast<float*>(c->lse.p), flags, s);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(out_host, c->out.p, c->out.n, cudaMemcpyDeviceToHost, s) ||
+        cudaMemcpyAsync(lse_host, c->lse.p, c->lse.n, cudaMemcpyDeviceToHost, s) ||
+        cudaStreamSynchronize(s))
+        return ETAP_ERR_CUDA;
+    return ETAP_OK;
+}
+
+void etap_mla_host_ctx_destroy(etap_mla_host_ctx* c) {
+    if (!c) return;
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t n_kv,
+                          int64_t d_qk, const double* v, int64_t d_v, double scale, int64_t b_r,
+                          int64_t b_c, int64_t stages, unsigned flags, double* o, double* l) {
+    // argument validation mirrors run_etap / make_problem (etap.cpp:104-106,
+    // attention.cpp:11-19): these are the cases the reference rejects with invalid_argument
+    if (b_r < 1 || b_c < 1 || stages < 1) return ETAP_ERR_SHAPE;  // "tile config fields must be >= 1"
+    if (!q || !k || !v || !o || !l || n_q < 1 || n_kv < 1) return ETAP_ERR_SHAPE;
+    if (d_qk != ETAP_MLA_D_QK || d_v != ETAP_MLA_D_V) return ETAP_ERR_SHAPE;  // MLA shapes only
+    if (!(scale >= 0.0) || !std::isfinite(scale)) return ETAP_ERR_SHAPE;
+    if (n_kv > (int64_t)1 << 30) return ETAP_ERR_SHAPE;
+    // MLA aliasing: V must be the first 512 columns of the latent KV rows
+    for (int64_t i = 0; i < n_kv; ++i)
+        if (std::memcmp(v + i * d_v, k + i * d_qk, sizeof(double) * d_v) != 0) return ETAP_ERR_SHAPE;
+
+    const int heads = static_cast<int>((n_q + ETAP_MLA_HEAD_GROUP - 1) / ETAP_MLA_HEAD_GROUP) *
+                      ETAP_MLA_HEAD_GROUP;
+    const int64_t pages = (n_kv + ETAP_MLA_PAGE_ROWS - 1) / ETAP_MLA_PAGE_ROWS;
+    if (pages > 0x7fffffff) return ETAP_ERR_SHAPE;
+    std::vector<uint16_t> qb(static_cast<size_t>(heads) * d_qk, 0);
+    std::vector<uint16_t> kvb(static_cast<size_t>(pages) * ETAP_MLA_PAGE_ROWS * d_qk, 0);
+    for (int64_t i = 0; i < n_q * d_qk; ++i) qb[i] = bf16_bits_rne(q[i]);
+    for (int64_t i = 0; i < n_kv * d_qk; ++i) kvb[i] = bf16_bits_rne(k[i]);
+    std::vector<int32_t> bt(pages);
+    for (int64_t i = 0; i < pages; ++i) bt[i] = static_cast<int32_t>(i);
+    const int32_t seqlen = static_cast<int32_t>(n_kv);
+    std::vector<float> of(static_cast<size_t>(heads) * d_v), lf(heads);
+
+    etap_mla_host_ctx* ctx = nullptr;
+    int rc = etap_mla_host_ctx_create(1, heads, pages, static_cast<int>(pages), &ctx);
+    if (rc) return rc;
+    rc = etap_mla_host_decode(ctx, qb.data(), kvb.data(), bt.data(), &seqlen,
+                              static_cast<float>(scale), flags, of.data(), lf.data());
+    etap_mla_host_ctx_destroy(ctx);
+    if (rc) return rc;
+    for (int64_t i = 0; i < n_q * d_v; ++i) o[i] = static_cast<double>(of[i]);
+    for (int64_t i = 0; i < n_q; ++i) l[i] = static_cast<double>(lf[i]);
+    return ETAP_OK;
+}
+
+}  // extern "C"

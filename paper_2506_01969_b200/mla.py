@@ -1,0 +1,146 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Device-side API over the C-ABI: paged MLA decode on torch CUDA tensors.
+
+PyTorch is used only for device memory and streams; all compute runs in the sm_100a kernels
+of libetap_mla.so (K1 scheduler, K2 transposed tcgen05 pipeline, K3 combine).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import check
+
+D_QK = 576
+D_V = 512
+PAGE_ROWS = 64
+TILE_ROWS = 128
+HEAD_GROUP = 16
+SCHED_INTS = 8
+
+
+def _dev_index(device: torch.device | str | int | None) -> int:
+    if device is None:
+        return torch.cuda.current_device()
+    if isinstance(device, int):
+        return device
+    device = torch.device(device)
+    return device.index if device.index is not None else torch.cuda.current_device()
+
+
+def num_sm_parts(device: torch.device | str | int | None = None) -> int:
+    out = C.c_int(0)
+    check(_lib.lib().etap_mla_num_sm_parts(_dev_index(device), C.byref(out)), "etap_mla_num_sm_parts")
+    return out.value
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream_ptr(stream: torch.cuda.Stream | None) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+@dataclass
+class MlaDecodePlan:
+    """Scratch buffers (schedule, split offsets, split-KV workspace) for one shape.
+
+    Mirrors the FlashMLA-style two-call protocol: ``metadata(seqlens)`` once per decode step
+    (reusable across layers), then ``decode(...)`` per layer.
+    """
+
+    batch: int
+    heads: int
+    device: torch.device
+    num_sm_parts: int
+    sched: torch.Tensor
+    split_off: torch.Tensor
+    workspace: torch.Tensor
+
+    @classmethod
+    def create(cls, batch: int, heads: int, device: torch.device | str = "cuda",
+               num_parts: int | None = None) -> "MlaDecodePlan":
+        device = torch.device(device)
+        if device.type != "cuda":
+            raise _lib.EtapShapeError("MlaDecodePlan needs a CUDA device (no CPU fallback)")
+        L = _lib.lib()
+        nparts = num_parts if num_parts is not None else num_sm_parts(device)
+        n_sched, n_so, ws = C.c_size_t(0), C.c_size_t(0), C.c_size_t(0)
+        check(L.etap_mla_sched_ints(batch, heads, nparts, C.byref(n_sched), C.byref(n_so)),
+              "etap_mla_sched_ints")
+        check(L.etap_mla_workspace_bytes(batch, heads, nparts, C.byref(ws)), "etap_mla_workspace_bytes")
+        return cls(
+            batch=batch, heads=heads, device=device, num_sm_parts=nparts,
+            sched=torch.empty(n_sched.value, dtype=torch.int32, device=device),
+            split_off=torch.empty(n_so.value, dtype=torch.int32, device=device),
+            workspace=torch.empty(ws.value, dtype=torch.uint8, device=device),
+        )
+
+    def metadata(self, seqlens: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
+        """K1: split-KV schedule for the current step's context lengths."""
+        _check_tensor(seqlens, torch.int32, (self.batch,), "seqlens")
+        check(_lib.lib().etap_mla_metadata(seqlens.data_ptr(), self.batch, self.heads, self.num_sm_parts,
+                                           self.sched.data_ptr(), self.split_off.data_ptr(),
+                                           _stream_ptr(stream)), "etap_mla_metadata")
+
+    def decode(self, q: torch.Tensor, kv_pool: torch.Tensor, block_table: torch.Tensor,
+               seqlens: torch.Tensor, scale: float, out: torch.Tensor | None = None,
+               lse: torch.Tensor | None = None, flags: int = 0, causal: bool = True,
+               stream: torch.cuda.Stream | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+        """K2 + K3. q [B,1,H,576] bf16, kv_pool [pages,64,576] bf16, block_table [B,max_pages]
+        int32, seqlens [B] int32 -> (out [B,1,H,512] fp32, lse [B,1,H] fp32, natural log)."""
+        B, H = self.batch, self.heads
+        if q.dim() == 3:
+            q = q.unsqueeze(1)
+        _check_tensor(q, torch.bfloat16, (B, 1, H, D_QK), "q")
+        if kv_pool.dim() != 3 or kv_pool.shape[1:] != (PAGE_ROWS, D_QK) or kv_pool.dtype != torch.bfloat16:
+            raise _lib.EtapShapeError(f"kv_pool must be [pages,64,576] bf16, got {tuple(kv_pool.shape)} {kv_pool.dtype}")
+        if not kv_pool.is_contiguous():
+            raise _lib.EtapShapeError("kv_pool must be contiguous")
+        if block_table.dim() != 2 or block_table.shape[0] != B or block_table.dtype != torch.int32 \
+                or not block_table.is_contiguous():
+            raise _lib.EtapShapeError("block_table must be contiguous [B, max_pages] int32")
+        _check_tensor(seqlens, torch.int32, (B,), "seqlens")
+        if out is None:
+            out = torch.empty((B, 1, H, D_V), dtype=torch.float32, device=q.device)
+        if lse is None:
+            lse = torch.empty((B, 1, H), dtype=torch.float32, device=q.device)
+        check(_lib.lib().etap_mla_decode(
+            q.data_ptr(), kv_pool.data_ptr(), kv_pool.shape[0], block_table.data_ptr(),
+            block_table.shape[1], seqlens.data_ptr(), B, 1, H, float(scale), int(causal),
+            self.sched.data_ptr(), self.split_off.data_ptr(), self.num_sm_parts,
+            self.workspace.data_ptr(), out.data_ptr(), lse.data_ptr(), int(flags),
+            _stream_ptr(stream)), "etap_mla_decode")
+        return out, lse
+
+
+def _check_tensor(t: torch.Tensor, dtype: torch.dtype, shape: tuple, name: str) -> None:
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise _lib.EtapShapeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous():
+        raise _lib.EtapShapeError(
+            f"{name} must be contiguous {tuple(shape)} {dtype}, got {tuple(t.shape)} {t.dtype}")
+
+
+def mla_decode(q: torch.Tensor, kv_pool: torch.Tensor, block_table: torch.Tensor,
+               seqlens: torch.Tensor, scale: float, flags: int = 0,
+               plan: MlaDecodePlan | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """One-shot convenience: K1 + K2 + K3 on the current stream."""
+    B, H = q.shape[0], q.shape[-2]
+    plan = plan or MlaDecodePlan.create(B, H, q.device)
+    plan.metadata(seqlens)
+    return plan.decode(q, kv_pool, block_table, seqlens, scale, flags=flags)
+
+
+def selftest_umma(k: torch.Tensor, q: torch.Tensor, p: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """Single-tile UMMA layout check: returns (S^T [128,16], O^T [512,16]) from TMEM."""
+    s_t = torch.empty((TILE_ROWS, HEAD_GROUP), dtype=torch.float32, device=k.device)
+    o_t = torch.empty((D_V, HEAD_GROUP), dtype=torch.float32, device=k.device)
+    check(_lib.lib().etap_mla_selftest_umma(k.data_ptr(), q.data_ptr(), p.data_ptr(), s_t.data_ptr(),
+                                            o_t.data_ptr(), _stream_ptr(None)), "etap_mla_selftest_umma")
+    return s_t, o_t
