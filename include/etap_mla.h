@@ -128,6 +128,16 @@ int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t
 int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* s_t, float* o_t,
                            void* stream);
 
+/* Debug: when device_buf is non-NULL, subsequent decode launches record per-tile
+ * %globaltimer stamps of the pipeline events into it: [cta][128 tiles][8] uint64
+ * (0/1 first/last chunk TMA issued, 2 last chunk landed, 3 S^T committed, 4 softmax saw S^T,
+ * 5 P^T written, 6 MMA saw P^T, 7 O^T update committed). NULL disables (the default). */
+int etap_mla_debug_trace(void* device_buf);
+
+/* Debug: tensor-pipe microbenchmark — `grid` CTAs each issue n tcgen05.mma of one operand
+ * layout variant; out_dev[0..1] (device, int64) = issue cycles, issue+completion cycles. */
+int etap_mla_umma_bench(int variant, int n, long long* out_dev, int grid);
+
 #ifdef __cplusplus
 }
 #endif

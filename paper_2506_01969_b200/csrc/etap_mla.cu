@@ -183,7 +183,6 @@ __device__ __forceinline__ bool split_at(const int32_t* sch, const int32_t* seql
     return d.t0 < d.t1;
 }
 
-template <int P_LAYOUT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     etap_mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv,
                            const __grid_constant__ CUtensorMap tm_q, const DecodeParams prm) {
@@ -199,22 +198,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tm_kv);
         ptx::prefetch_tmap(&tm_q);
-        for (int i = 0; i < NSLOT; ++i) {
+        for (int i = 0; i < NTB; ++i) {
             ptx::mbar_init(&bars[BAR_FULL + i], 1);
-            ptx::mbar_init(&bars[BAR_EMPTY + i], 1);
+            ptx::mbar_init(&bars[BAR_G2_DONE + i], 1);
         }
         ptx::mbar_init(&bars[BAR_Q_FULL], 1);
         ptx::mbar_init(&bars[BAR_Q_EMPTY], 1);
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&bars[BAR_S_FULL + i], 1);
             ptx::mbar_init(&bars[BAR_S_FREE + i], 128);
+            ptx::mbar_init(&bars[BAR_P_FULL + i], 128);
         }
-        ptx::mbar_init(&bars[BAR_P_FULL], 128);
-        ptx::mbar_init(&bars[BAR_O_DONE], 1);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
-    // zero the ring once: rows of a half-filled tile then always hold finite data
+    // zero the ring once: V rows that were never loaded always hold finite data
     {
         uint4* r = reinterpret_cast<uint4*>(smem + OFF_RING);
         for (int i = threadIdx.x; i < NSLOT * SLOT_BYTES / 16; i += NUM_THREADS)
@@ -234,14 +232,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int G = prm.groups;
     const uint32_t ring_addr = ptx::smem_u32(smem + OFF_RING);
     const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q);
-    const uint32_t phi_addr = ptx::smem_u32(smem + OFF_P);
-    const uint32_t plo_addr = phi_addr + P_BYTES;
+    const uint32_t p_addr = ptx::smem_u32(smem + OFF_P);
 
     if (warp == 0) {
         // ===================================================== TMA producer (whole warp)
+        // Tile gt occupies ring positions [9gt, 9gt+9); positions 0..5 reuse slots of tile
+        // gt-3, positions 6..8 slots of tile gt-2, so two waits on "GEMM2 done" per tile.
         const uint64_t pol_kv = ptx::policy_evict_first();
         const uint64_t pol_q = ptx::policy_evict_last();
-        uint32_t slot = 0, ring_phase = 0, gt = 0, nsplit = 0;
+        uint32_t gt = 0, nsplit = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
             if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
@@ -254,124 +253,109 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     ptx::tma_load_2d(smem + OFF_Q + c * Q_CHUNK_BYTES, &tm_q, &bars[BAR_Q_FULL],
                                      c * 64, qrow, pol_q);
             }
+            __syncwarp();
             ++nsplit;
             const int32_t* bt = prm.block_table + static_cast<size_t>(sd.b) * prm.max_pages;
-            const int n_pages = (sd.seqlen + PAGE - 1) / PAGE;
-            int pg0 = 0, pg1 = -1, base = -64;
+            int pg = 0, base = -64;
             for (int t = sd.t0; t < sd.t1; ++t) {
-                if (t - base >= 32) {  // fetch page ids of the next 32 tiles, one per lane
+                if (t - base >= 32) {  // page ids of the next 32 tiles, one per lane
                     base = t;
                     const int tt = base + lane;
-                    pg0 = (tt < sd.t1) ? __ldg(bt + 2 * tt) : 0;
-                    pg1 = (tt < sd.t1 && 2 * tt + 1 < n_pages) ? __ldg(bt + 2 * tt + 1) : -1;
+                    pg = (tt < sd.t1) ? __ldg(bt + tt) : 0;
                 }
-                const int p0 = __shfl_sync(0xffffffffu, pg0, t - base);
-                const int p1 = __shfl_sync(0xffffffffu, pg1, t - base);
-                const uint32_t bytes = p1 >= 0 ? 2 * HALF_SLOT : HALF_SLOT;
+                const int page = __shfl_sync(0xffffffffu, pg, t - base);
+                const uint32_t tb = gt % NTB;
+                const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
+                if (gt >= 3) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 3) % NTB], ((gt - 3) / NTB) & 1);
+                if (lane == 0) {
+                    ETAP_TRACE(prm, gt, 0);
+                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL + tb], NCHUNK * SLOT_BYTES);
 #pragma unroll 1
-                for (int pos = 0; pos < NCHUNK; ++pos) {
-                    ptx::mbar_wait(&bars[BAR_EMPTY + slot], ring_phase ^ 1);
-                    if (lane == 0) {
-                        const int chunk = chunk_at(pos, gt);
-                        uint8_t* dst = smem + OFF_RING + slot * SLOT_BYTES;
-                        ptx::mbar_arrive_expect_tx(&bars[BAR_FULL + slot], bytes);
-                        ptx::tma_load_2d(dst, &tm_kv, &bars[BAR_FULL + slot], chunk * 64, p0 * PAGE,
-                                         pol_kv);
-                        if (p1 >= 0)
-                            ptx::tma_load_2d(dst + HALF_SLOT, &tm_kv, &bars[BAR_FULL + slot],
-                                             chunk * 64, p1 * PAGE, pol_kv);
+                    for (int pos = 0; pos < 6; ++pos) {
+                        const uint32_t s = (pos0 + pos) % NSLOT;
+                        ptx::tma_load_2d(smem + OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL + tb],
+                                         chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
                     }
-                    __syncwarp();
-                    if (++slot == NSLOT) { slot = 0; ring_phase ^= 1; }
                 }
+                __syncwarp();
+                if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+                if (lane == 0) {
+#pragma unroll 1
+                    for (int pos = 6; pos < NCHUNK; ++pos) {
+                        const uint32_t s = (pos0 + pos) % NSLOT;
+                        ptx::tma_load_2d(smem + OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL + tb],
+                                         chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
+                    }
+                    ETAP_TRACE(prm, gt, 1);
+                }
+                __syncwarp();
                 ++gt;
             }
         }
     } else if (warp == 1) {
-        // ===================================================== MMA issuer (one thread)
-        if (lane == 0) {
-            uint32_t gt = 0, nsplit = 0;
-            // pending GEMM2 (the previous tile)
-            bool has_prev = false;
-            uint32_t prev_gt = 0;
-            int prev_nk = 8;
-            bool prev_first = false;
-            auto gemm2 = [&](uint32_t tg, int n_k, bool first_of_split) {
-                ptx::mbar_wait(&bars[BAR_P_FULL], tg & 1);
+        // ===================================================== GEMM1 issuer (whole warp, elect)
+        uint32_t gt = 0, nsplit = 0;
+        for (int vb = vb_begin; vb <= vb_end; ++vb) {
+            SplitDesc sd;
+            if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
+            ptx::mbar_wait(&bars[BAR_Q_FULL], nsplit & 1);
+            for (int t = sd.t0; t < sd.t1; ++t) {
+                const uint32_t buf = gt & 1;
+                if (gt >= 2) ptx::mbar_wait(&bars[BAR_S_FREE + buf], ((gt >> 1) - 1) & 1);
+                ptx::mbar_wait(&bars[BAR_FULL + gt % NTB], (gt / NTB) & 1);
+                __syncwarp();
                 ptx::tc_fence_after();
-                const uint32_t pos0 = (tg * NCHUNK) % NSLOT;
-#pragma unroll 1
-                for (int blk = 0; blk < 4; ++blk) {
-                    const uint32_t sa = (pos0 + pos_of_chunk(2 * blk, tg)) % NSLOT;
-                    issue_gemm2_block<P_LAYOUT>(tmem_base + TCOL_O + 16 * blk,
-                                                ring_addr + sa * SLOT_BYTES, phi_addr, plo_addr,
-                                                n_k, first_of_split);
-                    ptx::umma_commit(&bars[BAR_EMPTY + sa]);
-                    ptx::umma_commit(&bars[BAR_EMPTY + (sa + 1) % NSLOT]);
-                }
-                ptx::umma_commit(&bars[BAR_O_DONE]);
-            };
-            for (int vb = vb_begin; vb <= vb_end; ++vb) {
-                SplitDesc sd;
-                if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
-                const int n_pages = (sd.seqlen + PAGE - 1) / PAGE;
-                for (int t = sd.t0; t < sd.t1; ++t) {
-                    if (has_prev) {
-                        gemm2(prev_gt, prev_nk, prev_first);
-                        has_prev = false;
-                    }
-                    if (t == sd.t0) {
-                        ptx::mbar_wait(&bars[BAR_Q_FULL], nsplit & 1);
-                        ptx::tc_fence_after();
-                    }
-                    const uint32_t buf = gt & 1;
-                    if (gt >= 2) {
-                        ptx::mbar_wait(&bars[BAR_S_FREE + buf], ((gt >> 1) - 1) & 1);
-                        ptx::tc_fence_after();
-                    }
-                    const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
-                    const uint32_t ring_round0 = (gt * NCHUNK) / NSLOT;
-#pragma unroll 1
-                    for (int pos = 0; pos < NCHUNK; ++pos) {
-                        const uint32_t abs_pos = gt * NCHUNK + pos;
-                        const uint32_t s = (pos0 + pos) % NSLOT;
-                        (void)ring_round0;
-                        ptx::mbar_wait(&bars[BAR_FULL + s], (abs_pos / NSLOT) & 1);
-                        ptx::tc_fence_after();
-                        const int chunk = chunk_at(pos, gt);
-                        issue_gemm1_chunk(tmem_base + TCOL_S + 16 * buf, ring_addr + s * SLOT_BYTES,
-                                          q_addr + chunk * Q_CHUNK_BYTES, pos == 0);
-                        if (chunk == 8) ptx::umma_commit(&bars[BAR_EMPTY + s]);
-                    }
-                    ptx::umma_commit(&bars[BAR_S_FULL + buf]);
-                    if (t == sd.t1 - 1) ptx::umma_commit(&bars[BAR_Q_EMPTY]);
-                    has_prev = true;
-                    prev_gt = gt;
-                    prev_nk = (2 * t + 1 < n_pages) ? 8 : 4;
-                    prev_first = (t == sd.t0);
-                    ++gt;
-                }
-                ++nsplit;
+                ETAP_TRACE(prm, gt, 2);
+                issue_gemm1_tile(tmem_base + TCOL_S + 16 * buf, ring_addr, q_addr,
+                                 (gt * NCHUNK) % NSLOT, gt);
+                ptx::umma_commit_elect(&bars[BAR_S_FULL + buf]);
+                ETAP_TRACE(prm, gt, 3);
+                if (t == sd.t1 - 1) ptx::umma_commit_elect(&bars[BAR_Q_EMPTY]);
+                ++gt;
             }
-            if (has_prev) gemm2(prev_gt, prev_nk, prev_first);
+            ++nsplit;
         }
-        __syncwarp();
-    } else {
-        // ===================================================== softmax + epilogue (128 threads)
-        const int wq = warp & 3;           // TMEM lane quadrant accessible by this warp
-        const int row = wq * 32 + lane;    // KV row in the tile / d row within an O^T block
-        const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
-        float* red_max = reinterpret_cast<float*>(smem + OFF_RED);  // [2][4][16]
-        float* red_sum = red_max + 128;                               // [4][16]
-        uint8_t* p_hi = smem + OFF_P;
-        uint8_t* p_lo = p_hi + P_BYTES;
-        const bool negate = prm.flags & FLAG_NEGATE_RESCALE;
-        const bool eager = negate || (prm.flags & FLAG_EAGER_RESCALE);
+    } else if (warp == 2) {
+        // ===================================================== GEMM2 issuer (whole warp, elect)
         uint32_t gt = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
             if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
-            const int n_pages = (sd.seqlen + PAGE - 1) / PAGE;
+            for (int t = sd.t0; t < sd.t1; ++t) {
+                const uint32_t buf = gt & 1;
+                ptx::mbar_wait(&bars[BAR_P_FULL + buf], (gt >> 1) & 1);
+                __syncwarp();
+                ptx::tc_fence_after();
+                ETAP_TRACE(prm, gt, 6);
+                const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
+#pragma unroll
+                for (int blk = 0; blk < 4; ++blk) {
+                    uint32_t sa = pos0 + pos_of_chunk(2 * blk, gt);
+                    sa = sa >= NSLOT ? sa - NSLOT : sa;
+                    issue_gemm2_block(tmem_base + TCOL_O + 32 * blk, ring_addr + sa * SLOT_BYTES,
+                                      p_addr + buf * P_BYTES, t == sd.t0);
+                }
+                ptx::umma_commit_elect(&bars[BAR_G2_DONE + gt % NTB]);
+                ETAP_TRACE(prm, gt, 7);
+                ++gt;
+            }
+        }
+    } else if (warp >= SOFTMAX_WARP0) {
+        // ===================================================== softmax + epilogue (128 threads)
+        const int wq = warp & 3;               // TMEM lane quadrant accessible by this warp
+        const bool active = lane < 16;         // M=64 tile: rows in lanes 0-15 of each quadrant
+        const int row = s_row_of(wq, lane);    // KV row in the tile (active lanes)
+        const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
+        float* red_max = reinterpret_cast<float*>(smem + OFF_RED);  // [2][4][16]
+        float* red_sum = red_max + 128;                               // [4][16]
+        const bool negate = prm.flags & FLAG_NEGATE_RESCALE;
+        const bool eager = negate || (prm.flags & FLAG_EAGER_RESCALE);
+        const float thresh = eager ? 0.f : LAZY_RESCALE_LOG2;
+        const bool tracer = (threadIdx.x == SOFTMAX_WARP0 * 32);
+        uint32_t gt = 0;
+        for (int vb = vb_begin; vb <= vb_end; ++vb) {
+            SplitDesc sd;
+            if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
             float m_used[16], l_part[16];
 #pragma unroll
             for (int h = 0; h < 16; ++h) { m_used[h] = -INFINITY; l_part[h] = 0.f; }
@@ -380,6 +364,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint32_t buf = gt & 1;
                 ptx::mbar_wait(&bars[BAR_S_FULL + buf], (gt >> 1) & 1);
                 ptx::tc_fence_after();
+                if (tracer) ETAP_TRACE(prm, gt, 4);
                 uint32_t sr[16];
                 ptx::tmem_ld16(t_lane + TCOL_S + 16 * buf, sr);
                 ptx::tmem_wait_ld();
@@ -387,100 +372,112 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::mbar_arrive(&bars[BAR_S_FREE + buf]);
 
                 const int grow = t * TILE + row;
-                const bool valid = grow < sd.seqlen;
+                const bool valid = active && grow < sd.seqlen;
                 float x[16];
+                bool exceed = false;
 #pragma unroll
-                for (int h = 0; h < 16; ++h)
+                for (int h = 0; h < 16; ++h) {
                     x[h] = valid ? __uint_as_float(sr[h]) * prm.scale_log2 : -INFINITY;
-
-                // column max over the 128 rows of the tile
-                const float wm = warp_reduce16<true>(x, lane);
-                float* rm = red_max + (gt & 1) * 64;
-                if ((lane & 1) == 0) rm[wq * 16 + (lane >> 1)] = wm;
-                ptx::named_bar_sync(1, 128);
-                float mt[16];
-#pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    const float4 a = reinterpret_cast<const float4*>(rm)[q4];
-                    const float4 b = reinterpret_cast<const float4*>(rm + 16)[q4];
-                    const float4 c = reinterpret_cast<const float4*>(rm + 32)[q4];
-                    const float4 d = reinterpret_cast<const float4*>(rm + 48)[q4];
-                    mt[4 * q4 + 0] = fmaxf(fmaxf(a.x, b.x), fmaxf(c.x, d.x));
-                    mt[4 * q4 + 1] = fmaxf(fmaxf(a.y, b.y), fmaxf(c.y, d.y));
-                    mt[4 * q4 + 2] = fmaxf(fmaxf(a.z, b.z), fmaxf(c.z, d.z));
-                    mt[4 * q4 + 3] = fmaxf(fmaxf(a.w, b.w), fmaxf(c.w, d.w));
+                    exceed |= x[h] > m_used[h] + thresh;
                 }
                 const bool first = (t == sd.t0);
+                // one barrier decides, CTA-uniformly, whether any running max must move
+                const bool any = ptx::bar_red_or(1, 128, exceed || (negate && !first));
                 bool need_rescale = false;
                 float alpha[16];
 #pragma unroll
-                for (int h = 0; h < 16; ++h) {
-                    if (first) {
-                        m_used[h] = mt[h];
-                        alpha[h] = 0.f;
-                    } else {
-                        const float mn = fmaxf(m_used[h], mt[h]);
-                        const bool upd = eager ? (mn > m_used[h]) : (mn > m_used[h] + LAZY_RESCALE_LOG2);
-                        alpha[h] = upd ? exp2f(m_used[h] - mn) : 1.f;
-                        if (upd) { m_used[h] = mn; need_rescale = true; }
+                for (int h = 0; h < 16; ++h) alpha[h] = 1.f;
+                if (any) {
+                    const float wm = warp_reduce16<true>(x, lane);
+                    float* rm = red_max + (gt & 1) * 64;
+                    if ((lane & 1) == 0) rm[wq * 16 + (lane >> 1)] = wm;
+                    ptx::named_bar_sync(2, 128);
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const float4 a = reinterpret_cast<const float4*>(rm)[q4];
+                        const float4 b = reinterpret_cast<const float4*>(rm + 16)[q4];
+                        const float4 c = reinterpret_cast<const float4*>(rm + 32)[q4];
+                        const float4 d = reinterpret_cast<const float4*>(rm + 48)[q4];
+                        const float mt[4] = {fmaxf(fmaxf(a.x, b.x), fmaxf(c.x, d.x)),
+                                             fmaxf(fmaxf(a.y, b.y), fmaxf(c.y, d.y)),
+                                             fmaxf(fmaxf(a.z, b.z), fmaxf(c.z, d.z)),
+                                             fmaxf(fmaxf(a.w, b.w), fmaxf(c.w, d.w))};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int h = 4 * q4 + j;
+                            if (first) {
+                                m_used[h] = mt[j];
+                            } else {
+                                const float mn = fmaxf(m_used[h], mt[j]);
+                                if (mn > m_used[h] + thresh) {
+                                    alpha[h] = exp2f(m_used[h] - mn);
+                                    m_used[h] = mn;
+                                    need_rescale = true;
+                                }
+                            }
+                        }
                     }
+                    if (negate && !first) need_rescale = true;
                 }
-                if (negate && !first) need_rescale = true;
-                float p[16];
+                float pv[16];
 #pragma unroll
                 for (int h = 0; h < 16; ++h) {
-                    p[h] = exp2f(x[h] - m_used[h]);
-                    l_part[h] = first ? p[h] : fmaf(l_part[h], alpha[h], p[h]);
+                    pv[h] = exp2f(x[h] - m_used[h]);
+                    l_part[h] = first ? pv[h] : fmaf(l_part[h], alpha[h], pv[h]);
                 }
-                // GEMM2 of the previous tile must be complete before O^T is rescaled and P
-                // is overwritten
-                if (gt > 0) {
-                    ptx::mbar_wait(&bars[BAR_O_DONE], (gt - 1) & 1);
-                    ptx::tc_fence_after();
-                }
+                // the P buffer is reused every other tile: GEMM2(gt-2) must have read it
+                if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
                 if (need_rescale) {
+                    // O^T must contain GEMM2(gt-1) before it is rescaled
+                    ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 1) % NTB], ((gt - 1) / NTB) & 1);
+                    ptx::tc_fence_after();
 #pragma unroll 1
                     for (int blk = 0; blk < 4; ++blk) {
-                        uint32_t o[16];
-                        const uint32_t ta = t_lane + TCOL_O + 16 * blk;
-                        ptx::tmem_ld16(ta, o);
+                        uint32_t o[32];
+                        const uint32_t ta = t_lane + TCOL_O + 32 * blk;
+                        ptx::tmem_ld32(ta, o);
                         ptx::tmem_wait_ld();
 #pragma unroll
                         for (int h = 0; h < 16; ++h) {
                             const float a = negate ? -alpha[h] : alpha[h];
                             o[h] = __float_as_uint(__uint_as_float(o[h]) * a);
+                            o[16 + h] = __float_as_uint(__uint_as_float(o[16 + h]) * a);
                         }
-                        ptx::tmem_st16(ta, o);
+                        ptx::tmem_st32(ta, o);
                     }
                     ptx::tmem_wait_st();
                 }
-                write_p_hilo<P_LAYOUT>(p_hi, p_lo, row, p);
-                // rows of the last page past seqlen were loaded from HBM and may hold
-                // non-finite garbage; zero them in the V chunks (0 * NaN = NaN in the MMA)
-                const bool page1 = 2 * t + 1 < n_pages;
-                if (!valid && (row < PAGE || page1)) {
-                    const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
+                if (active) {
+                    write_p_hilo(smem + OFF_P + buf * P_BYTES, row, pv);
+                    // rows of the last page past seqlen were loaded from HBM and may hold
+                    // non-finite garbage; zero them in the V chunks (0 * NaN = NaN in the MMA)
+                    if (grow >= sd.seqlen) {
+                        const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
 #pragma unroll 1
-                    for (int c = 0; c < NVCHUNK; ++c) {
-                        const uint32_t s = (pos0 + pos_of_chunk(c, gt)) % NSLOT;
-                        uint4* dst = reinterpret_cast<uint4*>(smem + OFF_RING + s * SLOT_BYTES + row * 128);
+                        for (int c = 0; c < NVCHUNK; ++c) {
+                            const uint32_t s = (pos0 + pos_of_chunk(c, gt)) % NSLOT;
+                            uint4* dst = reinterpret_cast<uint4*>(smem + OFF_RING + s * SLOT_BYTES + row * 128);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) dst[j] = make_uint4(0, 0, 0, 0);
+                            for (int j = 0; j < 8; ++j) dst[j] = make_uint4(0, 0, 0, 0);
+                        }
                     }
                 }
                 ptx::fence_proxy_async_smem();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(&bars[BAR_P_FULL]);
+                if (tracer) ETAP_TRACE(prm, gt, 5);
+                ptx::mbar_arrive(&bars[BAR_P_FULL + buf]);
                 ++gt;
             }
 
-            // ---- epilogue: wait for the last GEMM2, reduce l, O = O^T / l (the single
-            // transpose of etap.cpp:140 is the TMEM lane->d mapping), L = m + log l
-            ptx::mbar_wait(&bars[BAR_O_DONE], (gt - 1) & 1);
+            // ---- epilogue: wait for the last GEMM2, reduce l, O = (O^T_hi + O^T_lo) / l
+            // (the single transpose of etap.cpp:140 is the TMEM lane -> d mapping),
+            // L = m + log l (etap.cpp:144)
+            const uint32_t last = gt - 1;
+            ptx::mbar_wait(&bars[BAR_G2_DONE + last % NTB], (last / NTB) & 1);
             ptx::tc_fence_after();
-            const float ws = warp_reduce16<false>(l_part, lane);
-            if ((lane & 1) == 0) red_sum[wq * 16 + (lane >> 1)] = ws;
-            ptx::named_bar_sync(1, 128);
+            const float wsum = warp_reduce16<false>(l_part, lane);
+            if ((lane & 1) == 0) red_sum[wq * 16 + (lane >> 1)] = wsum;
+            ptx::named_bar_sync(2, 128);
             float inv_l[16], l_tot[16];
 #pragma unroll
             for (int h = 0; h < 16; ++h) {
@@ -499,24 +496,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 dst = prm.ws_o + static_cast<size_t>(idx) * HG * D_V;
                 dst_lse = prm.ws_lse + static_cast<size_t>(idx) * HG;
             }
+            const int drow = wq * 32 + lane;  // M=128 layout: d row = TMEM lane
 #pragma unroll 1
             for (int blk = 0; blk < 4; ++blk) {
-                uint32_t o[16];
-                ptx::tmem_ld16(t_lane + TCOL_O + 16 * blk, o);
+                uint32_t o[32];
+                ptx::tmem_ld32(t_lane + TCOL_O + 32 * blk, o);
                 ptx::tmem_wait_ld();
-                const int d = blk * 128 + row;
+                const int d = blk * 128 + drow;
 #pragma unroll
-                for (int h = 0; h < 16; ++h) dst[h * D_V + d] = __uint_as_float(o[h]) * inv_l[h];
+                for (int h = 0; h < 16; ++h)
+                    dst[h * D_V + d] = (__uint_as_float(o[h]) + __uint_as_float(o[16 + h])) * inv_l[h];
             }
-            if (row < 16) {
+            if (wq == 0 && lane < 16) {
                 float v = 0.f;
 #pragma unroll
                 for (int h = 0; h < 16; ++h)
-                    if (h == row) v = (m_used[h] + log2f(l_tot[h])) * 0.69314718055994530942f;
-                dst_lse[row] = v;
+                    if (h == lane) v = (m_used[h] + log2f(l_tot[h])) * 0.69314718055994530942f;
+                dst_lse[lane] = v;
             }
             ptx::tc_fence_before();
-            // red_sum is rewritten by the next split's epilogue only after many barriers
         }
     }
 
@@ -602,7 +600,6 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
 // UMMA layout self-test: one CTA runs GEMM1 and GEMM2 of a single tile through exactly the
 // descriptors / smem layouts of the decode kernel and dumps the TMEM accumulators.
 // =============================================================================================
-template <int P_LAYOUT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     etap_mla_selftest_kernel(const __grid_constant__ CUtensorMap tm_k,
                              const __grid_constant__ CUtensorMap tm_q, const float* p_in,
@@ -616,7 +613,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (threadIdx.x == 0) {
         ptx::mbar_init(&bars[0], 1);
         ptx::mbar_init(&bars[1], 1);
-        ptx::mbar_init(&bars[2], 1);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
@@ -626,57 +622,52 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t ring_addr = ptx::smem_u32(smem + OFF_RING);
     const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q);
-    const uint32_t phi_addr = ptx::smem_u32(smem + OFF_P);
+    const uint32_t p_addr = ptx::smem_u32(smem + OFF_P);
 
     if (threadIdx.x == 0) {
         const uint64_t pol = ptx::policy_evict_first();
         ptx::mbar_arrive_expect_tx(&bars[0], NCHUNK * SLOT_BYTES + Q_BYTES);
-        for (int c = 0; c < NCHUNK; ++c) {
-            uint8_t* dst = smem + OFF_RING + c * SLOT_BYTES;  // chunk c in slot c
-            ptx::tma_load_2d(dst, &tm_k, &bars[0], c * 64, 0, pol);
-            ptx::tma_load_2d(dst + HALF_SLOT, &tm_k, &bars[0], c * 64, 64, pol);
+        for (int c = 0; c < NCHUNK; ++c) {  // chunk c in slot c
+            ptx::tma_load_2d(smem + OFF_RING + c * SLOT_BYTES, &tm_k, &bars[0], c * 64, 0, pol);
             ptx::tma_load_2d(smem + OFF_Q + c * Q_CHUNK_BYTES, &tm_q, &bars[0], c * 64, 0, pol);
         }
     }
-    // P (hi only, lo = 0) written by the softmax warps exactly as the decode kernel does
-    if (warp >= 2) {
-        const int row = (warp & 3) * 32 + lane;
+    // P = hi + lo of the input, written by the softmax warps exactly as the decode kernel does
+    if (warp >= SOFTMAX_WARP0 && lane < 16) {
+        const int row = s_row_of(warp & 3, lane);
         float p[16];
         for (int h = 0; h < 16; ++h) p[h] = p_in[row * 16 + h];
-        uint32_t hi[8];
-        for (int i = 0; i < 8; ++i) hi[i] = pack_bf16x2(p[2 * i], p[2 * i + 1]);
-        uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        PLayout<P_LAYOUT>::write_row(smem + OFF_P, row, hi);
-        PLayout<P_LAYOUT>::write_row(smem + OFF_P + P_BYTES, row, zero);
-        ptx::fence_proxy_async_smem();
+        write_p_hilo(smem + OFF_P, row, p);
     }
+    ptx::fence_proxy_async_smem();
     __syncthreads();
-    if (threadIdx.x == 32) {
+    if (warp == 1) {
         ptx::mbar_wait(&bars[0], 0);
+        __syncwarp();
         ptx::tc_fence_after();
-        for (int c = 0; c < NCHUNK; ++c)
-            issue_gemm1_chunk(tmem_base + TCOL_S, ring_addr + c * SLOT_BYTES,
-                              q_addr + c * Q_CHUNK_BYTES, c == 0);
+        issue_gemm1_tile(tmem_base + TCOL_S, ring_addr, q_addr, 0, 0);  // tile 0: chunk c in slot c
         for (int blk = 0; blk < 4; ++blk)
-            issue_gemm2_block<P_LAYOUT>(tmem_base + TCOL_O + 16 * blk,
-                                        ring_addr + (2 * blk) * SLOT_BYTES, phi_addr,
-                                        phi_addr + P_BYTES, 8, true);
-        ptx::umma_commit(&bars[1]);
+            issue_gemm2_block(tmem_base + TCOL_O + 32 * blk, ring_addr + (2 * blk) * SLOT_BYTES,
+                              p_addr, true);
+        ptx::umma_commit_elect(&bars[1]);
     }
-    if (warp >= 2) {
+    if (warp >= SOFTMAX_WARP0) {
         ptx::mbar_wait(&bars[1], 0);
         ptx::tc_fence_after();
         const int wq = warp & 3;
-        const int row = wq * 32 + lane;
         const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
-        uint32_t r[16];
-        ptx::tmem_ld16(t_lane + TCOL_S, r);
+        uint32_t r[32];
+        ptx::tmem_ld16(t_lane + TCOL_S, *reinterpret_cast<uint32_t(*)[16]>(r));
         ptx::tmem_wait_ld();
-        for (int h = 0; h < 16; ++h) s_out[row * 16 + h] = __uint_as_float(r[h]);
+        if (lane < 16) {
+            const int row = s_row_of(wq, lane);
+            for (int h = 0; h < 16; ++h) s_out[row * 16 + h] = __uint_as_float(r[h]);
+        }
         for (int blk = 0; blk < 4; ++blk) {
-            ptx::tmem_ld16(t_lane + TCOL_O + 16 * blk, r);
+            ptx::tmem_ld32(t_lane + TCOL_O + 32 * blk, r);
             ptx::tmem_wait_ld();
-            for (int h = 0; h < 16; ++h) o_out[(blk * 128 + row) * 16 + h] = __uint_as_float(r[h]);
+            for (int n = 0; n < 32; ++n)
+                o_out[(blk * 128 + wq * 32 + lane) * 32 + n] = __uint_as_float(r[n]);
         }
     }
     ptx::tc_fence_before();
@@ -739,13 +730,7 @@ int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_row
     return ETAP_OK;
 }
 
-int p_layout_choice() {
-    static int v = [] {
-        const char* e = std::getenv("ETAP_P_LAYOUT");
-        return (e && e[0] == '1') ? 1 : 0;
-    }();
-    return v;
-}
+void* g_trace_buf = nullptr;  // debug tracing target (etap_mla_debug_trace)
 
 template <typename K>
 int ensure_smem_attr(K kernel, int bytes) {
@@ -927,6 +912,7 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     prm.groups = groups;
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.flags = flags;
+    prm.trace = static_cast<unsigned long long*>(g_trace_buf);
 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaLaunchAttribute attr[1];
@@ -940,15 +926,9 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (p_layout_choice() == 1) {
-        static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<1>, SMEM_ALLOC);
-        if (attr_rc) return attr_rc;
-        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel<1>, tm_kv, tm_q, prm));
-    } else {
-        static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<0>, SMEM_ALLOC);
-        if (attr_rc) return attr_rc;
-        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel<0>, tm_kv, tm_q, prm));
-    }
+    static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel, SMEM_ALLOC);
+    if (attr_rc) return attr_rc;
+    ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel, tm_kv, tm_q, prm));
 
     cudaLaunchConfig_t cfg2 = {};
     cfg2.gridDim = dim3(batch * groups * HG);
@@ -962,24 +942,99 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     return ETAP_OK;
 }
 
+int etap_mla_debug_trace(void* device_buf) {
+    g_trace_buf = device_buf;
+    return ETAP_OK;
+}
+
 int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* s_t, float* o_t,
                            void* stream) {
     if (int rc = check_device()) return rc;
     CUtensorMap tm_k, tm_q;
-    if (int rc = make_map(&tm_k, k, TILE, PAGE)) return rc;
+    if (int rc = make_map(&tm_k, k, TILE, PAGE)) return rc;  // one 64-row page
     if (int rc = make_map(&tm_q, q, HG, HG)) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (p_layout_choice() == 1) {
-        static int attr_rc = ensure_smem_attr(etap_mla_selftest_kernel<1>, SMEM_ALLOC);
-        if (attr_rc) return attr_rc;
-        etap_mla_selftest_kernel<1><<<1, NUM_THREADS, SMEM_ALLOC, st>>>(tm_k, tm_q, p, s_t, o_t);
-    } else {
-        static int attr_rc = ensure_smem_attr(etap_mla_selftest_kernel<0>, SMEM_ALLOC);
-        if (attr_rc) return attr_rc;
-        etap_mla_selftest_kernel<0><<<1, NUM_THREADS, SMEM_ALLOC, st>>>(tm_k, tm_q, p, s_t, o_t);
-    }
+    static int attr_rc = ensure_smem_attr(etap_mla_selftest_kernel, SMEM_ALLOC);
+    if (attr_rc) return attr_rc;
+    etap_mla_selftest_kernel<<<1, NUM_THREADS, SMEM_ALLOC, st>>>(tm_k, tm_q, p, s_t, o_t);
     ETAP_CUDA(cudaGetLastError());
     return ETAP_OK;
 }
 
 }  // extern "C"
+
+// =============================================================================================
+// Tensor-pipe microbenchmark (debug): cycles for n back-to-back tcgen05.mma of one variant.
+//   0: M128 N16 A K-major SW128      1: M128 N16 A MN-major SW128 (GEMM2 style)
+//   2: M128 N32 A MN-major SW128     3: M64  N16 A K-major SW128
+//   4: M128 N64 A K-major SW128      5: M128 N16 A MN-major, B K-major SW128
+// =============================================================================================
+namespace {
+__global__ void __launch_bounds__(128, 1) etap_umma_bench_kernel(int variant, int n, long long* out) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    for (int i = threadIdx.x; i < 65536 / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    ptx::fence_proxy_async_smem();
+    if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::fence_mbar_init(); }
+    if (threadIdx.x < 32) ptx::tmem_alloc(&tslot, 256);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tbase = tslot;
+    const int mode = variant / 10;   // 0: lane-0 divergent issue, 1: warp-uniform elect in asm
+    const int shape = variant % 10;
+    if (threadIdx.x < 32 && (mode == 1 || threadIdx.x == 0)) {
+        const uint32_t a = ptx::smem_u32(smem), b = a + 32768;
+        uint32_t idesc;
+        uint64_t bd = ptx::smem_desc(b, 16, 1024, ptx::LAYOUT_SW128);
+        const bool mn = (shape == 1 || shape == 2 || shape == 5);
+        switch (shape) {
+            case 1: idesc = ptx::idesc_bf16_f32(128, 16, 1, 1); bd = ptx::smem_desc(b, 256, 128, ptx::LAYOUT_NONE); break;
+            case 2: idesc = ptx::idesc_bf16_f32(128, 32, 1, 1); bd = ptx::smem_desc(b, 512, 128, ptx::LAYOUT_NONE); break;
+            case 3: idesc = ptx::idesc_bf16_f32(64, 16, 0, 0); break;
+            case 4: idesc = ptx::idesc_bf16_f32(128, 64, 0, 0); break;
+            case 5: idesc = ptx::idesc_bf16_f32(128, 16, 1, 0); break;
+            case 6: idesc = ptx::idesc_bf16_f32(128, 256, 0, 0); break;
+            default: idesc = ptx::idesc_bf16_f32(128, 16, 0, 0); break;
+        }
+        const uint64_t ad0 = mn ? ptx::smem_desc(a, 16384, 1024, ptx::LAYOUT_SW128)
+                                : ptx::smem_desc(a, 16, 1024, ptx::LAYOUT_SW128);
+        for (int rep = 0; rep < 2; ++rep) {
+            if (mode == 1) __syncwarp();
+            const long long t0 = clock64();
+            if (mode == 0) {
+                for (int i = 0; i < n; ++i) {
+                    const uint64_t ad = ad0 + (mn ? (uint64_t)((i & 7) * 128) : (uint64_t)((i & 3) * 2));
+                    ptx::umma_f16(tbase, ad, bd, idesc, i > 0);
+                }
+            } else {
+                for (int i = 0; i < n; i += 4) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t ad = ad0 + (mn ? (uint64_t)(j * 128) : (uint64_t)(j * 2));
+                        ptx::umma_f16_elect(tbase, ad, bd, idesc, (i + j) > 0);
+                    }
+                }
+            }
+            const long long t1 = clock64();
+            if (mode == 0) ptx::umma_commit(&bar); else ptx::umma_commit_elect(&bar);
+            ptx::mbar_wait(&bar, rep & 1);
+            const long long t2 = clock64();
+            if (rep == 1 && (threadIdx.x == 0)) { out[0] = t1 - t0; out[1] = t2 - t0; }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 256); }
+}
+}  // namespace
+
+extern "C" int etap_mla_umma_bench(int variant, int n, long long* out_dev, int grid) {
+    cudaFuncSetAttribute(etap_umma_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+    etap_umma_bench_kernel<<<grid, 128, 66 * 1024>>>(variant, n, out_dev);
+    ETAP_CUDA(cudaGetLastError());
+    return ETAP_OK;
+}

@@ -8,13 +8,15 @@
 //   /root/reference/proj/src/etap.cpp:102-148 driver: block loop, epilogue O = (O^T / l)^T,
 //                                              L = m + log l
 // How it is computed here (B200-native, not a translation):
-//   * KV tile of 128 latent rows on the UMMA M axis, the 16 heads of a head group on N:
-//     S^T[128 x 16] = K_tile[128 x 576] . Q^T  -> TMEM (fp32), 36 tcgen05.mma (K=16 each)
-//   * column-wise online softmax by one warpgroup: thread = KV row = TMEM lane
-//   * O^T[512 x 16] += V^T[512 x 128] . P^T[128 x 16] -> TMEM (4 M=128 blocks), with P split
-//     into bf16 hi + lo parts (two MMAs) so the bf16 P rounding does not limit accuracy
-//   * V^T is read from the SAME smem tile as K (MN-major descriptor over the TMA SW128 tile)
-//   * paged latent-KV TMA loads into a 12-slot ring; one persistent CTA per SM
+//   * one 64-row latent-KV page per tile, KV rows on the UMMA M axis, the 16 heads of a head
+//     group on N:  S^T[64 x 16] = K_page[64 x 576] . Q^T  -> TMEM (fp32), 36 tcgen05.mma
+//   * column-wise online softmax (thread = KV row = TMEM lane) with a thresholded lazy
+//     rescale decided by one barrier-reduction (bar.red.or) per tile
+//   * O^T[512 x 32] += V^T[512 x 64] . [P_hi | P_lo]^T -> TMEM (4 M=128 d-blocks, N=32):
+//     P is split into bf16 hi + lo so the bf16 rounding of P does not limit accuracy, and both
+//     parts share one MMA (the A = V^T smem read dominates, N=32 costs the same as N=16)
+//   * V^T is read from the SAME smem chunks as K (MN-major descriptor over the TMA SW128 tile)
+//   * paged TMA loads into a 24-slot ring (2.6 pages in flight); one persistent CTA per SM
 #pragma once
 
 #include <cuda_bf16.h>
@@ -27,94 +29,72 @@ namespace etap_b200 {
 constexpr int D_QK = 576;
 constexpr int D_V = 512;
 constexpr int PAGE = 64;        // rows per KV page
-constexpr int TILE = 128;       // KV rows per UMMA tile (two pages)
-constexpr int HG = 16;          // heads per head group (UMMA N)
+constexpr int TILE = 64;        // KV rows per tile (one page)
+constexpr int HG = 16;          // heads per head group (UMMA N of GEMM1)
 constexpr int NCHUNK = 9;       // 576 / 64 column chunks (SW128 atoms are 64 bf16 wide)
 constexpr int NVCHUNK = 8;      // 512 / 64 chunks that are also V
-constexpr int NSLOT = 12;       // ring depth in chunk slots
-constexpr int SLOT_BYTES = TILE * 128;          // 128 rows x 128 B = 16 KiB
-constexpr int HALF_SLOT = PAGE * 128;           // one page of one chunk = 8 KiB
+constexpr int NSLOT = 24;       // ring depth in chunk slots
+constexpr int SLOT_BYTES = TILE * 128;          // 64 rows x 128 B = 8 KiB
 constexpr int Q_CHUNK_BYTES = HG * 128;         // 2 KiB
 constexpr int Q_BYTES = NCHUNK * Q_CHUNK_BYTES; // 18 KiB
-constexpr int P_BYTES = TILE * HG * 2;          // 4 KiB (one of hi / lo)
+constexpr int PN = 32;                          // GEMM2 N: 16 heads hi | 16 heads lo
+constexpr int P_BYTES = TILE * PN * 2;          // 4 KiB per P buffer
 
 constexpr int OFF_RING = 0;
 constexpr int OFF_Q = OFF_RING + NSLOT * SLOT_BYTES;  // 196608
-constexpr int OFF_P = OFF_Q + Q_BYTES;                // 215040
+constexpr int OFF_P = OFF_Q + Q_BYTES;                // 215040 (2 buffers)
 constexpr int OFF_RED = OFF_P + 2 * P_BYTES;          // 223232
 constexpr int RED_BYTES = 1024;                       // [2][4][16] max + [4][16] sum (floats)
 constexpr int OFF_BAR = OFF_RED + RED_BYTES;          // 224256
-constexpr int NBAR = 2 * NSLOT + 8;
+constexpr int NTB = 4;          // tile-barrier ring depth (tiles in flight <= NSLOT/9 + 1)
+constexpr int NBAR = 2 * NTB + 8;
 constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
 constexpr int SMEM_USED = OFF_TMEM + 16;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;  // slack for manual 1024 B alignment
 
 // barrier indices
-constexpr int BAR_FULL = 0;
-constexpr int BAR_EMPTY = NSLOT;
-constexpr int BAR_Q_FULL = 2 * NSLOT + 0;
-constexpr int BAR_Q_EMPTY = 2 * NSLOT + 1;
-constexpr int BAR_S_FULL = 2 * NSLOT + 2;  // [2]
-constexpr int BAR_S_FREE = 2 * NSLOT + 4;  // [2]
-constexpr int BAR_P_FULL = 2 * NSLOT + 6;
-constexpr int BAR_O_DONE = 2 * NSLOT + 7;
+constexpr int BAR_FULL = 0;             // [NTB] all 9 chunks of tile gt landed (gt % NTB)
+constexpr int BAR_G2_DONE = NTB;        // [NTB] GEMM2 of tile gt complete: its 9 ring slots
+                                        //       and its P buffer are free (gt % NTB)
+constexpr int BAR_Q_FULL = 2 * NTB + 0;
+constexpr int BAR_Q_EMPTY = 2 * NTB + 1;
+constexpr int BAR_S_FULL = 2 * NTB + 2;  // [2]
+constexpr int BAR_S_FREE = 2 * NTB + 4;  // [2]
+constexpr int BAR_P_FULL = 2 * NTB + 6;  // [2]
 
 // TMEM columns (128 lanes x 32 bit each)
-constexpr uint32_t TMEM_COLS = 128;
-constexpr uint32_t TCOL_S = 0;    // S^T double buffer: cols [0,16) and [16,32)
-constexpr uint32_t TCOL_O = 32;   // O^T d-block i at cols [32+16i, 48+16i)
+constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t TCOL_S = 0;    // S^T double buffer: cols [0,16) and [16,32), M=64 lane layout
+constexpr uint32_t TCOL_O = 32;   // O^T d-block i at cols [32+32i, 64+32i): 16 hi | 16 lo
 
-constexpr int NUM_THREADS = 192;  // warp0 TMA, warp1 MMA, warps 2..5 softmax/epilogue
+// warp 0 TMA producer, warp 1 GEMM1 issuer (+TMEM alloc), warp 2 GEMM2 issuer, warp 3 idle,
+// warps 4..7 softmax / epilogue (warp % 4 = TMEM lane quadrant)
+constexpr int NUM_THREADS = 256;
+constexpr int SOFTMAX_WARP0 = 4;
 constexpr float LAZY_RESCALE_LOG2 = 8.0f;  // rescale O^T only when the max grows by > 2^8
 
 constexpr int SCHED_INTS = 8;
-constexpr int META_FIXED_COST = 2;  // per-split overhead in tile units for the scheduler
+constexpr int META_FIXED_COST = 3;  // per-split overhead in tile (page) units for the scheduler
 
 enum : unsigned { FLAG_NEGATE_RESCALE = 1u, FLAG_EAGER_RESCALE = 2u };
 
-// P^T operand layouts (B of GEMM2). 0: MN-major, no swizzle (core matrices 8 rows x 8 heads);
-// 1: K-major SW128 (P stored head-major).
-template <int P_LAYOUT>
-struct PLayout;
+// P^T operand (B of GEMM2): MN-major, no swizzle. Core matrices of 8 KV rows x 8 columns
+// (16 B per row); columns 0-15 = P_hi heads 0-15, 16-31 = P_lo heads 0-15.
+//   offset(r, n) = (r/8)*512 + (n/8)*128 + (r%8)*16 + (n%8)*2
+// LBO = K-direction core stride (512), SBO = N-direction core stride (128).
+__device__ __forceinline__ uint64_t p_desc(uint32_t base, int kk) {
+    return ptx::smem_desc(base + kk * 1024, 512, 128, ptx::LAYOUT_NONE);
+}
 
-template <>
-struct PLayout<0> {
-    static constexpr uint32_t kMajorMN = 1;
-    // rows 16kk..16kk+15; LBO = K-direction core stride, SBO = MN-direction core stride
-    __device__ static uint64_t desc(uint32_t base, int kk) {
-        return ptx::smem_desc(base + kk * 512, 256, 128, ptx::LAYOUT_NONE);
-    }
-    __device__ static void write_row(uint8_t* p, int r, const uint32_t (&pk)[8]) {
-        uint8_t* dst = p + (r >> 3) * 256 + (r & 7) * 16;
-        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(dst + 128) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-    }
-};
-
-template <>
-struct PLayout<1> {
-    static constexpr uint32_t kMajorMN = 0;
-    __device__ static uint64_t desc(uint32_t base, int kk) {
-        return ptx::smem_desc(base + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024,
-                              ptx::LAYOUT_SW128);
-    }
-    __device__ static void write_row(uint8_t* p, int r, const uint32_t (&pk)[8]) {
-        const int rr = r & 63;
-        uint8_t* base = p + (r >> 6) * 2048 + (rr & 7) * 2;
-#pragma unroll
-        for (int h = 0; h < 16; ++h) {
-            const uint32_t w = pk[h >> 1];
-            const uint16_t v = (h & 1) ? static_cast<uint16_t>(w >> 16) : static_cast<uint16_t>(w);
-            uint8_t* dst = base + (h >> 3) * 1024 + (h & 7) * 128 + ((((rr >> 3) ^ (h & 7))) << 4);
-            *reinterpret_cast<uint16_t*>(dst) = v;
-        }
-    }
-};
+// M=64 accumulator layout (cta_group::1): row m lives in TMEM lane (m % 16) + 32 * (m / 16),
+// i.e. lanes 0-15 of each 32-lane quadrant. Warp q of the softmax group owns rows
+// 16q .. 16q+15 in its lanes 0-15.
+__device__ __forceinline__ int s_row_of(int quadrant, int lane) { return quadrant * 16 + lane; }
 
 // Ring position -> latent column chunk. Every tile consumes 9 ring positions starting at
 // 9*gt; V chunks (2i, 2i+1) must sit in adjacent slots so one MN-major descriptor covers
-// 128 d-rows (LBO = one slot). 12 is even, so pairs starting at even positions never wrap:
-// even tiles start on an even position ([V0..V7, rope]), odd tiles on an odd one
+// 128 d-rows (LBO = one slot). NSLOT is even, so pairs starting at even positions never
+// wrap: even tiles start on an even position ([V0..V7, rope]), odd tiles on an odd one
 // ([rope, V0..V7]).
 __device__ __forceinline__ int chunk_at(int pos, uint32_t gt) {
     if (gt & 1u) return pos == 0 ? 8 : pos - 1;
@@ -125,32 +105,39 @@ __device__ __forceinline__ int pos_of_chunk(int chunk, uint32_t gt) {
     return chunk;
 }
 
-// GEMM1 part for one latent column chunk: S^T[128x16] (+)= K[128 x 64] . Q^T[64 x 16]
-__device__ __forceinline__ void issue_gemm1_chunk(uint32_t s_tmem, uint32_t slot_addr,
-                                                  uint32_t q_chunk_addr, bool first_chunk) {
-    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, 16, 0, 0);
+// GEMM1 of one tile: S^T[64x16] = K[64 x 576] . Q^T[576 x 16], 9 chunks x 4 MMAs (K=16).
+// Whole-warp call (elect inside). pos0 = ring slot of the tile's first position.
+__device__ __forceinline__ void issue_gemm1_tile(uint32_t s_tmem, uint32_t ring_addr,
+                                                 uint32_t q_addr, uint32_t pos0, uint32_t gt) {
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(64, 16, 0, 0);
+    const uint64_t a_ring = ptx::smem_desc(ring_addr, 16, 1024, ptx::LAYOUT_SW128);
+    const uint64_t b_q = ptx::smem_desc(q_addr, 16, 1024, ptx::LAYOUT_SW128);
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-        const uint64_t a = ptx::smem_desc(slot_addr + kk * 32, 16, 1024, ptx::LAYOUT_SW128);
-        const uint64_t b = ptx::smem_desc(q_chunk_addr + kk * 32, 16, 1024, ptx::LAYOUT_SW128);
-        ptx::umma_f16(s_tmem, a, b, idesc, (first_chunk && kk == 0) ? 0u : 1u);
+    for (int pos = 0; pos < NCHUNK; ++pos) {
+        uint32_t s = pos0 + pos;
+        s = s >= NSLOT ? s - NSLOT : s;
+        const int chunk = chunk_at(pos, gt);
+        const uint64_t a0 = a_ring + static_cast<uint64_t>(s * (SLOT_BYTES >> 4));
+        const uint64_t b0 = b_q + static_cast<uint64_t>(chunk * (Q_CHUNK_BYTES >> 4));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // +32 B along K inside the 128 B swizzle row
+            ptx::umma_f16_elect(s_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc,
+                                (pos == 0 && kk == 0) ? 0u : 1u);
     }
 }
 
 // GEMM2 part for one d-block (128 latent columns = chunks 2i, 2i+1 in slots s, s+1):
-// O^T[128 x 16] (+)= V^T[128 x rows] . P^T[rows x 16], P = hi + lo.
-template <int P_LAYOUT>
+// O^T[128 x 32] (+)= V^T[128 x 64] . [P_hi | P_lo]^T[64 x 32]. Whole-warp call.
 __device__ __forceinline__ void issue_gemm2_block(uint32_t o_tmem, uint32_t slot_addr,
-                                                  uint32_t p_hi, uint32_t p_lo, int n_k,
-                                                  bool zero_init) {
-    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, 16, 1, PLayout<P_LAYOUT>::kMajorMN);
-    for (int kk = 0; kk < n_k; ++kk) {
-        // MN-major SW128: LBO = stride between 64-wide MN atoms (next slot), SBO = 8-row group
-        const uint64_t a = ptx::smem_desc(slot_addr + kk * 2048, SLOT_BYTES, 1024, ptx::LAYOUT_SW128);
-        ptx::umma_f16(o_tmem, a, PLayout<P_LAYOUT>::desc(p_hi, kk), idesc,
-                      (zero_init && kk == 0) ? 0u : 1u);
-        ptx::umma_f16(o_tmem, a, PLayout<P_LAYOUT>::desc(p_lo, kk), idesc, 1u);
-    }
+                                                  uint32_t p_addr, bool zero_init) {
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, PN, 1, 1);
+    // MN-major SW128: LBO = stride between 64-wide MN atoms (next slot), SBO = 8-row group
+    const uint64_t a0 = ptx::smem_desc(slot_addr, SLOT_BYTES, 1024, ptx::LAYOUT_SW128);
+    const uint64_t b0 = p_desc(p_addr, 0);
+#pragma unroll
+    for (int kk = 0; kk < TILE / 16; ++kk)
+        ptx::umma_f16_elect(o_tmem, a0 + kk * (2048 >> 4), b0 + kk * (1024 >> 4), idesc,
+                            (zero_init && kk == 0) ? 0u : 1u);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo_elem, float hi_elem) {
@@ -158,25 +145,24 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo_elem, float hi_elem) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// P (fp32, 16 heads of one KV row) -> bf16 hi and lo parts, written as row r of P^T.
-template <int P_LAYOUT>
-__device__ __forceinline__ void write_p_hilo(uint8_t* p_hi, uint8_t* p_lo, int r,
-                                             const float (&p)[16]) {
+// P (fp32, 16 heads of one KV row) -> bf16 hi and lo parts, written as row r of [P_hi|P_lo]^T.
+__device__ __forceinline__ void write_p_hilo(uint8_t* p, int r, const float (&pv)[16]) {
     uint32_t hi[8], lo[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const __nv_bfloat16 h0 = __float2bfloat16_rn(p[2 * i]);
-        const __nv_bfloat16 h1 = __float2bfloat16_rn(p[2 * i + 1]);
-        const float r0 = p[2 * i] - __bfloat162float(h0);
-        const float r1 = p[2 * i + 1] - __bfloat162float(h1);
+        const __nv_bfloat16 h0 = __float2bfloat16_rn(pv[2 * i]);
+        const __nv_bfloat16 h1 = __float2bfloat16_rn(pv[2 * i + 1]);
         __nv_bfloat162 hh;
         hh.x = h0;
         hh.y = h1;
         hi[i] = *reinterpret_cast<uint32_t*>(&hh);
-        lo[i] = pack_bf16x2(r0, r1);
+        lo[i] = pack_bf16x2(pv[2 * i] - __bfloat162float(h0), pv[2 * i + 1] - __bfloat162float(h1));
     }
-    PLayout<P_LAYOUT>::write_row(p_hi, r, hi);
-    PLayout<P_LAYOUT>::write_row(p_lo, r, lo);
+    uint8_t* dst = p + (r >> 3) * 512 + (r & 7) * 16;
+    *reinterpret_cast<uint4*>(dst) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4*>(dst + 128) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+    *reinterpret_cast<uint4*>(dst + 256) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    *reinterpret_cast<uint4*>(dst + 384) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
 }
 
 // Butterfly transpose-reduction: 16 per-lane values (one per head) reduced over the 32 lanes
@@ -228,6 +214,15 @@ struct DecodeParams {
     int groups;  // heads / 16
     float scale_log2;
     unsigned flags;
+    unsigned long long* trace;  // debug: [cta][TRACE_TILES][8] globaltimer stamps, or null
 };
+
+constexpr int TRACE_TILES = 256;
+#define ETAP_TRACE(prm, gt, slot)                                                              \
+    do {                                                                                       \
+        if ((prm).trace != nullptr && (gt) < TRACE_TILES)                                      \
+            (prm).trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + (gt)) * 8 + (slot)] = \
+                ptx::global_timer_ns();                                                        \
+    } while (0)
 
 }  // namespace etap_b200

@@ -17,7 +17,7 @@ from ._lib import check
 D_QK = 576
 D_V = 512
 PAGE_ROWS = 64
-TILE_ROWS = 128
+TILE_ROWS = 64
 HEAD_GROUP = 16
 SCHED_INTS = 8
 
@@ -138,9 +138,11 @@ def mla_decode(q: torch.Tensor, kv_pool: torch.Tensor, block_table: torch.Tensor
 
 
 def selftest_umma(k: torch.Tensor, q: torch.Tensor, p: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
-    """Single-tile UMMA layout check: returns (S^T [128,16], O^T [512,16]) from TMEM."""
+    """Single-tile UMMA layout check. k [64,576] bf16, q [16,576] bf16, p [64,16] fp32 ->
+    (S^T [64,16], O^T [512,32]) read back from TMEM; O^T columns 0-15 = V^T P_hi,
+    16-31 = V^T P_lo (P = P_hi + P_lo in bf16)."""
     s_t = torch.empty((TILE_ROWS, HEAD_GROUP), dtype=torch.float32, device=k.device)
-    o_t = torch.empty((D_V, HEAD_GROUP), dtype=torch.float32, device=k.device)
+    o_t = torch.empty((D_V, 2 * HEAD_GROUP), dtype=torch.float32, device=k.device)
     check(_lib.lib().etap_mla_selftest_umma(k.data_ptr(), q.data_ptr(), p.data_ptr(), s_t.data_ptr(),
                                             o_t.data_ptr(), _stream_ptr(None)), "etap_mla_selftest_umma")
     return s_t, o_t

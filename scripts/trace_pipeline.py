@@ -1,0 +1,86 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Per-tile pipeline trace of the decode kernel (debug %globaltimer stamps, see
+etap_mla_debug_trace in include/etap_mla.h). Prints where each tile's time goes.
+
+    python scripts/trace_pipeline.py [--batch 16 --ctx 65536]
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+
+from paper_2506_01969_b200 import _lib, inputs, mla
+
+TRACE_TILES = 256
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--ctx", type=int, default=65536)
+    ap.add_argument("--runs", type=int, default=3)
+    a = ap.parse_args()
+    inp = inputs.make_mla_inputs([a.ctx] * a.batch, heads=16, pad_value=0.0)
+    plan = mla.MlaDecodePlan.create(a.batch, 16, "cuda")
+    nparts = plan.num_sm_parts
+    buf = torch.zeros(nparts * TRACE_TILES * 8, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        plan.metadata(inp.seqlens)
+        plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
+    torch.cuda.synchronize()
+    _lib.lib().etap_mla_debug_trace(buf.data_ptr())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    plan.metadata(inp.seqlens)
+    plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
+    e1.record()
+    torch.cuda.synchronize()
+    _lib.lib().etap_mla_debug_trace(None)
+    print(f"traced step: {e0.elapsed_time(e1) * 1000:.1f} us")
+    t = buf.view(nparts, TRACE_TILES, 8).cpu().numpy().astype(np.float64)
+    valid = (t > 0).all(axis=2)
+    t0 = t[valid].min()
+    names = ["issue_first", "issue_last", "landed_last", "S_commit", "softmax_start", "P_written",
+             "mma_sees_P", "G2_commit"]
+    rows = []
+    for c in range(nparts):
+        n = int(valid[c].sum())
+        for g in range(2, n - 1):
+            e = t[c, g]
+            nxt = t[c, g + 1]
+            rows.append([
+                e[2] - e[1],            # latency of the last chunk (issue -> landed seen by MMA)
+                e[1] - e[0],            # producer: span issuing the tile's 9 chunks
+                e[3] - e[2],            # GEMM1 tail issue after last chunk
+                e[4] - e[3],            # S commit -> softmax sees S (GEMM1 execution)
+                e[5] - e[4],            # softmax duration
+                e[6] - e[5],            # P written -> MMA sees it
+                e[7] - e[6],            # GEMM2 issue
+                nxt[3] - e[3],          # tile period
+                nxt[0] - e[7],          # GEMM2(g) commit -> producer issues first chunk of g+1
+                nxt[1] - e[7],          # GEMM2(g) commit -> producer issued last chunk of g+1
+            ])
+    r = np.array(rows)
+    labels = ["lat_tile(last issue->seen)", "issue_span", "g1_issue", "s_ready_wait", "softmax", "p_to_mma",
+              "g2_issue", "PERIOD", "g2->next_first_issue", "g2->next_last_issue"]
+    print(f"{len(rows)} steady-state tiles over {nparts} CTAs (ns): median / p10 / p90")
+    for i, lab in enumerate(labels):
+        col = r[:, i]
+        print(f"  {lab:24s} {np.median(col):9.0f} {np.percentile(col, 10):9.0f} {np.percentile(col, 90):9.0f}")
+    # CTA span
+    span = [(t[c][valid[c]].max() - t[c][valid[c]].min()) for c in range(nparts) if valid[c].any()]
+    starts = [t[c][valid[c]].min() - t0 for c in range(nparts) if valid[c].any()]
+    print(f"CTA busy span us: median {np.median(span) / 1e3:.1f} max {np.max(span) / 1e3:.1f}; "
+          f"start offsets us: max {np.max(starts) / 1e3:.1f}")
+    print("tiles per CTA:", np.bincount(valid.sum(axis=1)).nonzero()[0].tolist())
+
+
+if __name__ == "__main__":
+    main()
