@@ -1,0 +1,381 @@
+# SPDX-License-Identifier: Apache-2.0
+"""ETAP MLA decode benchmark (BASELINE.json metric) — prints ONE JSON line on rank 0.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+Workload (BASELINE.json configs[1]): MLA decode, B=16 sequences x 64K latent-KV rows,
+16 heads per GPU, d_qk=576 / d_v=512, bf16 paged KV (64-row pages), fp32 O + LSE.
+A step = K1 (split-KV schedule) + K2 (transposed tcgen05 pipeline) + K3 (LSE combine) on
+inputs resident in HBM; with N > 1 GPUs every rank owns 16 of the 16*N heads (KV replicated)
+and the step ends with an NCCL all-gather of O (weak scaling).
+Inputs (1.2 GB of KV) exceed the 126 MB L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"] if (ROOT / "BASELINE.json").exists() else \
+    "MLA decode µs/step & HBM GB/s (B=16, ctx 64K, 16 heads/GPU); RMSE vs CPU"
+BATCH, CTX, HEADS = 16, 65536, 16
+WORKLOAD = "mla_decode_b16_ctx64k_h16_per_gpu"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------------ clocks (NVML)
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self.period, self.ok = period_s, False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - NVML missing
+            log(f"[bench] NVML unavailable: {e}")
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(self.period)
+
+    def sample(self):
+        if not self.ok:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            pass
+
+    def __enter__(self):
+        self.sample()
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join()
+        self.sample()
+
+    def summary(self) -> dict:
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(s)}
+
+
+# ------------------------------------------------------------------------ helpers
+def peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+def ncu_traffic() -> float | None:
+    """DRAM read+write bytes per K2 launch at this workload from the committed ncu capture."""
+    f = ROOT / "profiles" / "ncu_summary.json"
+    if not f.exists():
+        return None
+    try:
+        d = json.loads(f.read_text())
+        return float(d["decode_kernel"]["dram_bytes_per_launch"]) if d.get("workload") == WORKLOAD else None
+    except Exception:
+        return None
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def reference_cpu_sample(q_bits, kv_rows_bits, scale: float, nthreads: int):
+    """Time the reference's run_etap (oracle/_ref, the unmodified etaplab library) on the
+    given sample; returns seconds."""
+    import numpy as np
+
+    import oracle
+
+    q = oracle.bf16_widen(q_bits)            # [B, H, 576]
+    kv = oracle.bf16_widen(kv_rows_bits)     # [B, rows, 576]
+    t, _, _ = oracle.ref_mla_run_etap_batch(np.ascontiguousarray(q), np.ascontiguousarray(kv), scale, nthreads)
+    return t
+
+
+def sample_inputs_cpu(inp, rows: int):
+    """Contiguous first `rows` latent rows of every sequence as bf16 bits [B, rows, 576]."""
+    import numpy as np
+    import torch
+
+    B = inp.batch
+    pages = rows // 64
+    idx = inp.block_table[:, :pages].long()                       # [B, pages]
+    kv = inp.kv_pool[idx].reshape(B, pages * 64, 576)             # gather on device
+    qb = inp.q[:, 0].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+    kvb = kv.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+    return qb, kvb
+
+
+# ------------------------------------------------------------------------ reference arm
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference
+    import numpy as np
+
+    import oracle
+
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libetaplab_ref.so not built"}))
+        return
+    rows = args.ref_rows
+    threads = cpu_threads()
+    # the same bf16 inputs as the GPU arm, generated on the host with the reference generator
+    seeds = [42 + 7919 * b for b in range(BATCH)]
+    q = np.stack([oracle.bf16_bits(oracle.ref_matrix_from_seed(HEADS, 576, 3 * s + 1)) for s in seeds])
+    kv = np.stack([oracle.bf16_bits(oracle.ref_matrix_from_seed(rows, 576, 3 * s + 2)) for s in seeds])
+    scale = 1.0 / math.sqrt(576.0)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = reference_cpu_sample(q, kv, scale, threads)
+        if i >= args.warmup:
+            times.append(t)
+    scale_up = CTX / rows
+    us = float(np.median(times)) * 1e6 * scale_up
+    sample = (f"run_etap exact64 (reference etaplab, compiled from source) on all {BATCH} sequences x "
+              f"{rows} of {CTX} KV rows x {HEADS} heads per step, {threads} host threads (one per "
+              f"sequence), median of {args.steps} steps scaled x{scale_up:.0f} to the full workload")
+    line = {"metric": METRIC, "value": us, "unit": "us/step", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "batch": BATCH, "ctx": CTX, "heads_per_gpu": HEADS,
+                       "d_qk": 576, "d_v": 512},
+            "cpu_baseline": {"value": us, "unit": "us/step", "cores": threads, "kind": "reference", "sample": sample},
+            "e2e": {"value": us, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------ our arm
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_01969_b200 import inputs, mla, sharding
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"[bench] WORLD_SIZE={world} differs from --gpus {args.gpus}; using WORLD_SIZE")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    total_heads = HEADS * world
+    seqlens = [CTX] * BATCH
+    h0, _ = sharding.head_shard(total_heads, world, rank)
+    inp = inputs.make_mla_inputs(seqlens, heads=HEADS, seed=42, device=dev, pad_value=0.0,
+                                 head_offset=h0, total_heads=total_heads)
+    plan = mla.MlaDecodePlan.create(BATCH, HEADS, dev)
+    out = torch.empty((BATCH, 1, HEADS, 512), dtype=torch.float32, device=dev)
+    lse = torch.empty((BATCH, 1, HEADS), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        plan.metadata(inp.seqlens)
+        plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, out=out, lse=lse)
+        if world > 1:  # head-sharded output -> all 16*N heads on every rank (NCCL all-gather)
+            return sharding.gather_heads(out), sharding.gather_heads(lse)
+        return out, lse
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    us = ms * 1e3
+
+    # roofline pass: the dominant kernel (K2) timed alone with events on its stream
+    k2_ms = []
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in evs:
+        plan.metadata(inp.seqlens)
+        a.record(stream)
+        plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, out=out, lse=lse,
+                    flags=mla.FLAG_SKIP_COMBINE)
+        b.record(stream)
+        plan.combine(out, lse)
+    torch.cuda.synchronize(dev)
+    k2_ms = sorted(a.elapsed_time(b) for a, b in evs)
+    k2_avg_ms = sum(k2_ms) / len(k2_ms)
+
+    nbytes = inputs.algorithmic_bytes(seqlens, HEADS)
+    nflops = inputs.flops(seqlens, HEADS)
+    peak, peak_kind = peaks()
+    achieved = nbytes / (k2_avg_ms * 1e-3) / 1e9
+    traffic = ncu_traffic()
+
+    result = {}
+    if rank == 0:
+        clocks = clk.summary()
+        # e2e: the reference-facing C-ABI call with HOST buffers (H2D + K1/K2/K3 + D2H per step)
+        e2e = None
+        if world == 1 and args.e2e_steps > 0:
+            e2e = e2e_host(inp, args.e2e_steps, dev)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(inp, args)
+        result = {
+            "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "batch": BATCH, "ctx": CTX, "heads_per_gpu": HEADS,
+                       "total_heads": total_heads, "d_qk": 576, "d_v": 512, "page_rows": 64,
+                       "kv_bytes_per_gpu": inp.kv_bytes(), "l2": "inputs (1.2 GB KV) > 126 MB L2, no flush",
+                       "parallelism": f"head-shard tp{world} (KV replicated, NCCL all-gather of O)" if world > 1
+                       else "single GPU", "step": "K1 metadata + K2 decode + K3 combine" +
+                       (" + all-gather(O)" if world > 1 else "")},
+            "throughput": {"hbm_gbs_aggregate": nbytes * world / (us * 1e-6) / 1e9,
+                           "hbm_gbs_per_gpu": nbytes / (us * 1e-6) / 1e9,
+                           "tflops_aggregate": nflops * world / (us * 1e-6) / 1e12,
+                           "algorithmic_bytes_per_step_per_gpu": nbytes},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "etap_mla_decode_kernel (K2)",
+                         "kernel_avg_us": k2_avg_ms * 1e3, "peak_kind": peak_kind,
+                         "timing": f"second timed pass of {args.steps} steps, CUDA events around each K2 launch"},
+            "clocks": clocks,
+            "gpu_launches": 3 * args.steps,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+def e2e_host(inp, steps: int, dev) -> dict:
+    """Same workload through etap_mla_host_decode (pinned host buffers in, host results out)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2506_01969_b200 import _lib
+
+    L = _lib.lib()
+    q = inp.q.cpu().pin_memory()
+    kv = inp.kv_pool.cpu().pin_memory()
+    bt = inp.block_table.cpu().pin_memory()
+    sl = inp.seqlens.cpu().pin_memory()
+    out = torch.empty((inp.batch, inp.heads, 512), dtype=torch.float32).pin_memory()
+    lse = torch.empty((inp.batch, inp.heads), dtype=torch.float32).pin_memory()
+    ctx = C.c_void_p()
+    _lib.check(L.etap_mla_host_ctx_create(inp.batch, inp.heads, kv.shape[0], bt.shape[1], C.byref(ctx)), "ctx")
+    try:
+        def call():
+            _lib.check(L.etap_mla_host_decode(ctx, q.data_ptr(), kv.data_ptr(), bt.data_ptr(), sl.data_ptr(),
+                                              inp.scale, 0, out.data_ptr(), lse.data_ptr()), "host_decode")
+        call()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            call()
+        dt = (time.perf_counter() - t0) / steps
+    finally:
+        L.etap_mla_host_ctx_destroy(ctx)
+    h2d = q.numel() * 2 + kv.numel() * 2 + bt.numel() * 4 + sl.numel() * 4
+    d2h = out.numel() * 4 + lse.numel() * 4
+    return {"value": dt * 1e6, "unit": "us/step", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "api": "etap_mla_host_decode (C-ABI, pinned host buffers, synchronous)", "steps": steps}
+
+
+def cpu_baseline(inp, args) -> dict | None:
+    try:
+        import oracle
+
+        if not oracle.ref_available():
+            return None
+        rows = args.cpu_rows
+        threads = cpu_threads()
+        qb, kvb = sample_inputs_cpu(inp, rows)
+        t = reference_cpu_sample(qb, kvb, inp.scale, threads)
+        scale_up = CTX / rows
+        us = t * 1e6 * scale_up
+        return {"value": us, "unit": "us/step", "cores": threads, "kind": "reference",
+                "sample": (f"reference run_etap exact64 (oracle/_ref, etaplab compiled from source) on the same "
+                           f"bf16 inputs: {BATCH} sequences x first {rows} of {CTX} rows x {HEADS} heads, "
+                           f"{threads} threads, {t:.2f} s wall, scaled x{scale_up:.0f}")}
+    except Exception as e:  # pragma: no cover
+        log(f"[bench] cpu baseline failed: {e}")
+        return None
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-rows", type=int, default=16384, help="KV rows per sequence in the CPU baseline sample")
+    ap.add_argument("--ref-rows", type=int, default=2048, help="KV rows per sequence per reference-arm step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("[bench] warmup raised to 3 (contract minimum)")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

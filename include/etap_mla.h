@@ -59,6 +59,8 @@ extern "C" {
 #define ETAP_FLAG_EAGER_RESCALE 2u  /* rescale O^T whenever the running max grows (the
                                        reference's per-block order, etap.cpp:40-47,62-70)
                                        instead of the default thresholded lazy rescale */
+#define ETAP_FLAG_SKIP_COMBINE 4u   /* launch K2 only; the caller runs etap_mla_combine (used to
+                                       time K2 alone) */
 
 /* Thread-local description of the last error. Never NULL. */
 const char* etap_mla_last_error(void);
@@ -98,6 +100,11 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
                     int batch, int q_tokens, int heads, float scale, int causal,
                     const int32_t* sched, const int32_t* split_off, int num_sm_parts,
                     void* workspace, float* out, float* lse, unsigned flags, void* stream);
+
+/* K3 alone — log-sum-exp merge of the split partials left in `workspace` by a decode call
+ * made with ETAP_FLAG_SKIP_COMBINE (same batch/heads/num_sm_parts/split_off). */
+int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_parts,
+                     void* workspace, float* out, float* lse, void* stream);
 
 /* End-to-end call with HOST buffers (the reference-facing path: run_etap receives host
  * matrices): host->device copies, K1, K2, K3, device->host copies, synchronize.

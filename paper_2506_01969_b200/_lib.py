@@ -17,6 +17,7 @@ ETAP_ERR_SHAPE = 1
 ETAP_ERR_CUDA = 2
 FLAG_NEGATE_RESCALE = 1
 FLAG_EAGER_RESCALE = 2
+FLAG_SKIP_COMBINE = 4
 
 _lib = None
 
@@ -42,6 +43,7 @@ def _declare(lib: C.CDLL) -> None:
         "etap_mla_metadata_host": (i32, [vp, i32, i32, i32, vp, vp]),
         "etap_mla_decode": (i32, [vp, vp, i64, vp, i32, vp, i32, i32, i32, f32, i32, vp, vp, i32,
                                   vp, vp, vp, u32, vp]),
+        "etap_mla_combine": (i32, [vp, i32, i32, i32, vp, vp, vp, vp]),
         "etap_mla_host_ctx_create": (i32, [i32, i32, i64, i32, P(vp)]),
         "etap_mla_host_decode": (i32, [vp, vp, vp, vp, vp, f32, u32, vp, vp]),
         "etap_mla_host_ctx_destroy": (None, [vp]),

@@ -756,6 +756,11 @@ size_t max_partials(int batch, int heads, int num_sm_parts) {
 
 }  // namespace
 
+namespace etap_b200 {
+// error reporting for the host-buffer entry points in etap_mla_host.cpp
+int host_fail(int code, const char* msg) { return fail(code, msg); }
+}  // namespace etap_b200
+
 extern "C" {
 
 const char* etap_mla_last_error(void) { return g_last_error.c_str(); }
@@ -930,15 +935,31 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     if (attr_rc) return attr_rc;
     ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel, tm_kv, tm_q, prm));
 
+    if (flags & ETAP_FLAG_SKIP_COMBINE) return ETAP_OK;
+    return etap_mla_combine(split_off, batch, heads, num_sm_parts, workspace, out, lse, stream);
+}
+
+int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_parts,
+                     void* workspace, float* out, float* lse, void* stream) {
+    if (!split_off || !workspace || !out || !lse) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    if (batch < 1 || heads < HG || heads % HG != 0 || num_sm_parts < 1)
+        return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
+    const int groups = heads / HG;
+    const size_t np = max_partials(batch, heads, num_sm_parts);
+    float* ws_o = static_cast<float*>(workspace);
+    float* ws_lse = ws_o + np * HG * D_V;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg2 = {};
     cfg2.gridDim = dim3(batch * groups * HG);
     cfg2.blockDim = dim3(COMBINE_THREADS);
     cfg2.dynamicSmemBytes = 0;
-    cfg2.stream = st;
+    cfg2.stream = static_cast<cudaStream_t>(stream);
     cfg2.attrs = attr;
     cfg2.numAttrs = 1;
-    ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, prm.ws_o, prm.ws_lse, split_off,
-                                 groups, heads, out, lse));
+    ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, ws_o, ws_lse, split_off, groups,
+                                 heads, out, lse));
     return ETAP_OK;
 }
 

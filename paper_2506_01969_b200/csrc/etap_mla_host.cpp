@@ -15,9 +15,12 @@
 
 #include "../../include/etap_mla.h"
 
-namespace {
+namespace etap_b200 {
+int host_fail(int code, const char* msg);  // etap_mla.cu: sets etap_mla_last_error()
+}
+using etap_b200::host_fail;
 
-thread_local std::string g_host_error;
+namespace {
 
 struct DevBuf {
     void* p = nullptr;
@@ -68,11 +71,11 @@ extern "C" {
 
 int etap_mla_host_ctx_create(int batch, int heads, int64_t num_pages, int max_pages_per_seq,
                              etap_mla_host_ctx** ctx) {
-    if (!ctx) return ETAP_ERR_SHAPE;
+    if (!ctx) return host_fail(ETAP_ERR_SHAPE, "ctx is NULL");
     *ctx = nullptr;
     if (batch < 1 || heads < ETAP_MLA_HEAD_GROUP || heads % ETAP_MLA_HEAD_GROUP != 0 ||
         num_pages < 1 || max_pages_per_seq < 1)
-        return ETAP_ERR_SHAPE;
+        return host_fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, pages >= 1 required");
     auto* c = new etap_mla_host_ctx();
     c->batch = batch;
     c->heads = heads;
@@ -81,7 +84,8 @@ int etap_mla_host_ctx_create(int batch, int heads, int64_t num_pages, int max_pa
     int dev = 0;
     size_t sched_n = 0, so_n = 0, ws_n = 0;
     cudaError_t e = cudaGetDevice(&dev);
-    int rc = e == cudaSuccess ? etap_mla_num_sm_parts(dev, &c->num_sm_parts) : ETAP_ERR_CUDA;
+    int rc = e == cudaSuccess ? etap_mla_num_sm_parts(dev, &c->num_sm_parts)
+                              : host_fail(ETAP_ERR_CUDA, cudaGetErrorString(e));
     if (!rc) rc = etap_mla_sched_ints(batch, heads, c->num_sm_parts, &sched_n, &so_n);
     if (!rc) rc = etap_mla_workspace_bytes(batch, heads, c->num_sm_parts, &ws_n);
     if (!rc) {
@@ -93,7 +97,7 @@ int etap_mla_host_ctx_create(int batch, int heads, int64_t num_pages, int max_pa
             c->lse.alloc(rows * 4) || c->sched.alloc(sched_n * 4) ||
             c->split_off.alloc(so_n * 4) || c->ws.alloc(ws_n) ||
             cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking))
-            rc = ETAP_ERR_CUDA;
+            rc = host_fail(ETAP_ERR_CUDA, "device allocation failed");
     }
     if (rc) {
         delete c;
@@ -108,13 +112,13 @@ int etap_mla_host_decode(etap_mla_host_ctx* c, const void* q_host, const void* k
                          float scale, unsigned flags, float* out_host, float* lse_host) {
     if (!c || !q_host || !kv_pool_host || !block_table_host || !seqlens_host || !out_host ||
         !lse_host)
-        return ETAP_ERR_SHAPE;
+        return host_fail(ETAP_ERR_SHAPE, "NULL pointer argument");
     cudaStream_t s = c->stream;
     if (cudaMemcpyAsync(c->q.p, q_host, c->q.n, cudaMemcpyHostToDevice, s) ||
         cudaMemcpyAsync(c->kv.p, kv_pool_host, c->kv.n, cudaMemcpyHostToDevice, s) ||
         cudaMemcpyAsync(c->bt.p, block_table_host, c->bt.n, cudaMemcpyHostToDevice, s) ||
         cudaMemcpyAsync(c->sl.p, seqlens_host, c->sl.n, cudaMemcpyHostToDevice, s))
-        return ETAP_ERR_CUDA;
+        return host_fail(ETAP_ERR_CUDA, "host->device copy failed");
     int rc = etap_mla_metadata(static_cast<int32_t*>(c->sl.p), c->batch, c->heads,
                                c->num_sm_parts, static_cast<int32_t*>(c->sched.p),
                                static_cast<int32_t*>(c->split_off.p), s);
@@ -128,7 +132,7 @@ int etap_mla_host_decode(etap_mla_host_ctx* c, const void* q_host, const void* k
     if (cudaMemcpyAsync(out_host, c->out.p, c->out.n, cudaMemcpyDeviceToHost, s) ||
         cudaMemcpyAsync(lse_host, c->lse.p, c->lse.n, cudaMemcpyDeviceToHost, s) ||
         cudaStreamSynchronize(s))
-        return ETAP_ERR_CUDA;
+        return host_fail(ETAP_ERR_CUDA, "device->host copy / synchronize failed");
     return ETAP_OK;
 }
 
@@ -143,19 +147,24 @@ int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t
                           int64_t b_c, int64_t stages, unsigned flags, double* o, double* l) {
     // argument validation mirrors run_etap / make_problem (etap.cpp:104-106,
     // attention.cpp:11-19): these are the cases the reference rejects with invalid_argument
-    if (b_r < 1 || b_c < 1 || stages < 1) return ETAP_ERR_SHAPE;  // "tile config fields must be >= 1"
-    if (!q || !k || !v || !o || !l || n_q < 1 || n_kv < 1) return ETAP_ERR_SHAPE;
-    if (d_qk != ETAP_MLA_D_QK || d_v != ETAP_MLA_D_V) return ETAP_ERR_SHAPE;  // MLA shapes only
-    if (!(scale >= 0.0) || !std::isfinite(scale)) return ETAP_ERR_SHAPE;
-    if (n_kv > (int64_t)1 << 30) return ETAP_ERR_SHAPE;
+    if (b_r < 1 || b_c < 1 || stages < 1)
+        return host_fail(ETAP_ERR_SHAPE, "tile config fields must be >= 1");
+    if (!q || !k || !v || !o || !l || n_q < 1 || n_kv < 1)
+        return host_fail(ETAP_ERR_SHAPE, "matrix dimensions must be >= 1");
+    if (d_qk != ETAP_MLA_D_QK || d_v != ETAP_MLA_D_V)
+        return host_fail(ETAP_ERR_SHAPE, "GPU ETAP path is MLA decode: d_qk=576, d_v=512");
+    if (!(scale >= 0.0) || !std::isfinite(scale))
+        return host_fail(ETAP_ERR_SHAPE, "scale must be finite and >= 0");
+    if (n_kv > (int64_t)1 << 30) return host_fail(ETAP_ERR_SHAPE, "n_kv too large");
     // MLA aliasing: V must be the first 512 columns of the latent KV rows
     for (int64_t i = 0; i < n_kv; ++i)
-        if (std::memcmp(v + i * d_v, k + i * d_qk, sizeof(double) * d_v) != 0) return ETAP_ERR_SHAPE;
+        if (std::memcmp(v + i * d_v, k + i * d_qk, sizeof(double) * d_v) != 0)
+            return host_fail(ETAP_ERR_SHAPE, "V must be the first 512 columns of K (MLA aliasing)");
 
     const int heads = static_cast<int>((n_q + ETAP_MLA_HEAD_GROUP - 1) / ETAP_MLA_HEAD_GROUP) *
                       ETAP_MLA_HEAD_GROUP;
     const int64_t pages = (n_kv + ETAP_MLA_PAGE_ROWS - 1) / ETAP_MLA_PAGE_ROWS;
-    if (pages > 0x7fffffff) return ETAP_ERR_SHAPE;
+    if (pages > 0x7fffffff) return host_fail(ETAP_ERR_SHAPE, "too many pages");
     std::vector<uint16_t> qb(static_cast<size_t>(heads) * d_qk, 0);
     std::vector<uint16_t> kvb(static_cast<size_t>(pages) * ETAP_MLA_PAGE_ROWS * d_qk, 0);
     for (int64_t i = 0; i < n_q * d_qk; ++i) qb[i] = bf16_bits_rne(q[i]);

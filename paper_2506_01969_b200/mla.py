@@ -12,7 +12,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import check
+from ._lib import FLAG_EAGER_RESCALE, FLAG_NEGATE_RESCALE, FLAG_SKIP_COMBINE, check  # noqa: F401
 
 D_QK = 576
 D_V = 512
@@ -117,6 +117,12 @@ class MlaDecodePlan:
             self.workspace.data_ptr(), out.data_ptr(), lse.data_ptr(), int(flags),
             _stream_ptr(stream)), "etap_mla_decode")
         return out, lse
+
+    def combine(self, out: torch.Tensor, lse: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
+        """K3 alone, after a decode(..., flags=FLAG_SKIP_COMBINE)."""
+        check(_lib.lib().etap_mla_combine(self.split_off.data_ptr(), self.batch, self.heads, self.num_sm_parts,
+                                          self.workspace.data_ptr(), out.data_ptr(), lse.data_ptr(),
+                                          _stream_ptr(stream)), "etap_mla_combine")
 
 
 def _check_tensor(t: torch.Tensor, dtype: torch.dtype, shape: tuple, name: str) -> None:

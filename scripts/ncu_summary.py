@@ -1,0 +1,96 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Summarise an ncu capture of the decode kernel (K2) and a launch list into profiles/.
+
+    python scripts/ncu_summary.py gpurun_out/prof_r01.ncu-rep gpurun_out/launches_r01.csv r01
+writes profiles/ncu_summary.json (read by bench.py for roofline.traffic) and
+profiles/<tag>/ncu_decode_kernel.md.
+"""
+from __future__ import annotations
+
+import csv
+import io
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg", "launch__registers_per_thread",
+    "launch__grid_size", "launch__block_size", "lts__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "nsecond": 1e-9, "msecond": 1e-3,
+         "us": 1e-6, "ns": 1e-9}
+
+
+def raw(rep: str) -> dict:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d = {}
+    for h, u, v in zip(hdr, units, vals):
+        if h in KEYS:
+            try:
+                d[h] = (float(v.replace(",", "")), u)
+            except ValueError:
+                d[h] = (v, u)
+    return d
+
+
+def main() -> None:
+    rep, launches, tag = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None, sys.argv[3] if len(sys.argv) > 3 else "r01"
+    from paper_2506_01969_b200 import inputs
+
+    d = raw(rep)
+    rd = d["dram__bytes_read.sum"][0] * SCALE[d["dram__bytes_read.sum"][1]]
+    wr = d["dram__bytes_write.sum"][0] * SCALE[d["dram__bytes_write.sum"][1]]
+    dur = d["gpu__time_duration.sum"][0] * SCALE[d["gpu__time_duration.sum"][1]]
+    alg = inputs.algorithmic_bytes([65536] * 16, 16)
+    summary = {
+        "workload": "mla_decode_b16_ctx64k_h16_per_gpu", "tag": tag, "source": rep,
+        "decode_kernel": {
+            "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
+            "algorithmic_bytes": alg, "traffic_over_algorithmic": (rd + wr) / alg,
+            "duration_us_cold_serialised": dur * 1e6,
+            "dram_throughput_pct_of_ncu_peak": d["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"][0],
+            "tensor_pipe_active_pct": d["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"][0],
+            "sm_throughput_pct": d["sm__throughput.avg.pct_of_peak_sustained_elapsed"][0],
+            "sm_clock_ghz": d["sm__cycles_elapsed.avg"][0] / dur / 1e9,
+            "registers_per_thread": d["launch__registers_per_thread"][0],
+            "grid": d["launch__grid_size"][0], "block": d["launch__block_size"][0],
+            "l2_hit_rate_pct": d["lts__t_sector_hit_rate.pct"][0],
+        },
+    }
+    if launches and Path(launches).exists():
+        rows = [r for r in csv.DictReader(l for l in open(launches) if not l.startswith("==")) if r.get("Metric Name") == "gpu__time_duration.sum"]
+        ks = {}
+        for r in rows:
+            name = r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "")
+            ks.setdefault(name, []).append(float(r["Metric Value"]) * SCALE.get(r["Metric Unit"], 1e-9))
+        tot = sum(sum(v) for v in ks.values())
+        summary["launch_list"] = {k: {"launches": len(v), "avg_us": sum(v) / len(v) * 1e6,
+                                      "share": sum(v) / tot} for k, v in ks.items()}
+    (ROOT / "profiles" / "ncu_summary.json").write_text(json.dumps(summary, indent=1) + "\n")
+    tagdir = ROOT / "profiles" / tag
+    tagdir.mkdir(parents=True, exist_ok=True)
+    lines = [f"# ncu — etap_mla_decode_kernel (K2), B=16 x 64K, 16 heads ({tag})", "",
+             f"source: `{rep}` (`ncu --set full --clock-control none --import-source on`, one launch)", "",
+             "| metric | value |", "|---|---|"]
+    for k, v in summary["decode_kernel"].items():
+        lines.append(f"| {k} | {v:.6g} |" if isinstance(v, float) else f"| {k} | {v} |")
+    if "launch_list" in summary:
+        lines += ["", "## launch list (cold, serialised: compare shares)", "", "| kernel | launches | avg us | share |",
+                  "|---|---|---|---|"]
+        for k, v in summary["launch_list"].items():
+            lines.append(f"| {k} | {v['launches']} | {v['avg_us']:.2f} | {v['share']:.3f} |")
+    (tagdir / "ncu_decode_kernel.md").write_text("\n".join(lines) + "\n")
+    print(json.dumps(summary, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,124 @@
+# SPDX-License-Identifier: Apache-2.0
+"""CPU tests of the drop-in boundary: the C-ABI library loads, exports every symbol that
+include/etap_mla.h declares, validates arguments like the reference (std::invalid_argument ->
+ETAP_ERR_SHAPE) and refuses to compute without a GPU (no CPU fallback)."""
+from __future__ import annotations
+
+import ctypes as C
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2506_01969_b200 import _lib, etap, inputs
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols() -> list[str]:
+    text = (ROOT / "include" / "etap_mla.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(etap_mla_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(L, s), s
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (etap_mla_\w+)", out))
+    assert set(syms) <= exported
+
+
+def test_library_targets_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+    sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass  # tcgen05 + TMA, not HMMA
+    assert " HMMA" not in sass
+
+
+def test_sizes_and_shape_validation():
+    L = _lib.lib()
+    a, b = C.c_size_t(), C.c_size_t()
+    assert L.etap_mla_sched_ints(16, 16, 148, C.byref(a), C.byref(b)) == _lib.ETAP_OK
+    assert a.value == 148 * 8 and b.value == 17
+    assert L.etap_mla_sched_ints(16, 24, 148, C.byref(a), C.byref(b)) == _lib.ETAP_ERR_SHAPE
+    ws = C.c_size_t()
+    assert L.etap_mla_workspace_bytes(16, 16, 148, C.byref(ws)) == _lib.ETAP_OK
+    assert ws.value == (148 + 16) * 16 * (512 + 1) * 4
+    # decode rejects q_tokens != 1 and bad scale before touching the device
+    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 2, 16, 1.0, 1, 1, 1, 148, 1, 1, 1, 0, None)
+    assert rc == _lib.ETAP_ERR_SHAPE and "q_tokens" in _lib.last_error()
+    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 1, 16, float("nan"), 1, 1, 1, 148, 1, 1, 1, 0, None)
+    assert rc == _lib.ETAP_ERR_SHAPE and "scale" in _lib.last_error()
+
+
+def test_reference_error_behaviour_mirrored():
+    p = etap.make_mla_problem(42, 16, 100)
+    with pytest.raises(_lib.EtapShapeError, match="tile config"):
+        etap.run_etap(p, etap.TileConfig(1, 0, 2))
+    with pytest.raises(_lib.EtapShapeError, match="K head dimension"):
+        etap.make_problem(np.ones((2, 4)), np.ones((3, 5)), np.ones((3, 2)), 1.0)
+    with pytest.raises(_lib.EtapShapeError, match="scale"):
+        etap.make_problem(np.ones((2, 4)), np.ones((3, 4)), np.ones((3, 2)), -1.0)
+    with pytest.raises(_lib.EtapShapeError, match="MLA"):
+        etap.run_etap(etap.make_problem(np.ones((2, 4)), np.ones((3, 4)), np.ones((3, 2)), 1.0, "exact64"))
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    p = etap.make_mla_problem(42, 16, 100)
+    with pytest.raises(_lib.EtapError):
+        etap.run_etap(p)
+    L = _lib.lib()
+    n = C.c_int()
+    assert L.etap_mla_num_sm_parts(0, C.byref(n)) == _lib.ETAP_ERR_CUDA
+
+
+def test_host_metadata_partition_invariants():
+    """The split-KV schedule (host restatement of K1) covers every (sequence, head group,
+    page) exactly once, numbers partials contiguously per sequence and balances the load."""
+    L = _lib.lib()
+    cases = [([65536] * 16, 16, 148), (inputs.varlen_seqlens(32), 16, 148), ([0, 1, 64, 65, 0], 32, 148),
+             ([100], 16, 3), ([1024], 16, 148), ([10**6], 128, 148), ([7] * 300, 16, 148)]
+    for seqlens, heads, parts in cases:
+        B, G = len(seqlens), heads // 16
+        sched = np.zeros(parts * 8, np.int32)
+        so = np.zeros(B * G + 1, np.int32)
+        sl = np.array(seqlens, np.int32)
+        assert L.etap_mla_metadata_host(sl.ctypes.data_as(C.c_void_p), B, heads, parts,
+                                        sched.ctypes.data_as(C.c_void_p), so.ctypes.data_as(C.c_void_p)) == 0
+        tiles = [(s + 63) // 64 for s in seqlens for _ in range(G)]
+        cover = [np.zeros(t, np.int32) for t in tiles]
+        count = np.zeros(B * G, np.int32)
+        idx_seen = {}
+        work = []
+        for k in range(parts):
+            vb0, t0, vb1, t1, first = sched[k * 8:k * 8 + 5]
+            w = 0
+            for vb in range(vb0, vb1 + 1):
+                a = t0 if vb == vb0 else 0
+                e = t1 if vb == vb1 else tiles[vb]
+                if a < e:
+                    cover[vb][a:e] += 1
+                    idx = first if vb == vb0 else so[vb]
+                    assert so[vb] <= idx < so[vb + 1]
+                    assert idx not in idx_seen
+                    idx_seen[idx] = (k, vb)
+                    count[vb] += 1
+                    w += e - a
+            work.append(w)
+        for c in cover:
+            assert (c == 1).all()
+        assert np.array_equal(np.diff(so), count)
+        total = sum(tiles)
+        if total >= parts * 4:
+            assert max(work) <= total / parts + 4  # balanced to within the per-split overhead
