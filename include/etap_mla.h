@@ -145,6 +145,11 @@ int etap_mla_debug_trace(void* device_buf);
  * layout variant; out_dev[0..1] (device, int64) = issue cycles, issue+completion cycles. */
 int etap_mla_umma_bench(int variant, int n, long long* out_dev, int grid);
 
+/* Debug: stream the KV pool with the decode kernel's TMA access pattern and no compute
+ * (grid CTAs x pages_per_cta pages, ring of nslot 8 KB slots) — the attainable read rate. */
+int etap_mla_stream_bench(const void* kv_pool, int64_t num_pages, int pages_per_cta, int grid,
+                          int nslot, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

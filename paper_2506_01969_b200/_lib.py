@@ -52,6 +52,7 @@ def _declare(lib: C.CDLL) -> None:
         "etap_mla_selftest_umma": (i32, [vp, vp, vp, vp, vp, vp]),
         "etap_mla_debug_trace": (i32, [vp]),
         "etap_mla_umma_bench": (i32, [i32, i32, vp, i32]),
+        "etap_mla_stream_bench": (i32, [vp, i64, i32, i32, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -193,14 +193,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) ETAP_TRACE(prm, TRACE_TILES - 1, 0);
 
     // ---- prologue (overlaps the scheduler kernel under PDL)
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tm_kv);
         ptx::prefetch_tmap(&tm_q);
         for (int i = 0; i < NTB; ++i) {
-            ptx::mbar_init(&bars[BAR_FULL + i], 1);
+            ptx::mbar_init(&bars[BAR_FULL_A + i], 1);
+            ptx::mbar_init(&bars[BAR_FULL_B + i], 1);
             ptx::mbar_init(&bars[BAR_G2_DONE + i], 1);
+            ptx::mbar_init(&bars[BAR_G2_HALF + i], 1);
         }
         ptx::mbar_init(&bars[BAR_Q_FULL], 1);
         ptx::mbar_init(&bars[BAR_Q_EMPTY], 1);
@@ -212,13 +215,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
-    // zero the ring once: V rows that were never loaded always hold finite data
-    {
-        uint4* r = reinterpret_cast<uint4*>(smem + OFF_RING);
-        for (int i = threadIdx.x; i < NSLOT * SLOT_BYTES / 16; i += NUM_THREADS)
-            r[i] = make_uint4(0, 0, 0, 0);
-        ptx::fence_proxy_async_smem();
-    }
+    // (no ring zero-fill: every row a GEMM reads was written by a full-page TMA box of the
+    // same tile; garbage rows past seqlen are zeroed by the softmax warps before GEMM2)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -226,6 +224,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     ptx::grid_dep_wait();     // schedule written by K1
     ptx::grid_dep_launch();   // let the combine kernel get scheduled
+    if (threadIdx.x == 0) ETAP_TRACE(prm, TRACE_TILES - 1, 1);
 
     const int32_t* sch = prm.sched + blockIdx.x * SCHED_INTS;
     const int vb_begin = sch[0], vb_end = sch[2];
@@ -269,21 +268,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (gt >= 3) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 3) % NTB], ((gt - 3) / NTB) & 1);
                 if (lane == 0) {
                     ETAP_TRACE(prm, gt, 0);
-                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL + tb], NCHUNK * SLOT_BYTES);
+                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_A + tb], SPLIT_POS * SLOT_BYTES);
 #pragma unroll 1
-                    for (int pos = 0; pos < 6; ++pos) {
+                    for (int pos = 0; pos < SPLIT_POS; ++pos) {
                         const uint32_t s = (pos0 + pos) % NSLOT;
-                        ptx::tma_load_2d(smem + OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL + tb],
+                        ptx::tma_load_2d(smem + OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_A + tb],
                                          chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
                     }
                 }
                 __syncwarp();
-                if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+                // positions 6..8 reuse tile gt-2's positions 0..2 = {V0,V1,V2} (even gt) or
+                // {rope,V0,V1} (odd gt): free once GEMM2 d-blocks 0-1 of tile gt-2 completed
+                if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_HALF + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
                 if (lane == 0) {
+                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_B + tb], (NCHUNK - SPLIT_POS) * SLOT_BYTES);
 #pragma unroll 1
-                    for (int pos = 6; pos < NCHUNK; ++pos) {
+                    for (int pos = SPLIT_POS; pos < NCHUNK; ++pos) {
                         const uint32_t s = (pos0 + pos) % NSLOT;
-                        ptx::tma_load_2d(smem + OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL + tb],
+                        ptx::tma_load_2d(smem + OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_B + tb],
                                          chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
                     }
                     ETAP_TRACE(prm, gt, 1);
@@ -302,12 +304,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
                 if (gt >= 2) ptx::mbar_wait(&bars[BAR_S_FREE + buf], ((gt >> 1) - 1) & 1);
-                ptx::mbar_wait(&bars[BAR_FULL + gt % NTB], (gt / NTB) & 1);
+                const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
+                ptx::mbar_wait(&bars[BAR_FULL_A + gt % NTB], (gt / NTB) & 1);
+                __syncwarp();
+                ptx::tc_fence_after();
+                issue_gemm1_tile<0, SPLIT_POS>(tmem_base + TCOL_S + 16 * buf, ring_addr, q_addr, pos0, gt);
+                ptx::mbar_wait(&bars[BAR_FULL_B + gt % NTB], (gt / NTB) & 1);
                 __syncwarp();
                 ptx::tc_fence_after();
                 ETAP_TRACE(prm, gt, 2);
-                issue_gemm1_tile(tmem_base + TCOL_S + 16 * buf, ring_addr, q_addr,
-                                 (gt * NCHUNK) % NSLOT, gt);
+                issue_gemm1_tile<SPLIT_POS, NCHUNK>(tmem_base + TCOL_S + 16 * buf, ring_addr, q_addr, pos0, gt);
                 ptx::umma_commit_elect(&bars[BAR_S_FULL + buf]);
                 ETAP_TRACE(prm, gt, 3);
                 if (t == sd.t1 - 1) ptx::umma_commit_elect(&bars[BAR_Q_EMPTY]);
@@ -334,6 +340,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     sa = sa >= NSLOT ? sa - NSLOT : sa;
                     issue_gemm2_block(tmem_base + TCOL_O + 32 * blk, ring_addr + sa * SLOT_BYTES,
                                       p_addr + buf * P_BYTES, t == sd.t0);
+                    if (blk == 1) ptx::umma_commit_elect(&bars[BAR_G2_HALF + gt % NTB]);
                 }
                 ptx::umma_commit_elect(&bars[BAR_G2_DONE + gt % NTB]);
                 ETAP_TRACE(prm, gt, 7);
@@ -342,9 +349,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp >= SOFTMAX_WARP0) {
         // ===================================================== softmax + epilogue (128 threads)
+        // thread = (KV row, head half): lane l of warp q owns row 16q + l%16, heads 8*(l/16)..+7
         const int wq = warp & 3;               // TMEM lane quadrant accessible by this warp
-        const bool active = lane < 16;         // M=64 tile: rows in lanes 0-15 of each quadrant
-        const int row = s_row_of(wq, lane);    // KV row in the tile (active lanes)
+        const int half = lane >> 4;
+        const int row = s_row_of(wq, lane);    // KV row in the tile
         const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
         float* red_max = reinterpret_cast<float*>(smem + OFF_RED);  // [2][4][16]
         float* red_sum = red_max + 128;                               // [4][16]
@@ -356,29 +364,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
             if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
-            float m_used[16], l_part[16];
+            float m_used[16];   // running max per head (log2 units), replicated in all threads
+            float l_part[8];    // partial column sums of this thread's rows, own 8 heads
 #pragma unroll
-            for (int h = 0; h < 16; ++h) { m_used[h] = -INFINITY; l_part[h] = 0.f; }
+            for (int h = 0; h < 16; ++h) m_used[h] = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) l_part[j] = 0.f;
 
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
                 ptx::mbar_wait(&bars[BAR_S_FULL + buf], (gt >> 1) & 1);
                 ptx::tc_fence_after();
                 if (tracer) ETAP_TRACE(prm, gt, 4);
-                uint32_t sr[16];
-                ptx::tmem_ld16(t_lane + TCOL_S + 16 * buf, sr);
+                uint32_t sr[8];
+                ptx::tmem_ld16x2_8(t_lane + TCOL_S + 16 * buf, sr);
                 ptx::tmem_wait_ld();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&bars[BAR_S_FREE + buf]);
 
                 const int grow = t * TILE + row;
-                const bool valid = active && grow < sd.seqlen;
-                float x[16];
+                const bool valid = grow < sd.seqlen;
+                float x[8], mu[8];
                 bool exceed = false;
 #pragma unroll
-                for (int h = 0; h < 16; ++h) {
-                    x[h] = valid ? __uint_as_float(sr[h]) * prm.scale_log2 : -INFINITY;
-                    exceed |= x[h] > m_used[h] + thresh;
+                for (int j = 0; j < 8; ++j) {
+                    mu[j] = half ? m_used[8 + j] : m_used[j];
+                    x[j] = valid ? __uint_as_float(sr[j]) * prm.scale_log2 : -INFINITY;
+                    exceed |= x[j] > mu[j] + thresh;
                 }
                 const bool first = (t == sd.t0);
                 // one barrier decides, CTA-uniformly, whether any running max must move
@@ -388,9 +400,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int h = 0; h < 16; ++h) alpha[h] = 1.f;
                 if (any) {
-                    const float wm = warp_reduce16<true>(x, lane);
+                    const float wm = halfwarp_reduce8<true>(x, lane);
                     float* rm = red_max + (gt & 1) * 64;
-                    if ((lane & 1) == 0) rm[wq * 16 + (lane >> 1)] = wm;
+                    if ((lane & 1) == 0) rm[wq * 16 + half * 8 + ((lane & 15) >> 1)] = wm;
                     ptx::named_bar_sync(2, 128);
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {
@@ -418,12 +430,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         }
                     }
                     if (negate && !first) need_rescale = true;
-                }
-                float pv[16];
 #pragma unroll
-                for (int h = 0; h < 16; ++h) {
-                    pv[h] = exp2f(x[h] - m_used[h]);
-                    l_part[h] = first ? pv[h] : fmaf(l_part[h], alpha[h], pv[h]);
+                    for (int j = 0; j < 8; ++j) mu[j] = half ? m_used[8 + j] : m_used[j];
+                }
+                float pv[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    pv[j] = exp2f(x[j] - mu[j]);
+                    const float aj = half ? alpha[8 + j] : alpha[j];
+                    l_part[j] = first ? pv[j] : fmaf(l_part[j], aj, pv[j]);
                 }
                 // the P buffer is reused every other tile: GEMM2(gt-2) must have read it
                 if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
@@ -447,19 +462,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                     ptx::tmem_wait_st();
                 }
-                if (active) {
-                    write_p_hilo(smem + OFF_P + buf * P_BYTES, row, pv);
-                    // rows of the last page past seqlen were loaded from HBM and may hold
-                    // non-finite garbage; zero them in the V chunks (0 * NaN = NaN in the MMA)
-                    if (grow >= sd.seqlen) {
-                        const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
+                write_p_hilo8(smem + OFF_P + buf * P_BYTES, row, half, pv);
+                // rows of the last page past seqlen were loaded from HBM and may hold
+                // non-finite garbage; zero them in the V chunks (0 * NaN = NaN in the MMA)
+                if (grow >= sd.seqlen) {
+                    const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
 #pragma unroll 1
-                        for (int c = 0; c < NVCHUNK; ++c) {
-                            const uint32_t s = (pos0 + pos_of_chunk(c, gt)) % NSLOT;
-                            uint4* dst = reinterpret_cast<uint4*>(smem + OFF_RING + s * SLOT_BYTES + row * 128);
+                    for (int c = half * 4; c < half * 4 + 4; ++c) {
+                        const uint32_t s = (pos0 + pos_of_chunk(c, gt)) % NSLOT;
+                        uint4* dst = reinterpret_cast<uint4*>(smem + OFF_RING + s * SLOT_BYTES + row * 128);
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) dst[j] = make_uint4(0, 0, 0, 0);
-                        }
+                        for (int j = 0; j < 8; ++j) dst[j] = make_uint4(0, 0, 0, 0);
                     }
                 }
                 ptx::fence_proxy_async_smem();
@@ -475,8 +488,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t last = gt - 1;
             ptx::mbar_wait(&bars[BAR_G2_DONE + last % NTB], (last / NTB) & 1);
             ptx::tc_fence_after();
-            const float wsum = warp_reduce16<false>(l_part, lane);
-            if ((lane & 1) == 0) red_sum[wq * 16 + (lane >> 1)] = wsum;
+            const float wsum = halfwarp_reduce8<false>(l_part, lane);
+            if ((lane & 1) == 0) red_sum[wq * 16 + half * 8 + ((lane & 15) >> 1)] = wsum;
             ptx::named_bar_sync(2, 128);
             float inv_l[16], l_tot[16];
 #pragma unroll
@@ -515,11 +528,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 dst_lse[lane] = v;
             }
             ptx::tc_fence_before();
+            // red_sum is rewritten by the next epilogue only after the next split's barriers
+            ptx::named_bar_sync(2, 128);
         }
     }
 
     ptx::tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) ETAP_TRACE(prm, TRACE_TILES - 1, 2);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, TMEM_COLS);
@@ -633,11 +649,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     }
     // P = hi + lo of the input, written by the softmax warps exactly as the decode kernel does
-    if (warp >= SOFTMAX_WARP0 && lane < 16) {
-        const int row = s_row_of(warp & 3, lane);
-        float p[16];
-        for (int h = 0; h < 16; ++h) p[h] = p_in[row * 16 + h];
-        write_p_hilo(smem + OFF_P, row, p);
+    if (warp >= SOFTMAX_WARP0) {
+        const int row = s_row_of(warp & 3, lane), half = lane >> 4;
+        float p[8];
+        for (int j = 0; j < 8; ++j) p[j] = p_in[row * 16 + half * 8 + j];
+        write_p_hilo8(smem + OFF_P, row, half, p);
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
@@ -645,7 +661,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_wait(&bars[0], 0);
         __syncwarp();
         ptx::tc_fence_after();
-        issue_gemm1_tile(tmem_base + TCOL_S, ring_addr, q_addr, 0, 0);  // tile 0: chunk c in slot c
+        issue_gemm1_tile<0, NCHUNK>(tmem_base + TCOL_S, ring_addr, q_addr, 0, 0);  // tile 0: chunk c in slot c
         for (int blk = 0; blk < 4; ++blk)
             issue_gemm2_block(tmem_base + TCOL_O + 32 * blk, ring_addr + (2 * blk) * SLOT_BYTES,
                               p_addr, true);
@@ -657,11 +673,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int wq = warp & 3;
         const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
         uint32_t r[32];
-        ptx::tmem_ld16(t_lane + TCOL_S, *reinterpret_cast<uint32_t(*)[16]>(r));
+        ptx::tmem_ld16x2_8(t_lane + TCOL_S, *reinterpret_cast<uint32_t(*)[8]>(r));
         ptx::tmem_wait_ld();
-        if (lane < 16) {
-            const int row = s_row_of(wq, lane);
-            for (int h = 0; h < 16; ++h) s_out[row * 16 + h] = __uint_as_float(r[h]);
+        {
+            const int row = s_row_of(wq, lane), half = lane >> 4;
+            for (int j = 0; j < 8; ++j) s_out[row * 16 + half * 8 + j] = __uint_as_float(r[j]);
         }
         for (int blk = 0; blk < 4; ++blk) {
             ptx::tmem_ld32(t_lane + TCOL_O + 32 * blk, r);
@@ -1056,6 +1072,62 @@ __global__ void __launch_bounds__(128, 1) etap_umma_bench_kernel(int variant, in
 extern "C" int etap_mla_umma_bench(int variant, int n, long long* out_dev, int grid) {
     cudaFuncSetAttribute(etap_umma_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
     etap_umma_bench_kernel<<<grid, 128, 66 * 1024>>>(variant, n, out_dev);
+    ETAP_CUDA(cudaGetLastError());
+    return ETAP_OK;
+}
+
+// =============================================================================================
+// Streaming microbenchmark (debug): the decode kernel's TMA access pattern (9 boxes of
+// 64 rows x 64 cols per page, tile-level full barriers, 24-slot ring) with no compute, to
+// measure the attainable HBM read rate. Each CTA streams pages [cta*ppc, (cta+1)*ppc).
+// =============================================================================================
+namespace {
+__global__ void __launch_bounds__(64, 1) etap_stream_bench_kernel(const __grid_constant__ CUtensorMap tm_kv,
+                                                                   int pages_per_cta, int nslot) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 200 * 1024);
+    uint64_t* done = full + NTB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NTB; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&done[i], 1); }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    const int p0 = blockIdx.x * pages_per_cta;
+    const uint32_t tiles_in_ring = (uint32_t)nslot / NCHUNK;  // whole tiles that fit
+    if (warp == 0) {
+        const uint64_t pol = ptx::policy_evict_first();
+        for (uint32_t gt = 0; gt < (uint32_t)pages_per_cta; ++gt) {
+            if (gt >= tiles_in_ring)
+                ptx::mbar_wait(&done[(gt - tiles_in_ring) % NTB], ((gt - tiles_in_ring) / NTB) & 1);
+            if (lane == 0) {
+                ptx::mbar_arrive_expect_tx(&full[gt % NTB], NCHUNK * SLOT_BYTES);
+                const uint32_t base = (gt % tiles_in_ring) * NCHUNK;
+                for (int c = 0; c < NCHUNK; ++c)
+                    ptx::tma_load_2d(smem + (base + c) * SLOT_BYTES, &tm_kv, &full[gt % NTB], c * 64,
+                                     (p0 + gt) * PAGE, pol);
+            }
+            __syncwarp();
+        }
+    } else {
+        for (uint32_t gt = 0; gt < (uint32_t)pages_per_cta; ++gt) {
+            ptx::mbar_wait(&full[gt % NTB], (gt / NTB) & 1);
+            if (lane == 0) ptx::mbar_arrive(&done[gt % NTB]);
+            __syncwarp();
+        }
+    }
+}
+}  // namespace
+
+extern "C" int etap_mla_stream_bench(const void* kv_pool, int64_t num_pages, int pages_per_cta,
+                                     int grid, int nslot, void* stream) {
+    if (nslot < NCHUNK || nslot * SLOT_BYTES > 200 * 1024) return fail(ETAP_ERR_SHAPE, "bad nslot");
+    CUtensorMap tm;
+    if (int rc = make_map(&tm, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, PAGE)) return rc;
+    cudaFuncSetAttribute(etap_stream_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 202 * 1024);
+    etap_stream_bench_kernel<<<grid, 64, 202 * 1024, static_cast<cudaStream_t>(stream)>>>(tm, pages_per_cta, nslot);
     ETAP_CUDA(cudaGetLastError());
     return ETAP_OK;
 }

@@ -47,20 +47,24 @@ constexpr int OFF_RED = OFF_P + 2 * P_BYTES;          // 223232
 constexpr int RED_BYTES = 1024;                       // [2][4][16] max + [4][16] sum (floats)
 constexpr int OFF_BAR = OFF_RED + RED_BYTES;          // 224256
 constexpr int NTB = 4;          // tile-barrier ring depth (tiles in flight <= NSLOT/9 + 1)
-constexpr int NBAR = 2 * NTB + 8;
+constexpr int NBAR = 4 * NTB + 8;
 constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
 constexpr int SMEM_USED = OFF_TMEM + 16;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;  // slack for manual 1024 B alignment
 
 // barrier indices
-constexpr int BAR_FULL = 0;             // [NTB] all 9 chunks of tile gt landed (gt % NTB)
-constexpr int BAR_G2_DONE = NTB;        // [NTB] GEMM2 of tile gt complete: its 9 ring slots
+constexpr int BAR_FULL_A = 0;           // [NTB] ring positions 0..5 of tile gt landed (gt % NTB)
+constexpr int BAR_FULL_B = NTB;         // [NTB] ring positions 6..8 of tile gt landed
+constexpr int BAR_G2_DONE = 2 * NTB;    // [NTB] GEMM2 of tile gt complete: its 9 ring slots
                                         //       and its P buffer are free (gt % NTB)
-constexpr int BAR_Q_FULL = 2 * NTB + 0;
-constexpr int BAR_Q_EMPTY = 2 * NTB + 1;
-constexpr int BAR_S_FULL = 2 * NTB + 2;  // [2]
-constexpr int BAR_S_FREE = 2 * NTB + 4;  // [2]
-constexpr int BAR_P_FULL = 2 * NTB + 6;  // [2]
+constexpr int BAR_G2_HALF = 3 * NTB;    // [NTB] GEMM2 d-blocks 0-1 of tile gt complete: the
+                                        //       rope slot and V chunks 0-3 are free
+constexpr int BAR_Q_FULL = 4 * NTB + 0;
+constexpr int BAR_Q_EMPTY = 4 * NTB + 1;
+constexpr int BAR_S_FULL = 4 * NTB + 2;  // [2]
+constexpr int BAR_S_FREE = 4 * NTB + 4;  // [2]
+constexpr int BAR_P_FULL = 4 * NTB + 6;  // [2]
+constexpr int SPLIT_POS = 6;             // positions 0..5 reuse tile gt-3's slots, 6..8 gt-2's
 
 // TMEM columns (128 lanes x 32 bit each)
 constexpr uint32_t TMEM_COLS = 256;
@@ -88,8 +92,9 @@ __device__ __forceinline__ uint64_t p_desc(uint32_t base, int kk) {
 
 // M=64 accumulator layout (cta_group::1): row m lives in TMEM lane (m % 16) + 32 * (m / 16),
 // i.e. lanes 0-15 of each 32-lane quadrant. Warp q of the softmax group owns rows
-// 16q .. 16q+15 in its lanes 0-15.
-__device__ __forceinline__ int s_row_of(int quadrant, int lane) { return quadrant * 16 + lane; }
+// 16q .. 16q+15; with the 16x32bx2 TMEM load, lane l handles row 16q + (l % 16) and heads
+// 8*(l / 16) .. 8*(l / 16) + 7.
+__device__ __forceinline__ int s_row_of(int quadrant, int lane) { return quadrant * 16 + (lane & 15); }
 
 // Ring position -> latent column chunk. Every tile consumes 9 ring positions starting at
 // 9*gt; V chunks (2i, 2i+1) must sit in adjacent slots so one MN-major descriptor covers
@@ -105,15 +110,17 @@ __device__ __forceinline__ int pos_of_chunk(int chunk, uint32_t gt) {
     return chunk;
 }
 
-// GEMM1 of one tile: S^T[64x16] = K[64 x 576] . Q^T[576 x 16], 9 chunks x 4 MMAs (K=16).
-// Whole-warp call (elect inside). pos0 = ring slot of the tile's first position.
+// GEMM1 of one tile: S^T[64x16] = K[64 x 576] . Q^T[576 x 16], 9 chunks x 4 MMAs (K=16),
+// ring positions [POS_BEGIN, POS_END). Whole-warp call (elect inside). pos0 = ring slot of
+// the tile's first position.
+template <int POS_BEGIN, int POS_END>
 __device__ __forceinline__ void issue_gemm1_tile(uint32_t s_tmem, uint32_t ring_addr,
                                                  uint32_t q_addr, uint32_t pos0, uint32_t gt) {
     constexpr uint32_t idesc = ptx::idesc_bf16_f32(64, 16, 0, 0);
     const uint64_t a_ring = ptx::smem_desc(ring_addr, 16, 1024, ptx::LAYOUT_SW128);
     const uint64_t b_q = ptx::smem_desc(q_addr, 16, 1024, ptx::LAYOUT_SW128);
 #pragma unroll
-    for (int pos = 0; pos < NCHUNK; ++pos) {
+    for (int pos = POS_BEGIN; pos < POS_END; ++pos) {
         uint32_t s = pos0 + pos;
         s = s >= NSLOT ? s - NSLOT : s;
         const int chunk = chunk_at(pos, gt);
@@ -145,11 +152,12 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo_elem, float hi_elem) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// P (fp32, 16 heads of one KV row) -> bf16 hi and lo parts, written as row r of [P_hi|P_lo]^T.
-__device__ __forceinline__ void write_p_hilo(uint8_t* p, int r, const float (&pv)[16]) {
-    uint32_t hi[8], lo[8];
+// P (fp32, 8 heads [8*half, 8*half+8) of KV row r) -> bf16 hi and lo parts, written into row r
+// of [P_hi | P_lo]^T: hi heads at columns 8*half.., lo heads at 16 + 8*half..
+__device__ __forceinline__ void write_p_hilo8(uint8_t* p, int r, int half, const float (&pv)[8]) {
+    uint32_t hi[4], lo[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 4; ++i) {
         const __nv_bfloat16 h0 = __float2bfloat16_rn(pv[2 * i]);
         const __nv_bfloat16 h1 = __float2bfloat16_rn(pv[2 * i + 1]);
         __nv_bfloat162 hh;
@@ -158,11 +166,36 @@ __device__ __forceinline__ void write_p_hilo(uint8_t* p, int r, const float (&pv
         hi[i] = *reinterpret_cast<uint32_t*>(&hh);
         lo[i] = pack_bf16x2(pv[2 * i] - __bfloat162float(h0), pv[2 * i + 1] - __bfloat162float(h1));
     }
-    uint8_t* dst = p + (r >> 3) * 512 + (r & 7) * 16;
+    uint8_t* dst = p + (r >> 3) * 512 + (r & 7) * 16 + half * 128;
     *reinterpret_cast<uint4*>(dst) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    *reinterpret_cast<uint4*>(dst + 128) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
     *reinterpret_cast<uint4*>(dst + 256) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-    *reinterpret_cast<uint4*>(dst + 384) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+}
+
+// Butterfly transpose-reduction of 8 per-lane values (heads) over the 16 lanes of a half-warp
+// (8 shuffles); on return lane l holds the reduction for head (l & 15) >> 1 of its half.
+template <bool kMax>
+__device__ __forceinline__ float halfwarp_reduce8(const float (&x)[8], int lane) {
+    auto op = [](float a, float b) { return kMax ? fmaxf(a, b) : a + b; };
+    float y[4];
+    const bool b3 = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float keep = b3 ? x[i + 4] : x[i];
+        const float send = b3 ? x[i] : x[i + 4];
+        y[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+    }
+    float z[2];
+    const bool b2 = lane & 4;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float keep = b2 ? y[i + 2] : y[i];
+        const float send = b2 ? y[i] : y[i + 2];
+        z[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+    }
+    const bool b1 = lane & 2;
+    float v = op(b1 ? z[1] : z[0], __shfl_xor_sync(0xffffffffu, b1 ? z[0] : z[1], 2));
+    v = op(v, __shfl_xor_sync(0xffffffffu, v, 1));
+    return v;
 }
 
 // Butterfly transpose-reduction: 16 per-lane values (one per head) reduced over the 32 lanes

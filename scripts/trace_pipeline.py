@@ -45,6 +45,8 @@ def main() -> None:
     _lib.lib().etap_mla_debug_trace(None)
     print(f"traced step: {e0.elapsed_time(e1) * 1000:.1f} us")
     t = buf.view(nparts, TRACE_TILES, 8).cpu().numpy().astype(np.float64)
+    ent = t[:, TRACE_TILES - 1, :3].copy()
+    t[:, TRACE_TILES - 1, :] = 0
     valid = (t > 0).all(axis=2)
     t0 = t[valid].min()
     names = ["issue_first", "issue_last", "landed_last", "S_commit", "softmax_start", "P_written",
@@ -80,6 +82,14 @@ def main() -> None:
     print(f"CTA busy span us: median {np.median(span) / 1e3:.1f} max {np.max(span) / 1e3:.1f}; "
           f"start offsets us: max {np.max(starts) / 1e3:.1f}")
     print("tiles per CTA:", np.bincount(valid.sum(axis=1)).nonzero()[0].tolist())
+    e0 = ent[:, 0].min()
+    first_issue = np.array([t[c][valid[c]][:, 0].min() if valid[c].any() else np.nan for c in range(nparts)])
+    last_g2 = np.array([t[c][valid[c]][:, 7].max() if valid[c].any() else np.nan for c in range(nparts)])
+    print(f"kernel entry spread us: {(ent[:, 0].max() - e0) / 1e3:.2f}; prologue+dep-wait us (median): "
+          f"{np.median(ent[:, 1] - ent[:, 0]) / 1e3:.2f}; dep-wait done -> first TMA issue us (median): "
+          f"{np.nanmedian(first_issue - ent[:, 1]) / 1e3:.2f}")
+    print(f"last G2 commit -> CTA exit us (median/max): {np.nanmedian(ent[:, 2] - last_g2) / 1e3:.2f} / "
+          f"{np.nanmax(ent[:, 2] - last_g2) / 1e3:.2f}; entry -> last exit us: {(ent[:, 2].max() - e0) / 1e3:.1f}")
 
 
 if __name__ == "__main__":
