@@ -61,6 +61,11 @@ extern "C" {
                                        instead of the default thresholded lazy rescale */
 #define ETAP_FLAG_SKIP_COMBINE 4u   /* launch K2 only; the caller runs etap_mla_combine (used to
                                        time K2 alone) */
+#define ETAP_FLAG_EXTERNAL_SCHEDULE 8u /* read sched / split_off produced by etap_mla_metadata.
+                                       Without it (and when batch*heads/16 <= 256) K2 computes
+                                       the same schedule in its prologue and writes it to
+                                       sched / split_off, so K1 is off the per-step critical
+                                       path; above 256 virtual sequences K1 is required. */
 
 /* Thread-local description of the last error. Never NULL. */
 const char* etap_mla_last_error(void);

@@ -18,6 +18,7 @@ ETAP_ERR_CUDA = 2
 FLAG_NEGATE_RESCALE = 1
 FLAG_EAGER_RESCALE = 2
 FLAG_SKIP_COMBINE = 4
+FLAG_EXTERNAL_SCHEDULE = 8
 
 _lib = None
 

@@ -171,6 +171,93 @@ struct SplitDesc {
     int vb, b, g, seqlen, t0, t1;
 };
 
+// exclusive prefix over the 256 threads of the CTA (one value per thread)
+__device__ __forceinline__ int cta_excl_scan256(int v, int* s_wt, int& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wt[warp] = x;
+    __syncthreads();
+    int pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NUM_THREADS / 32; ++w) {
+        const int t = s_wt[w];
+        pre += (w < warp) ? t : 0;
+        tot += t;
+    }
+    __syncthreads();
+    total = tot;
+    return pre + x - v;
+}
+
+// The split schedule of etap_mla_metadata_kernel (K1) computed by every CTA for itself:
+// cost prefix -> closed-form split counts per virtual sequence (CTA k covers vb iff
+// (k+1)T > P[vb]+F and kT < P[vb+1]) -> split offsets -> this CTA's range. Identical output
+// to K1 (GPU test); CTA 0 publishes split_off for the combine kernel, every CTA its sched row.
+__device__ void inkernel_schedule(const DecodeParams& prm, int* s_pref, int* s_soff, int* s_tiles,
+                                  int* s_sched, int* s_wt) {
+    const int G = prm.groups;
+    const int nvb = prm.batch * G;
+    const int parts = gridDim.x;
+    const int tid = threadIdx.x;
+    int tiles = 0, cost = 0;
+    if (tid < nvb) {
+        const int len = max(0, prm.seqlens[tid / G]);
+        tiles = (len + TILE - 1) / TILE;
+        cost = tiles > 0 ? tiles + META_FIXED_COST : 0;
+        s_tiles[tid] = tiles;
+    }
+    int total;
+    const int pref = cta_excl_scan256(cost, s_wt, total);
+    if (tid < nvb) s_pref[tid] = pref;
+    if (tid == 0) s_pref[nvb] = total;
+    __syncthreads();
+    const int T = max(1, (total + parts - 1) / parts);
+    int ns = 0;
+    if (tid < nvb && tiles > 0) {
+        const int kf = (pref + META_FIXED_COST) / T;
+        const int kl = (s_pref[tid + 1] + T - 1) / T - 1;
+        ns = kl - kf + 1;
+    }
+    int nsplits;
+    const int so = cta_excl_scan256(ns, s_wt, nsplits);
+    if (tid < nvb) s_soff[tid] = so;
+    if (tid == 0) s_soff[nvb] = nsplits;
+    __syncthreads();
+    if (tid == 0) {
+        const int k = blockIdx.x;
+        auto map = [&](int x, int& vb, int& t) {
+            int lo = 0, hi = nvb - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_pref[mid] <= x) lo = mid; else hi = mid - 1;
+            }
+            while (lo + 1 < nvb && s_pref[lo + 1] <= x) ++lo;
+            vb = lo;
+            t = min(max(0, x - s_pref[lo] - META_FIXED_COST), s_tiles[lo]);
+        };
+        const int x0 = k * T, x1 = min(total, (k + 1) * T);
+        int b0 = 0, tb = 0, b1 = -1, te = 0, first = 0;
+        if (x0 < total) {
+            map(x0, b0, tb);
+            if (x1 >= total) { b1 = nvb - 1; te = s_tiles[nvb - 1]; }
+            else map(x1, b1, te);
+            if (b1 >= b0) first = s_soff[b0] + (k - (s_pref[b0] + META_FIXED_COST) / T);
+        }
+        s_sched[0] = b0; s_sched[1] = tb; s_sched[2] = b1; s_sched[3] = te; s_sched[4] = first;
+        s_sched[5] = 0; s_sched[6] = 0; s_sched[7] = 0;
+        int32_t* g = prm.sched_out + k * SCHED_INTS;
+        for (int i = 0; i < SCHED_INTS; ++i) g[i] = s_sched[i];
+    }
+    if (blockIdx.x == 0)
+        for (int i = tid; i <= nvb; i += NUM_THREADS) prm.split_off_out[i] = s_soff[i];
+    __syncthreads();
+}
+
 __device__ __forceinline__ bool split_at(const int32_t* sch, const int32_t* seqlens, int groups,
                                          int vb, SplitDesc& d) {
     d.vb = vb;
@@ -222,11 +309,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    ptx::grid_dep_wait();     // schedule written by K1
+    ptx::grid_dep_wait();     // inputs / schedule written by earlier kernels in the stream
     ptx::grid_dep_launch();   // let the combine kernel get scheduled
+    const int32_t* sch;
+    const int32_t* soff;      // split offsets per virtual sequence
+    if (prm.inkernel_sched) {
+        int* s_pref = reinterpret_cast<int*>(smem + OFF_SCHED);
+        int* s_soff = s_pref + MAX_FUSED_VB + 1;
+        int* s_tiles = s_soff + MAX_FUSED_VB + 1;
+        int* s_sched = s_tiles + MAX_FUSED_VB;
+        inkernel_schedule(prm, s_pref, s_soff, s_tiles, s_sched, s_sched + 8);
+        sch = s_sched;
+        soff = s_soff;
+    } else {
+        sch = prm.sched + blockIdx.x * SCHED_INTS;
+        soff = prm.split_off;
+    }
     if (threadIdx.x == 0) ETAP_TRACE(prm, TRACE_TILES - 1, 1);
 
-    const int32_t* sch = prm.sched + blockIdx.x * SCHED_INTS;
     const int vb_begin = sch[0], vb_end = sch[2];
     const int G = prm.groups;
     const uint32_t ring_addr = ptx::smem_u32(smem + OFF_RING);
@@ -497,7 +597,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 l_tot[h] = red_sum[h] + red_sum[16 + h] + red_sum[32 + h] + red_sum[48 + h];
                 inv_l[h] = 1.f / l_tot[h];
             }
-            const int ns = prm.split_off[vb + 1] - prm.split_off[vb];
+            const int ns = soff[vb + 1] - soff[vb];
             float* dst;
             float* dst_lse;
             if (ns == 1) {
@@ -505,7 +605,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 dst = prm.out + hrow * D_V;
                 dst_lse = prm.lse + hrow;
             } else {
-                const int idx = (vb == sch[0]) ? sch[4] : prm.split_off[vb];
+                const int idx = (vb == sch[0]) ? sch[4] : soff[vb];
                 dst = prm.ws_o + static_cast<size_t>(idx) * HG * D_V;
                 dst_lse = prm.ws_lse + static_cast<size_t>(idx) * HG;
             }
@@ -548,21 +648,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // invariance, acceptance.cpp:209-229). Grid: one CTA of 128 threads per (vb, head).
 // =============================================================================================
 constexpr int COMBINE_THREADS = 128;
-constexpr int COMBINE_MAX_SPLITS = 1024;
 
 __global__ void __launch_bounds__(COMBINE_THREADS)
     etap_mla_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
                             const int32_t* __restrict__ split_off, int groups, int heads,
                             float* __restrict__ out, float* __restrict__ lse) {
-    __shared__ float w[COMBINE_MAX_SPLITS];
-    __shared__ float red[COMBINE_THREADS / 32];
-    __shared__ float s_scale;
     ptx::grid_dep_wait();
     const int vb = blockIdx.x / HG;
     const int h = blockIdx.x - vb * HG;
     const int b = vb / groups, g = vb - b * groups;
-    const int s0 = split_off[vb];
-    const int ns = split_off[vb + 1] - s0;
+    const int s0 = __ldg(split_off + vb);
+    const int ns = __ldg(split_off + vb + 1) - s0;
     if (ns == 1) return;
     const size_t hrow = static_cast<size_t>(b) * heads + g * HG + h;
     float4* o4 = reinterpret_cast<float4*>(out + hrow * D_V);
@@ -571,43 +667,47 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
         if (threadIdx.x == 0) lse[hrow] = -INFINITY;
         return;
     }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // every warp reduces the split LSEs redundantly (no block barrier): max, then sum of exps
+    const int lane = threadIdx.x & 31;
+    const float* l_base = ws_lse + static_cast<size_t>(s0) * HG + h;
     float mx = -INFINITY;
-    for (int s = threadIdx.x; s < ns; s += COMBINE_THREADS) {
-        const float v = ws_lse[static_cast<size_t>(s0 + s) * HG + h];
-        w[s] = v;
-        mx = fmaxf(mx, v);
-    }
+    for (int s = lane; s < ns; s += 32) mx = fmaxf(mx, __ldg(l_base + static_cast<size_t>(s) * HG));
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) red[warp] = mx;
-    __syncthreads();
-    mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-    __syncthreads();
     float sum = 0.f;
-    for (int s = threadIdx.x; s < ns; s += COMBINE_THREADS) {
-        const float e = expf(w[s] - mx);
-        w[s] = e;
-        sum += e;
-    }
+    for (int s = lane; s < ns; s += 32) sum += __expf(__ldg(l_base + static_cast<size_t>(s) * HG) - mx);
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0) red[warp] = sum;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const float tot = red[0] + red[1] + red[2] + red[3];
-        s_scale = 1.f / tot;
-        lse[hrow] = mx + logf(tot);
-    }
-    __syncthreads();
-    const float inv = s_scale;
+    const float inv = 1.f / sum;
+    if (threadIdx.x == 0) lse[hrow] = mx + logf(sum);
+    // O = sum_s w_s O_s, 4 independent partial loads in flight per thread
+    const float4* p4 = reinterpret_cast<const float4*>(ws_o + (static_cast<size_t>(s0) * HG + h) * D_V) + threadIdx.x;
+    const size_t stride4 = static_cast<size_t>(HG) * D_V / 4;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < ns; ++s) {
-        const float ws = w[s] * inv;
-        const float4 v = reinterpret_cast<const float4*>(
-            ws_o + (static_cast<size_t>(s0 + s) * HG + h) * D_V)[threadIdx.x];
-        acc.x = fmaf(ws, v.x, acc.x);
-        acc.y = fmaf(ws, v.y, acc.y);
-        acc.z = fmaf(ws, v.z, acc.z);
-        acc.w = fmaf(ws, v.w, acc.w);
+    int s = 0;
+    for (; s + 4 <= ns; s += 4) {
+        float4 v[4];
+        float w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            v[j] = __ldg(p4 + (s + j) * stride4);
+            w[j] = __expf(__ldg(l_base + static_cast<size_t>(s + j) * HG) - mx) * inv;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            acc.x = fmaf(w[j], v[j].x, acc.x);
+            acc.y = fmaf(w[j], v[j].y, acc.y);
+            acc.z = fmaf(w[j], v[j].z, acc.z);
+            acc.w = fmaf(w[j], v[j].w, acc.w);
+        }
+    }
+    for (; s < ns; ++s) {
+        const float4 v = __ldg(p4 + s * stride4);
+        const float w = __expf(__ldg(l_base + static_cast<size_t>(s) * HG) - mx) * inv;
+        acc.x = fmaf(w, v.x, acc.x);
+        acc.y = fmaf(w, v.y, acc.y);
+        acc.z = fmaf(w, v.z, acc.z);
+        acc.w = fmaf(w, v.w, acc.w);
     }
     o4[threadIdx.x] = acc;
 }
@@ -929,8 +1029,12 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     prm.ws_o = static_cast<float*>(workspace);
     prm.ws_lse = prm.ws_o + np * HG * D_V;
     prm.max_pages = max_pages_per_seq;
+    prm.batch = batch;
     prm.heads = heads;
     prm.groups = groups;
+    prm.sched_out = const_cast<int32_t*>(sched);
+    prm.split_off_out = const_cast<int32_t*>(split_off);
+    prm.inkernel_sched = (batch * groups <= MAX_FUSED_VB && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.flags = flags;
     prm.trace = static_cast<unsigned long long*>(g_trace_buf);

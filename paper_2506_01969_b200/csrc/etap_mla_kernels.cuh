@@ -49,7 +49,11 @@ constexpr int OFF_BAR = OFF_RED + RED_BYTES;          // 224256
 constexpr int NTB = 4;          // tile-barrier ring depth (tiles in flight <= NSLOT/9 + 1)
 constexpr int NBAR = 4 * NTB + 8;
 constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
-constexpr int SMEM_USED = OFF_TMEM + 16;
+// in-kernel split schedule (fused K1): cost prefix, split offsets, tiles per virtual sequence
+constexpr int MAX_FUSED_VB = 256;
+constexpr int OFF_SCHED = OFF_TMEM + 16;
+constexpr int SCHED_SMEM_INTS = 3 * MAX_FUSED_VB + 2 + 8 + 8;
+constexpr int SMEM_USED = OFF_SCHED + SCHED_SMEM_INTS * 4;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;  // slack for manual 1024 B alignment
 
 // barrier indices
@@ -80,7 +84,12 @@ constexpr float LAZY_RESCALE_LOG2 = 8.0f;  // rescale O^T only when the max grow
 constexpr int SCHED_INTS = 8;
 constexpr int META_FIXED_COST = 3;  // per-split overhead in tile (page) units for the scheduler
 
-enum : unsigned { FLAG_NEGATE_RESCALE = 1u, FLAG_EAGER_RESCALE = 2u };
+enum : unsigned {
+    FLAG_NEGATE_RESCALE = 1u,
+    FLAG_EAGER_RESCALE = 2u,
+    FLAG_SKIP_COMBINE = 4u,
+    FLAG_EXTERNAL_SCHEDULE = 8u
+};
 
 // P^T operand (B of GEMM2): MN-major, no swizzle. Core matrices of 8 KV rows x 8 columns
 // (16 B per row); columns 0-15 = P_hi heads 0-15, 16-31 = P_lo heads 0-15.
@@ -238,13 +247,17 @@ struct DecodeParams {
     const int32_t* seqlens;
     const int32_t* sched;
     const int32_t* split_off;
+    int32_t* sched_out;      // in-kernel schedule published here (same buffers as K1 writes)
+    int32_t* split_off_out;
     float* out;
     float* lse;
     float* ws_o;
     float* ws_lse;
     int max_pages;
+    int batch;
     int heads;
     int groups;  // heads / 16
+    int inkernel_sched;  // 1: compute the split schedule in the prologue (and publish it)
     float scale_log2;
     unsigned flags;
     unsigned long long* trace;  // debug: [cta][TRACE_TILES][8] globaltimer stamps, or null

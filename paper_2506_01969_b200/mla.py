@@ -12,7 +12,8 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import FLAG_EAGER_RESCALE, FLAG_NEGATE_RESCALE, FLAG_SKIP_COMBINE, check  # noqa: F401
+from ._lib import (FLAG_EAGER_RESCALE, FLAG_EXTERNAL_SCHEDULE, FLAG_NEGATE_RESCALE,  # noqa: F401
+                   FLAG_SKIP_COMBINE, check)
 
 D_QK = 576
 D_V = 512
@@ -117,6 +118,23 @@ class MlaDecodePlan:
             self.workspace.data_ptr(), out.data_ptr(), lse.data_ptr(), int(flags),
             _stream_ptr(stream)), "etap_mla_decode")
         return out, lse
+
+    def capture(self, q: torch.Tensor, kv_pool: torch.Tensor, block_table: torch.Tensor,
+                seqlens: torch.Tensor, scale: float, out: torch.Tensor, lse: torch.Tensor,
+                flags: int = 0, with_metadata: bool = True) -> torch.cuda.CUDAGraph:
+        """Capture one decode step (K1 -> K2 -> K3, programmatic dependent launches) into a
+        CUDA graph; replay() re-runs it on the same buffers with one host call."""
+        for _ in range(2):  # one-time host init (smem attributes) happens outside the capture
+            if with_metadata:
+                self.metadata(seqlens)
+            self.decode(q, kv_pool, block_table, seqlens, scale, out=out, lse=lse, flags=flags)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            if with_metadata:
+                self.metadata(seqlens)
+            self.decode(q, kv_pool, block_table, seqlens, scale, out=out, lse=lse, flags=flags)
+        return g
 
     def combine(self, out: torch.Tensor, lse: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
         """K3 alone, after a decode(..., flags=FLAG_SKIP_COMBINE)."""
