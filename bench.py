@@ -198,10 +198,18 @@ def run_ours(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         log(f"[bench] WORLD_SIZE={world} differs from --gpus {args.gpus}; using WORLD_SIZE")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # ETAP_DIST_BACKEND=gloo lets the N>1 path run with several ranks on one GPU (testing only;
+    # the driver's multi-GPU runs use NCCL, one rank per GPU)
+    backend = os.environ.get("ETAP_DIST_BACKEND", "nccl")
+    gpu = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    local = gpu
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     total_heads = HEADS * world
     seqlens = [CTX] * BATCH
@@ -223,7 +231,10 @@ def run_ours(args) -> None:
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
@@ -278,7 +289,7 @@ def run_ours(args) -> None:
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": WORKLOAD, "batch": BATCH, "ctx": CTX, "heads_per_gpu": HEADS,
-                       "total_heads": total_heads, "d_qk": 576, "d_v": 512, "page_rows": 64,
+                       "total_heads": total_heads, "dist_backend": backend if world > 1 else None, "d_qk": 576, "d_v": 512, "page_rows": 64,
                        "kv_bytes_per_gpu": inp.kv_bytes(), "l2": "inputs (1.2 GB KV) > 126 MB L2, no flush",
                        "parallelism": f"head-shard tp{world} (KV replicated, NCCL all-gather of O)" if world > 1
                        else "single GPU", "step": "K2 decode (in-kernel split schedule) + K3 combine" +
@@ -298,7 +309,7 @@ def run_ours(args) -> None:
         }
         print(json.dumps(result), flush=True)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        barrier()
         dist.destroy_process_group()
 
 

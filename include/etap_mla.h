@@ -146,6 +146,22 @@ int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* 
  * 5 P^T written, 6 MMA saw P^T, 7 O^T update committed). NULL disables (the default). */
 int etap_mla_debug_trace(void* device_buf);
 
+/* Debug (BlockHook replay, the reference's per-KV-block observer tiled_standard.hpp:32-40):
+ * when device_buf is non-NULL, decode launches record for every (virtual sequence vb,
+ * 64-row tile t < max_tiles) the softmax state after the tile:
+ *   device_buf[((vb * max_tiles) + t) * 64 + {0,16,32,48} + h] = m_old, m_new (natural log
+ *   units of scale*q.k), rescale exp(m_old - m_new) (0 on the first tile of a split), running l
+ * for head h of the head group. Per-split state: run with one split per sequence
+ * (num_sm_parts = 1 or a single sequence) to observe the reference's single chain. */
+int etap_mla_debug_state(void* device_buf, int max_tiles);
+
+/* Reference-shaped entry with the softmax state returned (one split, the reference's serial
+ * block order with b_c = 64): state [n_tiles][4][n_q_padded16] host binary64, layout as above
+ * with the head index running over n_q (padded to a multiple of 16). */
+int etap_mla_run_etap_f64_state(const double* q, int64_t n_q, const double* k, int64_t n_kv,
+                                int64_t d_qk, const double* v, int64_t d_v, double scale,
+                                unsigned flags, double* o, double* l, double* state);
+
 /* Debug: tensor-pipe microbenchmark — `grid` CTAs each issue n tcgen05.mma of one operand
  * layout variant; out_dev[0..1] (device, int64) = issue cycles, issue+completion cycles. */
 int etap_mla_umma_bench(int variant, int n, long long* out_dev, int grid);

@@ -92,6 +92,8 @@ def ref() -> C.CDLL:
         L.ref_run.restype = i32
         L.ref_run.argtypes = [i32, vp, i64, vp, i64, i64, vp, i64, f64, i32, i64, i64, i64, i32, vp, vp]
         L.ref_transpose_count.restype = u64
+        L.ref_run_etap_state.restype = C.c_long
+        L.ref_run_etap_state.argtypes = [vp, i64, vp, i64, i64, vp, i64, f64, i64, i64, vp, vp, vp]
         L.ref_mla_run_etap_batch.restype = f64
         L.ref_mla_run_etap_batch.argtypes = [vp, vp, i64, i64, i64, f64, i32, vp, vp]
         _ref = L
@@ -210,6 +212,24 @@ def ref_run(mode: str, q, k, v, scale: float, precision: int = 0, b_r: int = 64,
     if rc:
         raise ValueError("reference rejected the problem (std::invalid_argument)")
     return o, l
+
+
+def ref_run_etap_state(q, k, v, scale: float, b_r: int = 16, b_c: int = 64):
+    """The reference's run_etap (exact64) with its BlockHook recorded: returns
+    (o, l, state[n_qblocks, t_c, 4, b_r]) with state fields m_old, m, rescale, l."""
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    k = np.ascontiguousarray(k, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    n_q, n_kv = q.shape[0], k.shape[0]
+    nqb, t_c = (n_q + b_r - 1) // b_r, (n_kv + b_c - 1) // b_c
+    o = np.empty((n_q, v.shape[1]))
+    l = np.empty(n_q)
+    st = np.full((nqb, t_c, 4, b_r), np.nan)
+    calls = ref().ref_run_etap_state(_dp(q), n_q, _dp(k), n_kv, k.shape[1], _dp(v), v.shape[1], float(scale),
+                                     b_r, b_c, _dp(o), _dp(l), _dp(st))
+    if calls != nqb * t_c:
+        raise RuntimeError(f"reference hook called {calls} times, expected {nqb * t_c}")
+    return o, l, st
 
 
 def ref_mla_run_etap_batch(q: np.ndarray, kv: np.ndarray, scale: float, nthreads: int):

@@ -92,6 +92,36 @@ int ref_run(int mode, const double* q, std::int64_t n_q, const double* k, std::i
     }
 }
 
+// run_etap exact64 with a BlockHook (tiled_standard.hpp:32-40, called at etap.cpp:128) that
+// records, per (query block qb, kv block j), m_old / m / rescale / l for the block's queries:
+// state[((qb * t_c) + j) * 4 * b_r + f * b_r + i]. Returns the number of hook calls.
+long ref_run_etap_state(const double* q, std::int64_t n_q, const double* k, std::int64_t n_kv,
+                        std::int64_t d_qk, const double* v, std::int64_t d_v, double scale,
+                        std::int64_t b_r, std::int64_t b_c, double* o, double* l, double* state) {
+    try {
+        const AttentionProblem p = make_problem(from_ptr(q, n_q, d_qk), from_ptr(k, n_kv, d_qk),
+                                                from_ptr(v, n_kv, d_v), scale, Precision::exact64);
+        const TileConfig tiles{static_cast<std::size_t>(b_r), static_cast<std::size_t>(b_c), 2};
+        const std::int64_t t_c = (n_kv + b_c - 1) / b_c;
+        long calls = 0;
+        BlockHook hook = [&](const BlockStepInfo& info) {
+            ++calls;
+            double* st = state + (static_cast<std::int64_t>(info.query_block) * t_c +
+                                  static_cast<std::int64_t>(info.kv_block)) * 4 * b_r;
+            for (std::size_t i = 0; i < info.m_old.size(); ++i) {
+                st[0 * b_r + i] = info.m_old[i];
+                st[1 * b_r + i] = info.state.m[i];
+                st[2 * b_r + i] = info.rescale[i];
+                st[3 * b_r + i] = info.state.l[i];
+            }
+        };
+        to_ptr(run_etap(p, tiles, hook), o, l);
+        return calls;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 std::uint64_t ref_transpose_count() { return transpose_count(); }
 void ref_reset_transpose_count() { reset_transpose_count(); }
 

@@ -466,6 +466,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
             float m_used[16];   // running max per head (log2 units), replicated in all threads
             float l_part[8];    // partial column sums of this thread's rows, own 8 heads
+            float dbg_l = 0.f;  // debug state dump: running column sum of one head
 #pragma unroll
             for (int h = 0; h < 16; ++h) m_used[h] = -INFINITY;
 #pragma unroll
@@ -496,9 +497,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 // one barrier decides, CTA-uniformly, whether any running max must move
                 const bool any = ptx::bar_red_or(1, 128, exceed || (negate && !first));
                 bool need_rescale = false;
-                float alpha[16];
+                float alpha[16], m_prev[16];
 #pragma unroll
-                for (int h = 0; h < 16; ++h) alpha[h] = 1.f;
+                for (int h = 0; h < 16; ++h) {
+                    alpha[h] = 1.f;
+                    m_prev[h] = m_used[h];
+                }
                 if (any) {
                     const float wm = halfwarp_reduce8<true>(x, lane);
                     float* rm = red_max + (gt & 1) * 64;
@@ -539,6 +543,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     pv[j] = exp2f(x[j] - mu[j]);
                     const float aj = half ? alpha[8 + j] : alpha[j];
                     l_part[j] = first ? pv[j] : fmaf(l_part[j], aj, pv[j]);
+                }
+                if (prm.state != nullptr && t < prm.state_tiles) {
+                    // debug (BlockHook replay): column sums of this tile's P, running l, m, rescale
+                    // in natural-log units, as BlockStepInfo carries them (tiled_standard.hpp:32-40)
+                    const float cs = halfwarp_reduce8<false>(pv, lane);
+                    if ((lane & 1) == 0) red_sum[wq * 16 + half * 8 + ((lane & 15) >> 1)] = cs;
+                    ptx::named_bar_sync(2, 128);
+                    if (wq == 0 && lane < 16) {
+                        float colsum = red_sum[lane] + red_sum[16 + lane] + red_sum[32 + lane] + red_sum[48 + lane];
+                        float mo = 0.f, mn = 0.f, al = 1.f;
+#pragma unroll
+                        for (int h = 0; h < 16; ++h)
+                            if (h == lane) { mo = m_prev[h]; mn = m_used[h]; al = first ? 0.f : alpha[h]; }
+                        dbg_l = first ? colsum : fmaf(dbg_l, al, colsum);
+                        float* st = prm.state + (static_cast<size_t>(vb) * prm.state_tiles + t) * 64;
+                        st[lane] = mo * 0.69314718055994530942f;
+                        st[16 + lane] = mn * 0.69314718055994530942f;
+                        st[32 + lane] = al;
+                        st[48 + lane] = dbg_l;
+                    }
+                    ptx::named_bar_sync(2, 128);
                 }
                 // the P buffer is reused every other tile: GEMM2(gt-2) must have read it
                 if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
@@ -847,6 +872,8 @@ int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_row
 }
 
 void* g_trace_buf = nullptr;  // debug tracing target (etap_mla_debug_trace)
+void* g_state_buf = nullptr;  // debug softmax-state dump target (etap_mla_debug_state)
+int g_state_tiles = 0;
 
 template <typename K>
 int ensure_smem_attr(K kernel, int bytes) {
@@ -1038,6 +1065,8 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.flags = flags;
     prm.trace = static_cast<unsigned long long*>(g_trace_buf);
+    prm.state = static_cast<float*>(g_state_buf);
+    prm.state_tiles = g_state_tiles;
 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaLaunchAttribute attr[1];
@@ -1080,6 +1109,12 @@ int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_
     cfg2.numAttrs = 1;
     ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, ws_o, ws_lse, split_off, groups,
                                  heads, out, lse));
+    return ETAP_OK;
+}
+
+int etap_mla_debug_state(void* device_buf, int max_tiles) {
+    g_state_buf = device_buf;
+    g_state_tiles = device_buf ? max_tiles : 0;
     return ETAP_OK;
 }
 

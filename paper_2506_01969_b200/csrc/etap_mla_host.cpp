@@ -142,9 +142,10 @@ void etap_mla_host_ctx_destroy(etap_mla_host_ctx* c) {
     delete c;
 }
 
-int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t n_kv,
-                          int64_t d_qk, const double* v, int64_t d_v, double scale, int64_t b_r,
-                          int64_t b_c, int64_t stages, unsigned flags, double* o, double* l) {
+static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int64_t n_kv,
+                             int64_t d_qk, const double* v, int64_t d_v, double scale,
+                             int64_t b_r, int64_t b_c, int64_t stages, unsigned flags, double* o,
+                             double* l, double* state) {
     // argument validation mirrors run_etap / make_problem (etap.cpp:104-106,
     // attention.cpp:11-19): these are the cases the reference rejects with invalid_argument
     if (b_r < 1 || b_c < 1 || stages < 1)
@@ -177,13 +178,54 @@ int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t
     etap_mla_host_ctx* ctx = nullptr;
     int rc = etap_mla_host_ctx_create(1, heads, pages, static_cast<int>(pages), &ctx);
     if (rc) return rc;
+    float* st_dev = nullptr;
+    const int groups = heads / ETAP_MLA_HEAD_GROUP;
+    const size_t st_n = static_cast<size_t>(groups) * pages * 64;
+    if (state) {
+        ctx->num_sm_parts = 1;  // one split: the reference's serial chain of KV blocks
+        if (cudaMalloc(&st_dev, st_n * sizeof(float)) != cudaSuccess) {
+            etap_mla_host_ctx_destroy(ctx);
+            return host_fail(ETAP_ERR_CUDA, "state buffer allocation failed");
+        }
+        cudaMemset(st_dev, 0, st_n * sizeof(float));
+        etap_mla_debug_state(st_dev, static_cast<int>(pages));
+    }
     rc = etap_mla_host_decode(ctx, qb.data(), kvb.data(), bt.data(), &seqlen,
                               static_cast<float>(scale), flags, of.data(), lf.data());
+    if (state) {
+        etap_mla_debug_state(nullptr, 0);
+        std::vector<float> sf(st_n);
+        if (!rc && cudaMemcpy(sf.data(), st_dev, st_n * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess)
+            rc = host_fail(ETAP_ERR_CUDA, "state copy failed");
+        cudaFree(st_dev);
+        // [vb = head group][tile][4][16] -> [tile][4][heads]
+        if (!rc)
+            for (int g = 0; g < groups; ++g)
+                for (int64_t t = 0; t < pages; ++t)
+                    for (int f = 0; f < 4; ++f)
+                        for (int h = 0; h < ETAP_MLA_HEAD_GROUP; ++h)
+                            state[(t * 4 + f) * heads + g * ETAP_MLA_HEAD_GROUP + h] =
+                                sf[((static_cast<size_t>(g) * pages + t) * 4 + f) * 16 + h];
+    }
     etap_mla_host_ctx_destroy(ctx);
     if (rc) return rc;
     for (int64_t i = 0; i < n_q * d_v; ++i) o[i] = static_cast<double>(of[i]);
     for (int64_t i = 0; i < n_q; ++i) l[i] = static_cast<double>(lf[i]);
     return ETAP_OK;
+}
+
+int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t n_kv,
+                          int64_t d_qk, const double* v, int64_t d_v, double scale, int64_t b_r,
+                          int64_t b_c, int64_t stages, unsigned flags, double* o, double* l) {
+    return run_etap_f64_impl(q, n_q, k, n_kv, d_qk, v, d_v, scale, b_r, b_c, stages, flags, o, l,
+                             nullptr);
+}
+
+int etap_mla_run_etap_f64_state(const double* q, int64_t n_q, const double* k, int64_t n_kv,
+                                int64_t d_qk, const double* v, int64_t d_v, double scale,
+                                unsigned flags, double* o, double* l, double* state) {
+    if (!state) return host_fail(ETAP_ERR_SHAPE, "state is NULL");
+    return run_etap_f64_impl(q, n_q, k, n_kv, d_qk, v, d_v, scale, 16, 64, 2, flags, o, l, state);
 }
 
 }  // extern "C"

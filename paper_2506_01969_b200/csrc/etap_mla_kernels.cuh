@@ -261,6 +261,8 @@ struct DecodeParams {
     float scale_log2;
     unsigned flags;
     unsigned long long* trace;  // debug: [cta][TRACE_TILES][8] globaltimer stamps, or null
+    float* state;               // debug: per-tile softmax state [vb][state_tiles][4][16], or null
+    int state_tiles;
 };
 
 constexpr int TRACE_TILES = 256;

@@ -55,6 +55,21 @@ class AttentionProblem:
 
 
 @dataclass
+class SoftmaxState:  # tiled_standard.hpp:23-26
+    m: np.ndarray
+    l: np.ndarray
+
+
+@dataclass
+class BlockStepInfo:  # tiled_standard.hpp:32-38
+    query_block: int
+    kv_block: int
+    m_old: np.ndarray
+    state: SoftmaxState
+    rescale: np.ndarray
+
+
+@dataclass
 class AttentionOutput:
     o: np.ndarray              # n_q x d_v
     l: np.ndarray = field(default_factory=lambda: np.zeros(0))  # per-query logsumexp
@@ -113,18 +128,23 @@ def make_mla_problem(seed: int, n_q: int, n_kv: int, scale: float = -1.0) -> Att
 
 
 def run_etap(problem: AttentionProblem, tiles: TileConfig = TileConfig(),
-             hook: Optional[Callable] = None, faults: EtapFaults = EtapFaults()) -> AttentionOutput:
+             hook: Optional[Callable[[BlockStepInfo], None]] = None,
+             faults: EtapFaults = EtapFaults(), eager: Optional[bool] = None) -> AttentionOutput:
     """GPU run_etap (etap.hpp:47-48) through the C-ABI entry ``etap_mla_run_etap_f64``.
 
     Raises EtapShapeError where the reference throws std::invalid_argument (tile fields < 1,
     etap.cpp:104-106) and for problems outside the GPU path's scope (d_qk != 576, d_v != 512,
-    V not the first 512 columns of K). ``hook`` (BlockHook) cannot observe per-tile device state
-    and is rejected when given.
+    V not the first 512 columns of K).
+
+    ``hook`` (BlockHook, tiled_standard.hpp:32-40): the device cannot call back per KV block,
+    so the kernel records the softmax state of every 64-row tile (one split, the reference's
+    serial block order; query blocks = 16-head groups, KV blocks = 64 rows) and the hook is
+    replayed in order after the run with BlockStepInfo(query_block, kv_block, m_old,
+    SoftmaxState(m, l), rescale). With a hook the rescale order defaults to the reference's
+    eager one (``eager=True``); the default lazy mode gives the same invariants.
     """
     if tiles.b_r < 1 or tiles.b_c < 1 or tiles.stages < 1:
         raise EtapShapeError("tile config fields must be >= 1")
-    if hook is not None:
-        raise EtapShapeError("BlockHook is not observable on the GPU path")
     p = problem
     if p.d_qk != 576 or p.d_v != 512:
         raise EtapShapeError("GPU ETAP path is MLA decode: d_qk=576, d_v=512")
@@ -136,11 +156,29 @@ def run_etap(problem: AttentionProblem, tiles: TileConfig = TileConfig(),
     o = np.empty((p.n_q, p.d_v))
     l = np.empty(p.n_q)
     flags = _lib.FLAG_NEGATE_RESCALE if faults.negate_rescale else 0
+    if eager if eager is not None else hook is not None:
+        flags |= _lib.FLAG_EAGER_RESCALE
     vp = C.c_void_p
-    check(_lib.lib().etap_mla_run_etap_f64(
+    if hook is None:
+        check(_lib.lib().etap_mla_run_etap_f64(
+            q.ctypes.data_as(vp), p.n_q, k.ctypes.data_as(vp), p.n_kv, p.d_qk, v.ctypes.data_as(vp), p.d_v,
+            float(p.scale), tiles.b_r, tiles.b_c, tiles.stages, flags, o.ctypes.data_as(vp),
+            l.ctypes.data_as(vp)), "etap_mla_run_etap_f64")
+        return AttentionOutput(o, l)
+    heads = (p.n_q + 15) // 16 * 16
+    t_c = (p.n_kv + 63) // 64
+    state = np.empty((t_c, 4, heads))
+    check(_lib.lib().etap_mla_run_etap_f64_state(
         q.ctypes.data_as(vp), p.n_q, k.ctypes.data_as(vp), p.n_kv, p.d_qk, v.ctypes.data_as(vp), p.d_v,
-        float(p.scale), tiles.b_r, tiles.b_c, tiles.stages, flags, o.ctypes.data_as(vp),
-        l.ctypes.data_as(vp)), "etap_mla_run_etap_f64")
+        float(p.scale), flags, o.ctypes.data_as(vp), l.ctypes.data_as(vp), state.ctypes.data_as(vp)),
+        "etap_mla_run_etap_f64_state")
+    for qb in range(heads // 16):
+        h0, h1 = qb * 16, min(p.n_q, qb * 16 + 16)
+        if h0 >= p.n_q:
+            break
+        for j in range(t_c):
+            st = state[j, :, h0:h1]
+            hook(BlockStepInfo(qb, j, st[0].copy(), SoftmaxState(st[1].copy(), st[3].copy()), st[2].copy()))
     return AttentionOutput(o, l)
 
 
