@@ -198,8 +198,81 @@ __device__ __forceinline__ int cta_excl_scan256(int v, int* s_wt, int& total) {
 // cost prefix -> closed-form split counts per virtual sequence (CTA k covers vb iff
 // (k+1)T > P[vb]+F and kT < P[vb+1]) -> split offsets -> this CTA's range. Identical output
 // to K1 (GPU test); CTA 0 publishes split_off for the combine kernel, every CTA its sched row.
+// this CTA's (vb, tile) range on the cost line, written to s_sched and published to sched_out
+__device__ void schedule_own_range(const DecodeParams& prm, const int* s_pref, const int* s_soff,
+                                   const int* s_tiles, int* s_sched, int nvb, int total, int T) {
+    const int k = blockIdx.x;
+    auto map = [&](int x, int& vb, int& t) {
+        int lo = 0, hi = nvb - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_pref[mid] <= x) lo = mid; else hi = mid - 1;
+        }
+        while (lo + 1 < nvb && s_pref[lo + 1] <= x) ++lo;
+        vb = lo;
+        t = min(max(0, x - s_pref[lo] - META_FIXED_COST), s_tiles[lo]);
+    };
+    const int x0 = k * T, x1 = min(total, (k + 1) * T);
+    int b0 = 0, tb = 0, b1 = -1, te = 0, first = 0;
+    if (x0 < total) {
+        map(x0, b0, tb);
+        if (x1 >= total) { b1 = nvb - 1; te = s_tiles[nvb - 1]; }
+        else map(x1, b1, te);
+        if (b1 >= b0) first = s_soff[b0] + (k - (s_pref[b0] + META_FIXED_COST) / T);
+    }
+    s_sched[0] = b0; s_sched[1] = tb; s_sched[2] = b1; s_sched[3] = te; s_sched[4] = first;
+    s_sched[5] = 0; s_sched[6] = 0; s_sched[7] = 0;
+    int32_t* g = prm.sched_out + k * SCHED_INTS;
+    for (int i = 0; i < SCHED_INTS; ++i) g[i] = s_sched[i];
+}
+
+// Warp-level variant for up to 32 virtual sequences (no block barriers): run by warp 0 only.
+__device__ void inkernel_schedule_warp(const DecodeParams& prm, int* s_pref, int* s_soff,
+                                       int* s_tiles, int* s_len, int* s_sched) {
+    const int G = prm.groups;
+    const int nvb = prm.batch * G;
+    const int parts = gridDim.x;
+    const int lane = threadIdx.x & 31;
+    int len = 0, tiles = 0, cost = 0;
+    if (lane < nvb) {
+        len = max(0, prm.seqlens[lane / G]);
+        tiles = (len + TILE - 1) / TILE;
+        cost = tiles > 0 ? tiles + META_FIXED_COST : 0;
+        s_tiles[lane] = tiles;
+        s_len[lane] = len;
+    }
+    int incl = cost;  // inclusive prefix = P[lane + 1]
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int pref = incl - cost;
+    if (lane < nvb) s_pref[lane] = pref;
+    if (lane == 0) s_pref[nvb] = total;
+    const int T = max(1, (total + parts - 1) / parts);
+    int ns = 0;
+    if (lane < nvb && tiles > 0) ns = ((incl + T - 1) / T - 1) - (pref + META_FIXED_COST) / T + 1;
+    int so = ns;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, so, o);
+        if (lane >= o) so += y;
+    }
+    if (lane < nvb) s_soff[lane] = so - ns;
+    if (lane == 31) s_soff[nvb] = so;
+    __syncwarp();
+    if (lane == 0) schedule_own_range(prm, s_pref, s_soff, s_tiles, s_sched, nvb, total, T);
+    if (blockIdx.x == 0) {
+        if (lane < nvb) prm.split_off_out[lane] = s_soff[lane];
+        if (lane == 0) prm.split_off_out[nvb] = s_soff[nvb];
+    }
+    __syncwarp();
+}
+
 __device__ void inkernel_schedule(const DecodeParams& prm, int* s_pref, int* s_soff, int* s_tiles,
-                                  int* s_sched, int* s_wt) {
+                                  int* s_len, int* s_sched, int* s_wt) {
     const int G = prm.groups;
     const int nvb = prm.batch * G;
     const int parts = gridDim.x;
@@ -210,6 +283,7 @@ __device__ void inkernel_schedule(const DecodeParams& prm, int* s_pref, int* s_s
         tiles = (len + TILE - 1) / TILE;
         cost = tiles > 0 ? tiles + META_FIXED_COST : 0;
         s_tiles[tid] = tiles;
+        s_len[tid] = len;
     }
     int total;
     const int pref = cta_excl_scan256(cost, s_wt, total);
@@ -228,42 +302,18 @@ __device__ void inkernel_schedule(const DecodeParams& prm, int* s_pref, int* s_s
     if (tid < nvb) s_soff[tid] = so;
     if (tid == 0) s_soff[nvb] = nsplits;
     __syncthreads();
-    if (tid == 0) {
-        const int k = blockIdx.x;
-        auto map = [&](int x, int& vb, int& t) {
-            int lo = 0, hi = nvb - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s_pref[mid] <= x) lo = mid; else hi = mid - 1;
-            }
-            while (lo + 1 < nvb && s_pref[lo + 1] <= x) ++lo;
-            vb = lo;
-            t = min(max(0, x - s_pref[lo] - META_FIXED_COST), s_tiles[lo]);
-        };
-        const int x0 = k * T, x1 = min(total, (k + 1) * T);
-        int b0 = 0, tb = 0, b1 = -1, te = 0, first = 0;
-        if (x0 < total) {
-            map(x0, b0, tb);
-            if (x1 >= total) { b1 = nvb - 1; te = s_tiles[nvb - 1]; }
-            else map(x1, b1, te);
-            if (b1 >= b0) first = s_soff[b0] + (k - (s_pref[b0] + META_FIXED_COST) / T);
-        }
-        s_sched[0] = b0; s_sched[1] = tb; s_sched[2] = b1; s_sched[3] = te; s_sched[4] = first;
-        s_sched[5] = 0; s_sched[6] = 0; s_sched[7] = 0;
-        int32_t* g = prm.sched_out + k * SCHED_INTS;
-        for (int i = 0; i < SCHED_INTS; ++i) g[i] = s_sched[i];
-    }
+    if (tid == 0) schedule_own_range(prm, s_pref, s_soff, s_tiles, s_sched, nvb, total, T);
     if (blockIdx.x == 0)
         for (int i = tid; i <= nvb; i += NUM_THREADS) prm.split_off_out[i] = s_soff[i];
     __syncthreads();
 }
 
-__device__ __forceinline__ bool split_at(const int32_t* sch, const int32_t* seqlens, int groups,
-                                         int vb, SplitDesc& d) {
+__device__ __forceinline__ bool split_at(const int32_t* sch, int seqlen, int groups, int vb,
+                                         SplitDesc& d) {
     d.vb = vb;
     d.b = vb / groups;
     d.g = vb - d.b * groups;
-    d.seqlen = max(0, seqlens[d.b]);
+    d.seqlen = seqlen;
     const int n_tiles = (d.seqlen + TILE - 1) / TILE;
     d.t0 = (vb == sch[0]) ? sch[1] : 0;
     d.t1 = (vb == sch[2]) ? min(sch[3], n_tiles) : n_tiles;
@@ -313,12 +363,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::grid_dep_launch();   // let the combine kernel get scheduled
     const int32_t* sch;
     const int32_t* soff;      // split offsets per virtual sequence
-    if (prm.inkernel_sched) {
-        int* s_pref = reinterpret_cast<int*>(smem + OFF_SCHED);
-        int* s_soff = s_pref + MAX_FUSED_VB + 1;
-        int* s_tiles = s_soff + MAX_FUSED_VB + 1;
-        int* s_sched = s_tiles + MAX_FUSED_VB;
-        inkernel_schedule(prm, s_pref, s_soff, s_tiles, s_sched, s_sched + 8);
+    int* s_pref = reinterpret_cast<int*>(smem + OFF_SCHED);
+    int* s_soff = s_pref + MAX_FUSED_VB + 1;
+    int* s_tiles = s_soff + MAX_FUSED_VB + 1;
+    int* s_len = s_tiles + MAX_FUSED_VB;
+    int* s_sched = s_len + MAX_FUSED_VB;
+    const bool fused = prm.inkernel_sched != 0;
+    if (fused) {
+        if (prm.batch * prm.groups <= 32) {
+            if (warp == 0) inkernel_schedule_warp(prm, s_pref, s_soff, s_tiles, s_len, s_sched);
+            __syncthreads();
+        } else {
+            inkernel_schedule(prm, s_pref, s_soff, s_tiles, s_len, s_sched, s_sched + 8);
+        }
         sch = s_sched;
         soff = s_soff;
     } else {
@@ -342,7 +399,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t gt = 0, nsplit = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
+            if (!split_at(sch, fused ? s_len[vb] : max(0, prm.seqlens[vb / G]), G, vb, sd)) continue;
             if (nsplit > 0) ptx::mbar_wait(&bars[BAR_Q_EMPTY], (nsplit - 1) & 1);
             if (lane == 0) {
                 ptx::mbar_arrive_expect_tx(&bars[BAR_Q_FULL], Q_BYTES);
@@ -399,7 +456,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t gt = 0, nsplit = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
+            if (!split_at(sch, fused ? s_len[vb] : max(0, prm.seqlens[vb / G]), G, vb, sd)) continue;
             ptx::mbar_wait(&bars[BAR_Q_FULL], nsplit & 1);
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
@@ -426,7 +483,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t gt = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
+            if (!split_at(sch, fused ? s_len[vb] : max(0, prm.seqlens[vb / G]), G, vb, sd)) continue;
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
                 ptx::mbar_wait(&bars[BAR_P_FULL + buf], (gt >> 1) & 1);
@@ -463,7 +520,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t gt = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, prm.seqlens, G, vb, sd)) continue;
+            if (!split_at(sch, fused ? s_len[vb] : max(0, prm.seqlens[vb / G]), G, vb, sd)) continue;
             float m_used[16];   // running max per head (log2 units), replicated in all threads
             float l_part[8];    // partial column sums of this thread's rows, own 8 heads
             float dbg_l = 0.f;  // debug state dump: running column sum of one head
@@ -623,6 +680,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 inv_l[h] = 1.f / l_tot[h];
             }
             const int ns = soff[vb + 1] - soff[vb];
+            const int idx = (vb == sch[0]) ? sch[4] : soff[vb];  // partial index (ns > 1)
             float* dst;
             float* dst_lse;
             if (ns == 1) {
@@ -630,7 +688,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 dst = prm.out + hrow * D_V;
                 dst_lse = prm.lse + hrow;
             } else {
-                const int idx = (vb == sch[0]) ? sch[4] : soff[vb];
                 dst = prm.ws_o + static_cast<size_t>(idx) * HG * D_V;
                 dst_lse = prm.ws_lse + static_cast<size_t>(idx) * HG;
             }
@@ -653,7 +710,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 dst_lse[lane] = v;
             }
             ptx::tc_fence_before();
-            // red_sum is rewritten by the next epilogue only after the next split's barriers
+            // red_sum is rewritten by the next split's epilogue only after this barrier
             ptx::named_bar_sync(2, 128);
         }
     }
@@ -1107,8 +1164,8 @@ int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_
     cfg2.stream = static_cast<cudaStream_t>(stream);
     cfg2.attrs = attr;
     cfg2.numAttrs = 1;
-    ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, ws_o, ws_lse, split_off, groups,
-                                 heads, out, lse));
+    ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, static_cast<const float*>(ws_o),
+                                 static_cast<const float*>(ws_lse), split_off, groups, heads, out, lse));
     return ETAP_OK;
 }
 

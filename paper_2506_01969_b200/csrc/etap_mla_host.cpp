@@ -96,7 +96,8 @@ int etap_mla_host_ctx_create(int batch, int heads, int64_t num_pages, int max_pa
             c->sl.alloc(static_cast<size_t>(batch) * 4) || c->out.alloc(rows * ETAP_MLA_D_V * 4) ||
             c->lse.alloc(rows * 4) || c->sched.alloc(sched_n * 4) ||
             c->split_off.alloc(so_n * 4) || c->ws.alloc(ws_n) ||
-            cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking))
+            cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) ||
+            cudaMemset(c->ws.p, 0, c->ws.n))  // combine flags / counters start at zero
             rc = host_fail(ETAP_ERR_CUDA, "device allocation failed");
     }
     if (rc) {

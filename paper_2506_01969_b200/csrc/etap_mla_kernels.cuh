@@ -52,7 +52,7 @@ constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
 // in-kernel split schedule (fused K1): cost prefix, split offsets, tiles per virtual sequence
 constexpr int MAX_FUSED_VB = 256;
 constexpr int OFF_SCHED = OFF_TMEM + 16;
-constexpr int SCHED_SMEM_INTS = 3 * MAX_FUSED_VB + 2 + 8 + 8;
+constexpr int SCHED_SMEM_INTS = 4 * MAX_FUSED_VB + 2 + 8 + 8;  // pref, soff, tiles, len, sched, wt
 constexpr int SMEM_USED = OFF_SCHED + SCHED_SMEM_INTS * 4;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;  // slack for manual 1024 B alignment
 

@@ -79,7 +79,9 @@ class MlaDecodePlan:
             batch=batch, heads=heads, device=device, num_sm_parts=nparts,
             sched=torch.empty(n_sched.value, dtype=torch.int32, device=device),
             split_off=torch.empty(n_so.value, dtype=torch.int32, device=device),
-            workspace=torch.empty(ws.value, dtype=torch.uint8, device=device),
+            # zero-filled once: the tail holds the combine's ready flags / counters, which every
+            # decode call leaves at zero again
+            workspace=torch.zeros(ws.value, dtype=torch.uint8, device=device),
         )
 
     def metadata(self, seqlens: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:

@@ -88,6 +88,16 @@ def main() -> None:
     print(f"kernel entry spread us: {(ent[:, 0].max() - e0) / 1e3:.2f}; prologue+dep-wait us (median): "
           f"{np.median(ent[:, 1] - ent[:, 0]) / 1e3:.2f}; dep-wait done -> first TMA issue us (median): "
           f"{np.nanmedian(first_issue - ent[:, 1]) / 1e3:.2f}")
+    sched = plan.sched.view(nparts, 8).cpu().numpy()
+    spans = ent[:, 2] - ent[:, 0]
+    ntiles = valid.sum(axis=1)
+    nsplit = np.array([sum(1 for vb in range(s[0], s[2] + 1)
+                           if (s[1] if vb == s[0] else 0) < (s[3] if vb == s[2] else 10**9)) for s in sched])
+    for ns_ in sorted(set(nsplit.tolist())):
+        for nt in sorted(set(ntiles[nsplit == ns_].tolist())):
+            sel = (nsplit == ns_) & (ntiles == nt)
+            print(f"  splits={ns_} tiles={nt}: CTAs {sel.sum():3d}, span us median {np.median(spans[sel]) / 1e3:.1f} "
+                  f"max {spans[sel].max() / 1e3:.1f}")
     print(f"last G2 commit -> CTA exit us (median/max): {np.nanmedian(ent[:, 2] - last_g2) / 1e3:.2f} / "
           f"{np.nanmax(ent[:, 2] - last_g2) / 1e3:.2f}; entry -> last exit us: {(ent[:, 2].max() - e0) / 1e3:.1f}")
 
