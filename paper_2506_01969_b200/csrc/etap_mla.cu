@@ -1105,6 +1105,7 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     const size_t np = max_partials(batch, heads, num_sm_parts);
     DecodeParams prm;
     prm.block_table = block_table;
+
     prm.seqlens = seqlens;
     prm.sched = sched;
     prm.split_off = split_off;
