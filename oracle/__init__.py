@@ -94,6 +94,10 @@ def ref() -> C.CDLL:
         L.ref_transpose_count.restype = u64
         L.ref_run_etap_state.restype = C.c_long
         L.ref_run_etap_state.argtypes = [vp, i64, vp, i64, i64, vp, i64, f64, i64, i64, vp, vp, vp]
+        L.ref_save_matrix.restype = i32
+        L.ref_save_matrix.argtypes = [C.c_char_p, vp, i64, i64]
+        L.ref_load_matrix.restype = i32
+        L.ref_load_matrix.argtypes = [C.c_char_p, vp, i64, C.POINTER(i64), C.POINTER(i64)]
         L.ref_mla_run_etap_batch.restype = f64
         L.ref_mla_run_etap_batch.argtypes = [vp, vp, i64, i64, i64, f64, i32, vp, vp]
         _ref = L
@@ -230,6 +234,21 @@ def ref_run_etap_state(q, k, v, scale: float, b_r: int = 16, b_c: int = 64):
     if calls != nqb * t_c:
         raise RuntimeError(f"reference hook called {calls} times, expected {nqb * t_c}")
     return o, l, st
+
+
+def ref_save_matrix(path: str, m: np.ndarray) -> None:
+    m = np.ascontiguousarray(m, dtype=np.float64)
+    if ref().ref_save_matrix(str(path).encode(), _dp(m), m.shape[0], m.shape[1]):
+        raise RuntimeError("reference save_matrix failed")
+
+
+def ref_load_matrix(path: str, cap: int = 1 << 24) -> np.ndarray:
+    out = np.empty(cap)
+    r, c = C.c_int64(), C.c_int64()
+    rc = ref().ref_load_matrix(str(path).encode(), _dp(out), cap, C.byref(r), C.byref(c))
+    if rc:
+        raise RuntimeError("reference load_matrix failed")
+    return out[: r.value * c.value].reshape(r.value, c.value).copy()
 
 
 def ref_mla_run_etap_batch(q: np.ndarray, kv: np.ndarray, scale: float, nthreads: int):

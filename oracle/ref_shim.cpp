@@ -9,12 +9,14 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <string>
 #include <thread>
 #include <vector>
 
 #include "etaplab/attention.hpp"
 #include "etaplab/etap.hpp"
 #include "etaplab/matrix.hpp"
+#include "etaplab/matrix_io.hpp"
 #include "etaplab/tiled_standard.hpp"
 
 using namespace etaplab;
@@ -119,6 +121,30 @@ long ref_run_etap_state(const double* q, std::int64_t n_q, const double* k, std:
         return calls;
     } catch (const std::exception&) {
         return -1;
+    }
+}
+
+// matrix_io (ATNM): save from / load into plain arrays. Returns 0, or 1 on std::runtime_error.
+int ref_save_matrix(const char* path, const double* data, std::int64_t rows, std::int64_t cols) {
+    try {
+        save_matrix(std::string(path), from_ptr(data, rows, cols));
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+int ref_load_matrix(const char* path, double* out, std::int64_t cap, std::int64_t* rows,
+                    std::int64_t* cols) {
+    try {
+        const Matrix m = load_matrix(std::string(path));
+        *rows = static_cast<std::int64_t>(m.rows());
+        *cols = static_cast<std::int64_t>(m.cols());
+        if (static_cast<std::int64_t>(m.size()) > cap) return 2;
+        std::memcpy(out, m.data(), sizeof(double) * m.size());
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
     }
 }
 
