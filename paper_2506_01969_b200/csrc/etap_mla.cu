@@ -717,7 +717,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     ptx::tc_fence_before();
     __syncthreads();
-    if (threadIdx.x == 0) ETAP_TRACE(prm, TRACE_TILES - 1, 2);
+    if (threadIdx.x == 0) {
+        ETAP_TRACE(prm, TRACE_TILES - 1, 2);
+        if (prm.trace != nullptr) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            prm.trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + TRACE_TILES - 1) * 8 + 3] = smid;
+        }
+    }
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, TMEM_COLS);

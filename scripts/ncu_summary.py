@@ -70,7 +70,7 @@ def main() -> None:
         rows = [r for r in csv.DictReader(l for l in open(launches) if not l.startswith("==")) if r.get("Metric Name") == "gpu__time_duration.sum"]
         ks = {}
         for r in rows:
-            name = r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "")
+            name = r["Kernel Name"].replace("<unnamed>::", "").replace("void ", "").split("(")[0].split("<")[0]
             ks.setdefault(name, []).append(float(r["Metric Value"]) * SCALE.get(r["Metric Unit"], 1e-9))
         tot = sum(sum(v) for v in ks.values())
         summary["launch_list"] = {k: {"launches": len(v), "avg_us": sum(v) / len(v) * 1e6,

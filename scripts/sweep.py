@@ -1,0 +1,70 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Measure the BASELINE.json configs besides the headline one (one JSON line each):
+config 1 (B=1, 16 heads, 1K), config 3 (B=16, 16 heads, ctx 1K..64K), config 4 (B=32
+varlen 4K..128K), and the 128-head single-GPU point of config 5. Device time per step with
+CUDA events (median of repeated blocks), stream launches and CUDA-graph replay; L2 is flushed
+between steps for working sets below 2x L2 (KV buffer rotation)."""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_2506_01969_b200 import inputs, mla
+
+L2_BYTES = 126 * 1024 * 1024
+
+
+def measure(seqlens, heads, label, iters=50):
+    kv_bytes = sum(seqlens) * 576 * 2
+    ncopies = max(1, min(8, (2 * L2_BYTES) // max(1, kv_bytes) + 1))  # rotate through > L2
+    inps = [inputs.make_mla_inputs(seqlens, heads=heads, seed=42 + i, pad_value=0.0) for i in range(ncopies)]
+    B = len(seqlens)
+    plan = mla.MlaDecodePlan.create(B, heads, "cuda")
+    out = torch.empty((B, 1, heads, 512), dtype=torch.float32, device="cuda")
+    lse = torch.empty((B, 1, heads), dtype=torch.float32, device="cuda")
+    graphs = [plan.capture(i.q, i.kv_pool, i.block_table, i.seqlens, i.scale, out, lse, with_metadata=False)
+              for i in inps]
+
+    def timed(fn):
+        for j in range(5):
+            fn(j)
+        torch.cuda.synchronize()
+        res = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for j in range(iters):
+                fn(j)
+            e1.record()
+            torch.cuda.synchronize()
+            res.append(e0.elapsed_time(e1) * 1000 / iters)
+        return sorted(res)[1]
+
+    def stream_step(j):
+        i = inps[j % ncopies]
+        plan.decode(i.q, i.kv_pool, i.block_table, i.seqlens, i.scale, out=out, lse=lse)
+
+    us_stream = timed(stream_step)
+    us_graph = timed(lambda j: graphs[j % ncopies].replay())
+    nbytes = inputs.algorithmic_bytes(seqlens, heads)
+    best = min(us_stream, us_graph)
+    line = {"config": label, "batch": B, "heads": heads, "ctx_total": sum(seqlens),
+            "ctx_min": min(seqlens), "ctx_max": max(seqlens), "us_per_step_stream": us_stream,
+            "us_per_step_graph": us_graph, "hbm_gbs": nbytes / best / 1e3,
+            "tflops": inputs.flops(seqlens, heads) / best / 1e6, "algorithmic_bytes": nbytes,
+            "l2_rotation_copies": ncopies}
+    print(json.dumps(line), flush=True)
+    del inps, graphs
+    torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    measure([1024], 16, "config1 B=1 H=16 ctx=1K")
+    for ctx in (1024, 2048, 4096, 8192, 16384, 32768, 65536):
+        measure([ctx] * 16, 16, f"config3 B=16 H=16 ctx={ctx}")
+    measure(inputs.varlen_seqlens(32), 16, "config4 B=32 varlen 4K-128K")
+    measure([65536] * 16, 128, "config5 single-GPU B=16 H=128 ctx=64K (8 head groups)", iters=10)

@@ -69,13 +69,26 @@ def main() -> None:
                 nxt[0] - e[7],          # GEMM2(g) commit -> producer issues first chunk of g+1
                 nxt[1] - e[7],          # GEMM2(g) commit -> producer issued last chunk of g+1
             ])
-    r = np.array(rows)
+    r = np.array(rows) if rows else np.zeros((0, 10))
     labels = ["lat_tile(last issue->seen)", "issue_span", "g1_issue", "s_ready_wait", "softmax", "p_to_mma",
               "g2_issue", "PERIOD", "g2->next_first_issue", "g2->next_last_issue"]
     print(f"{len(rows)} steady-state tiles over {nparts} CTAs (ns): median / p10 / p90")
     for i, lab in enumerate(labels):
+        if not len(r):
+            break
         col = r[:, i]
         print(f"  {lab:24s} {np.median(col):9.0f} {np.percentile(col, 10):9.0f} {np.percentile(col, 90):9.0f}")
+    # first tile of every working CTA, relative to kernel entry (us)
+    first = [(t[c, 0] - ent[c, 0]) / 1e3 for c in range(nparts) if valid[c, 0]]
+    if first:
+        f = np.array(first)
+        names0 = ["producer: first 6 chunks issued", "last 3 chunks issued", "G1 sees tile", "S committed",
+                  "softmax sees S", "P written", "G2 sees P", "G2 committed"]
+        print("first tile, us after kernel entry (median over CTAs):")
+        for i, n in enumerate(names0):
+            print(f"  {n:34s} {np.median(f[:, i]):7.2f}")
+        print(f"  {'schedule done':34s} {np.median((ent[:, 1] - ent[:, 0]) / 1e3):7.2f}")
+        print(f"  {'CTA exit':34s} {np.median((ent[:, 2] - ent[:, 0]) / 1e3):7.2f}")
     # CTA span
     span = [(t[c][valid[c]].max() - t[c][valid[c]].min()) for c in range(nparts) if valid[c].any()]
     starts = [t[c][valid[c]].min() - t0 for c in range(nparts) if valid[c].any()]
