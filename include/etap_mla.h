@@ -146,6 +146,9 @@ int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* 
  * 5 P^T written, 6 MMA saw P^T, 7 O^T update committed). NULL disables (the default). */
 int etap_mla_debug_trace(void* device_buf);
 
+/* Debug: combine-kernel stamps [block][4] (entry, after grid-dependency wait, exit) or NULL. */
+int etap_mla_debug_trace_combine(void* device_buf);
+
 /* Debug (BlockHook replay, the reference's per-KV-block observer tiled_standard.hpp:32-40):
  * when device_buf is non-NULL, decode launches record for every (virtual sequence vb,
  * 64-row tile t < max_tiles) the softmax state after the tile:

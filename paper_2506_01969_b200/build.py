@@ -19,9 +19,10 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libetap_mla.so"
+BENCH = LIBDIR / "etap_bench"
 
 SOURCES = [CSRC / "etap_mla.cu", CSRC / "etap_mla_host.cpp"]
-DEPS = SOURCES + [CSRC / "sm100_ptx.cuh", CSRC / "etap_mla_kernels.cuh", ROOT / "include" / "etap_mla.h"]
+DEPS = SOURCES + [CSRC / "etap_bench.cpp", CSRC / "sm100_ptx.cuh", CSRC / "etap_mla_kernels.cuh", ROOT / "include" / "etap_mla.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -66,6 +67,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if verbose:
         sys.stderr.write(res.stderr)
     os.replace(tmp, LIB)
+    # native benchmark driver (C-ABI, no Python in the launch path)
+    res = subprocess.run([nvcc(), "-O3", "-std=c++17", str(CSRC / "etap_bench.cpp"), "-o", str(BENCH),
+                          "-L", str(LIBDIR), "-letap_mla", "-Xlinker", "-rpath=$ORIGIN"],
+                         capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("etap_bench build failed")
     return LIB
 
 

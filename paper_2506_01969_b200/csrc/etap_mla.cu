@@ -737,18 +737,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // invariance, acceptance.cpp:209-229). Grid: one CTA of 128 threads per (vb, head).
 // =============================================================================================
 constexpr int COMBINE_THREADS = 128;
+constexpr int COMBINE_BATCH = 16;  // partial float4 loads in flight per thread
 
 __global__ void __launch_bounds__(COMBINE_THREADS)
     etap_mla_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
                             const int32_t* __restrict__ split_off, int groups, int heads,
-                            float* __restrict__ out, float* __restrict__ lse) {
+                            float* __restrict__ out, float* __restrict__ lse,
+                            unsigned long long* trace) {
+    if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 0] = ptx::global_timer_ns();
     ptx::grid_dep_wait();
+    ptx::grid_dep_launch();  // the next decode step's prologue may overlap this combine
+    if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 1] = ptx::global_timer_ns();
     const int vb = blockIdx.x / HG;
     const int h = blockIdx.x - vb * HG;
     const int b = vb / groups, g = vb - b * groups;
     const int s0 = __ldg(split_off + vb);
     const int ns = __ldg(split_off + vb + 1) - s0;
-    if (ns == 1) return;
+    if (ns == 1) {
+        if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 2] = ptx::global_timer_ns();
+        return;
+    }
     const size_t hrow = static_cast<size_t>(b) * heads + g * HG + h;
     float4* o4 = reinterpret_cast<float4*>(out + hrow * D_V);
     if (ns <= 0) {  // empty context: O = 0, L = -inf
@@ -756,49 +764,50 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
         if (threadIdx.x == 0) lse[hrow] = -INFINITY;
         return;
     }
-    // every warp reduces the split LSEs redundantly (no block barrier): max, then sum of exps
-    const int lane = threadIdx.x & 31;
+    // One round trip after split_off: every thread issues all of its partial loads (one float4
+    // per split, up to COMBINE_BATCH in flight) together with the split LSEs, then merges.
     const float* l_base = ws_lse + static_cast<size_t>(s0) * HG + h;
-    float mx = -INFINITY;
-    for (int s = lane; s < ns; s += 32) mx = fmaxf(mx, __ldg(l_base + static_cast<size_t>(s) * HG));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float sum = 0.f;
-    for (int s = lane; s < ns; s += 32) sum += __expf(__ldg(l_base + static_cast<size_t>(s) * HG) - mx);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const float inv = 1.f / sum;
-    if (threadIdx.x == 0) lse[hrow] = mx + logf(sum);
-    // O = sum_s w_s O_s, 4 independent partial loads in flight per thread
     const float4* p4 = reinterpret_cast<const float4*>(ws_o + (static_cast<size_t>(s0) * HG + h) * D_V) + threadIdx.x;
     const size_t stride4 = static_cast<size_t>(HG) * D_V / 4;
+    float mx = -INFINITY, sum = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int s = 0;
-    for (; s + 4 <= ns; s += 4) {
-        float4 v[4];
-        float w[4];
+    for (int s = 0; s < ns; s += COMBINE_BATCH) {
+        const int n = min(COMBINE_BATCH, ns - s);
+        float4 v[COMBINE_BATCH];
+        float l[COMBINE_BATCH];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            v[j] = __ldg(p4 + (s + j) * stride4);
-            w[j] = __expf(__ldg(l_base + static_cast<size_t>(s + j) * HG) - mx) * inv;
+        for (int j = 0; j < COMBINE_BATCH; ++j) {
+            if (j < n) {
+                v[j] = __ldg(p4 + (s + j) * stride4);
+                l[j] = __ldg(l_base + static_cast<size_t>(s + j) * HG);
+            }
         }
+        // online merge of this batch (same algebra as L = m + log l, etap.cpp:144)
+        float bm = mx;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            acc.x = fmaf(w[j], v[j].x, acc.x);
-            acc.y = fmaf(w[j], v[j].y, acc.y);
-            acc.z = fmaf(w[j], v[j].z, acc.z);
-            acc.w = fmaf(w[j], v[j].w, acc.w);
+        for (int j = 0; j < COMBINE_BATCH; ++j)
+            if (j < n) bm = fmaxf(bm, l[j]);
+        const float corr = __expf(mx - bm);  // 0 on the first batch (mx = -inf)
+        sum *= corr;
+        acc.x *= corr; acc.y *= corr; acc.z *= corr; acc.w *= corr;
+#pragma unroll
+        for (int j = 0; j < COMBINE_BATCH; ++j) {
+            if (j < n) {
+                const float w = __expf(l[j] - bm);
+                sum += w;
+                acc.x = fmaf(w, v[j].x, acc.x);
+                acc.y = fmaf(w, v[j].y, acc.y);
+                acc.z = fmaf(w, v[j].z, acc.z);
+                acc.w = fmaf(w, v[j].w, acc.w);
+            }
         }
+        mx = bm;
     }
-    for (; s < ns; ++s) {
-        const float4 v = __ldg(p4 + s * stride4);
-        const float w = __expf(__ldg(l_base + static_cast<size_t>(s) * HG) - mx) * inv;
-        acc.x = fmaf(w, v.x, acc.x);
-        acc.y = fmaf(w, v.y, acc.y);
-        acc.z = fmaf(w, v.z, acc.z);
-        acc.w = fmaf(w, v.w, acc.w);
-    }
+    const float inv = 1.f / sum;
+    acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+    if (threadIdx.x == 0) lse[hrow] = mx + logf(sum);
     o4[threadIdx.x] = acc;
+    if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 2] = ptx::global_timer_ns();
 }
 
 // =============================================================================================
@@ -937,6 +946,7 @@ int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_row
 
 void* g_trace_buf = nullptr;  // debug tracing target (etap_mla_debug_trace)
 void* g_state_buf = nullptr;  // debug softmax-state dump target (etap_mla_debug_state)
+void* g_combine_trace_buf = nullptr;  // debug: [block][4] stamps of the combine kernel
 int g_state_tiles = 0;
 
 template <typename K>
@@ -948,12 +958,42 @@ int ensure_smem_attr(K kernel, int bytes) {
 int check_device() {
     int dev = 0;
     ETAP_CUDA(cudaGetDevice(&dev));
+    // per-thread cache of verified devices (the attribute queries cost ~1 us per call)
+    thread_local uint64_t verified = 0;
+    if (dev < 64 && (verified >> dev & 1ull)) return ETAP_OK;
     int major = 0, minor = 0;
     ETAP_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
     ETAP_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
     if (major != 10 || minor != 0)
         return fail(ETAP_ERR_CUDA, "etap_mla requires an sm_100 (B200) device, found sm_" +
                                        std::to_string(major) + std::to_string(minor));
+    if (dev < 64) verified |= 1ull << dev;
+    return ETAP_OK;
+}
+
+// Tensor maps are pure functions of (base, rows, box rows); serving loops reuse the same
+// buffers every call, so the last few encodings are cached per thread (encoding costs ~1-2 us).
+struct MapCacheEntry {
+    const void* base = nullptr;
+    uint64_t rows = 0;
+    uint32_t box_rows = 0;
+    CUtensorMap map;
+};
+
+int cached_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_rows) {
+    thread_local MapCacheEntry cache[8];
+    thread_local unsigned next = 0;
+    for (auto& e : cache)
+        if (e.base == base && e.rows == rows && e.box_rows == box_rows) {
+            *map = e.map;
+            return ETAP_OK;
+        }
+    if (int rc = make_map(map, base, rows, box_rows)) return rc;
+    MapCacheEntry& e = cache[next++ % 8];
+    e.base = base;
+    e.rows = rows;
+    e.box_rows = box_rows;
+    e.map = *map;
     return ETAP_OK;
 }
 
@@ -1105,8 +1145,8 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     if (int rc = check_device()) return rc;
 
     CUtensorMap tm_kv, tm_q;
-    if (int rc = make_map(&tm_kv, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, PAGE)) return rc;
-    if (int rc = make_map(&tm_q, q, static_cast<uint64_t>(batch) * heads, HG)) return rc;
+    if (int rc = cached_map(&tm_kv, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, PAGE)) return rc;
+    if (int rc = cached_map(&tm_q, q, static_cast<uint64_t>(batch) * heads, HG)) return rc;
 
     const int groups = heads / HG;
     const size_t np = max_partials(batch, heads, num_sm_parts);
@@ -1173,7 +1213,8 @@ int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_
     cfg2.attrs = attr;
     cfg2.numAttrs = 1;
     ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, static_cast<const float*>(ws_o),
-                                 static_cast<const float*>(ws_lse), split_off, groups, heads, out, lse));
+                                 static_cast<const float*>(ws_lse), split_off, groups, heads, out, lse,
+                                 static_cast<unsigned long long*>(g_combine_trace_buf)));
     return ETAP_OK;
 }
 
@@ -1185,6 +1226,11 @@ int etap_mla_debug_state(void* device_buf, int max_tiles) {
 
 int etap_mla_debug_trace(void* device_buf) {
     g_trace_buf = device_buf;
+    return ETAP_OK;
+}
+
+int etap_mla_debug_trace_combine(void* device_buf) {
+    g_combine_trace_buf = device_buf;
     return ETAP_OK;
 }
 

@@ -1,0 +1,34 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Cross-kernel timeline of consecutive decode steps (K2 + K3) from %globaltimer stamps."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_2506_01969_b200 import _lib, inputs, mla
+
+B, CTX = int(os.environ.get("B", 16)), int(os.environ.get("CTX", 1024))
+inp = inputs.make_mla_inputs([CTX] * B, heads=16, pad_value=0.0)
+plan = mla.MlaDecodePlan.create(B, 16, "cuda")
+n, TT, STEPS = plan.num_sm_parts, 256, 4
+k2 = [torch.zeros(n * TT * 8, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
+k3 = [torch.zeros(B * 16 * 4, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
+L = _lib.lib()
+f = lambda: plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
+for _ in range(5): f()
+torch.cuda.synchronize()
+for i in range(STEPS):  # back to back, a different trace buffer per step
+    L.etap_mla_debug_trace(k2[i].data_ptr())
+    L.etap_mla_debug_trace_combine(k3[i].data_ptr())
+    f()
+L.etap_mla_debug_trace(None); L.etap_mla_debug_trace_combine(None)
+torch.cuda.synchronize()
+t0 = None
+for i in range(STEPS):
+    a = k2[i].view(n, TT, 8).cpu().numpy()[:, TT - 1, :3].astype(np.float64)
+    c = k3[i].view(-1, 4).cpu().numpy()[:, :3].astype(np.float64)
+    c = c[c[:, 2] > 0]
+    if t0 is None: t0 = a[:, 0].min()
+    r = lambda x: (x - t0) / 1e3
+    print(f"step {i}: K2 entry {r(a[:,0].min()):7.2f}..{r(a[:,0].max()):7.2f}  sched-done med {r(np.median(a[:,1])):7.2f}  "
+          f"exit med {r(np.median(a[:,2])):7.2f} max {r(a[:,2].max()):7.2f} | K3 entry min {r(c[:,0].min()):7.2f} "
+          f"wait-release min {r(c[:,1].min()):7.2f} exit max {r(c[:,2].max()):7.2f}")
