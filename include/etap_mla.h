@@ -44,8 +44,8 @@ extern "C" {
 #define ETAP_MLA_D_QK 576
 #define ETAP_MLA_D_V 512
 #define ETAP_MLA_PAGE_ROWS 64
-#define ETAP_MLA_TILE_ROWS 128     /* KV rows per UMMA tile (M of S^T = K Q^T) */
-#define ETAP_MLA_HEAD_GROUP 16     /* heads per CTA work unit (N of both UMMAs) */
+#define ETAP_MLA_TILE_ROWS 64      /* KV rows per pipeline tile (M of S^T = K Q^T) */
+#define ETAP_MLA_HEAD_GROUP 16     /* minimum heads per CTA work unit (see etap_mla_head_group) */
 #define ETAP_MLA_SCHED_INTS 8      /* int32 per CTA in the schedule */
 
 #define ETAP_OK 0
@@ -62,10 +62,11 @@ extern "C" {
 #define ETAP_FLAG_SKIP_COMBINE 4u   /* launch K2 only; the caller runs etap_mla_combine (used to
                                        time K2 alone) */
 #define ETAP_FLAG_EXTERNAL_SCHEDULE 8u /* read sched / split_off produced by etap_mla_metadata.
-                                       Without it (and when batch*heads/16 <= 256) K2 computes
-                                       the same schedule in its prologue and writes it to
-                                       sched / split_off, so K1 is off the per-step critical
-                                       path; above 256 virtual sequences K1 is required. */
+                                       Without it K2 computes the same schedule in its
+                                       prologue and writes it to sched / split_off when
+                                       batch*heads/head_group <= 256 (K1 off the per-step
+                                       critical path); above 256 virtual sequences
+                                       etap_mla_decode launches K1 itself first. */
 
 /* Thread-local description of the last error. Never NULL. */
 const char* etap_mla_last_error(void);
@@ -73,12 +74,17 @@ const char* etap_mla_last_error(void);
 /* Library build identification (for the driver's "which .so was loaded" evidence). */
 const char* etap_mla_version(void);
 
+/* Heads per CTA work unit the library uses for `heads` query heads: 32 when heads is a
+ * multiple of 32 (N = 32 / 64 UMMAs), else 16 (ETAP_HEAD_GROUP=16 in the environment forces
+ * 16). Sizes below, the split_off layout and the debug state dump follow it. */
+int etap_mla_head_group(int heads, int* head_group);
+
 /* Number of persistent CTAs the decode kernel uses on `device` (= its SM count). */
 int etap_mla_num_sm_parts(int device, int* num_sm_parts);
 
 /* Sizes of the caller-owned scratch buffers.
  *   sched     : num_sm_parts * ETAP_MLA_SCHED_INTS int32
- *   split_off : batch * heads/16 + 1 int32
+ *   split_off : batch * heads/head_group + 1 int32
  *   workspace : bytes for split-KV partial O / LSE */
 int etap_mla_sched_ints(int batch, int heads, int num_sm_parts, size_t* sched_ints,
                         size_t* split_off_ints);
@@ -86,7 +92,7 @@ int etap_mla_workspace_bytes(int batch, int heads, int num_sm_parts, size_t* byt
 
 /* K1 — split-KV work scheduler (no reference analog: run_etap streams every KV block in one
  * serial loop, etap.cpp:122-129, kv_block_count tiled_standard.cpp:21-23). Integer partition
- * of the (sequence, head-group, 128-row tile) space over num_sm_parts persistent CTAs. */
+ * of the (sequence, head-group, 64-row tile) space over num_sm_parts persistent CTAs. */
 int etap_mla_metadata(const int32_t* seqlens /*device [batch]*/, int batch, int heads,
                       int num_sm_parts, int32_t* sched /*device*/, int32_t* split_off /*device*/,
                       void* stream);
@@ -135,8 +141,9 @@ int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t
                           double* l);
 
 /* UMMA descriptor self-test (one CTA, one tile): S^T = K Q^T and O^T = V^T P^T through the
- * same smem layouts as the decode kernel. Device pointers: k [128][576] bf16, q [16][576]
- * bf16, p [128][16] fp32; outputs s_t [128][16] fp32, o_t [512][16] fp32. */
+ * same smem layouts as the 16-head decode kernel. Device pointers: k [64][576] bf16,
+ * q [16][576] bf16, p [64][16] fp32; outputs s_t [64][16] fp32, o_t [512][32] fp32 (columns
+ * 0-15 = V^T P_hi, 16-31 = V^T P_lo). */
 int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* s_t, float* o_t,
                            void* stream);
 

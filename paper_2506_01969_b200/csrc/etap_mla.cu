@@ -320,19 +320,22 @@ __device__ __forceinline__ bool split_at(const int32_t* sch, int seqlen, int gro
     return d.t0 < d.t1;
 }
 
+template <int HG_>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     etap_mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv,
                            const __grid_constant__ CUtensorMap tm_q, const DecodeParams prm) {
+    using C = Cfg<HG_>;
+    constexpr int HG = C::HG, HH = C::HH;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) ETAP_TRACE(prm, TRACE_TILES - 1, 0);
 
-    // ---- prologue (overlaps the scheduler kernel under PDL)
+    // ---- prologue (overlaps the previous kernel under programmatic dependent launch)
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tm_kv);
         ptx::prefetch_tmap(&tm_q);
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         ptx::fence_mbar_init();
     }
-    if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
     // (no ring zero-fill: every row a GEMM reads was written by a full-page TMA box of the
     // same tile; garbage rows past seqlen are zeroed by the softmax warps before GEMM2)
     ptx::tc_fence_before();
@@ -363,7 +366,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::grid_dep_launch();   // let the combine kernel get scheduled
     const int32_t* sch;
     const int32_t* soff;      // split offsets per virtual sequence
-    int* s_pref = reinterpret_cast<int*>(smem + OFF_SCHED);
+    int* s_pref = reinterpret_cast<int*>(smem + C::OFF_SCHED);
     int* s_soff = s_pref + MAX_FUSED_VB + 1;
     int* s_tiles = s_soff + MAX_FUSED_VB + 1;
     int* s_len = s_tiles + MAX_FUSED_VB;
@@ -386,27 +389,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     const int vb_begin = sch[0], vb_end = sch[2];
     const int G = prm.groups;
-    const uint32_t ring_addr = ptx::smem_u32(smem + OFF_RING);
-    const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q);
-    const uint32_t p_addr = ptx::smem_u32(smem + OFF_P);
+    const uint32_t ring_addr = ptx::smem_u32(smem + C::OFF_RING);
+    const uint32_t q_addr = ptx::smem_u32(smem + C::OFF_Q);
+    const uint32_t p_addr = ptx::smem_u32(smem + C::OFF_P);
+    auto seqlen_of = [&](int vb) { return fused ? s_len[vb] : max(0, prm.seqlens[vb / G]); };
 
     if (warp == 0) {
         // ===================================================== TMA producer (whole warp)
-        // Tile gt occupies ring positions [9gt, 9gt+9); positions 0..5 reuse slots of tile
-        // gt-3, positions 6..8 slots of tile gt-2, so two waits on "GEMM2 done" per tile.
+        // Tile gt occupies ring positions [9gt, 9gt+9); positions [0, SPLIT_POS) reuse slots
+        // of tile gt-3, the rest slots of tile gt-2: two waits on "GEMM2 done" per tile.
         const uint64_t pol_kv = ptx::policy_evict_first();
         const uint64_t pol_q = ptx::policy_evict_last();
         uint32_t gt = 0, nsplit = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, fused ? s_len[vb] : max(0, prm.seqlens[vb / G]), G, vb, sd)) continue;
+            if (!split_at(sch, seqlen_of(vb), G, vb, sd)) continue;
             if (nsplit > 0) ptx::mbar_wait(&bars[BAR_Q_EMPTY], (nsplit - 1) & 1);
             if (lane == 0) {
-                ptx::mbar_arrive_expect_tx(&bars[BAR_Q_FULL], Q_BYTES);
+                ptx::mbar_arrive_expect_tx(&bars[BAR_Q_FULL], C::Q_BYTES);
                 const int qrow = sd.b * prm.heads + sd.g * HG;
 #pragma unroll 1
                 for (int c = 0; c < NCHUNK; ++c)
-                    ptx::tma_load_2d(smem + OFF_Q + c * Q_CHUNK_BYTES, &tm_q, &bars[BAR_Q_FULL],
+                    ptx::tma_load_2d(smem + C::OFF_Q + c * C::Q_CHUNK_BYTES, &tm_q, &bars[BAR_Q_FULL],
                                      c * 64, qrow, pol_q);
             }
             __syncwarp();
@@ -421,28 +425,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
                 const int page = __shfl_sync(0xffffffffu, pg, t - base);
                 const uint32_t tb = gt % NTB;
-                const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
+                const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
                 if (gt >= 3) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 3) % NTB], ((gt - 3) / NTB) & 1);
                 if (lane == 0) {
                     ETAP_TRACE(prm, gt, 0);
-                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_A + tb], SPLIT_POS * SLOT_BYTES);
+                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_A + tb], C::SPLIT_POS * SLOT_BYTES);
 #pragma unroll 1
-                    for (int pos = 0; pos < SPLIT_POS; ++pos) {
-                        const uint32_t s = (pos0 + pos) % NSLOT;
-                        ptx::tma_load_2d(smem + OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_A + tb],
+                    for (int pos = 0; pos < C::SPLIT_POS; ++pos) {
+                        const uint32_t s = (pos0 + pos) % C::NSLOT;
+                        ptx::tma_load_2d(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_A + tb],
                                          chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
                     }
                 }
                 __syncwarp();
-                // positions 6..8 reuse tile gt-2's positions 0..2 = {V0,V1,V2} (even gt) or
-                // {rope,V0,V1} (odd gt): free once GEMM2 d-blocks 0-1 of tile gt-2 completed
-                if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_HALF + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+                // the remaining positions reuse tile gt-2's first 9 - SPLIT_POS positions: with
+                // the 24-slot ring those are {V0,V1,V2} or {rope,V0,V1}, free once GEMM2
+                // d-blocks 0-1 of tile gt-2 completed; otherwise wait for the whole GEMM2
+                if (gt >= 2)
+                    ptx::mbar_wait(&bars[(C::EARLY_HALF ? BAR_G2_HALF : BAR_G2_DONE) + (gt - 2) % NTB],
+                                   ((gt - 2) / NTB) & 1);
                 if (lane == 0) {
-                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_B + tb], (NCHUNK - SPLIT_POS) * SLOT_BYTES);
+                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_B + tb], (NCHUNK - C::SPLIT_POS) * SLOT_BYTES);
 #pragma unroll 1
-                    for (int pos = SPLIT_POS; pos < NCHUNK; ++pos) {
-                        const uint32_t s = (pos0 + pos) % NSLOT;
-                        ptx::tma_load_2d(smem + OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_B + tb],
+                    for (int pos = C::SPLIT_POS; pos < NCHUNK; ++pos) {
+                        const uint32_t s = (pos0 + pos) % C::NSLOT;
+                        ptx::tma_load_2d(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_B + tb],
                                          chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
                     }
                     ETAP_TRACE(prm, gt, 1);
@@ -456,21 +463,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t gt = 0, nsplit = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, fused ? s_len[vb] : max(0, prm.seqlens[vb / G]), G, vb, sd)) continue;
+            if (!split_at(sch, seqlen_of(vb), G, vb, sd)) continue;
             ptx::mbar_wait(&bars[BAR_Q_FULL], nsplit & 1);
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
+                const uint32_t s_tmem = tmem_base + C::TCOL_S + HG * buf;
                 if (gt >= 2) ptx::mbar_wait(&bars[BAR_S_FREE + buf], ((gt >> 1) - 1) & 1);
-                const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
+                const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
                 ptx::mbar_wait(&bars[BAR_FULL_A + gt % NTB], (gt / NTB) & 1);
                 __syncwarp();
                 ptx::tc_fence_after();
-                issue_gemm1_tile<0, SPLIT_POS>(tmem_base + TCOL_S + 16 * buf, ring_addr, q_addr, pos0, gt);
+                issue_gemm1_tile<C, 0, C::SPLIT_POS>(s_tmem, ring_addr, q_addr, pos0, gt);
                 ptx::mbar_wait(&bars[BAR_FULL_B + gt % NTB], (gt / NTB) & 1);
                 __syncwarp();
                 ptx::tc_fence_after();
                 ETAP_TRACE(prm, gt, 2);
-                issue_gemm1_tile<SPLIT_POS, NCHUNK>(tmem_base + TCOL_S + 16 * buf, ring_addr, q_addr, pos0, gt);
+                issue_gemm1_tile<C, C::SPLIT_POS, NCHUNK>(s_tmem, ring_addr, q_addr, pos0, gt);
                 ptx::umma_commit_elect(&bars[BAR_S_FULL + buf]);
                 ETAP_TRACE(prm, gt, 3);
                 if (t == sd.t1 - 1) ptx::umma_commit_elect(&bars[BAR_Q_EMPTY]);
@@ -483,20 +491,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t gt = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, fused ? s_len[vb] : max(0, prm.seqlens[vb / G]), G, vb, sd)) continue;
+            if (!split_at(sch, seqlen_of(vb), G, vb, sd)) continue;
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
                 ptx::mbar_wait(&bars[BAR_P_FULL + buf], (gt >> 1) & 1);
                 __syncwarp();
                 ptx::tc_fence_after();
                 ETAP_TRACE(prm, gt, 6);
-                const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
+                const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
 #pragma unroll
                 for (int blk = 0; blk < 4; ++blk) {
                     uint32_t sa = pos0 + pos_of_chunk(2 * blk, gt);
-                    sa = sa >= NSLOT ? sa - NSLOT : sa;
-                    issue_gemm2_block(tmem_base + TCOL_O + 32 * blk, ring_addr + sa * SLOT_BYTES,
-                                      p_addr + buf * P_BYTES, t == sd.t0);
+                    sa = sa >= C::NSLOT ? sa - C::NSLOT : sa;
+                    issue_gemm2_block<C>(tmem_base + C::TCOL_O + C::OBLK * blk, ring_addr + sa * SLOT_BYTES,
+                                         p_addr + buf * C::P_BYTES, t == sd.t0);
                     if (blk == 1) ptx::umma_commit_elect(&bars[BAR_G2_HALF + gt % NTB]);
                 }
                 ptx::umma_commit_elect(&bars[BAR_G2_DONE + gt % NTB]);
@@ -506,153 +514,155 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp >= SOFTMAX_WARP0) {
         // ===================================================== softmax + epilogue (128 threads)
-        // thread = (KV row, head half): lane l of warp q owns row 16q + l%16, heads 8*(l/16)..+7
+        // thread = (KV row, head half): lane l of warp q owns row 16q + l%16, heads HH*(l/16)..
         const int wq = warp & 3;               // TMEM lane quadrant accessible by this warp
         const int half = lane >> 4;
         const int row = s_row_of(wq, lane);    // KV row in the tile
         const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
-        float* red_max = reinterpret_cast<float*>(smem + OFF_RED);  // [2][4][16]
-        float* red_sum = red_max + 128;                               // [4][16]
+        float* red_max = reinterpret_cast<float*>(smem + C::OFF_RED);  // [2][4][HG]
+        float* red_sum = red_max + 8 * HG;                               // [4][HG]
+        float* s_m = red_sum + 4 * HG;         // [HG] running max per head (log2 units)
+        float* s_alpha = s_m + HG;             // [HG] rescale factors of the current tile
         const bool negate = prm.flags & FLAG_NEGATE_RESCALE;
         const bool eager = negate || (prm.flags & FLAG_EAGER_RESCALE);
         const float thresh = eager ? 0.f : LAZY_RESCALE_LOG2;
         const bool tracer = (threadIdx.x == SOFTMAX_WARP0 * 32);
+        const bool head_owner = wq == 0 && (lane & 15) == 0;  // writes s_m / s_alpha of its half
+        const int rhead = halfwarp_reduce_head<HH>(lane);   // head (of the half) a reduction leaves here
+        const bool rwriter = HH == 16 || (lane & 1) == 0;
         uint32_t gt = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, fused ? s_len[vb] : max(0, prm.seqlens[vb / G]), G, vb, sd)) continue;
-            float m_used[16];   // running max per head (log2 units), replicated in all threads
-            float l_part[8];    // partial column sums of this thread's rows, own 8 heads
-            float dbg_l = 0.f;  // debug state dump: running column sum of one head
+            if (!split_at(sch, seqlen_of(vb), G, vb, sd)) continue;
+            float m_own[HH];    // running max of this thread's heads (log2 units)
+            float l_part[HH];   // partial column sums of this thread's rows, own heads
+            float dbg_l = 0.f;  // debug state dump: running column sum of head `lane`
 #pragma unroll
-            for (int h = 0; h < 16; ++h) m_used[h] = -INFINITY;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) l_part[j] = 0.f;
+            for (int j = 0; j < HH; ++j) {
+                m_own[j] = -INFINITY;
+                l_part[j] = 0.f;
+            }
 
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
                 ptx::mbar_wait(&bars[BAR_S_FULL + buf], (gt >> 1) & 1);
                 ptx::tc_fence_after();
                 if (tracer) ETAP_TRACE(prm, gt, 4);
-                uint32_t sr[8];
-                ptx::tmem_ld16x2_8(t_lane + TCOL_S + 16 * buf, sr);
+                uint32_t sr[HH];
+                ptx::tmem_ld16x2<HH>(t_lane + C::TCOL_S + HG * buf, sr);
                 ptx::tmem_wait_ld();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&bars[BAR_S_FREE + buf]);
 
                 const int grow = t * TILE + row;
                 const bool valid = grow < sd.seqlen;
-                float x[8], mu[8];
+                float x[HH];
                 bool exceed = false;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    mu[j] = half ? m_used[8 + j] : m_used[j];
+                for (int j = 0; j < HH; ++j) {
                     x[j] = valid ? __uint_as_float(sr[j]) * prm.scale_log2 : -INFINITY;
-                    exceed |= x[j] > mu[j] + thresh;
+                    exceed |= x[j] > m_own[j] + thresh;
                 }
                 const bool first = (t == sd.t0);
+                const bool debug = prm.state != nullptr && t < prm.state_tiles;
+                const float dbg_m_old = (debug && wq == 0 && lane < HG && !first) ? s_m[lane] : -INFINITY;
                 // one barrier decides, CTA-uniformly, whether any running max must move
                 const bool any = ptx::bar_red_or(1, 128, exceed || (negate && !first));
                 bool need_rescale = false;
-                float alpha[16], m_prev[16];
+                float alpha_own[HH];
 #pragma unroll
-                for (int h = 0; h < 16; ++h) {
-                    alpha[h] = 1.f;
-                    m_prev[h] = m_used[h];
-                }
+                for (int j = 0; j < HH; ++j) alpha_own[j] = first ? 0.f : 1.f;
                 if (any) {
-                    const float wm = halfwarp_reduce8<true>(x, lane);
-                    float* rm = red_max + (gt & 1) * 64;
-                    if ((lane & 1) == 0) rm[wq * 16 + half * 8 + ((lane & 15) >> 1)] = wm;
+                    const float wm = halfwarp_reduce<true, HH>(x, lane);
+                    float* rm = red_max + (gt & 1) * 4 * HG;
+                    if (rwriter) rm[wq * HG + half * HH + rhead] = wm;
                     ptx::named_bar_sync(2, 128);
+                    bool upd = false;
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        const float4 a = reinterpret_cast<const float4*>(rm)[q4];
-                        const float4 b = reinterpret_cast<const float4*>(rm + 16)[q4];
-                        const float4 c = reinterpret_cast<const float4*>(rm + 32)[q4];
-                        const float4 d = reinterpret_cast<const float4*>(rm + 48)[q4];
-                        const float mt[4] = {fmaxf(fmaxf(a.x, b.x), fmaxf(c.x, d.x)),
-                                             fmaxf(fmaxf(a.y, b.y), fmaxf(c.y, d.y)),
-                                             fmaxf(fmaxf(a.z, b.z), fmaxf(c.z, d.z)),
-                                             fmaxf(fmaxf(a.w, b.w), fmaxf(c.w, d.w))};
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int h = 4 * q4 + j;
-                            if (first) {
-                                m_used[h] = mt[j];
-                            } else {
-                                const float mn = fmaxf(m_used[h], mt[j]);
-                                if (mn > m_used[h] + thresh) {
-                                    alpha[h] = exp2f(m_used[h] - mn);
-                                    m_used[h] = mn;
-                                    need_rescale = true;
-                                }
+                    for (int j = 0; j < HH; ++j) {
+                        const int h = half * HH + j;
+                        const float mt = fmaxf(fmaxf(rm[h], rm[HG + h]), fmaxf(rm[2 * HG + h], rm[3 * HG + h]));
+                        if (first) {
+                            m_own[j] = mt;
+                        } else {
+                            const float mn = fmaxf(m_own[j], mt);
+                            if (mn > m_own[j] + thresh) {
+                                alpha_own[j] = exp2f(m_own[j] - mn);
+                                m_own[j] = mn;
+                                upd = true;
                             }
                         }
                     }
-                    if (negate && !first) need_rescale = true;
+                    // CTA-uniform decision (also orders all reads of s_m before the writes below)
+                    need_rescale = ptx::bar_red_or(2, 128, upd) || (negate && !first);
+                    if (head_owner) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) mu[j] = half ? m_used[8 + j] : m_used[j];
+                        for (int j = 0; j < HH; ++j) {
+                            s_m[half * HH + j] = m_own[j];
+                            s_alpha[half * HH + j] = alpha_own[j];
+                        }
+                    }
                 }
-                float pv[8];
+                float pv[HH];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    pv[j] = exp2f(x[j] - mu[j]);
-                    const float aj = half ? alpha[8 + j] : alpha[j];
-                    l_part[j] = first ? pv[j] : fmaf(l_part[j], aj, pv[j]);
+                for (int j = 0; j < HH; ++j) {
+                    pv[j] = exp2f(x[j] - m_own[j]);
+                    l_part[j] = first ? pv[j] : fmaf(l_part[j], alpha_own[j], pv[j]);
                 }
-                if (prm.state != nullptr && t < prm.state_tiles) {
-                    // debug (BlockHook replay): column sums of this tile's P, running l, m, rescale
-                    // in natural-log units, as BlockStepInfo carries them (tiled_standard.hpp:32-40)
-                    const float cs = halfwarp_reduce8<false>(pv, lane);
-                    if ((lane & 1) == 0) red_sum[wq * 16 + half * 8 + ((lane & 15) >> 1)] = cs;
+                if (debug) {
+                    // BlockHook replay: column sums of this tile's P, running l, m, rescale in
+                    // natural-log units, as BlockStepInfo carries them (tiled_standard.hpp:32-40)
+                    const float cs = halfwarp_reduce<false, HH>(pv, lane);
+                    if (rwriter) red_sum[wq * HG + half * HH + rhead] = cs;
                     ptx::named_bar_sync(2, 128);
-                    if (wq == 0 && lane < 16) {
-                        float colsum = red_sum[lane] + red_sum[16 + lane] + red_sum[32 + lane] + red_sum[48 + lane];
-                        float mo = 0.f, mn = 0.f, al = 1.f;
-#pragma unroll
-                        for (int h = 0; h < 16; ++h)
-                            if (h == lane) { mo = m_prev[h]; mn = m_used[h]; al = first ? 0.f : alpha[h]; }
+                    if (wq == 0 && lane < HG) {
+                        const float colsum = red_sum[lane] + red_sum[HG + lane] + red_sum[2 * HG + lane] +
+                                             red_sum[3 * HG + lane];
+                        const float mn = s_m[lane];
+                        const float al = first ? 0.f : (any ? s_alpha[lane] : 1.f);
                         dbg_l = first ? colsum : fmaf(dbg_l, al, colsum);
-                        float* st = prm.state + (static_cast<size_t>(vb) * prm.state_tiles + t) * 64;
-                        st[lane] = mo * 0.69314718055994530942f;
-                        st[16 + lane] = mn * 0.69314718055994530942f;
-                        st[32 + lane] = al;
-                        st[48 + lane] = dbg_l;
+                        float* st = prm.state + (static_cast<size_t>(vb) * prm.state_tiles + t) * 4 * HG;
+                        st[lane] = dbg_m_old * 0.69314718055994530942f;
+                        st[HG + lane] = mn * 0.69314718055994530942f;
+                        st[2 * HG + lane] = al;
+                        st[3 * HG + lane] = dbg_l;
                     }
                     ptx::named_bar_sync(2, 128);
                 }
                 // the P buffer is reused every other tile: GEMM2(gt-2) must have read it
                 if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
                 if (need_rescale) {
-                    // O^T must contain GEMM2(gt-1) before it is rescaled
+                    // O^T must contain GEMM2(gt-1) before it is rescaled; s_alpha written above
+                    ptx::named_bar_sync(2, 128);
                     ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 1) % NTB], ((gt - 1) / NTB) & 1);
                     ptx::tc_fence_after();
 #pragma unroll 1
                     for (int blk = 0; blk < 4; ++blk) {
-                        uint32_t o[32];
-                        const uint32_t ta = t_lane + TCOL_O + 32 * blk;
-                        ptx::tmem_ld32(ta, o);
-                        ptx::tmem_wait_ld();
 #pragma unroll
-                        for (int h = 0; h < 16; ++h) {
-                            const float a = negate ? -alpha[h] : alpha[h];
-                            o[h] = __float_as_uint(__uint_as_float(o[h]) * a);
-                            o[16 + h] = __float_as_uint(__uint_as_float(o[16 + h]) * a);
+                        for (int part = 0; part < static_cast<int>(C::OBLK) / 32; ++part) {
+                            uint32_t o[32];
+                            const uint32_t ta = t_lane + C::TCOL_O + C::OBLK * blk + 32 * part;
+                            ptx::tmem_ld32(ta, o);
+                            ptx::tmem_wait_ld();
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) {
+                                const float a = s_alpha[(32 * part + c) % HG];
+                                o[c] = __float_as_uint(__uint_as_float(o[c]) * (negate ? -a : a));
+                            }
+                            ptx::tmem_st32(ta, o);
                         }
-                        ptx::tmem_st32(ta, o);
                     }
                     ptx::tmem_wait_st();
                 }
-                write_p_hilo8(smem + OFF_P + buf * P_BYTES, row, half, pv);
+                write_p_hilo<C>(smem + C::OFF_P + buf * C::P_BYTES, row, half, pv);
                 // rows of the last page past seqlen were loaded from HBM and may hold
                 // non-finite garbage; zero them in the V chunks (0 * NaN = NaN in the MMA)
                 if (grow >= sd.seqlen) {
-                    const uint32_t pos0 = (gt * NCHUNK) % NSLOT;
+                    const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
 #pragma unroll 1
                     for (int c = half * 4; c < half * 4 + 4; ++c) {
-                        const uint32_t s = (pos0 + pos_of_chunk(c, gt)) % NSLOT;
-                        uint4* dst = reinterpret_cast<uint4*>(smem + OFF_RING + s * SLOT_BYTES + row * 128);
+                        const uint32_t s = (pos0 + pos_of_chunk(c, gt)) % C::NSLOT;
+                        uint4* dst = reinterpret_cast<uint4*>(smem + C::OFF_RING + s * SLOT_BYTES + row * 128);
 #pragma unroll
                         for (int j = 0; j < 8; ++j) dst[j] = make_uint4(0, 0, 0, 0);
                     }
@@ -670,15 +680,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t last = gt - 1;
             ptx::mbar_wait(&bars[BAR_G2_DONE + last % NTB], (last / NTB) & 1);
             ptx::tc_fence_after();
-            const float wsum = halfwarp_reduce8<false>(l_part, lane);
-            if ((lane & 1) == 0) red_sum[wq * 16 + half * 8 + ((lane & 15) >> 1)] = wsum;
+            const float wsum = halfwarp_reduce<false, HH>(l_part, lane);
+            if (rwriter) red_sum[wq * HG + half * HH + rhead] = wsum;
             ptx::named_bar_sync(2, 128);
-            float inv_l[16], l_tot[16];
+            float inv_l[HG];
 #pragma unroll
-            for (int h = 0; h < 16; ++h) {
-                l_tot[h] = red_sum[h] + red_sum[16 + h] + red_sum[32 + h] + red_sum[48 + h];
-                inv_l[h] = 1.f / l_tot[h];
-            }
+            for (int h = 0; h < HG; ++h)
+                inv_l[h] = 1.f / (red_sum[h] + red_sum[HG + h] + red_sum[2 * HG + h] + red_sum[3 * HG + h]);
             const int ns = soff[vb + 1] - soff[vb];
             const int idx = (vb == sch[0]) ? sch[4] : soff[vb];  // partial index (ns > 1)
             float* dst;
@@ -694,23 +702,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int drow = wq * 32 + lane;  // M=128 layout: d row = TMEM lane
 #pragma unroll 1
             for (int blk = 0; blk < 4; ++blk) {
-                uint32_t o[32];
-                ptx::tmem_ld32(t_lane + TCOL_O + 32 * blk, o);
+                uint32_t o[2 * HG];
+#pragma unroll
+                for (int part = 0; part < 2 * HG / 32; ++part)
+                    ptx::tmem_ld32(t_lane + C::TCOL_O + C::OBLK * blk + 32 * part,
+                                   *reinterpret_cast<uint32_t(*)[32]>(o + 32 * part));
                 ptx::tmem_wait_ld();
                 const int d = blk * 128 + drow;
 #pragma unroll
-                for (int h = 0; h < 16; ++h)
-                    dst[h * D_V + d] = (__uint_as_float(o[h]) + __uint_as_float(o[16 + h])) * inv_l[h];
+                for (int h = 0; h < HG; ++h)
+                    dst[h * D_V + d] = (__uint_as_float(o[h]) + __uint_as_float(o[HG + h])) * inv_l[h];
             }
-            if (wq == 0 && lane < 16) {
-                float v = 0.f;
-#pragma unroll
-                for (int h = 0; h < 16; ++h)
-                    if (h == lane) v = (m_used[h] + log2f(l_tot[h])) * 0.69314718055994530942f;
-                dst_lse[lane] = v;
+            if (wq == 0 && lane < HG) {
+                const float l = red_sum[lane] + red_sum[HG + lane] + red_sum[2 * HG + lane] + red_sum[3 * HG + lane];
+                dst_lse[lane] = (s_m[lane] + log2f(l)) * 0.69314718055994530942f;
             }
             ptx::tc_fence_before();
-            // red_sum is rewritten by the next split's epilogue only after this barrier
+            // red_sum / s_m are rewritten by the next split only after this barrier
             ptx::named_bar_sync(2, 128);
         }
     }
@@ -727,7 +735,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+        ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
     }
 }
 
@@ -741,15 +749,15 @@ constexpr int COMBINE_BATCH = 16;  // partial float4 loads in flight per thread
 
 __global__ void __launch_bounds__(COMBINE_THREADS)
     etap_mla_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
-                            const int32_t* __restrict__ split_off, int groups, int heads,
+                            const int32_t* __restrict__ split_off, int hg, int groups, int heads,
                             float* __restrict__ out, float* __restrict__ lse,
                             unsigned long long* trace) {
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 0] = ptx::global_timer_ns();
     ptx::grid_dep_wait();
     ptx::grid_dep_launch();  // the next decode step's prologue may overlap this combine
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 1] = ptx::global_timer_ns();
-    const int vb = blockIdx.x / HG;
-    const int h = blockIdx.x - vb * HG;
+    const int vb = blockIdx.x / hg;
+    const int h = blockIdx.x - vb * hg;
     const int b = vb / groups, g = vb - b * groups;
     const int s0 = __ldg(split_off + vb);
     const int ns = __ldg(split_off + vb + 1) - s0;
@@ -757,7 +765,7 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
         if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 2] = ptx::global_timer_ns();
         return;
     }
-    const size_t hrow = static_cast<size_t>(b) * heads + g * HG + h;
+    const size_t hrow = static_cast<size_t>(b) * heads + g * hg + h;
     float4* o4 = reinterpret_cast<float4*>(out + hrow * D_V);
     if (ns <= 0) {  // empty context: O = 0, L = -inf
         o4[threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -766,9 +774,9 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
     }
     // One round trip after split_off: every thread issues all of its partial loads (one float4
     // per split, up to COMBINE_BATCH in flight) together with the split LSEs, then merges.
-    const float* l_base = ws_lse + static_cast<size_t>(s0) * HG + h;
-    const float4* p4 = reinterpret_cast<const float4*>(ws_o + (static_cast<size_t>(s0) * HG + h) * D_V) + threadIdx.x;
-    const size_t stride4 = static_cast<size_t>(HG) * D_V / 4;
+    const float* l_base = ws_lse + static_cast<size_t>(s0) * hg + h;
+    const float4* p4 = reinterpret_cast<const float4*>(ws_o + (static_cast<size_t>(s0) * hg + h) * D_V) + threadIdx.x;
+    const size_t stride4 = static_cast<size_t>(hg) * D_V / 4;
     float mx = -INFINITY, sum = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < ns; s += COMBINE_BATCH) {
@@ -779,7 +787,7 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
         for (int j = 0; j < COMBINE_BATCH; ++j) {
             if (j < n) {
                 v[j] = __ldg(p4 + (s + j) * stride4);
-                l[j] = __ldg(l_base + static_cast<size_t>(s + j) * HG);
+                l[j] = __ldg(l_base + static_cast<size_t>(s + j) * hg);
             }
         }
         // online merge of this batch (same algebra as L = m + log l, etap.cpp:144)
@@ -818,32 +826,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     etap_mla_selftest_kernel(const __grid_constant__ CUtensorMap tm_k,
                              const __grid_constant__ CUtensorMap tm_q, const float* p_in,
                              float* s_out, float* o_out) {
+    using C = Cfg<16>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         ptx::mbar_init(&bars[0], 1);
         ptx::mbar_init(&bars[1], 1);
         ptx::fence_mbar_init();
     }
-    if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const uint32_t ring_addr = ptx::smem_u32(smem + OFF_RING);
-    const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q);
-    const uint32_t p_addr = ptx::smem_u32(smem + OFF_P);
+    const uint32_t ring_addr = ptx::smem_u32(smem + C::OFF_RING);
+    const uint32_t q_addr = ptx::smem_u32(smem + C::OFF_Q);
+    const uint32_t p_addr = ptx::smem_u32(smem + C::OFF_P);
 
     if (threadIdx.x == 0) {
         const uint64_t pol = ptx::policy_evict_first();
-        ptx::mbar_arrive_expect_tx(&bars[0], NCHUNK * SLOT_BYTES + Q_BYTES);
+        ptx::mbar_arrive_expect_tx(&bars[0], NCHUNK * SLOT_BYTES + C::Q_BYTES);
         for (int c = 0; c < NCHUNK; ++c) {  // chunk c in slot c
-            ptx::tma_load_2d(smem + OFF_RING + c * SLOT_BYTES, &tm_k, &bars[0], c * 64, 0, pol);
-            ptx::tma_load_2d(smem + OFF_Q + c * Q_CHUNK_BYTES, &tm_q, &bars[0], c * 64, 0, pol);
+            ptx::tma_load_2d(smem + C::OFF_RING + c * SLOT_BYTES, &tm_k, &bars[0], c * 64, 0, pol);
+            ptx::tma_load_2d(smem + C::OFF_Q + c * C::Q_CHUNK_BYTES, &tm_q, &bars[0], c * 64, 0, pol);
         }
     }
     // P = hi + lo of the input, written by the softmax warps exactly as the decode kernel does
@@ -851,7 +860,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int row = s_row_of(warp & 3, lane), half = lane >> 4;
         float p[8];
         for (int j = 0; j < 8; ++j) p[j] = p_in[row * 16 + half * 8 + j];
-        write_p_hilo8(smem + OFF_P, row, half, p);
+        write_p_hilo<C>(smem + C::OFF_P, row, half, p);
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
@@ -859,9 +868,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_wait(&bars[0], 0);
         __syncwarp();
         ptx::tc_fence_after();
-        issue_gemm1_tile<0, NCHUNK>(tmem_base + TCOL_S, ring_addr, q_addr, 0, 0);  // tile 0: chunk c in slot c
+        issue_gemm1_tile<C, 0, NCHUNK>(tmem_base + C::TCOL_S, ring_addr, q_addr, 0, 0);  // tile 0: chunk c in slot c
         for (int blk = 0; blk < 4; ++blk)
-            issue_gemm2_block(tmem_base + TCOL_O + 32 * blk, ring_addr + (2 * blk) * SLOT_BYTES,
+            issue_gemm2_block<C>(tmem_base + C::TCOL_O + C::OBLK * blk, ring_addr + (2 * blk) * SLOT_BYTES,
                               p_addr, true);
         ptx::umma_commit_elect(&bars[1]);
     }
@@ -871,14 +880,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int wq = warp & 3;
         const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
         uint32_t r[32];
-        ptx::tmem_ld16x2_8(t_lane + TCOL_S, *reinterpret_cast<uint32_t(*)[8]>(r));
-        ptx::tmem_wait_ld();
         {
+            uint32_t sr[8];
+            ptx::tmem_ld16x2<8>(t_lane + C::TCOL_S, sr);
+            ptx::tmem_wait_ld();
             const int row = s_row_of(wq, lane), half = lane >> 4;
-            for (int j = 0; j < 8; ++j) s_out[row * 16 + half * 8 + j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 8; ++j) s_out[row * 16 + half * 8 + j] = __uint_as_float(sr[j]);
         }
         for (int blk = 0; blk < 4; ++blk) {
-            ptx::tmem_ld32(t_lane + TCOL_O + 32 * blk, r);
+            ptx::tmem_ld32(t_lane + C::TCOL_O + C::OBLK * blk, r);
             ptx::tmem_wait_ld();
             for (int n = 0; n < 32; ++n)
                 o_out[(blk * 128 + wq * 32 + lane) * 32 + n] = __uint_as_float(r[n]);
@@ -888,7 +898,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+        ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
     }
 }
 
@@ -997,8 +1007,22 @@ int cached_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_r
     return ETAP_OK;
 }
 
+// Heads per CTA work unit: 32 when the head count allows it (N = 32 / 64 UMMAs halve the
+// tensor-pipe issue count per KV byte, which is what bounds 64+ heads on one GPU), else 16.
+// ETAP_HEAD_GROUP=16 in the environment forces 16 (A/B runs); read once per process.
+int head_group_of(int heads) {
+    static const int forced = [] {
+        const char* e = std::getenv("ETAP_HEAD_GROUP");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced == 16) return 16;
+    return heads % 32 == 0 ? 32 : 16;
+}
+
+bool heads_ok(int heads) { return heads >= 16 && heads % 16 == 0; }
+
 size_t max_partials(int batch, int heads, int num_sm_parts) {
-    return static_cast<size_t>(num_sm_parts) + static_cast<size_t>(batch) * (heads / HG);
+    return static_cast<size_t>(num_sm_parts) + static_cast<size_t>(batch) * (heads / head_group_of(heads));
 }
 
 }  // namespace
@@ -1014,6 +1038,13 @@ const char* etap_mla_last_error(void) { return g_last_error.c_str(); }
 
 const char* etap_mla_version(void) { return ETAP_MLA_VERSION; }
 
+int etap_mla_head_group(int heads, int* head_group) {
+    if (!head_group) return fail(ETAP_ERR_SHAPE, "head_group is NULL");
+    if (!heads_ok(heads)) return fail(ETAP_ERR_SHAPE, "heads must be a multiple of 16");
+    *head_group = head_group_of(heads);
+    return ETAP_OK;
+}
+
 int etap_mla_num_sm_parts(int device, int* num_sm_parts) {
     if (!num_sm_parts) return fail(ETAP_ERR_SHAPE, "num_sm_parts is NULL");
     int n = 0;
@@ -1024,18 +1055,19 @@ int etap_mla_num_sm_parts(int device, int* num_sm_parts) {
 
 int etap_mla_sched_ints(int batch, int heads, int num_sm_parts, size_t* sched_ints,
                         size_t* split_off_ints) {
-    if (batch < 1 || heads < HG || heads % HG != 0 || num_sm_parts < 1)
+    if (batch < 1 || !heads_ok(heads) || num_sm_parts < 1)
         return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
     if (sched_ints) *sched_ints = static_cast<size_t>(num_sm_parts) * SCHED_INTS;
-    if (split_off_ints) *split_off_ints = static_cast<size_t>(batch) * (heads / HG) + 1;
+    if (split_off_ints) *split_off_ints = static_cast<size_t>(batch) * (heads / head_group_of(heads)) + 1;
     return ETAP_OK;
 }
 
 int etap_mla_workspace_bytes(int batch, int heads, int num_sm_parts, size_t* bytes) {
-    if (batch < 1 || heads < HG || heads % HG != 0 || num_sm_parts < 1 || !bytes)
+    if (batch < 1 || !heads_ok(heads) || num_sm_parts < 1 || !bytes)
         return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
     const size_t np = max_partials(batch, heads, num_sm_parts);
-    *bytes = np * HG * D_V * sizeof(float) + np * HG * sizeof(float);
+    const size_t hg = head_group_of(heads);
+    *bytes = np * hg * D_V * sizeof(float) + np * hg * sizeof(float);
     return ETAP_OK;
 }
 
@@ -1044,11 +1076,11 @@ int etap_mla_metadata_host(const int32_t* seqlens, int batch, int heads, int num
     // Serial host restatement of etap_mla_metadata_kernel (same cost line, same mapping);
     // used by tests to pin the device schedule and by callers that plan on the host.
     if (!seqlens || !sched || !split_off) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
-    if (batch < 1 || heads < HG || heads % HG != 0)
+    if (batch < 1 || !heads_ok(heads))
         return fail(ETAP_ERR_SHAPE, "batch >= 1 and heads a multiple of 16 required");
-    const int groups = heads / HG;
+    const int groups = heads / head_group_of(heads);
     const int nvb = batch * groups;
-    if (nvb > META_MAX_VB) return fail(ETAP_ERR_SHAPE, "batch * heads/16 too large");
+    if (nvb > META_MAX_VB) return fail(ETAP_ERR_SHAPE, "batch * head groups too large");
     if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
         return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
     std::vector<int> tiles(nvb), pref(nvb + 1, 0), ns(nvb, 0), first(nvb, 0x7fffffff);
@@ -1100,11 +1132,11 @@ int etap_mla_metadata_host(const int32_t* seqlens, int batch, int heads, int num
 int etap_mla_metadata(const int32_t* seqlens, int batch, int heads, int num_sm_parts,
                       int32_t* sched, int32_t* split_off, void* stream) {
     if (!seqlens || !sched || !split_off) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
-    if (batch < 1 || heads < HG || heads % HG != 0)
+    if (batch < 1 || !heads_ok(heads))
         return fail(ETAP_ERR_SHAPE, "batch >= 1 and heads a multiple of 16 required");
-    const int groups = heads / HG;
+    const int groups = heads / head_group_of(heads);
     if (batch * groups > META_MAX_VB)
-        return fail(ETAP_ERR_SHAPE, "batch * heads/16 exceeds " + std::to_string(META_MAX_VB));
+        return fail(ETAP_ERR_SHAPE, "batch * head groups exceeds " + std::to_string(META_MAX_VB));
     if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
         return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
     cudaLaunchConfig_t cfg = {};
@@ -1132,7 +1164,7 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
         !out || !lse)
         return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
     if (q_tokens != 1) return fail(ETAP_ERR_SHAPE, "q_tokens must be 1 (decode)");
-    if (batch < 1 || heads < HG || heads % HG != 0)
+    if (batch < 1 || !heads_ok(heads))
         return fail(ETAP_ERR_SHAPE, "batch >= 1 and heads a multiple of 16 required");
     if (num_pages < 1 || max_pages_per_seq < 1)
         return fail(ETAP_ERR_SHAPE, "num_pages and max_pages_per_seq must be >= 1");
@@ -1146,9 +1178,10 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
 
     CUtensorMap tm_kv, tm_q;
     if (int rc = cached_map(&tm_kv, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, PAGE)) return rc;
-    if (int rc = cached_map(&tm_q, q, static_cast<uint64_t>(batch) * heads, HG)) return rc;
+    const int hg = head_group_of(heads);
+    if (int rc = cached_map(&tm_q, q, static_cast<uint64_t>(batch) * heads, hg)) return rc;
 
-    const int groups = heads / HG;
+    const int groups = heads / hg;
     const size_t np = max_partials(batch, heads, num_sm_parts);
     DecodeParams prm;
     prm.block_table = block_table;
@@ -1159,7 +1192,7 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     prm.out = out;
     prm.lse = lse;
     prm.ws_o = static_cast<float*>(workspace);
-    prm.ws_lse = prm.ws_o + np * HG * D_V;
+    prm.ws_lse = prm.ws_o + np * hg * D_V;
     prm.max_pages = max_pages_per_seq;
     prm.batch = batch;
     prm.heads = heads;
@@ -1167,6 +1200,12 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     prm.sched_out = const_cast<int32_t*>(sched);
     prm.split_off_out = const_cast<int32_t*>(split_off);
     prm.inkernel_sched = (batch * groups <= MAX_FUSED_VB && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
+    if (!prm.inkernel_sched && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) {
+        // too many virtual sequences for the fused prologue: run K1 first on the same stream
+        if (int rc = etap_mla_metadata(seqlens, batch, heads, num_sm_parts, const_cast<int32_t*>(sched),
+                                       const_cast<int32_t*>(split_off), stream))
+            return rc;
+    }
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.flags = flags;
     prm.trace = static_cast<unsigned long long*>(g_trace_buf);
@@ -1181,13 +1220,20 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(num_sm_parts);
     cfg.blockDim = dim3(NUM_THREADS);
-    cfg.dynamicSmemBytes = SMEM_ALLOC;
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel, SMEM_ALLOC);
-    if (attr_rc) return attr_rc;
-    ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel, tm_kv, tm_q, prm));
+    if (hg == 32) {
+        cfg.dynamicSmemBytes = Cfg<32>::SMEM_ALLOC;
+        static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<32>, Cfg<32>::SMEM_ALLOC);
+        if (attr_rc) return attr_rc;
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel<32>, tm_kv, tm_q, prm));
+    } else {
+        cfg.dynamicSmemBytes = Cfg<16>::SMEM_ALLOC;
+        static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<16>, Cfg<16>::SMEM_ALLOC);
+        if (attr_rc) return attr_rc;
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel<16>, tm_kv, tm_q, prm));
+    }
 
     if (flags & ETAP_FLAG_SKIP_COMBINE) return ETAP_OK;
     return etap_mla_combine(split_off, batch, heads, num_sm_parts, workspace, out, lse, stream);
@@ -1196,24 +1242,25 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
 int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_parts,
                      void* workspace, float* out, float* lse, void* stream) {
     if (!split_off || !workspace || !out || !lse) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
-    if (batch < 1 || heads < HG || heads % HG != 0 || num_sm_parts < 1)
+    if (batch < 1 || !heads_ok(heads) || num_sm_parts < 1)
         return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
-    const int groups = heads / HG;
+    const int hg = head_group_of(heads);
+    const int groups = heads / hg;
     const size_t np = max_partials(batch, heads, num_sm_parts);
     float* ws_o = static_cast<float*>(workspace);
-    float* ws_lse = ws_o + np * HG * D_V;
+    float* ws_lse = ws_o + np * hg * D_V;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg2 = {};
-    cfg2.gridDim = dim3(batch * groups * HG);
+    cfg2.gridDim = dim3(batch * groups * hg);
     cfg2.blockDim = dim3(COMBINE_THREADS);
     cfg2.dynamicSmemBytes = 0;
     cfg2.stream = static_cast<cudaStream_t>(stream);
     cfg2.attrs = attr;
     cfg2.numAttrs = 1;
     ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, static_cast<const float*>(ws_o),
-                                 static_cast<const float*>(ws_lse), split_off, groups, heads, out, lse,
+                                 static_cast<const float*>(ws_lse), split_off, hg, groups, heads, out, lse,
                                  static_cast<unsigned long long*>(g_combine_trace_buf)));
     return ETAP_OK;
 }
@@ -1239,11 +1286,11 @@ int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* 
     if (int rc = check_device()) return rc;
     CUtensorMap tm_k, tm_q;
     if (int rc = make_map(&tm_k, k, TILE, PAGE)) return rc;  // one 64-row page
-    if (int rc = make_map(&tm_q, q, HG, HG)) return rc;
+    if (int rc = make_map(&tm_q, q, 16, 16)) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    static int attr_rc = ensure_smem_attr(etap_mla_selftest_kernel, SMEM_ALLOC);
+    static int attr_rc = ensure_smem_attr(etap_mla_selftest_kernel, Cfg<16>::SMEM_ALLOC);
     if (attr_rc) return attr_rc;
-    etap_mla_selftest_kernel<<<1, NUM_THREADS, SMEM_ALLOC, st>>>(tm_k, tm_q, p, s_t, o_t);
+    etap_mla_selftest_kernel<<<1, NUM_THREADS, Cfg<16>::SMEM_ALLOC, st>>>(tm_k, tm_q, p, s_t, o_t);
     ETAP_CUDA(cudaGetLastError());
     return ETAP_OK;
 }

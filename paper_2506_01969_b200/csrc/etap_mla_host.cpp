@@ -180,8 +180,13 @@ static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int6
     int rc = etap_mla_host_ctx_create(1, heads, pages, static_cast<int>(pages), &ctx);
     if (rc) return rc;
     float* st_dev = nullptr;
-    const int groups = heads / ETAP_MLA_HEAD_GROUP;
-    const size_t st_n = static_cast<size_t>(groups) * pages * 64;
+    int hg = ETAP_MLA_HEAD_GROUP;
+    if (int e = etap_mla_head_group(heads, &hg)) {
+        etap_mla_host_ctx_destroy(ctx);
+        return e;
+    }
+    const int groups = heads / hg;
+    const size_t st_n = static_cast<size_t>(groups) * pages * 4 * hg;
     if (state) {
         ctx->num_sm_parts = 1;  // one split: the reference's serial chain of KV blocks
         if (cudaMalloc(&st_dev, st_n * sizeof(float)) != cudaSuccess) {
@@ -199,14 +204,14 @@ static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int6
         if (!rc && cudaMemcpy(sf.data(), st_dev, st_n * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess)
             rc = host_fail(ETAP_ERR_CUDA, "state copy failed");
         cudaFree(st_dev);
-        // [vb = head group][tile][4][16] -> [tile][4][heads]
+        // [vb = head group][tile][4][hg] -> [tile][4][heads]
         if (!rc)
             for (int g = 0; g < groups; ++g)
                 for (int64_t t = 0; t < pages; ++t)
                     for (int f = 0; f < 4; ++f)
-                        for (int h = 0; h < ETAP_MLA_HEAD_GROUP; ++h)
-                            state[(t * 4 + f) * heads + g * ETAP_MLA_HEAD_GROUP + h] =
-                                sf[((static_cast<size_t>(g) * pages + t) * 4 + f) * 16 + h];
+                        for (int h = 0; h < hg; ++h)
+                            state[(t * 4 + f) * heads + g * hg + h] =
+                                sf[((static_cast<size_t>(g) * pages + t) * 4 + f) * hg + h];
     }
     etap_mla_host_ctx_destroy(ctx);
     if (rc) return rc;

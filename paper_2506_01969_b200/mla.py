@@ -19,8 +19,15 @@ D_QK = 576
 D_V = 512
 PAGE_ROWS = 64
 TILE_ROWS = 64
-HEAD_GROUP = 16
+HEAD_GROUP = 16  # minimum heads per CTA work unit; see head_group()
 SCHED_INTS = 8
+
+
+def head_group(heads: int) -> int:
+    """Heads per CTA work unit the library uses (32 when heads % 32 == 0, else 16)."""
+    out = C.c_int(0)
+    check(_lib.lib().etap_mla_head_group(heads, C.byref(out)), "etap_mla_head_group")
+    return out.value
 
 
 def _dev_index(device: torch.device | str | int | None) -> int:

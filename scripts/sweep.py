@@ -63,6 +63,14 @@ def measure(seqlens, heads, label, iters=50):
 
 
 if __name__ == "__main__":
+    if "--heads" in sys.argv:  # head-count sweep at the headline context (head group per ETAP_HEAD_GROUP)
+        hg = os.environ.get("ETAP_HEAD_GROUP", "auto")
+        for h in (16, 32, 64, 128):
+            measure([65536] * 16, h, f"B=16 ctx=64K H={h} head_group={mla.head_group(h) if hg == 'auto' else hg}",
+                    iters=20)
+        measure([4096] * 64, 128, f"B=64 ctx=4K H=128 head_group={mla.head_group(128) if hg == 'auto' else hg}",
+                iters=20)
+        sys.exit(0)
     measure([1024], 16, "config1 B=1 H=16 ctx=1K")
     for ctx in (1024, 2048, 4096, 8192, 16384, 32768, 65536):
         measure([ctx] * 16, 16, f"config3 B=16 H=16 ctx={ctx}")

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2506_01969_b200 import _lib, etap, inputs
+from paper_2506_01969_b200 import _lib, etap, inputs, mla
 
 ROOT = Path(__file__).resolve().parents[1]
 
@@ -54,6 +54,13 @@ def test_sizes_and_shape_validation():
     ws = C.c_size_t()
     assert L.etap_mla_workspace_bytes(16, 16, 148, C.byref(ws)) == _lib.ETAP_OK
     assert ws.value == (148 + 16) * 16 * (512 + 1) * 4
+    # head groups: 32 heads per work unit when heads % 32 == 0, else 16
+    assert [mla.head_group(h) for h in (16, 32, 48, 64, 128)] == [16, 32, 16, 32, 32]
+    assert L.etap_mla_sched_ints(4, 128, 148, C.byref(a), C.byref(b)) == _lib.ETAP_OK and b.value == 4 * 4 + 1
+    assert L.etap_mla_workspace_bytes(4, 128, 148, C.byref(ws)) == _lib.ETAP_OK
+    assert ws.value == (148 + 16) * 32 * (512 + 1) * 4
+    hg = C.c_int()
+    assert L.etap_mla_head_group(24, C.byref(hg)) == _lib.ETAP_ERR_SHAPE
     # decode rejects q_tokens != 1 and bad scale before touching the device
     rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 2, 16, 1.0, 1, 1, 1, 148, 1, 1, 1, 0, None)
     assert rc == _lib.ETAP_ERR_SHAPE and "q_tokens" in _lib.last_error()
@@ -90,7 +97,7 @@ def test_host_metadata_partition_invariants():
     cases = [([65536] * 16, 16, 148), (inputs.varlen_seqlens(32), 16, 148), ([0, 1, 64, 65, 0], 32, 148),
              ([100], 16, 3), ([1024], 16, 148), ([10**6], 128, 148), ([7] * 300, 16, 148)]
     for seqlens, heads, parts in cases:
-        B, G = len(seqlens), heads // 16
+        B, G = len(seqlens), heads // mla.head_group(heads)
         sched = np.zeros(parts * 8, np.int32)
         so = np.zeros(B * G + 1, np.int32)
         sl = np.array(seqlens, np.int32)
