@@ -33,12 +33,15 @@ using namespace etap_b200;
 // =============================================================================================
 // K1: split-KV scheduler. One CTA of 1024 threads.
 //
-// Virtual sequences vb = b * groups + g (sequence x head group). Each owns
-// tiles(vb) = ceil(seqlen_b / 128) KV tiles and a cost of tiles + META_FIXED_COST (0 if empty).
-// The cost line [0, total) is cut into num_parts equal intervals; CTA k takes
-// [k*T, (k+1)*T) mapped back to (vb, tile) coordinates. Partials of one vb are numbered
-// contiguously in CTA order: split_off[vb] .. split_off[vb+1].
-// sched[k] = {vb_begin, tile_begin, vb_end, tile_end (exclusive), first_partial_idx, 0,0,0}
+// Virtual sequences vb = g * batch + b (head group major). Each owns tiles(vb) =
+// ceil(seqlen_b / 64) KV tiles and a cost of tiles + META_FIXED_COST (0 if empty). The CTAs
+// are dealt into line_shape().lanes lanes of p_line CTAs; the cost line of one lane's
+// line_n virtual sequences [0, total) is cut into p_line equal intervals and line CTA k takes
+// [k*T, (k+1)*T) mapped back to (line position, tile). Every lane uses the same cut, so with
+// several head groups the lanes stream the same pages in lock step (L2 sharing). Partials of
+// one vb are numbered contiguously in CTA order: split_off[vb] .. split_off[vb+1].
+// sched[cta] = {pos_begin, tile_begin, pos_end, tile_end (exclusive), first_partial_idx,
+//               vb offset of the lane (vb = offset + pos), partial offset of the lane, 0}
 // =============================================================================================
 namespace {
 
@@ -89,51 +92,58 @@ __device__ void block_scan_array(const int* a, int* out, int n, int* warp_tot) {
 
 __global__ void __launch_bounds__(META_THREADS, 1)
     etap_mla_metadata_kernel(const int32_t* __restrict__ seqlens, int batch, int groups,
-                             int num_parts, int32_t* __restrict__ sched,
+                             int num_parts, int lanes_on, int32_t* __restrict__ sched,
                              int32_t* __restrict__ split_off) {
     ptx::grid_dep_launch();
     __shared__ int s_tiles[META_MAX_VB];
     __shared__ int s_pref[META_MAX_VB + 1];
     __shared__ int s_ns[META_MAX_VB];
     __shared__ int s_first[META_MAX_VB];
+    __shared__ int s_soff[META_MAX_VB + 1];
     __shared__ int warp_tot[32];
-    const int nvb = batch * groups;
+    const LineShape ls = line_shape(batch, groups, num_parts, lanes_on != 0);
+    const int n = ls.line_n;
 
-    for (int i = threadIdx.x; i < nvb; i += blockDim.x) {
-        const int len = max(0, seqlens[i / groups]);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int len = max(0, seqlens[i % batch]);
         s_tiles[i] = (len + TILE - 1) / TILE;
         s_ns[i] = s_tiles[i] > 0 ? s_tiles[i] + META_FIXED_COST : 0;  // cost, reused below
         s_first[i] = 0x7fffffff;
     }
     __syncthreads();
-    block_scan_array(s_ns, s_pref, nvb, warp_tot);
-    const int total = s_pref[nvb];
-    for (int i = threadIdx.x; i < nvb; i += blockDim.x) s_ns[i] = 0;
+    block_scan_array(s_ns, s_pref, n, warp_tot);
+    const int total = s_pref[n];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s_ns[i] = 0;
     __syncthreads();
 
-    const int T = max(1, (total + num_parts - 1) / num_parts);
-    // map a cost coordinate x in [0, total) to (vb, tile)
+    const int T = max(1, (total + ls.p_line - 1) / ls.p_line);
+    // map a cost coordinate x in [0, total) to (line index, tile)
     auto map = [&](int x, int& vb, int& t) {
-        int lo = 0, hi = nvb - 1;  // largest vb with s_pref[vb] <= x and nonzero cost
+        int lo = 0, hi = n - 1;  // largest index with s_pref <= x and nonzero cost
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (s_pref[mid] <= x) lo = mid; else hi = mid - 1;
         }
         // skip zero-cost sequences that share the same prefix value
-        while (lo + 1 < nvb && s_pref[lo + 1] <= x) ++lo;
+        while (lo + 1 < n && s_pref[lo + 1] <= x) ++lo;
         vb = lo;
         t = min(max(0, x - s_pref[lo] - META_FIXED_COST), s_tiles[lo]);
     };
 
-    int vb_b = 0, t_b = 0, vb_e = -1, t_e = 0;
-    const int k = threadIdx.x;
-    for (int kk = k; kk < num_parts; kk += blockDim.x) {
-        const int x0 = kk * T, x1 = min(total, (kk + 1) * T);
-        int b0 = 0, tb = 0, b1 = -1, te = 0;
+    // line CTA kl's range [kl*T, (kl+1)*T) in (line index, tile) coordinates
+    auto range = [&](int kl, int& b0, int& tb, int& b1, int& te) {
+        const int x0 = kl * T, x1 = min(total, (kl + 1) * T);
+        b0 = 0; tb = 0; b1 = -1; te = 0;
         if (x0 < total) {
             map(x0, b0, tb);
-            if (x1 >= total) { b1 = nvb - 1; te = s_tiles[nvb - 1]; }
+            if (x1 >= total) { b1 = n - 1; te = s_tiles[n - 1]; }
             else map(x1, b1, te);
+        }
+    };
+    for (int kk = threadIdx.x; kk < ls.p_line; kk += blockDim.x) {
+        int b0, tb, b1, te;
+        range(kk, b0, tb, b1, te);
+        {
             for (int vb = b0; vb <= b1; ++vb) {
                 const int t0 = vb == b0 ? tb : 0;
                 const int t1 = vb == b1 ? te : s_tiles[vb];
@@ -143,21 +153,24 @@ __global__ void __launch_bounds__(META_THREADS, 1)
                 }
             }
         }
-        if (kk == k) { vb_b = b0; t_b = tb; vb_e = b1; t_e = te; }
     }
     __syncthreads();
-    block_scan_array(s_ns, s_pref, nvb, warp_tot);  // s_pref now = split offsets
-    for (int i = threadIdx.x; i <= nvb; i += blockDim.x) split_off[i] = s_pref[i];
-    for (int kk = k; kk < num_parts; kk += blockDim.x) {
-        int b0 = vb_b, tb = t_b, b1 = vb_e, te = t_e;
-        if (kk != k) {  // only reachable when num_parts > blockDim (not in practice)
-            b0 = 0; tb = 0; b1 = -1; te = 0;
-        }
+    block_scan_array(s_ns, s_soff, n, warp_tot);  // split offsets along the line
+    const int ns_line = s_soff[n];
+    // split_off over all batch * groups virtual sequences: lane-major copies of the line's
+    for (int v = threadIdx.x; v <= batch * groups; v += blockDim.x) {
+        const int lane = v / n, i = v - lane * n;
+        split_off[v] = lane * ns_line + s_soff[i];
+    }
+    for (int kk = threadIdx.x; kk < num_parts; kk += blockDim.x) {
+        const int lane = kk / ls.p_line, kl = kk - lane * ls.p_line;
+        int b0 = 0, tb = 0, b1 = -1, te = 0;  // CTAs past the last lane idle
+        if (lane < ls.lanes) range(kl, b0, tb, b1, te);
         int first_idx = 0;
-        if (b1 >= b0 && b0 < nvb) first_idx = s_pref[b0] + (kk - min(s_first[b0], kk));
+        if (b1 >= b0 && b0 < n) first_idx = lane * ns_line + s_soff[b0] + (kl - min(s_first[b0], kl));
         int32_t* s = sched + kk * SCHED_INTS;
         s[0] = b0; s[1] = tb; s[2] = b1; s[3] = te; s[4] = first_idx;
-        s[5] = 0; s[6] = 0; s[7] = 0;
+        s[5] = min(lane, ls.lanes - 1) * n; s[6] = min(lane, ls.lanes - 1) * ns_line; s[7] = 0;
     }
 }
 
@@ -195,47 +208,57 @@ __device__ __forceinline__ int cta_excl_scan256(int v, int* s_wt, int& total) {
 }
 
 // The split schedule of etap_mla_metadata_kernel (K1) computed by every CTA for itself:
-// cost prefix -> closed-form split counts per virtual sequence (CTA k covers vb iff
-// (k+1)T > P[vb]+F and kT < P[vb+1]) -> split offsets -> this CTA's range. Identical output
+// cost prefix along the line -> closed-form split counts per line entry (line CTA k covers i
+// iff (k+1)T > P[i]+F and kT < P[i+1]) -> split offsets -> this CTA's range. Identical output
 // to K1 (GPU test); CTA 0 publishes split_off for the combine kernel, every CTA its sched row.
-// this CTA's (vb, tile) range on the cost line, written to s_sched and published to sched_out
-__device__ void schedule_own_range(const DecodeParams& prm, const int* s_pref, const int* s_soff,
-                                   const int* s_tiles, int* s_sched, int nvb, int total, int T) {
-    const int k = blockIdx.x;
+__device__ void schedule_own_range(const DecodeParams& prm, const LineShape& ls, const int* s_pref,
+                                   const int* s_soff, const int* s_tiles, int* s_sched, int total, int T) {
+    const int n = ls.line_n;
+    const int lane = blockIdx.x / ls.p_line, k = blockIdx.x - lane * ls.p_line;
     auto map = [&](int x, int& vb, int& t) {
-        int lo = 0, hi = nvb - 1;
+        int lo = 0, hi = n - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (s_pref[mid] <= x) lo = mid; else hi = mid - 1;
         }
-        while (lo + 1 < nvb && s_pref[lo + 1] <= x) ++lo;
+        while (lo + 1 < n && s_pref[lo + 1] <= x) ++lo;
         vb = lo;
         t = min(max(0, x - s_pref[lo] - META_FIXED_COST), s_tiles[lo]);
     };
     const int x0 = k * T, x1 = min(total, (k + 1) * T);
     int b0 = 0, tb = 0, b1 = -1, te = 0, first = 0;
-    if (x0 < total) {
+    if (lane < ls.lanes && x0 < total) {
         map(x0, b0, tb);
-        if (x1 >= total) { b1 = nvb - 1; te = s_tiles[nvb - 1]; }
+        if (x1 >= total) { b1 = n - 1; te = s_tiles[n - 1]; }
         else map(x1, b1, te);
-        if (b1 >= b0) first = s_soff[b0] + (k - (s_pref[b0] + META_FIXED_COST) / T);
+        if (b1 >= b0) first = lane * s_soff[n] + s_soff[b0] + (k - (s_pref[b0] + META_FIXED_COST) / T);
     }
     s_sched[0] = b0; s_sched[1] = tb; s_sched[2] = b1; s_sched[3] = te; s_sched[4] = first;
-    s_sched[5] = 0; s_sched[6] = 0; s_sched[7] = 0;
-    int32_t* g = prm.sched_out + k * SCHED_INTS;
+    s_sched[5] = min(lane, ls.lanes - 1) * n;         // virtual-sequence offset of the lane
+    s_sched[6] = min(lane, ls.lanes - 1) * s_soff[n];  // partial-index offset of the lane
+    s_sched[7] = 0;
+    int32_t* g = prm.sched_out + blockIdx.x * SCHED_INTS;
     for (int i = 0; i < SCHED_INTS; ++i) g[i] = s_sched[i];
 }
 
-// Warp-level variant for up to 32 virtual sequences (no block barriers): run by warp 0 only.
-__device__ void inkernel_schedule_warp(const DecodeParams& prm, int* s_pref, int* s_soff,
-                                       int* s_tiles, int* s_len, int* s_sched) {
-    const int G = prm.groups;
-    const int nvb = prm.batch * G;
-    const int parts = gridDim.x;
+// split_off over all batch * groups virtual sequences (lane-major copies of the line's)
+__device__ __forceinline__ void publish_split_off(const DecodeParams& prm, const LineShape& ls,
+                                                  const int* s_soff, int tid, int nthreads) {
+    const int n = ls.line_n, nv = prm.batch * prm.groups;
+    for (int v = tid; v <= nv; v += nthreads) {
+        const int lane = v / n, i = v - lane * n;
+        prm.split_off_out[v] = lane * s_soff[n] + s_soff[i];
+    }
+}
+
+// Warp-level variant for lines of up to 32 entries (no block barriers): run by warp 0 only.
+__device__ void inkernel_schedule_warp(const DecodeParams& prm, const LineShape& ls, int* s_pref,
+                                       int* s_soff, int* s_tiles, int* s_len, int* s_sched) {
+    const int n = ls.line_n;
     const int lane = threadIdx.x & 31;
     int len = 0, tiles = 0, cost = 0;
-    if (lane < nvb) {
-        len = max(0, prm.seqlens[lane / G]);
+    if (lane < n) {
+        len = max(0, prm.seqlens[lane % prm.batch]);
         tiles = (len + TILE - 1) / TILE;
         cost = tiles > 0 ? tiles + META_FIXED_COST : 0;
         s_tiles[lane] = tiles;
@@ -249,37 +272,32 @@ __device__ void inkernel_schedule_warp(const DecodeParams& prm, int* s_pref, int
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     const int pref = incl - cost;
-    if (lane < nvb) s_pref[lane] = pref;
-    if (lane == 0) s_pref[nvb] = total;
-    const int T = max(1, (total + parts - 1) / parts);
+    if (lane < n) s_pref[lane] = pref;
+    if (lane == 0) s_pref[n] = total;
+    const int T = max(1, (total + ls.p_line - 1) / ls.p_line);
     int ns = 0;
-    if (lane < nvb && tiles > 0) ns = ((incl + T - 1) / T - 1) - (pref + META_FIXED_COST) / T + 1;
+    if (lane < n && tiles > 0) ns = ((incl + T - 1) / T - 1) - (pref + META_FIXED_COST) / T + 1;
     int so = ns;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, so, o);
         if (lane >= o) so += y;
     }
-    if (lane < nvb) s_soff[lane] = so - ns;
-    if (lane == 31) s_soff[nvb] = so;
+    if (lane < n) s_soff[lane] = so - ns;
+    if (lane == 31) s_soff[n] = so;
     __syncwarp();
-    if (lane == 0) schedule_own_range(prm, s_pref, s_soff, s_tiles, s_sched, nvb, total, T);
-    if (blockIdx.x == 0) {
-        if (lane < nvb) prm.split_off_out[lane] = s_soff[lane];
-        if (lane == 0) prm.split_off_out[nvb] = s_soff[nvb];
-    }
+    if (lane == 0) schedule_own_range(prm, ls, s_pref, s_soff, s_tiles, s_sched, total, T);
+    if (blockIdx.x == 0) publish_split_off(prm, ls, s_soff, lane, 32);
     __syncwarp();
 }
 
-__device__ void inkernel_schedule(const DecodeParams& prm, int* s_pref, int* s_soff, int* s_tiles,
-                                  int* s_len, int* s_sched, int* s_wt) {
-    const int G = prm.groups;
-    const int nvb = prm.batch * G;
-    const int parts = gridDim.x;
+__device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, int* s_pref, int* s_soff,
+                                  int* s_tiles, int* s_len, int* s_sched, int* s_wt) {
+    const int n = ls.line_n;
     const int tid = threadIdx.x;
     int tiles = 0, cost = 0;
-    if (tid < nvb) {
-        const int len = max(0, prm.seqlens[tid / G]);
+    if (tid < n) {
+        const int len = max(0, prm.seqlens[tid % prm.batch]);
         tiles = (len + TILE - 1) / TILE;
         cost = tiles > 0 ? tiles + META_FIXED_COST : 0;
         s_tiles[tid] = tiles;
@@ -287,36 +305,37 @@ __device__ void inkernel_schedule(const DecodeParams& prm, int* s_pref, int* s_s
     }
     int total;
     const int pref = cta_excl_scan256(cost, s_wt, total);
-    if (tid < nvb) s_pref[tid] = pref;
-    if (tid == 0) s_pref[nvb] = total;
+    if (tid < n) s_pref[tid] = pref;
+    if (tid == 0) s_pref[n] = total;
     __syncthreads();
-    const int T = max(1, (total + parts - 1) / parts);
+    const int T = max(1, (total + ls.p_line - 1) / ls.p_line);
     int ns = 0;
-    if (tid < nvb && tiles > 0) {
+    if (tid < n && tiles > 0) {
         const int kf = (pref + META_FIXED_COST) / T;
         const int kl = (s_pref[tid + 1] + T - 1) / T - 1;
         ns = kl - kf + 1;
     }
     int nsplits;
     const int so = cta_excl_scan256(ns, s_wt, nsplits);
-    if (tid < nvb) s_soff[tid] = so;
-    if (tid == 0) s_soff[nvb] = nsplits;
+    if (tid < n) s_soff[tid] = so;
+    if (tid == 0) s_soff[n] = nsplits;
     __syncthreads();
-    if (tid == 0) schedule_own_range(prm, s_pref, s_soff, s_tiles, s_sched, nvb, total, T);
-    if (blockIdx.x == 0)
-        for (int i = tid; i <= nvb; i += NUM_THREADS) prm.split_off_out[i] = s_soff[i];
+    if (tid == 0) schedule_own_range(prm, ls, s_pref, s_soff, s_tiles, s_sched, total, T);
+    if (blockIdx.x == 0) publish_split_off(prm, ls, s_soff, tid, NUM_THREADS);
     __syncthreads();
 }
 
-__device__ __forceinline__ bool split_at(const int32_t* sch, int seqlen, int groups, int vb,
+// Split i of the CTA's range along the line: virtual sequence vb = lane_off + i (head-group
+// major: b = vb % batch, g = vb / batch) and the tile interval this CTA owns of it.
+__device__ __forceinline__ bool split_at(const int32_t* sch, int seqlen, int batch, int i,
                                          SplitDesc& d) {
-    d.vb = vb;
-    d.b = vb / groups;
-    d.g = vb - d.b * groups;
+    d.vb = sch[5] + i;
+    d.g = d.vb / batch;
+    d.b = d.vb - d.g * batch;
     d.seqlen = seqlen;
     const int n_tiles = (d.seqlen + TILE - 1) / TILE;
-    d.t0 = (vb == sch[0]) ? sch[1] : 0;
-    d.t1 = (vb == sch[2]) ? min(sch[3], n_tiles) : n_tiles;
+    d.t0 = (i == sch[0]) ? sch[1] : 0;
+    d.t1 = (i == sch[2]) ? min(sch[3], n_tiles) : n_tiles;
     return d.t0 < d.t1;
 }
 
@@ -372,38 +391,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int* s_len = s_tiles + MAX_FUSED_VB;
     int* s_sched = s_len + MAX_FUSED_VB;
     const bool fused = prm.inkernel_sched != 0;
+    int idx_off = 0;          // partial-index offset of this CTA's lane (fused schedule)
     if (fused) {
-        if (prm.batch * prm.groups <= 32) {
-            if (warp == 0) inkernel_schedule_warp(prm, s_pref, s_soff, s_tiles, s_len, s_sched);
+        const LineShape ls = line_shape(prm.batch, prm.groups, gridDim.x, prm.lanes_on != 0);
+        if (ls.line_n <= 32) {
+            if (warp == 0) inkernel_schedule_warp(prm, ls, s_pref, s_soff, s_tiles, s_len, s_sched);
             __syncthreads();
         } else {
-            inkernel_schedule(prm, s_pref, s_soff, s_tiles, s_len, s_sched, s_sched + 8);
+            inkernel_schedule(prm, ls, s_pref, s_soff, s_tiles, s_len, s_sched, s_sched + 8);
         }
         sch = s_sched;
-        soff = s_soff;
+        soff = s_soff;        // line-local split offsets
+        idx_off = sch[6];
     } else {
         sch = prm.sched + blockIdx.x * SCHED_INTS;
-        soff = prm.split_off;
+        soff = prm.split_off + sch[5];  // indexed by line position like the fused copy
     }
     if (threadIdx.x == 0) ETAP_TRACE(prm, TRACE_TILES - 1, 1);
 
-    const int vb_begin = sch[0], vb_end = sch[2];
-    const int G = prm.groups;
+    const int vb_begin = sch[0], vb_end = sch[2];  // line positions (vb = sch[5] + position)
+    const int B = prm.batch;
     const uint32_t ring_addr = ptx::smem_u32(smem + C::OFF_RING);
     const uint32_t q_addr = ptx::smem_u32(smem + C::OFF_Q);
     const uint32_t p_addr = ptx::smem_u32(smem + C::OFF_P);
-    auto seqlen_of = [&](int vb) { return fused ? s_len[vb] : max(0, prm.seqlens[vb / G]); };
+    auto seqlen_of = [&](int i) { return fused ? s_len[i] : max(0, prm.seqlens[(sch[5] + i) % B]); };
 
     if (warp == 0) {
         // ===================================================== TMA producer (whole warp)
         // Tile gt occupies ring positions [9gt, 9gt+9); positions [0, SPLIT_POS) reuse slots
         // of tile gt-3, the rest slots of tile gt-2: two waits on "GEMM2 done" per tile.
-        const uint64_t pol_kv = ptx::policy_evict_first();
+        // KV pages are streamed once per head group: with head-group lanes the other groups'
+        // CTAs read the same page shortly after, so it stays evict-normal in L2
+        const bool kv_shared = line_shape(B, prm.groups, gridDim.x, prm.lanes_on != 0).lanes > 1;
+        const uint64_t pol_kv = kv_shared ? ptx::policy_evict_normal() : ptx::policy_evict_first();
         const uint64_t pol_q = ptx::policy_evict_last();
         uint32_t gt = 0, nsplit = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, seqlen_of(vb), G, vb, sd)) continue;
+            if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
             if (nsplit > 0) ptx::mbar_wait(&bars[BAR_Q_EMPTY], (nsplit - 1) & 1);
             if (lane == 0) {
                 ptx::mbar_arrive_expect_tx(&bars[BAR_Q_FULL], C::Q_BYTES);
@@ -463,7 +488,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t gt = 0, nsplit = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, seqlen_of(vb), G, vb, sd)) continue;
+            if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
             ptx::mbar_wait(&bars[BAR_Q_FULL], nsplit & 1);
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
@@ -491,7 +516,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t gt = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, seqlen_of(vb), G, vb, sd)) continue;
+            if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
                 ptx::mbar_wait(&bars[BAR_P_FULL + buf], (gt >> 1) & 1);
@@ -533,7 +558,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t gt = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
-            if (!split_at(sch, seqlen_of(vb), G, vb, sd)) continue;
+            if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
             float m_own[HH];    // running max of this thread's heads (log2 units)
             float l_part[HH];   // partial column sums of this thread's rows, own heads
             float dbg_l = 0.f;  // debug state dump: running column sum of head `lane`
@@ -621,7 +646,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         const float mn = s_m[lane];
                         const float al = first ? 0.f : (any ? s_alpha[lane] : 1.f);
                         dbg_l = first ? colsum : fmaf(dbg_l, al, colsum);
-                        float* st = prm.state + (static_cast<size_t>(vb) * prm.state_tiles + t) * 4 * HG;
+                        float* st = prm.state + (static_cast<size_t>(sd.vb) * prm.state_tiles + t) * 4 * HG;
                         st[lane] = dbg_m_old * 0.69314718055994530942f;
                         st[HG + lane] = mn * 0.69314718055994530942f;
                         st[2 * HG + lane] = al;
@@ -688,7 +713,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int h = 0; h < HG; ++h)
                 inv_l[h] = 1.f / (red_sum[h] + red_sum[HG + h] + red_sum[2 * HG + h] + red_sum[3 * HG + h]);
             const int ns = soff[vb + 1] - soff[vb];
-            const int idx = (vb == sch[0]) ? sch[4] : soff[vb];  // partial index (ns > 1)
+            const int idx = (vb == sch[0]) ? sch[4] : soff[vb] + idx_off;  // partial index (ns > 1)
             float* dst;
             float* dst_lse;
             if (ns == 1) {
@@ -749,7 +774,7 @@ constexpr int COMBINE_BATCH = 16;  // partial float4 loads in flight per thread
 
 __global__ void __launch_bounds__(COMBINE_THREADS)
     etap_mla_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
-                            const int32_t* __restrict__ split_off, int hg, int groups, int heads,
+                            const int32_t* __restrict__ split_off, int hg, int batch, int heads,
                             float* __restrict__ out, float* __restrict__ lse,
                             unsigned long long* trace) {
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 0] = ptx::global_timer_ns();
@@ -758,7 +783,7 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 1] = ptx::global_timer_ns();
     const int vb = blockIdx.x / hg;
     const int h = blockIdx.x - vb * hg;
-    const int b = vb / groups, g = vb - b * groups;
+    const int g = vb / batch, b = vb - g * batch;  // head-group-major virtual sequences
     const int s0 = __ldg(split_off + vb);
     const int ns = __ldg(split_off + vb + 1) - s0;
     if (ns == 1) {
@@ -1021,6 +1046,15 @@ int head_group_of(int heads) {
 
 bool heads_ok(int heads) { return heads >= 16 && heads % 16 == 0; }
 
+// Head-group lanes of the split schedule (line_shape); ETAP_GROUP_LANES=0 disables them (A/B).
+bool lanes_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("ETAP_GROUP_LANES");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 size_t max_partials(int batch, int heads, int num_sm_parts) {
     return static_cast<size_t>(num_sm_parts) + static_cast<size_t>(batch) * (heads / head_group_of(heads));
 }
@@ -1073,7 +1107,7 @@ int etap_mla_workspace_bytes(int batch, int heads, int num_sm_parts, size_t* byt
 
 int etap_mla_metadata_host(const int32_t* seqlens, int batch, int heads, int num_sm_parts,
                            int32_t* sched, int32_t* split_off) {
-    // Serial host restatement of etap_mla_metadata_kernel (same cost line, same mapping);
+    // Serial host restatement of etap_mla_metadata_kernel (same line, lanes and mapping);
     // used by tests to pin the device schedule and by callers that plan on the host.
     if (!seqlens || !sched || !split_off) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
     if (batch < 1 || !heads_ok(heads))
@@ -1083,31 +1117,33 @@ int etap_mla_metadata_host(const int32_t* seqlens, int batch, int heads, int num
     if (nvb > META_MAX_VB) return fail(ETAP_ERR_SHAPE, "batch * head groups too large");
     if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
         return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
-    std::vector<int> tiles(nvb), pref(nvb + 1, 0), ns(nvb, 0), first(nvb, 0x7fffffff);
-    for (int i = 0; i < nvb; ++i) {
-        const int len = std::max(0, seqlens[i / groups]);
+    const LineShape ls = line_shape(batch, groups, num_sm_parts, lanes_enabled());
+    const int n = ls.line_n;
+    std::vector<int> tiles(n), pref(n + 1, 0), ns(n, 0), first(n, 0x7fffffff), soff(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+        const int len = std::max(0, seqlens[i % batch]);
         tiles[i] = (len + TILE - 1) / TILE;
         pref[i + 1] = pref[i] + (tiles[i] > 0 ? tiles[i] + META_FIXED_COST : 0);
     }
-    const int total = pref[nvb];
-    const int T = std::max(1, (total + num_sm_parts - 1) / num_sm_parts);
+    const int total = pref[n];
+    const int T = std::max(1, (total + ls.p_line - 1) / ls.p_line);
     auto map = [&](int x, int& vb, int& t) {
-        int lo = 0, hi = nvb - 1;
+        int lo = 0, hi = n - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (pref[mid] <= x) lo = mid; else hi = mid - 1;
         }
-        while (lo + 1 < nvb && pref[lo + 1] <= x) ++lo;
+        while (lo + 1 < n && pref[lo + 1] <= x) ++lo;
         vb = lo;
         t = std::min(std::max(0, x - pref[lo] - META_FIXED_COST), tiles[lo]);
     };
-    std::vector<int> rb(num_sm_parts), rt(num_sm_parts), re(num_sm_parts), rte(num_sm_parts);
-    for (int k = 0; k < num_sm_parts; ++k) {
+    std::vector<int> rb(ls.p_line), rt(ls.p_line), re(ls.p_line), rte(ls.p_line);
+    for (int k = 0; k < ls.p_line; ++k) {
         const int x0 = k * T, x1 = std::min(total, (k + 1) * T);
         int b0 = 0, tb = 0, b1 = -1, te = 0;
         if (x0 < total) {
             map(x0, b0, tb);
-            if (x1 >= total) { b1 = nvb - 1; te = tiles[nvb - 1]; }
+            if (x1 >= total) { b1 = n - 1; te = tiles[n - 1]; }
             else map(x1, b1, te);
             for (int vb = b0; vb <= b1; ++vb) {
                 const int t0 = vb == b0 ? tb : 0;
@@ -1117,14 +1153,21 @@ int etap_mla_metadata_host(const int32_t* seqlens, int batch, int heads, int num
         }
         rb[k] = b0; rt[k] = tb; re[k] = b1; rte[k] = te;
     }
-    split_off[0] = 0;
-    for (int i = 0; i < nvb; ++i) split_off[i + 1] = split_off[i] + ns[i];
-    for (int k = 0; k < num_sm_parts; ++k) {
-        int first_idx = 0;
-        if (re[k] >= rb[k] && rb[k] < nvb) first_idx = split_off[rb[k]] + (k - std::min(first[rb[k]], k));
-        int32_t* s = sched + k * SCHED_INTS;
-        s[0] = rb[k]; s[1] = rt[k]; s[2] = re[k]; s[3] = rte[k]; s[4] = first_idx;
-        s[5] = 0; s[6] = 0; s[7] = 0;
+    for (int i = 0; i < n; ++i) soff[i + 1] = soff[i] + ns[i];
+    const int ns_line = soff[n];
+    for (int v = 0; v <= nvb; ++v) split_off[v] = (v / n) * ns_line + soff[v % n];
+    for (int kk = 0; kk < num_sm_parts; ++kk) {
+        const int lane = kk / ls.p_line, k = kk - lane * ls.p_line;
+        int32_t* s = sched + kk * SCHED_INTS;
+        const int lo = std::min(lane, ls.lanes - 1);
+        if (lane >= ls.lanes) {
+            s[0] = 0; s[1] = 0; s[2] = -1; s[3] = 0; s[4] = 0;
+        } else {
+            int first_idx = 0;
+            if (re[k] >= rb[k] && rb[k] < n) first_idx = lane * ns_line + soff[rb[k]] + (k - std::min(first[rb[k]], k));
+            s[0] = rb[k]; s[1] = rt[k]; s[2] = re[k]; s[3] = rte[k]; s[4] = first_idx;
+        }
+        s[5] = lo * n; s[6] = lo * ns_line; s[7] = 0;
     }
     return ETAP_OK;
 }
@@ -1150,7 +1193,7 @@ int etap_mla_metadata(const int32_t* seqlens, int batch, int heads, int num_sm_p
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_metadata_kernel, seqlens, batch, groups,
-                                 num_sm_parts, sched, split_off));
+                                 num_sm_parts, lanes_enabled() ? 1 : 0, sched, split_off));
     return ETAP_OK;
 }
 
@@ -1199,7 +1242,9 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     prm.groups = groups;
     prm.sched_out = const_cast<int32_t*>(sched);
     prm.split_off_out = const_cast<int32_t*>(split_off);
-    prm.inkernel_sched = (batch * groups <= MAX_FUSED_VB && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
+    prm.lanes_on = lanes_enabled() ? 1 : 0;
+    const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
+    prm.inkernel_sched = (ls.line_n <= MAX_FUSED_VB && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
     if (!prm.inkernel_sched && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) {
         // too many virtual sequences for the fused prologue: run K1 first on the same stream
         if (int rc = etap_mla_metadata(seqlens, batch, heads, num_sm_parts, const_cast<int32_t*>(sched),
@@ -1260,7 +1305,7 @@ int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_
     cfg2.attrs = attr;
     cfg2.numAttrs = 1;
     ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, static_cast<const float*>(ws_o),
-                                 static_cast<const float*>(ws_lse), split_off, hg, groups, heads, out, lse,
+                                 static_cast<const float*>(ws_lse), split_off, hg, batch, heads, out, lse,
                                  static_cast<unsigned long long*>(g_combine_trace_buf)));
     return ETAP_OK;
 }

@@ -249,6 +249,24 @@ __device__ __forceinline__ int halfwarp_reduce_head(int lane) {
     return N == 8 ? ((lane & 15) >> 1) : (lane & 15);
 }
 
+// Split-KV work line. Virtual sequences are numbered head-group-major, vb = g * batch + b.
+// With several head groups the SMs are dealt into `lanes` = groups equal lanes of p_line CTAs;
+// every lane partitions the same line of `line_n` = batch sequences identically, so CTA
+// (lane, k') and CTA (lane', k') stream the same KV pages at the same time and all but one
+// of the head groups' reads of a page hit L2. One lane (lanes = 1, line of batch * groups
+// virtual sequences) when there is one group, fewer CTAs than groups, or lanes are disabled.
+struct LineShape {
+    int lanes, line_n, p_line;
+};
+
+__host__ __device__ inline LineShape line_shape(int batch, int groups, int parts, bool lanes_on) {
+    LineShape s;
+    s.lanes = (lanes_on && groups > 1 && parts >= groups) ? groups : 1;
+    s.line_n = s.lanes > 1 ? batch : batch * groups;
+    s.p_line = parts / s.lanes;
+    return s;
+}
+
 struct DecodeParams {
     const int32_t* block_table;
     const int32_t* seqlens;
@@ -265,6 +283,7 @@ struct DecodeParams {
     int heads;
     int groups;  // heads / HG
     int inkernel_sched;  // 1: compute the split schedule in the prologue (and publish it)
+    int lanes_on;        // head-group lanes enabled (line_shape)
     float scale_log2;
     unsigned flags;
     unsigned long long* trace;  // debug: [cta][TRACE_TILES][8] globaltimer stamps, or null

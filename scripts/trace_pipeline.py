@@ -26,9 +26,10 @@ def main() -> None:
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--ctx", type=int, default=65536)
     ap.add_argument("--runs", type=int, default=3)
+    ap.add_argument("--heads", type=int, default=16)
     a = ap.parse_args()
-    inp = inputs.make_mla_inputs([a.ctx] * a.batch, heads=16, pad_value=0.0)
-    plan = mla.MlaDecodePlan.create(a.batch, 16, "cuda")
+    inp = inputs.make_mla_inputs([a.ctx] * a.batch, heads=a.heads, pad_value=0.0)
+    plan = mla.MlaDecodePlan.create(a.batch, a.heads, "cuda")
     nparts = plan.num_sm_parts
     buf = torch.zeros(nparts * TRACE_TILES * 8, dtype=torch.int64, device="cuda")
     for _ in range(2):

@@ -92,10 +92,14 @@ def test_no_cpu_fallback():
 
 def test_host_metadata_partition_invariants():
     """The split-KV schedule (host restatement of K1) covers every (sequence, head group,
-    page) exactly once, numbers partials contiguously per sequence and balances the load."""
+    page) exactly once, numbers partials contiguously per sequence and balances the load.
+    Virtual sequences are head-group major (vb = g * batch + b); with several head groups the
+    CTAs form one lane per group and every lane cuts the same line (same page ranges)."""
     L = _lib.lib()
     cases = [([65536] * 16, 16, 148), (inputs.varlen_seqlens(32), 16, 148), ([0, 1, 64, 65, 0], 32, 148),
-             ([100], 16, 3), ([1024], 16, 148), ([10**6], 128, 148), ([7] * 300, 16, 148)]
+             ([100], 16, 3), ([1024], 16, 148), ([10**6], 128, 148), ([7] * 300, 16, 148),
+             ([65536] * 16, 128, 148), ([4096] * 64, 128, 148), ([100, 3000], 64, 3), ([5000], 128, 2),
+             ([0, 0, 900], 96, 148)]
     for seqlens, heads, parts in cases:
         B, G = len(seqlens), heads // mla.head_group(heads)
         sched = np.zeros(parts * 8, np.int32)
@@ -103,20 +107,26 @@ def test_host_metadata_partition_invariants():
         sl = np.array(seqlens, np.int32)
         assert L.etap_mla_metadata_host(sl.ctypes.data_as(C.c_void_p), B, heads, parts,
                                         sched.ctypes.data_as(C.c_void_p), so.ctypes.data_as(C.c_void_p)) == 0
-        tiles = [(s + 63) // 64 for s in seqlens for _ in range(G)]
+        lanes = G if (G > 1 and parts >= G) else 1
+        p_line = parts // lanes
+        tiles = [(seqlens[vb % B] + 63) // 64 for vb in range(B * G)]
         cover = [np.zeros(t, np.int32) for t in tiles]
         count = np.zeros(B * G, np.int32)
         idx_seen = {}
         work = []
         for k in range(parts):
-            vb0, t0, vb1, t1, first = sched[k * 8:k * 8 + 5]
+            p0, t0, p1, t1, first, off = sched[k * 8:k * 8 + 6]
+            if lanes > 1 and k < lanes * p_line:  # lanes share the cut of line CTA k % p_line
+                assert off == (k // p_line) * B
+                assert np.array_equal(sched[k * 8:k * 8 + 4], sched[(k % p_line) * 8:(k % p_line) * 8 + 4])
             w = 0
-            for vb in range(vb0, vb1 + 1):
-                a = t0 if vb == vb0 else 0
-                e = t1 if vb == vb1 else tiles[vb]
+            for pos in range(p0, p1 + 1):
+                vb = off + pos
+                a = t0 if pos == p0 else 0
+                e = t1 if pos == p1 else tiles[vb]
                 if a < e:
                     cover[vb][a:e] += 1
-                    idx = first if vb == vb0 else so[vb]
+                    idx = first if pos == p0 else so[vb]
                     assert so[vb] <= idx < so[vb + 1]
                     assert idx not in idx_seen
                     idx_seen[idx] = (k, vb)
@@ -127,5 +137,6 @@ def test_host_metadata_partition_invariants():
             assert (c == 1).all()
         assert np.array_equal(np.diff(so), count)
         total = sum(tiles)
-        if total >= parts * 4:
-            assert max(work) <= total / parts + 4  # balanced to within the per-split overhead
+        active = lanes * p_line
+        if total >= active * 4:
+            assert max(work) <= total / active + 4  # balanced to within the per-split overhead
