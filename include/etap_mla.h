@@ -21,15 +21,20 @@
  *     returns ETAP_ERR_CUDA.
  *
  * Layouts (MLA latent attention, DeepSeek shapes)
- *   q          [batch][q_tokens=1][heads][576]  bf16, row-major (heads folded into n_q as in
+ *   q          [batch][q_tokens][heads][576]    bf16, row-major (heads folded into n_q as in
  *              the reference bench harness, cli.cpp:214)
  *   kv_pool    [num_pages][64][576]             bf16, the latent KV cache; V is the first 512
  *              columns of every row (MLA aliasing; the reference keeps V separate,
  *              attention.cpp:38-40, and callers build V = K[:, :512] with col_block)
  *   block_table[batch][max_pages]               int32 page ids
  *   seqlens    [batch]                          int32 context lengths (varlen; 0 allowed)
- *   out        [batch][q_tokens=1][heads][512]  fp32  O = softmax(scale * Q K^T) V
- *   lse        [batch][q_tokens=1][heads]       fp32  L = m + log l, natural log (etap.cpp:144)
+ *   out        [batch][q_tokens][heads][512]    fp32  O = softmax(scale * Q K^T) V
+ *   lse        [batch][q_tokens][heads]         fp32  L = m + log l, natural log (etap.cpp:144)
+ *   q_tokens > 1 (multi-token / MTP decode, no reference analog: SPEC.md:12,146,249 put it out
+ *   of scope) folds the tokens into the head axis, n_q = q_tokens * heads rows per sequence
+ *   (the reference bench's own folding, cli.cpp:214); with `causal` token j sees KV rows
+ *   [0, seqlen - q_tokens + j]. The sizing and metadata entry points below take that folded
+ *   row count as `heads`. A query row that sees no KV row gets O = 0, L = -inf.
  */
 #ifndef ETAP_MLA_H
 #define ETAP_MLA_H
@@ -47,6 +52,7 @@ extern "C" {
 #define ETAP_MLA_TILE_ROWS 64      /* KV rows per pipeline tile (M of S^T = K Q^T) */
 #define ETAP_MLA_HEAD_GROUP 16     /* minimum heads per CTA work unit (see etap_mla_head_group) */
 #define ETAP_MLA_SCHED_INTS 8      /* int32 per CTA in the schedule */
+#define ETAP_MLA_MAX_Q_TOKENS 8    /* query tokens per sequence (multi-token / MTP decode) */
 
 #define ETAP_OK 0
 #define ETAP_ERR_SHAPE 1
@@ -104,8 +110,10 @@ int etap_mla_metadata_host(const int32_t* seqlens /*host [batch]*/, int batch, i
 
 /* K2 + K3 — the transposed pipeline (run_etap + block_update_impl, etap.cpp:15-148) on
  * tcgen05/TMEM/TMA, followed by the log-sum-exp combine of split partials.
- * All pointers are device pointers. q_tokens must be 1 (decode); `causal` is accepted and is
- * a no-op for one query token. heads must be a multiple of 16. */
+ * All pointers are device pointers. 1 <= q_tokens <= ETAP_MLA_MAX_Q_TOKENS; heads is per
+ * token and q_tokens * heads must be a multiple of 16 (the value to pass as `heads` to the
+ * sizing / metadata / combine entry points). `causal` masks the trailing rows per token
+ * (a no-op for q_tokens = 1). */
 int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
                     const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,
                     int batch, int q_tokens, int heads, float scale, int causal,

@@ -184,6 +184,26 @@ def mla_decode_bf16(q_bits: np.ndarray, kv_pool_bits: np.ndarray, block_table: n
     return o, l
 
 
+def mla_decode_bf16_tokens(q_bits: np.ndarray, kv_pool_bits: np.ndarray, block_table: np.ndarray,
+                           seqlens: np.ndarray, scale: float, causal: bool = True,
+                           nthreads: int | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Multi-token (MTP) decode oracle: q [B,T,H,576] uint16 -> o [B,T,H,512], l [B,T,H].
+    No reference analog (SPEC.md:12,146,249 put multi-token decode out of scope); the causal
+    rule is that token j of T sees KV rows [0, seqlen - T + j], i.e. each token is the
+    single-token oracle above on a shortened context (attention_ref per row,
+    attention.cpp:44-77). A token that sees no row gets O = 0, L = -inf."""
+    q_bits = np.ascontiguousarray(q_bits, dtype=np.uint16)
+    B, T, H = q_bits.shape[0], q_bits.shape[1], q_bits.shape[2]
+    sl = np.asarray(seqlens, dtype=np.int64)
+    o = np.empty((B, T, H, 512))
+    l = np.empty((B, T, H))
+    for j in range(T):
+        slj = np.maximum(sl - (T - 1 - j), 0) if causal else sl
+        o[:, j], l[:, j] = mla_decode_bf16(q_bits[:, j], kv_pool_bits, block_table, slj.astype(np.int32),
+                                           scale, nthreads)
+    return o, l
+
+
 # ------------------------------------------------------------------ reference (oracle/_ref)
 def ref_matrix_from_seed(rows: int, cols: int, seed: int, dist: str = "normal") -> np.ndarray:
     out = np.empty((rows, cols), dtype=np.float64)

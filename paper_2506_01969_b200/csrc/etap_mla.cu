@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const float thresh = eager ? 0.f : LAZY_RESCALE_LOG2;
         const bool tracer = (threadIdx.x == SOFTMAX_WARP0 * 32);
         const bool head_owner = wq == 0 && (lane & 15) == 0;  // writes s_m / s_alpha of its half
+        const bool mtp = prm.q_tokens > 1;
         const int rhead = halfwarp_reduce_head<HH>(lane);   // head (of the half) a reduction leaves here
         const bool rwriter = HH == 16 || (lane & 1) == 0;
         uint32_t gt = 0;
@@ -562,10 +563,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float m_own[HH];    // running max of this thread's heads (log2 units)
             float l_part[HH];   // partial column sums of this thread's rows, own heads
             float dbg_l = 0.f;  // debug state dump: running column sum of head `lane`
+            int row_lim[HH];    // causal multi-token decode: rows visible to each column
 #pragma unroll
             for (int j = 0; j < HH; ++j) {
                 m_own[j] = -INFINITY;
                 l_part[j] = 0.f;
+                const int tok = (sd.g * HG + half * HH + j) / prm.heads_per_token;
+                row_lim[j] = sd.seqlen - (prm.causal ? prm.q_tokens - 1 - tok : 0);
             }
 
             for (int t = sd.t0; t < sd.t1; ++t) {
@@ -580,12 +584,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::mbar_arrive(&bars[BAR_S_FREE + buf]);
 
                 const int grow = t * TILE + row;
-                const bool valid = grow < sd.seqlen;
                 float x[HH];
                 bool exceed = false;
 #pragma unroll
                 for (int j = 0; j < HH; ++j) {
-                    x[j] = valid ? __uint_as_float(sr[j]) * prm.scale_log2 : -INFINITY;
+                    x[j] = grow < row_lim[j] ? __uint_as_float(sr[j]) * prm.scale_log2 : -INFINITY;
                     exceed |= x[j] > m_own[j] + thresh;
                 }
                 const bool first = (t == sd.t0);
@@ -631,7 +634,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 float pv[HH];
 #pragma unroll
                 for (int j = 0; j < HH; ++j) {
-                    pv[j] = exp2f(x[j] - m_own[j]);
+                    // a column may have no visible row yet (multi-token causal mask): m = -inf
+                    const float mu = (mtp && m_own[j] == -INFINITY) ? 0.f : m_own[j];
+                    pv[j] = exp2f(x[j] - mu);
                     l_part[j] = first ? pv[j] : fmaf(l_part[j], alpha_own[j], pv[j]);
                 }
                 if (debug) {
@@ -710,8 +715,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::named_bar_sync(2, 128);
             float inv_l[HG];
 #pragma unroll
-            for (int h = 0; h < HG; ++h)
-                inv_l[h] = 1.f / (red_sum[h] + red_sum[HG + h] + red_sum[2 * HG + h] + red_sum[3 * HG + h]);
+            for (int h = 0; h < HG; ++h) {
+                const float l = red_sum[h] + red_sum[HG + h] + red_sum[2 * HG + h] + red_sum[3 * HG + h];
+                inv_l[h] = l > 0.f ? 1.f / l : 0.f;  // l = 0: column saw no row (O = 0, L = -inf)
+            }
             const int ns = soff[vb + 1] - soff[vb];
             const int idx = (vb == sch[0]) ? sch[4] : soff[vb] + idx_off;  // partial index (ns > 1)
             float* dst;
@@ -820,13 +827,14 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
 #pragma unroll
         for (int j = 0; j < COMBINE_BATCH; ++j)
             if (j < n) bm = fmaxf(bm, l[j]);
-        const float corr = __expf(mx - bm);  // 0 on the first batch (mx = -inf)
+        const float bs = bm == -INFINITY ? 0.f : bm;  // all partials empty so far (causal MTP)
+        const float corr = __expf(mx - bs);  // 0 on the first batch (mx = -inf)
         sum *= corr;
         acc.x *= corr; acc.y *= corr; acc.z *= corr; acc.w *= corr;
 #pragma unroll
         for (int j = 0; j < COMBINE_BATCH; ++j) {
             if (j < n) {
-                const float w = __expf(l[j] - bm);
+                const float w = __expf(l[j] - bs);
                 sum += w;
                 acc.x = fmaf(w, v[j].x, acc.x);
                 acc.y = fmaf(w, v[j].y, acc.y);
@@ -836,7 +844,7 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
         }
         mx = bm;
     }
-    const float inv = 1.f / sum;
+    const float inv = sum > 0.f ? 1.f / sum : 0.f;
     acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
     if (threadIdx.x == 0) lse[hrow] = mx + logf(sum);
     o4[threadIdx.x] = acc;
@@ -1199,16 +1207,19 @@ int etap_mla_metadata(const int32_t* seqlens, int batch, int heads, int num_sm_p
 
 int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
                     const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,
-                    int batch, int q_tokens, int heads, float scale, int causal,
+                    int batch, int q_tokens, int heads_per_token, float scale, int causal,
                     const int32_t* sched, const int32_t* split_off, int num_sm_parts,
                     void* workspace, float* out, float* lse, unsigned flags, void* stream) {
-    (void)causal;  // one query token: the causal mask is the full context
     if (!q || !kv_pool || !block_table || !seqlens || !sched || !split_off || !workspace ||
         !out || !lse)
         return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
-    if (q_tokens != 1) return fail(ETAP_ERR_SHAPE, "q_tokens must be 1 (decode)");
+    if (q_tokens < 1 || q_tokens > ETAP_MLA_MAX_Q_TOKENS)
+        return fail(ETAP_ERR_SHAPE, "q_tokens must be in [1, " + std::to_string(ETAP_MLA_MAX_Q_TOKENS) + "]");
+    if (heads_per_token < 1) return fail(ETAP_ERR_SHAPE, "heads must be >= 1");
+    // the q_tokens query tokens of a sequence are folded into its head axis (rows of Q / O)
+    const int heads = q_tokens * heads_per_token;
     if (batch < 1 || !heads_ok(heads))
-        return fail(ETAP_ERR_SHAPE, "batch >= 1 and heads a multiple of 16 required");
+        return fail(ETAP_ERR_SHAPE, "batch >= 1 and q_tokens * heads a multiple of 16 required");
     if (num_pages < 1 || max_pages_per_seq < 1)
         return fail(ETAP_ERR_SHAPE, "num_pages and max_pages_per_seq must be >= 1");
     if (num_pages * PAGE > (int64_t)0x7fffffff)
@@ -1240,6 +1251,9 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     prm.batch = batch;
     prm.heads = heads;
     prm.groups = groups;
+    prm.q_tokens = q_tokens;
+    prm.heads_per_token = heads_per_token;
+    prm.causal = causal ? 1 : 0;
     prm.sched_out = const_cast<int32_t*>(sched);
     prm.split_off_out = const_cast<int32_t*>(split_off);
     prm.lanes_on = lanes_enabled() ? 1 : 0;

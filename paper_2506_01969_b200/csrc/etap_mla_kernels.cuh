@@ -280,8 +280,11 @@ struct DecodeParams {
     float* ws_lse;
     int max_pages;
     int batch;
-    int heads;
+    int heads;            // query rows per sequence (all tokens folded)
     int groups;  // heads / HG
+    int q_tokens;         // query tokens per sequence (MTP: > 1); heads = q_tokens * heads_per_token
+    int heads_per_token;
+    int causal;           // q_tokens > 1: token j sees KV rows [0, seqlen - q_tokens + j]
     int inkernel_sched;  // 1: compute the split schedule in the prologue (and publish it)
     int lanes_on;        // head-group lanes enabled (line_shape)
     float scale_log2;

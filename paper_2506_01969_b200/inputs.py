@@ -92,7 +92,7 @@ def varlen_seqlens(batch: int, lo: int = 4096, hi: int = 131072, seed: int = 250
 
 @dataclass
 class MlaInputs:
-    q: torch.Tensor            # [B, 1, H, 576] bf16
+    q: torch.Tensor            # [B, T, H, 576] bf16 (T query tokens per sequence, 1 for decode)
     kv_pool: torch.Tensor      # [pages, 64, 576] bf16
     block_table: torch.Tensor  # [B, max_pages] int32
     seqlens: torch.Tensor      # [B] int32
@@ -107,6 +107,10 @@ class MlaInputs:
     def heads(self) -> int:
         return self.q.shape[2]
 
+    @property
+    def q_tokens(self) -> int:
+        return self.q.shape[1]
+
     def kv_bytes(self) -> int:
         return sum(self.seqlens_list) * D_QK * 2
 
@@ -115,9 +119,11 @@ def make_mla_inputs(seqlens: list[int], heads: int = 16, seed: int = 42,
                     device: torch.device | str = "cuda", pad_value: float = float("nan"),
                     head_offset: int = 0, total_heads: int | None = None,
                     scale: float | None = None, shuffle_pages: bool = True,
-                    q_scale: float = 1.0) -> MlaInputs:
+                    q_scale: float = 1.0, q_tokens: int = 1) -> MlaInputs:
     """Build paged inputs. With ``total_heads`` > heads, Q is drawn for all heads and the
-    slice [head_offset, head_offset + heads) is kept (head sharding across ranks)."""
+    slice [head_offset, head_offset + heads) is kept (head sharding across ranks). With
+    ``q_tokens`` > 1 the Q stream of a sequence holds q_tokens consecutive [total_heads, 576]
+    blocks (multi-token decode)."""
     device = torch.device(device)
     B = len(seqlens)
     th = total_heads or heads
@@ -133,11 +139,11 @@ def make_mla_inputs(seqlens: list[int], heads: int = 16, seed: int = 42,
         off += np_
     bt = bt.to(device)
     pool = torch.empty((n_pages, PAGE_ROWS, D_QK), dtype=torch.bfloat16, device=device)
-    q = torch.empty((B, 1, heads, D_QK), dtype=torch.bfloat16, device=device)
+    q = torch.empty((B, q_tokens, heads, D_QK), dtype=torch.bfloat16, device=device)
     for b, s in enumerate(seqlens):
         sb = seed + 7919 * b
-        qb = splitmix_normal(th * D_QK, 3 * sb + 1, device).view(th, D_QK)[head_offset:head_offset + heads]
-        q[b, 0] = bf16_rne(qb * q_scale)
+        qb = splitmix_normal(q_tokens * th * D_QK, 3 * sb + 1, device).view(q_tokens, th, D_QK)
+        q[b] = bf16_rne(qb[:, head_offset:head_offset + heads] * q_scale)
         if pages[b] == 0:
             continue
         rows = pages[b] * PAGE_ROWS

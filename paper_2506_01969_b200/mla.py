@@ -69,21 +69,28 @@ class MlaDecodePlan:
     sched: torch.Tensor
     split_off: torch.Tensor
     workspace: torch.Tensor
+    q_tokens: int = 1  # query tokens per sequence (multi-token / MTP decode)
+
+    @property
+    def rows(self) -> int:
+        """Query rows per sequence (tokens folded into heads): the C-ABI's sizing `heads`."""
+        return self.q_tokens * self.heads
 
     @classmethod
     def create(cls, batch: int, heads: int, device: torch.device | str = "cuda",
-               num_parts: int | None = None) -> "MlaDecodePlan":
+               num_parts: int | None = None, q_tokens: int = 1) -> "MlaDecodePlan":
         device = torch.device(device)
         if device.type != "cuda":
             raise _lib.EtapShapeError("MlaDecodePlan needs a CUDA device (no CPU fallback)")
         L = _lib.lib()
         nparts = num_parts if num_parts is not None else num_sm_parts(device)
         n_sched, n_so, ws = C.c_size_t(0), C.c_size_t(0), C.c_size_t(0)
-        check(L.etap_mla_sched_ints(batch, heads, nparts, C.byref(n_sched), C.byref(n_so)),
+        rows = q_tokens * heads
+        check(L.etap_mla_sched_ints(batch, rows, nparts, C.byref(n_sched), C.byref(n_so)),
               "etap_mla_sched_ints")
-        check(L.etap_mla_workspace_bytes(batch, heads, nparts, C.byref(ws)), "etap_mla_workspace_bytes")
+        check(L.etap_mla_workspace_bytes(batch, rows, nparts, C.byref(ws)), "etap_mla_workspace_bytes")
         return cls(
-            batch=batch, heads=heads, device=device, num_sm_parts=nparts,
+            batch=batch, heads=heads, device=device, num_sm_parts=nparts, q_tokens=q_tokens,
             sched=torch.empty(n_sched.value, dtype=torch.int32, device=device),
             split_off=torch.empty(n_so.value, dtype=torch.int32, device=device),
             # zero-filled once: the tail holds the combine's ready flags / counters, which every
@@ -94,7 +101,7 @@ class MlaDecodePlan:
     def metadata(self, seqlens: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
         """K1: split-KV schedule for the current step's context lengths."""
         _check_tensor(seqlens, torch.int32, (self.batch,), "seqlens")
-        check(_lib.lib().etap_mla_metadata(seqlens.data_ptr(), self.batch, self.heads, self.num_sm_parts,
+        check(_lib.lib().etap_mla_metadata(seqlens.data_ptr(), self.batch, self.rows, self.num_sm_parts,
                                            self.sched.data_ptr(), self.split_off.data_ptr(),
                                            _stream_ptr(stream)), "etap_mla_metadata")
 
@@ -102,12 +109,13 @@ class MlaDecodePlan:
                seqlens: torch.Tensor, scale: float, out: torch.Tensor | None = None,
                lse: torch.Tensor | None = None, flags: int = 0, causal: bool = True,
                stream: torch.cuda.Stream | None = None) -> tuple[torch.Tensor, torch.Tensor]:
-        """K2 + K3. q [B,1,H,576] bf16, kv_pool [pages,64,576] bf16, block_table [B,max_pages]
-        int32, seqlens [B] int32 -> (out [B,1,H,512] fp32, lse [B,1,H] fp32, natural log)."""
-        B, H = self.batch, self.heads
-        if q.dim() == 3:
+        """K2 + K3. q [B,T,H,576] bf16 (T = q_tokens), kv_pool [pages,64,576] bf16, block_table
+        [B,max_pages] int32, seqlens [B] int32 -> (out [B,T,H,512] fp32, lse [B,T,H] fp32, natural
+        log). With T > 1 and ``causal`` token j sees KV rows [0, seqlen - T + j]."""
+        B, H, T = self.batch, self.heads, self.q_tokens
+        if q.dim() == 3 and T == 1:
             q = q.unsqueeze(1)
-        _check_tensor(q, torch.bfloat16, (B, 1, H, D_QK), "q")
+        _check_tensor(q, torch.bfloat16, (B, T, H, D_QK), "q")
         if kv_pool.dim() != 3 or kv_pool.shape[1:] != (PAGE_ROWS, D_QK) or kv_pool.dtype != torch.bfloat16:
             raise _lib.EtapShapeError(f"kv_pool must be [pages,64,576] bf16, got {tuple(kv_pool.shape)} {kv_pool.dtype}")
         if not kv_pool.is_contiguous():
@@ -117,12 +125,12 @@ class MlaDecodePlan:
             raise _lib.EtapShapeError("block_table must be contiguous [B, max_pages] int32")
         _check_tensor(seqlens, torch.int32, (B,), "seqlens")
         if out is None:
-            out = torch.empty((B, 1, H, D_V), dtype=torch.float32, device=q.device)
+            out = torch.empty((B, T, H, D_V), dtype=torch.float32, device=q.device)
         if lse is None:
-            lse = torch.empty((B, 1, H), dtype=torch.float32, device=q.device)
+            lse = torch.empty((B, T, H), dtype=torch.float32, device=q.device)
         check(_lib.lib().etap_mla_decode(
             q.data_ptr(), kv_pool.data_ptr(), kv_pool.shape[0], block_table.data_ptr(),
-            block_table.shape[1], seqlens.data_ptr(), B, 1, H, float(scale), int(causal),
+            block_table.shape[1], seqlens.data_ptr(), B, T, H, float(scale), int(causal),
             self.sched.data_ptr(), self.split_off.data_ptr(), self.num_sm_parts,
             self.workspace.data_ptr(), out.data_ptr(), lse.data_ptr(), int(flags),
             _stream_ptr(stream)), "etap_mla_decode")
@@ -147,7 +155,7 @@ class MlaDecodePlan:
 
     def combine(self, out: torch.Tensor, lse: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
         """K3 alone, after a decode(..., flags=FLAG_SKIP_COMBINE)."""
-        check(_lib.lib().etap_mla_combine(self.split_off.data_ptr(), self.batch, self.heads, self.num_sm_parts,
+        check(_lib.lib().etap_mla_combine(self.split_off.data_ptr(), self.batch, self.rows, self.num_sm_parts,
                                           self.workspace.data_ptr(), out.data_ptr(), lse.data_ptr(),
                                           _stream_ptr(stream)), "etap_mla_combine")
 
@@ -163,9 +171,11 @@ def _check_tensor(t: torch.Tensor, dtype: torch.dtype, shape: tuple, name: str) 
 def mla_decode(q: torch.Tensor, kv_pool: torch.Tensor, block_table: torch.Tensor,
                seqlens: torch.Tensor, scale: float, flags: int = 0,
                plan: MlaDecodePlan | None = None) -> tuple[torch.Tensor, torch.Tensor]:
-    """One-shot convenience: K1 + K2 + K3 on the current stream."""
+    """One-shot convenience: K1 + K2 + K3 on the current stream. q [B,H,576] or
+    [B,T,H,576] (T query tokens per sequence, causal)."""
     B, H = q.shape[0], q.shape[-2]
-    plan = plan or MlaDecodePlan.create(B, H, q.device)
+    T = q.shape[1] if q.dim() == 4 else 1
+    plan = plan or MlaDecodePlan.create(B, H, q.device, q_tokens=T)
     plan.metadata(seqlens)
     return plan.decode(q, kv_pool, block_table, seqlens, scale, flags=flags)
 

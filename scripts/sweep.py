@@ -18,14 +18,15 @@ from paper_2506_01969_b200 import inputs, mla
 L2_BYTES = 126 * 1024 * 1024
 
 
-def measure(seqlens, heads, label, iters=50):
+def measure(seqlens, heads, label, iters=50, q_tokens=1):
     kv_bytes = sum(seqlens) * 576 * 2
     ncopies = max(1, min(8, (2 * L2_BYTES) // max(1, kv_bytes) + 1))  # rotate through > L2
-    inps = [inputs.make_mla_inputs(seqlens, heads=heads, seed=42 + i, pad_value=0.0) for i in range(ncopies)]
+    inps = [inputs.make_mla_inputs(seqlens, heads=heads, seed=42 + i, pad_value=0.0, q_tokens=q_tokens)
+            for i in range(ncopies)]
     B = len(seqlens)
-    plan = mla.MlaDecodePlan.create(B, heads, "cuda")
-    out = torch.empty((B, 1, heads, 512), dtype=torch.float32, device="cuda")
-    lse = torch.empty((B, 1, heads), dtype=torch.float32, device="cuda")
+    plan = mla.MlaDecodePlan.create(B, heads, "cuda", q_tokens=q_tokens)
+    out = torch.empty((B, q_tokens, heads, 512), dtype=torch.float32, device="cuda")
+    lse = torch.empty((B, q_tokens, heads), dtype=torch.float32, device="cuda")
     graphs = [plan.capture(i.q, i.kv_pool, i.block_table, i.seqlens, i.scale, out, lse, with_metadata=False)
               for i in inps]
 
@@ -50,12 +51,12 @@ def measure(seqlens, heads, label, iters=50):
 
     us_stream = timed(stream_step)
     us_graph = timed(lambda j: graphs[j % ncopies].replay())
-    nbytes = inputs.algorithmic_bytes(seqlens, heads)
+    nbytes = inputs.algorithmic_bytes(seqlens, heads * q_tokens)
     best = min(us_stream, us_graph)
     line = {"config": label, "batch": B, "heads": heads, "ctx_total": sum(seqlens),
             "ctx_min": min(seqlens), "ctx_max": max(seqlens), "us_per_step_stream": us_stream,
             "us_per_step_graph": us_graph, "hbm_gbs": nbytes / best / 1e3,
-            "tflops": inputs.flops(seqlens, heads) / best / 1e6, "algorithmic_bytes": nbytes,
+            "tflops": inputs.flops(seqlens, heads * q_tokens) / best / 1e6, "q_tokens": q_tokens, "algorithmic_bytes": nbytes,
             "l2_rotation_copies": ncopies}
     print(json.dumps(line), flush=True)
     del inps, graphs
@@ -63,6 +64,10 @@ def measure(seqlens, heads, label, iters=50):
 
 
 if __name__ == "__main__":
+    if "--mtp" in sys.argv:  # multi-token decode: T tokens per sequence against the same context
+        for t in (1, 2, 4):
+            measure([65536] * 16, 16, f"B=16 ctx=64K H=16 q_tokens={t}", iters=20, q_tokens=t)
+        sys.exit(0)
     if "--heads" in sys.argv:  # head-count sweep at the headline context (head group per ETAP_HEAD_GROUP)
         hg = os.environ.get("ETAP_HEAD_GROUP", "auto")
         for h in (16, 32, 64, 128):

@@ -61,9 +61,14 @@ def test_sizes_and_shape_validation():
     assert ws.value == (148 + 16) * 32 * (512 + 1) * 4
     hg = C.c_int()
     assert L.etap_mla_head_group(24, C.byref(hg)) == _lib.ETAP_ERR_SHAPE
-    # decode rejects q_tokens != 1 and bad scale before touching the device
-    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 2, 16, 1.0, 1, 1, 1, 148, 1, 1, 1, 0, None)
+    # decode rejects q_tokens outside [1, 8], q_tokens * heads not a multiple of 16 and a bad
+    # scale before touching the device
+    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 9, 16, 1.0, 1, 1, 1, 148, 1, 1, 1, 0, None)
     assert rc == _lib.ETAP_ERR_SHAPE and "q_tokens" in _lib.last_error()
+    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 0, 16, 1.0, 1, 1, 1, 148, 1, 1, 1, 0, None)
+    assert rc == _lib.ETAP_ERR_SHAPE and "q_tokens" in _lib.last_error()
+    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 3, 8, 1.0, 1, 1, 1, 148, 1, 1, 1, 0, None)
+    assert rc == _lib.ETAP_ERR_SHAPE and "multiple of 16" in _lib.last_error()
     rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 1, 16, float("nan"), 1, 1, 1, 148, 1, 1, 1, 0, None)
     assert rc == _lib.ETAP_ERR_SHAPE and "scale" in _lib.last_error()
 
