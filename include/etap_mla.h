@@ -155,10 +155,12 @@ int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t
 int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* s_t, float* o_t,
                            void* stream);
 
-/* Debug: when device_buf is non-NULL, subsequent decode launches record per-tile
- * %globaltimer stamps of the pipeline events into it: [cta][128 tiles][8] uint64
- * (0/1 first/last chunk TMA issued, 2 last chunk landed, 3 S^T committed, 4 softmax saw S^T,
- * 5 P^T written, 6 MMA saw P^T, 7 O^T update committed). NULL disables (the default). */
+/* Debug: when device_buf is non-NULL, subsequent decode launches record per-tile %clock64
+ * stamps of the pipeline events into it: [cta][256][16] uint64, row = tile (< 255): 0/1 first /
+ * last chunk TMA issued, 2 last chunk landed, 3 S^T committed, 4 softmax saw S^T, 5 P^T
+ * written, 6 MMA saw P^T, 7 O^T update committed, 8 softmax exp done, 9 P buffer free.
+ * Row 255: %globaltimer ns at 0 entry, 1 schedule done, 2 exit; 3 SM id; %clock64 at 5 entry,
+ * 6 exit. NULL disables (the default). */
 int etap_mla_debug_trace(void* device_buf);
 
 /* Debug: combine-kernel stamps [block][4] (entry, after grid-dependency wait, exit) or NULL. */
@@ -167,9 +169,10 @@ int etap_mla_debug_trace_combine(void* device_buf);
 /* Debug (BlockHook replay, the reference's per-KV-block observer tiled_standard.hpp:32-40):
  * when device_buf is non-NULL, decode launches record for every (virtual sequence vb,
  * 64-row tile t < max_tiles) the softmax state after the tile:
- *   device_buf[((vb * max_tiles) + t) * 64 + {0,16,32,48} + h] = m_old, m_new (natural log
- *   units of scale*q.k), rescale exp(m_old - m_new) (0 on the first tile of a split), running l
- * for head h of the head group. Per-split state: run with one split per sequence
+ *   device_buf[((vb * max_tiles) + t) * 4 * hg + {0, hg, 2 hg, 3 hg} + h] = m_old, m_new
+ *   (natural log units of scale*q.k), rescale exp(m_old - m_new) (0 on the first tile of a
+ *   split), running l
+ * for head h of the head group (hg = etap_mla_head_group(heads), vb head-group major). Per-split state: run with one split per sequence
  * (num_sm_parts = 1 or a single sequence) to observe the reference's single chain. */
 int etap_mla_debug_state(void* device_buf, int max_tiles);
 

@@ -352,7 +352,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) ETAP_TRACE(prm, TRACE_TILES - 1, 0);
+    if (threadIdx.x == 0) {
+        ETAP_TRACE_G(prm, 0);
+        ETAP_TRACE_CLK(prm, 5);
+    }
 
     // ---- prologue (overlaps the previous kernel under programmatic dependent launch)
     if (warp == 0 && lane == 0) {
@@ -407,7 +410,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sch = prm.sched + blockIdx.x * SCHED_INTS;
         soff = prm.split_off + sch[5];  // indexed by line position like the fused copy
     }
-    if (threadIdx.x == 0) ETAP_TRACE(prm, TRACE_TILES - 1, 1);
+    if (threadIdx.x == 0) ETAP_TRACE_G(prm, 1);
 
     const int vb_begin = sch[0], vb_end = sch[2];  // line positions (vb = sch[5] + position)
     const int B = prm.batch;
@@ -659,8 +662,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                     ptx::named_bar_sync(2, 128);
                 }
+                if (tracer) ETAP_TRACE(prm, gt, 8);
                 // the P buffer is reused every other tile: GEMM2(gt-2) must have read it
                 if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+                if (tracer) ETAP_TRACE(prm, gt, 9);
                 if (need_rescale) {
                     // O^T must contain GEMM2(gt-1) before it is rescaled; s_alpha written above
                     ptx::named_bar_sync(2, 128);
@@ -758,11 +763,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
-        ETAP_TRACE(prm, TRACE_TILES - 1, 2);
+        ETAP_TRACE_G(prm, 2);
+        ETAP_TRACE_CLK(prm, 6);
         if (prm.trace != nullptr) {
             uint32_t smid;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            prm.trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + TRACE_TILES - 1) * 8 + 3] = smid;
+            prm.trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + TRACE_TILES - 1) * TRACE_SLOTS + 3] = smid;
         }
     }
     if (warp == 1) {

@@ -289,17 +289,33 @@ struct DecodeParams {
     int lanes_on;        // head-group lanes enabled (line_shape)
     float scale_log2;
     unsigned flags;
-    unsigned long long* trace;  // debug: [cta][TRACE_TILES][8] globaltimer stamps, or null
+    unsigned long long* trace;  // debug: [cta][TRACE_TILES][TRACE_SLOTS] stamps (ETAP_TRACE), or null
     float* state;               // debug: per-tile softmax state [vb][state_tiles][4][16], or null
     int state_tiles;
 };
 
 constexpr int TRACE_TILES = 256;
-#define ETAP_TRACE(prm, gt, slot)                                                              \
-    do {                                                                                       \
-        if ((prm).trace != nullptr && (gt) < TRACE_TILES)                                      \
-            (prm).trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + (gt)) * 8 + (slot)] = \
-                ptx::global_timer_ns();                                                        \
+constexpr int TRACE_SLOTS = 16;
+// Debug stamps: [cta][TRACE_TILES][TRACE_SLOTS]. Tile rows hold %clock64 (SM cycles, fine
+// grained); the last row holds %globaltimer ns (entry / schedule done / exit, comparable
+// across SMs) plus %clock64 at entry and exit (slots 5, 6) to convert cycles to ns.
+#define ETAP_TRACE(prm, gt, slot)                                                                   \
+    do {                                                                                            \
+        if ((prm).trace != nullptr && (gt) < TRACE_TILES - 1)                                       \
+            (prm).trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + (gt)) * TRACE_SLOTS + (slot)] = \
+                clock64();                                                                          \
+    } while (0)
+#define ETAP_TRACE_G(prm, slot)                                                                     \
+    do {                                                                                            \
+        if ((prm).trace != nullptr)                                                                 \
+            (prm).trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + TRACE_TILES - 1) * TRACE_SLOTS + \
+                        (slot)] = ptx::global_timer_ns();                                           \
+    } while (0)
+#define ETAP_TRACE_CLK(prm, slot)                                                                   \
+    do {                                                                                            \
+        if ((prm).trace != nullptr)                                                                 \
+            (prm).trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + TRACE_TILES - 1) * TRACE_SLOTS + \
+                        (slot)] = clock64();                                                        \
     } while (0)
 
 }  // namespace etap_b200

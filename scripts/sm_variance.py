@@ -10,7 +10,7 @@ TT = 256
 inp = inputs.make_mla_inputs([65536] * 16, heads=16, pad_value=0.0)
 plan = mla.MlaDecodePlan.create(16, 16, "cuda")
 n = plan.num_sm_parts
-buf = torch.zeros(n * TT * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(n * TT * 16, dtype=torch.int64, device="cuda")
 for _ in range(3):
     plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
 torch.cuda.synchronize()
@@ -21,8 +21,8 @@ for r in range(6):
     plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
     torch.cuda.synchronize()
     _lib.lib().etap_mla_debug_trace(None)
-    t = buf.view(n, TT, 8).cpu().numpy()
-    ent = t[:, TT - 1].astype(np.float64)
+    t = buf.view(n, TT, 16).cpu().numpy()
+    ent = (t[:, TT - 1] - t[:, TT - 1, 0].min()).astype(np.float64)  # int64 re-base: float64 ulp at 1.7e18 is 256
     span = (ent[:, 2] - ent[:, 0]) / 1e3
     smid = t[:, TT - 1, 3]
     runs.append((span, smid))

@@ -10,7 +10,7 @@ B, CTX = int(os.environ.get("B", 16)), int(os.environ.get("CTX", 1024))
 inp = inputs.make_mla_inputs([CTX] * B, heads=16, pad_value=0.0)
 plan = mla.MlaDecodePlan.create(B, 16, "cuda")
 n, TT, STEPS = plan.num_sm_parts, 256, 4
-k2 = [torch.zeros(n * TT * 8, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
+k2 = [torch.zeros(n * TT * 16, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
 k3 = [torch.zeros(B * 16 * 4, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
 L = _lib.lib()
 f = lambda: plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
@@ -22,12 +22,13 @@ for i in range(STEPS):  # back to back, a different trace buffer per step
     f()
 L.etap_mla_debug_trace(None); L.etap_mla_debug_trace_combine(None)
 torch.cuda.synchronize()
-t0 = None
+# re-base %globaltimer ns in int64 before float conversion (float64 ulp at 1.7e18 ns is 256 ns)
+gbase = int(k2[0].view(n, TT, 16)[:, TT - 1, 0].min().item())
+t0 = 0.0
 for i in range(STEPS):
-    a = k2[i].view(n, TT, 8).cpu().numpy()[:, TT - 1, :3].astype(np.float64)
-    c = k3[i].view(-1, 4).cpu().numpy()[:, :3].astype(np.float64)
-    c = c[c[:, 2] > 0]
-    if t0 is None: t0 = a[:, 0].min()
+    a = (k2[i].view(n, TT, 16).cpu().numpy()[:, TT - 1, :3] - gbase).astype(np.float64)
+    c = k3[i].view(-1, 4).cpu().numpy()[:, :3]
+    c = (c[c[:, 2] > 0] - gbase).astype(np.float64)
     r = lambda x: (x - t0) / 1e3
     print(f"step {i}: K2 entry {r(a[:,0].min()):7.2f}..{r(a[:,0].max()):7.2f}  sched-done med {r(np.median(a[:,1])):7.2f}  "
           f"exit med {r(np.median(a[:,2])):7.2f} max {r(a[:,2].max()):7.2f} | K3 entry min {r(c[:,0].min()):7.2f} "

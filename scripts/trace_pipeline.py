@@ -31,7 +31,7 @@ def main() -> None:
     inp = inputs.make_mla_inputs([a.ctx] * a.batch, heads=a.heads, pad_value=0.0)
     plan = mla.MlaDecodePlan.create(a.batch, a.heads, "cuda")
     nparts = plan.num_sm_parts
-    buf = torch.zeros(nparts * TRACE_TILES * 8, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(nparts * TRACE_TILES * 16, dtype=torch.int64, device="cuda")
     for _ in range(2):
         plan.metadata(inp.seqlens)
         plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
@@ -45,13 +45,18 @@ def main() -> None:
     torch.cuda.synchronize()
     _lib.lib().etap_mla_debug_trace(None)
     print(f"traced step: {e0.elapsed_time(e1) * 1000:.1f} us")
-    t = buf.view(nparts, TRACE_TILES, 8).cpu().numpy().astype(np.float64)
-    ent = t[:, TRACE_TILES - 1, :3].copy()
-    t[:, TRACE_TILES - 1, :] = 0
-    valid = (t > 0).all(axis=2)
+    raw = buf.view(nparts, TRACE_TILES, 16).cpu().numpy()
+    # re-base in int64 first: %globaltimer ns since the epoch (~1.7e18) has a float64 ulp of 256
+    gbase = raw[:, TRACE_TILES - 1, 0].min()
+    ent = (raw[:, TRACE_TILES - 1, :3] - gbase).astype(np.float64)
+    # tile rows are SM clock64 cycles: convert with each CTA's measured clock (row 255, 5/6)
+    ghz = (raw[:, TRACE_TILES - 1, 6] - raw[:, TRACE_TILES - 1, 5]).astype(np.float64) / np.maximum(1.0, ent[:, 2] - ent[:, 0])
+    print(f"SM clock during the step: {np.median(ghz):.3f} GHz (median over CTAs)")
+    valid = (raw[:, :TRACE_TILES - 1, :8] > 0).all(axis=2)
+    # cycles -> ns on each CTA's clock, re-based to the CTA's global entry time
+    t = (raw[:, :TRACE_TILES - 1, :] - raw[:, TRACE_TILES - 1, 5][:, None, None]).astype(np.float64)
+    t = t / ghz[:, None, None] + ent[:, 0][:, None, None]
     t0 = t[valid].min()
-    names = ["issue_first", "issue_last", "landed_last", "S_commit", "softmax_start", "P_written",
-             "mma_sees_P", "G2_commit"]
     rows = []
     for c in range(nparts):
         n = int(valid[c].sum())
@@ -63,22 +68,26 @@ def main() -> None:
                 e[1] - e[0],            # producer: span issuing the tile's 9 chunks
                 e[3] - e[2],            # GEMM1 tail issue after last chunk
                 e[4] - e[3],            # S commit -> softmax sees S (GEMM1 execution)
-                e[5] - e[4],            # softmax duration
+                e[8] - e[4],            # softmax: S -> exp done
+                e[9] - e[8],            # softmax: wait for the P buffer (GEMM2 of tile g-2)
+                e[5] - e[9],            # softmax: P write + fences
                 e[6] - e[5],            # P written -> MMA sees it
                 e[7] - e[6],            # GEMM2 issue
                 nxt[3] - e[3],          # tile period
                 nxt[0] - e[7],          # GEMM2(g) commit -> producer issues first chunk of g+1
                 nxt[1] - e[7],          # GEMM2(g) commit -> producer issued last chunk of g+1
+                nxt[4] - e[5],          # softmax idle: P(g) written -> sees S(g+1)
             ])
-    r = np.array(rows) if rows else np.zeros((0, 10))
-    labels = ["lat_tile(last issue->seen)", "issue_span", "g1_issue", "s_ready_wait", "softmax", "p_to_mma",
-              "g2_issue", "PERIOD", "g2->next_first_issue", "g2->next_last_issue"]
+    r = np.array(rows) if rows else np.zeros((0, 13))
+    labels = ["lat_tile(last issue->seen)", "issue_span", "g1_issue", "s_ready_wait", "softmax_exp",
+              "softmax_pbuf_wait", "softmax_pwrite", "p_to_mma", "g2_issue", "PERIOD", "g2->next_first_issue",
+              "g2->next_last_issue", "softmax_idle"]
     print(f"{len(rows)} steady-state tiles over {nparts} CTAs (ns): median / p10 / p90")
     for i, lab in enumerate(labels):
         if not len(r):
             break
         col = r[:, i]
-        print(f"  {lab:24s} {np.median(col):9.0f} {np.percentile(col, 10):9.0f} {np.percentile(col, 90):9.0f}")
+        print(f"  {lab:26s} {np.median(col):9.0f} {np.percentile(col, 10):9.0f} {np.percentile(col, 90):9.0f}")
     # first tile of every working CTA, relative to kernel entry (us)
     first = [(t[c, 0] - ent[c, 0]) / 1e3 for c in range(nparts) if valid[c, 0]]
     if first:
