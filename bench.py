@@ -220,10 +220,26 @@ def run_ours(args) -> None:
     out = torch.empty((BATCH, 1, HEADS, 512), dtype=torch.float32, device=dev)
     lse = torch.empty((BATCH, 1, HEADS), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    # N > 1: the all-gather of O is fused into the kernels over NVLink peer memory
+    # (etap_mla_decode_peer) when every local GPU pair has peer access; ETAP_GATHER=nccl (or no
+    # peer access) uses decode + ncclAllGather instead
+    gather = None
+    if world > 1:
+        gather = os.environ.get("ETAP_GATHER", "peer")
+        ndev = torch.cuda.device_count()
+        if gather == "peer" and not all(torch.cuda.can_device_access_peer(gpu, d) for d in range(ndev) if d != gpu):
+            log("[bench] no peer access between all GPUs: falling back to NCCL all-gather")
+            gather = "nccl"
+        if gather == "peer":
+            from paper_2506_01969_b200 import peer
+
+            pg = peer.PeerGather(BATCH, HEADS, world, rank, device=dev)
 
     def step():
         # K2 computes the split schedule in its prologue (same partition as K1, which is the
         # per-step metadata call of the API and is off the critical path here) + K3 combine
+        if gather == "peer":  # K2 + K3 store every rank's copy, K4 = arrival flags
+            return pg.decode(plan, inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
         plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, out=out, lse=lse)
         if world > 1:  # head-sharded output -> all 16*N heads on every rank (NCCL all-gather)
             return sharding.gather_heads(out), sharding.gather_heads(lse)
@@ -291,9 +307,11 @@ def run_ours(args) -> None:
             "config": {"workload": WORKLOAD, "batch": BATCH, "ctx": CTX, "heads_per_gpu": HEADS,
                        "total_heads": total_heads, "dist_backend": backend if world > 1 else None, "d_qk": 576, "d_v": 512, "page_rows": 64,
                        "kv_bytes_per_gpu": inp.kv_bytes(), "l2": "inputs (1.2 GB KV) > 126 MB L2, no flush",
-                       "parallelism": f"head-shard tp{world} (KV replicated, NCCL all-gather of O)" if world > 1
+                       "parallelism": (f"head-shard tp{world} (KV replicated, all-gather of O fused into K2/K3 "
+                                       "over NVLink peer memory)" if gather == "peer" else
+                                       f"head-shard tp{world} (KV replicated, NCCL all-gather of O)") if world > 1
                        else "single GPU", "step": "K2 decode (in-kernel split schedule) + K3 combine" +
-                       (" + all-gather(O)" if world > 1 else "")},
+                       ((" + K4 peer arrival" if gather == "peer" else " + NCCL all-gather(O)") if world > 1 else "")},
             "throughput": {"hbm_gbs_aggregate": nbytes * world / (us * 1e-6) / 1e9,
                            "hbm_gbs_per_gpu": nbytes / (us * 1e-6) / 1e9,
                            "tflops_aggregate": nflops * world / (us * 1e-6) / 1e12,
@@ -303,13 +321,15 @@ def run_ours(args) -> None:
                          "kernel_avg_us": k2_avg_ms * 1e3, "peak_kind": peak_kind,
                          "timing": f"second timed pass of {args.steps} steps, CUDA events around each K2 launch"},
             "clocks": clocks,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": (3 if gather == "peer" else 2) * args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
         print(json.dumps(result), flush=True)
     if world > 1:
         barrier()
+        if gather == "peer":
+            pg.close()
         dist.destroy_process_group()
 
 

@@ -120,6 +120,49 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
                     const int32_t* sched, const int32_t* split_off, int num_sm_parts,
                     void* workspace, float* out, float* lse, unsigned flags, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Head-sharded decode with a fused all-gather over NVLink peer memory (each
+ * rank owns heads [head_offset, head_offset + heads) against the replicated latent KV; the
+ * only exchange is the all-gather of O / LSE, which the reference lacks: single process).
+ * Instead of a decode followed by ncclAllGather, K2's epilogue and K3 store every finished
+ * O / LSE row straight into every rank's full-head output buffer (peer-mapped through CUDA
+ * IPC), then a one-warp kernel publishes `epoch` into every rank's arrival words (release,
+ * system scope) and waits until every rank's word in its own array reached `epoch` (acquire).
+ * On return (stream order) this rank's out[rank] / lse[rank] hold all heads_total heads.
+ * Buffers: out [batch][q_tokens][heads_total][512] fp32, lse [batch][q_tokens][heads_total]
+ * fp32, flags ETAP_MLA_MAX_PEERS uint32 zero-initialised; epochs are nonzero and increase
+ * per call. A caller that reuses one output buffer must not start call k+1 on any rank before
+ * every rank consumed call k (alternate two buffer sets by epoch parity to avoid that).
+ * ------------------------------------------------------------------------------------- */
+#define ETAP_MLA_MAX_PEERS 8
+#define ETAP_MLA_IPC_HANDLE_BYTES 64
+
+typedef struct etap_mla_peer_gather {
+    int world;        /* ranks sharing the output, 1..ETAP_MLA_MAX_PEERS */
+    int rank;         /* this rank */
+    int heads_total;  /* heads per token over all ranks */
+    int head_offset;  /* first head of this rank */
+    float* out[ETAP_MLA_MAX_PEERS];     /* rank r's full output, mapped in this process */
+    float* lse[ETAP_MLA_MAX_PEERS];
+    uint32_t* flags[ETAP_MLA_MAX_PEERS]; /* rank r's arrival words */
+} etap_mla_peer_gather;
+
+/* etap_mla_decode + fused all-gather (see above); out / lse come from `pg`. */
+int etap_mla_decode_peer(const void* q, const void* kv_pool, int64_t num_pages,
+                         const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,
+                         int batch, int q_tokens, int heads, float scale, int causal,
+                         const int32_t* sched, const int32_t* split_off, int num_sm_parts,
+                         void* workspace, const etap_mla_peer_gather* pg, uint32_t epoch,
+                         unsigned flags, void* stream);
+
+/* CUDA IPC plumbing for the peer buffers: allocate a zeroed device buffer on the current
+ * device and export its handle (ETAP_MLA_IPC_HANDLE_BYTES bytes); map a peer's handle into
+ * this process (peer access enabled lazily); unmap; free. */
+int etap_mla_ipc_alloc(size_t bytes, void** dev_ptr, void* handle);
+int etap_mla_ipc_open(const void* handle, void** dev_ptr);
+int etap_mla_ipc_close(void* dev_ptr);
+int etap_mla_ipc_free(void* dev_ptr);
+
 /* K3 alone — log-sum-exp merge of the split partials left in `workspace` by a decode call
  * made with ETAP_FLAG_SKIP_COMBINE (same batch/heads/num_sm_parts/split_off). */
 int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_parts,

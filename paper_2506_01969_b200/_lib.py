@@ -46,6 +46,12 @@ def _declare(lib: C.CDLL) -> None:
         "etap_mla_decode": (i32, [vp, vp, i64, vp, i32, vp, i32, i32, i32, f32, i32, vp, vp, i32,
                                   vp, vp, vp, u32, vp]),
         "etap_mla_combine": (i32, [vp, i32, i32, i32, vp, vp, vp, vp]),
+        "etap_mla_decode_peer": (i32, [vp, vp, i64, vp, i32, vp, i32, i32, i32, f32, i32, vp, vp, i32,
+                                       vp, vp, u32, u32, vp]),
+        "etap_mla_ipc_alloc": (i32, [sz, P(vp), vp]),
+        "etap_mla_ipc_open": (i32, [vp, P(vp)]),
+        "etap_mla_ipc_close": (i32, [vp]),
+        "etap_mla_ipc_free": (i32, [vp]),
         "etap_mla_host_ctx_create": (i32, [i32, i32, i64, i32, P(vp)]),
         "etap_mla_host_decode": (i32, [vp, vp, vp, vp, vp, f32, u32, vp, vp]),
         "etap_mla_host_ctx_destroy": (None, [vp]),

@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         float* red_sum = red_max + 8 * HG;                               // [4][HG]
         float* s_m = red_sum + 4 * HG;         // [HG] running max per head (log2 units)
         float* s_alpha = s_m + HG;             // [HG] rescale factors of the current tile
+        int* s_row = reinterpret_cast<int*>(s_alpha + HG);  // [HG] output row of each head (epilogue)
         const bool negate = prm.flags & FLAG_NEGATE_RESCALE;
         const bool eager = negate || (prm.flags & FLAG_EAGER_RESCALE);
         const float thresh = eager ? 0.f : LAZY_RESCALE_LOG2;
@@ -717,6 +718,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tc_fence_after();
             const float wsum = halfwarp_reduce<false, HH>(l_part, lane);
             if (rwriter) red_sum[wq * HG + half * HH + rhead] = wsum;
+            const int ns = soff[vb + 1] - soff[vb];
+            const bool direct = ns == 1;  // one split: final O / L rows, else a split partial
+            if (direct && wq == 0 && lane < HG) s_row[lane] = static_cast<int>(prm.om.row(sd.b, sd.g * HG + lane));
             ptx::named_bar_sync(2, 128);
             float inv_l[HG];
 #pragma unroll
@@ -724,18 +728,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const float l = red_sum[h] + red_sum[HG + h] + red_sum[2 * HG + h] + red_sum[3 * HG + h];
                 inv_l[h] = l > 0.f ? 1.f / l : 0.f;  // l = 0: column saw no row (O = 0, L = -inf)
             }
-            const int ns = soff[vb + 1] - soff[vb];
             const int idx = (vb == sch[0]) ? sch[4] : soff[vb] + idx_off;  // partial index (ns > 1)
-            float* dst;
-            float* dst_lse;
-            if (ns == 1) {
-                const size_t hrow = static_cast<size_t>(sd.b) * prm.heads + sd.g * HG;
-                dst = prm.out + hrow * D_V;
-                dst_lse = prm.lse + hrow;
-            } else {
-                dst = prm.ws_o + static_cast<size_t>(idx) * HG * D_V;
-                dst_lse = prm.ws_lse + static_cast<size_t>(idx) * HG;
-            }
+            float* part_o = prm.ws_o + static_cast<size_t>(idx) * HG * D_V;
             const int drow = wq * 32 + lane;  // M=128 layout: d row = TMEM lane
 #pragma unroll 1
             for (int blk = 0; blk < 4; ++blk) {
@@ -746,13 +740,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                    *reinterpret_cast<uint32_t(*)[32]>(o + 32 * part));
                 ptx::tmem_wait_ld();
                 const int d = blk * 128 + drow;
+                float v[HG];
 #pragma unroll
-                for (int h = 0; h < HG; ++h)
-                    dst[h * D_V + d] = (__uint_as_float(o[h]) + __uint_as_float(o[HG + h])) * inv_l[h];
+                for (int h = 0; h < HG; ++h) v[h] = (__uint_as_float(o[h]) + __uint_as_float(o[HG + h])) * inv_l[h];
+                if (direct) {
+                    // every output copy (peer gather: each rank's buffer over NVLink)
+#pragma unroll 1
+                    for (int r = 0; r < prm.om.n_out; ++r) {
+                        float* dst = prm.om.out[r] + d;
+#pragma unroll
+                        for (int h = 0; h < HG; ++h) dst[static_cast<size_t>(s_row[h]) * D_V] = v[h];
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < HG; ++h) part_o[h * D_V + d] = v[h];
+                }
             }
             if (wq == 0 && lane < HG) {
                 const float l = red_sum[lane] + red_sum[HG + lane] + red_sum[2 * HG + lane] + red_sum[3 * HG + lane];
-                dst_lse[lane] = (s_m[lane] + log2f(l)) * 0.69314718055994530942f;
+                const float L = (s_m[lane] + log2f(l)) * 0.69314718055994530942f;
+                if (direct) {
+                    for (int r = 0; r < prm.om.n_out; ++r) prm.om.lse[r][s_row[lane]] = L;
+                } else {
+                    prm.ws_lse[static_cast<size_t>(idx) * HG + lane] = L;
+                }
             }
             ptx::tc_fence_before();
             // red_sum / s_m are rewritten by the next split only after this barrier
@@ -787,9 +798,8 @@ constexpr int COMBINE_BATCH = 16;  // partial float4 loads in flight per thread
 
 __global__ void __launch_bounds__(COMBINE_THREADS)
     etap_mla_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
-                            const int32_t* __restrict__ split_off, int hg, int batch, int heads,
-                            float* __restrict__ out, float* __restrict__ lse,
-                            unsigned long long* trace) {
+                            const int32_t* __restrict__ split_off, int hg, int batch,
+                            const __grid_constant__ OutMap om, unsigned long long* trace) {
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 0] = ptx::global_timer_ns();
     ptx::grid_dep_wait();
     ptx::grid_dep_launch();  // the next decode step's prologue may overlap this combine
@@ -803,11 +813,12 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
         if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 2] = ptx::global_timer_ns();
         return;
     }
-    const size_t hrow = static_cast<size_t>(b) * heads + g * hg + h;
-    float4* o4 = reinterpret_cast<float4*>(out + hrow * D_V);
+    const size_t orow = om.row(b, g * hg + h);
     if (ns <= 0) {  // empty context: O = 0, L = -inf
-        o4[threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (threadIdx.x == 0) lse[hrow] = -INFINITY;
+        for (int r = 0; r < om.n_out; ++r) {
+            reinterpret_cast<float4*>(om.out[r] + orow * D_V)[threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (threadIdx.x == 0) om.lse[r][orow] = -INFINITY;
+        }
         return;
     }
     // One round trip after split_off: every thread issues all of its partial loads (one float4
@@ -852,8 +863,10 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
     }
     const float inv = sum > 0.f ? 1.f / sum : 0.f;
     acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
-    if (threadIdx.x == 0) lse[hrow] = mx + logf(sum);
-    o4[threadIdx.x] = acc;
+    for (int r = 0; r < om.n_out; ++r) {  // every output copy (peer gather: each rank's buffer)
+        if (threadIdx.x == 0) om.lse[r][orow] = mx + logf(sum);
+        reinterpret_cast<float4*>(om.out[r] + orow * D_V)[threadIdx.x] = acc;
+    }
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 2] = ptx::global_timer_ns();
 }
 
@@ -1211,13 +1224,52 @@ int etap_mla_metadata(const int32_t* seqlens, int batch, int heads, int num_sm_p
     return ETAP_OK;
 }
 
-int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
-                    const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,
-                    int batch, int q_tokens, int heads_per_token, float scale, int causal,
-                    const int32_t* sched, const int32_t* split_off, int num_sm_parts,
-                    void* workspace, float* out, float* lse, unsigned flags, void* stream) {
-    if (!q || !kv_pool || !block_table || !seqlens || !sched || !split_off || !workspace ||
-        !out || !lse)
+}  // extern "C"
+
+namespace {
+
+OutMap local_outmap(int heads, float* out, float* lse) {
+    OutMap om = {};
+    om.q_tokens = 1;
+    om.heads_per_token = heads;  // tokens folded: [B][T][H] rows are [B][T*H] rows
+    om.out_heads = heads;
+    om.out_head0 = 0;
+    om.n_out = 1;
+    om.out[0] = out;
+    om.lse[0] = lse;
+    return om;
+}
+
+int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_parts, void* workspace,
+                 const OutMap& om, void* stream) {
+    const int hg = head_group_of(heads);
+    const int groups = heads / hg;
+    const size_t np = max_partials(batch, heads, num_sm_parts);
+    float* ws_o = static_cast<float*>(workspace);
+    float* ws_lse = ws_o + np * hg * D_V;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg2 = {};
+    cfg2.gridDim = dim3(batch * groups * hg);
+    cfg2.blockDim = dim3(COMBINE_THREADS);
+    cfg2.dynamicSmemBytes = 0;
+    cfg2.stream = static_cast<cudaStream_t>(stream);
+    cfg2.attrs = attr;
+    cfg2.numAttrs = 1;
+    ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, static_cast<const float*>(ws_o),
+                                 static_cast<const float*>(ws_lse), split_off, hg, batch, om,
+                                 static_cast<unsigned long long*>(g_combine_trace_buf)));
+    return ETAP_OK;
+}
+
+// K2 (+ K3 unless SKIP_COMBINE) for one call; final rows go wherever `om` says.
+int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int32_t* block_table,
+                int max_pages_per_seq, const int32_t* seqlens, int batch, int q_tokens,
+                int heads_per_token, float scale, int causal, const int32_t* sched,
+                const int32_t* split_off, int num_sm_parts, void* workspace, const OutMap& om,
+                unsigned flags, void* stream) {
+    if (!q || !kv_pool || !block_table || !seqlens || !sched || !split_off || !workspace)
         return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
     if (q_tokens < 1 || q_tokens > ETAP_MLA_MAX_Q_TOKENS)
         return fail(ETAP_ERR_SHAPE, "q_tokens must be in [1, " + std::to_string(ETAP_MLA_MAX_Q_TOKENS) + "]");
@@ -1245,12 +1297,10 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     const size_t np = max_partials(batch, heads, num_sm_parts);
     DecodeParams prm;
     prm.block_table = block_table;
-
     prm.seqlens = seqlens;
     prm.sched = sched;
     prm.split_off = split_off;
-    prm.out = out;
-    prm.lse = lse;
+    prm.om = om;
     prm.ws_o = static_cast<float*>(workspace);
     prm.ws_lse = prm.ws_o + np * hg * D_V;
     prm.max_pages = max_pages_per_seq;
@@ -1301,7 +1351,61 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
     }
 
     if (flags & ETAP_FLAG_SKIP_COMBINE) return ETAP_OK;
-    return etap_mla_combine(split_off, batch, heads, num_sm_parts, workspace, out, lse, stream);
+    return combine_impl(split_off, batch, heads, num_sm_parts, workspace, om, stream);
+}
+
+}  // namespace
+
+namespace etap_b200 {
+int peer_signal_wait(const etap_mla_peer_gather* pg, uint32_t epoch, void* stream);  // etap_peer.cu
+}
+
+extern "C" {
+
+int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
+                    const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,
+                    int batch, int q_tokens, int heads_per_token, float scale, int causal,
+                    const int32_t* sched, const int32_t* split_off, int num_sm_parts,
+                    void* workspace, float* out, float* lse, unsigned flags, void* stream) {
+    if (!out || !lse) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    const OutMap om = local_outmap(q_tokens * heads_per_token, out, lse);
+    return decode_impl(q, kv_pool, num_pages, block_table, max_pages_per_seq, seqlens, batch, q_tokens,
+                       heads_per_token, scale, causal, sched, split_off, num_sm_parts, workspace, om,
+                       flags, stream);
+}
+
+int etap_mla_decode_peer(const void* q, const void* kv_pool, int64_t num_pages,
+                         const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,
+                         int batch, int q_tokens, int heads_per_token, float scale, int causal,
+                         const int32_t* sched, const int32_t* split_off, int num_sm_parts,
+                         void* workspace, const etap_mla_peer_gather* pg, uint32_t epoch,
+                         unsigned flags, void* stream) {
+    if (!pg) return fail(ETAP_ERR_SHAPE, "peer gather descriptor is NULL");
+    if (pg->world < 1 || pg->world > ETAP_MLA_MAX_PEERS || pg->rank < 0 || pg->rank >= pg->world)
+        return fail(ETAP_ERR_SHAPE, "peer gather: world must be in [1, 8] and 0 <= rank < world");
+    if (pg->head_offset < 0 || pg->head_offset + heads_per_token > pg->heads_total)
+        return fail(ETAP_ERR_SHAPE, "peer gather: head_offset + heads exceeds heads_total");
+    if (flags & ETAP_FLAG_SKIP_COMBINE) return fail(ETAP_ERR_SHAPE, "peer gather: SKIP_COMBINE not allowed");
+    if (epoch == 0) return fail(ETAP_ERR_SHAPE, "peer gather: epoch must be nonzero");
+    OutMap om = {};
+    om.q_tokens = q_tokens;
+    om.heads_per_token = heads_per_token;
+    om.out_heads = pg->heads_total;
+    om.out_head0 = pg->head_offset;
+    om.n_out = pg->world;
+    for (int r = 0; r < pg->world; ++r) {
+        if (!pg->out[r] || !pg->lse[r] || !pg->flags[r])
+            return fail(ETAP_ERR_SHAPE, "peer gather: NULL output / flag pointer");
+        // own copy first: the local rows are written before the remote ones
+        const int src = (pg->rank + r) % pg->world;
+        om.out[r] = pg->out[src];
+        om.lse[r] = pg->lse[src];
+    }
+    if (int rc = decode_impl(q, kv_pool, num_pages, block_table, max_pages_per_seq, seqlens, batch,
+                             q_tokens, heads_per_token, scale, causal, sched, split_off, num_sm_parts,
+                             workspace, om, flags, stream))
+        return rc;
+    return etap_b200::peer_signal_wait(pg, epoch, stream);
 }
 
 int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_parts,
@@ -1309,25 +1413,7 @@ int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_
     if (!split_off || !workspace || !out || !lse) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
     if (batch < 1 || !heads_ok(heads) || num_sm_parts < 1)
         return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
-    const int hg = head_group_of(heads);
-    const int groups = heads / hg;
-    const size_t np = max_partials(batch, heads, num_sm_parts);
-    float* ws_o = static_cast<float*>(workspace);
-    float* ws_lse = ws_o + np * hg * D_V;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cudaLaunchConfig_t cfg2 = {};
-    cfg2.gridDim = dim3(batch * groups * hg);
-    cfg2.blockDim = dim3(COMBINE_THREADS);
-    cfg2.dynamicSmemBytes = 0;
-    cfg2.stream = static_cast<cudaStream_t>(stream);
-    cfg2.attrs = attr;
-    cfg2.numAttrs = 1;
-    ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, static_cast<const float*>(ws_o),
-                                 static_cast<const float*>(ws_lse), split_off, hg, batch, heads, out, lse,
-                                 static_cast<unsigned long long*>(g_combine_trace_buf)));
-    return ETAP_OK;
+    return combine_impl(split_off, batch, heads, num_sm_parts, workspace, local_outmap(heads, out, lse), stream);
 }
 
 int etap_mla_debug_state(void* device_buf, int max_tiles) {

@@ -89,8 +89,8 @@ struct Cfg {
     static constexpr int OFF_RING = 0;
     static constexpr int OFF_Q = OFF_RING + NSLOT * SLOT_BYTES;
     static constexpr int OFF_P = OFF_Q + Q_BYTES;        // 2 buffers
-    static constexpr int OFF_RED = OFF_P + 2 * P_BYTES;  // red_max[2][4][HG], red_sum[4][HG], m[HG], alpha[HG]
-    static constexpr int RED_FLOATS = 2 * 4 * HG + 4 * HG + HG + HG;
+    static constexpr int OFF_RED = OFF_P + 2 * P_BYTES;  // red_max[2][4][HG], red_sum[4][HG], m[HG], alpha[HG], row[HG]
+    static constexpr int RED_FLOATS = 2 * 4 * HG + 4 * HG + HG + HG + HG;  // + output row per head
     static constexpr int OFF_BAR = align_up(OFF_RED + RED_FLOATS * 4, 16);
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr int OFF_SCHED = OFF_TMEM + 16;
@@ -267,6 +267,22 @@ __host__ __device__ inline LineShape line_shape(int batch, int groups, int parts
     return s;
 }
 
+// Where final O / LSE rows go. Query row f (tokens folded into heads) of sequence b lands at
+// output row (b * q_tokens + f / heads_per_token) * out_heads + out_head0 + f % heads_per_token
+// of every one of the n_out copies: one local buffer, or (peer gather, fused all-gather of a
+// head-sharded decode) every rank's full-head buffer through peer-mapped NVLink memory.
+constexpr int MAX_OUT_COPIES = 8;
+struct OutMap {
+    int q_tokens, heads_per_token, out_heads, out_head0, n_out;
+    float* out[MAX_OUT_COPIES];
+    float* lse[MAX_OUT_COPIES];
+
+    __device__ __forceinline__ size_t row(int b, int f) const {
+        const int tok = f / heads_per_token;
+        return (static_cast<size_t>(b) * q_tokens + tok) * out_heads + out_head0 + (f - tok * heads_per_token);
+    }
+};
+
 struct DecodeParams {
     const int32_t* block_table;
     const int32_t* seqlens;
@@ -274,8 +290,7 @@ struct DecodeParams {
     const int32_t* split_off;
     int32_t* sched_out;      // in-kernel schedule published here (same buffers as K1 writes)
     int32_t* split_off_out;
-    float* out;
-    float* lse;
+    OutMap om;               // final outputs (sequences finished by one split)
     float* ws_o;
     float* ws_lse;
     int max_pages;

@@ -145,3 +145,24 @@ def test_host_metadata_partition_invariants():
         active = lanes * p_line
         if total >= active * 4:
             assert max(work) <= total / active + 4  # balanced to within the per-split overhead
+
+
+def test_peer_gather_descriptor_and_validation():
+    """etap_mla_peer_gather (include/etap_mla.h) as seen from Python, and the fused-all-gather
+    entry point rejecting bad descriptors before touching the device."""
+    from paper_2506_01969_b200 import peer
+
+    assert C.sizeof(peer.PeerGatherDesc) == 4 * 4 + 3 * 8 * 8
+    L = _lib.lib()
+    d = peer.PeerGatherDesc()
+    d.world, d.rank, d.heads_total, d.head_offset = 9, 0, 128, 0
+    args = (1, 1, 1, 1, 1, 1, 1, 1, 16, 1.0, 1, 1, 1, 148, 1)
+    assert L.etap_mla_decode_peer(*args, C.byref(d), 1, 0, None) == _lib.ETAP_ERR_SHAPE
+    assert "world" in _lib.last_error()
+    d.world, d.rank, d.head_offset = 2, 1, 120
+    assert L.etap_mla_decode_peer(*args, C.byref(d), 1, 0, None) == _lib.ETAP_ERR_SHAPE
+    assert "head_offset" in _lib.last_error()
+    d.head_offset = 16
+    assert L.etap_mla_decode_peer(*args, C.byref(d), 0, 0, None) == _lib.ETAP_ERR_SHAPE
+    assert "epoch" in _lib.last_error()
+    assert L.etap_mla_decode_peer(*args, None, 1, 0, None) == _lib.ETAP_ERR_SHAPE
