@@ -574,6 +574,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 l_part[j] = 0.f;
                 const int tok = (sd.g * HG + half * HH + j) / prm.heads_per_token;
                 row_lim[j] = sd.seqlen - (prm.causal ? prm.q_tokens - 1 - tok : 0);
+                // a split whose first tile shows no row to any column skips the max exchange
+                // (bar.red.or is false), so s_m must already read -inf for the epilogue
+                // (the previous split's epilogue released s_m with its final barrier)
+                if (head_owner) s_m[half * HH + j] = -INFINITY;
             }
 
             for (int t = sd.t0; t < sd.t1; ++t) {
