@@ -26,10 +26,21 @@ torch.cuda.synchronize()
 gbase = int(k2[0].view(n, TT, 16)[:, TT - 1, 0].min().item())
 t0 = 0.0
 for i in range(STEPS):
-    a = (k2[i].view(n, TT, 16).cpu().numpy()[:, TT - 1, :3] - gbase).astype(np.float64)
+    g = k2[i].view(n, TT, 16).cpu().numpy()[:, TT - 1, :]
+    a = (g[:, :3] - gbase).astype(np.float64)
+    ex = (g[:, 7:12] - gbase).astype(np.float64)  # dep-wait done, seqlens in, first KV TMA, last epilogue, softmax done
     c = k3[i].view(-1, 4).cpu().numpy()[:, :3]
     c = (c[c[:, 2] > 0] - gbase).astype(np.float64)
     r = lambda x: (x - t0) / 1e3
     print(f"step {i}: K2 entry {r(a[:,0].min()):7.2f}..{r(a[:,0].max()):7.2f}  sched-done med {r(np.median(a[:,1])):7.2f}  "
           f"exit med {r(np.median(a[:,2])):7.2f} max {r(a[:,2].max()):7.2f} | K3 entry min {r(c[:,0].min()):7.2f} "
           f"wait-release min {r(c[:,1].min()):7.2f} exit max {r(c[:,2].max()):7.2f}")
+    m = lambda j: r(np.median(ex[:, j]))
+    print(f"        dep-wait done med {m(0):7.2f} (min {r(ex[:,0].min()):7.2f})  seqlens-in med {m(1):7.2f}  "
+          f"first-KV-TMA med {m(2):7.2f}  last-epilogue med {m(3):7.2f}  softmax-done med {m(4):7.2f}")
+    ck = g[:, 12:16].astype(np.int64)
+    d = np.median(ck[:, 1:] - ck[:, :1], axis=0)
+    print(f"        clock64 after dep-wait: seqlens-in +{d[0]:.0f}  sched-done +{d[1]:.0f}  first-KV-TMA +{d[2]:.0f} cycles")
+    m = lambda j: r(np.median(ex[:, j]))
+    print(f"        dep-wait done med {m(0):7.2f} (min {r(ex[:,0].min()):7.2f})  seqlens-in med {m(1):7.2f}  "
+          f"first-KV-TMA med {m(2):7.2f}  last-epilogue med {m(3):7.2f}  softmax-done med {m(4):7.2f}")
