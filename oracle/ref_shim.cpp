@@ -18,6 +18,7 @@
 #include "etaplab/matrix.hpp"
 #include "etaplab/matrix_io.hpp"
 #include "etaplab/tiled_standard.hpp"
+#include "etaplab/wgmma_model.hpp"
 
 using namespace etaplab;
 
@@ -185,6 +186,29 @@ double ref_mla_run_etap_batch(const double* q, const double* kv, std::int64_t ba
         return std::chrono::duration<double>(t1 - t0).count();
     } catch (const std::exception&) {
         return -1.0;
+    }
+}
+
+// utilization / predicted_speedup (wgmma_model.cpp:54-86) with the given WgmmaSpec.
+// out = {useful_macs, issued_macs, utilization, qk m-axis util, pv m-axis util, speedup}
+int ref_wgmma_model(int mode, std::int64_t heads, std::int64_t q_tokens, std::int64_t kv_len,
+                    std::int64_t d_qk, std::int64_t d_v, std::int64_t batch, std::int64_t m_min,
+                    std::int64_t n_step, std::int64_t k_step, double* out) {
+    try {
+        DecodeShape s;
+        s.heads = heads; s.q_tokens = q_tokens; s.kv_len = kv_len; s.d_qk = d_qk; s.d_v = d_v; s.batch = batch;
+        WgmmaSpec w;
+        w.m_min = m_min; w.n_step = n_step; w.k_step = k_step;
+        const UtilizationReport r = utilization(mode == 1 ? ComputeMode::etap : ComputeMode::original, s, w);
+        out[0] = static_cast<double>(r.useful_macs);
+        out[1] = static_cast<double>(r.issued_macs);
+        out[2] = r.utilization;
+        out[3] = r.qk.m_axis_utilization();
+        out[4] = r.pv.m_axis_utilization();
+        out[5] = predicted_speedup(s, w);
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
     }
 }
 

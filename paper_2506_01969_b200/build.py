@@ -20,6 +20,7 @@ CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libetap_mla.so"
 BENCH = LIBDIR / "etap_bench"
+MODEL = LIBDIR / "etap_model"
 
 SOURCES = [CSRC / "etap_mla.cu", CSRC / "etap_peer.cu", CSRC / "etap_mla_host.cpp"]
 DEPS = SOURCES + [CSRC / "etap_bench.cpp", CSRC / "sm100_ptx.cuh", CSRC / "etap_mla_kernels.cuh", ROOT / "include" / "etap_mla.h"]
@@ -74,7 +75,23 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("etap_bench build failed")
+    build_model()
     return LIB
+
+
+def build_model() -> Path:
+    """Host-only tool: the reference's `etaplab model` report for tcgen05 (no CUDA)."""
+    src = CSRC / "etap_model.cpp"
+    hdr = ROOT / "include" / "etaplab_b200_umma.hpp"
+    if MODEL.exists() and MODEL.stat().st_mtime >= max(src.stat().st_mtime, hdr.stat().st_mtime):
+        return MODEL
+    LIBDIR.mkdir(exist_ok=True)
+    cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
+    res = subprocess.run([cxx, "-O2", "-std=c++17", "-Wall", str(src), "-o", str(MODEL)], capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("etap_model build failed")
+    return MODEL
 
 
 if __name__ == "__main__":
