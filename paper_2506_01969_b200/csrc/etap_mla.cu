@@ -776,29 +776,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int idx = (vb == sch[0]) ? sch[4] : soff[vb] + idx_off;  // partial index (ns > 1)
             float* part_o = prm.ws_o + static_cast<size_t>(idx) * HG * D_V;
             const int drow = wq * 32 + lane;  // M=128 layout: d row = TMEM lane
+            // BPW d-blocks per TMEM load wait (HG = 16: two blocks = 64 registers in flight)
+            constexpr int BPW = HG == 16 ? 2 : 1;
 #pragma unroll 1
-            for (int blk = 0; blk < 4; ++blk) {
-                uint32_t o[2 * HG];
+            for (int blk0 = 0; blk0 < 4; blk0 += BPW) {
+                uint32_t o[BPW][2 * HG];
 #pragma unroll
-                for (int part = 0; part < 2 * HG / 32; ++part)
-                    ptx::tmem_ld32(t_lane + C::TCOL_O + C::OBLK * blk + 32 * part,
-                                   *reinterpret_cast<uint32_t(*)[32]>(o + 32 * part));
+                for (int bb = 0; bb < BPW; ++bb)
+#pragma unroll
+                    for (int part = 0; part < 2 * HG / 32; ++part)
+                        ptx::tmem_ld32(t_lane + C::TCOL_O + C::OBLK * (blk0 + bb) + 32 * part,
+                                       *reinterpret_cast<uint32_t(*)[32]>(&o[bb][32 * part]));
                 ptx::tmem_wait_ld();
-                const int d = blk * 128 + drow;
-                float v[HG];
 #pragma unroll
-                for (int h = 0; h < HG; ++h) v[h] = (__uint_as_float(o[h]) + __uint_as_float(o[HG + h])) * inv_l[h];
-                if (direct) {
-                    // every output copy (peer gather: each rank's buffer over NVLink)
+                for (int bb = 0; bb < BPW; ++bb) {
+                    const int d = (blk0 + bb) * 128 + drow;
+                    float v[HG];
+#pragma unroll
+                    for (int h = 0; h < HG; ++h)
+                        v[h] = (__uint_as_float(o[bb][h]) + __uint_as_float(o[bb][HG + h])) * inv_l[h];
+                    if (direct) {
+                        // every output copy (peer gather: each rank's buffer over NVLink)
 #pragma unroll 1
-                    for (int r = 0; r < prm.om.n_out; ++r) {
-                        float* dst = prm.om.out[r] + d;
+                        for (int r = 0; r < prm.om.n_out; ++r) {
+                            float* dst = prm.om.out[r] + d;
 #pragma unroll
-                        for (int h = 0; h < HG; ++h) dst[static_cast<size_t>(s_row[h]) * D_V] = v[h];
+                            for (int h = 0; h < HG; ++h) dst[static_cast<size_t>(s_row[h]) * D_V] = v[h];
+                        }
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < HG; ++h) part_o[h * D_V + d] = v[h];
                     }
-                } else {
-#pragma unroll
-                    for (int h = 0; h < HG; ++h) part_o[h * D_V + d] = v[h];
                 }
             }
             if (wq == 0 && lane < HG) {
@@ -845,16 +853,62 @@ constexpr int COMBINE_BATCH = 16;  // partial float4 loads in flight per thread
 __global__ void __launch_bounds__(COMBINE_THREADS)
     etap_mla_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
                             const int32_t* __restrict__ split_off, int hg, int batch,
-                            const __grid_constant__ OutMap om, unsigned long long* trace) {
+                            const __grid_constant__ OutMap om, unsigned long long* trace,
+                            const int32_t* __restrict__ seqlens, int parts, int lanes_on) {
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 0] = ptx::global_timer_ns();
-    ptx::grid_dep_wait();
-    ptx::grid_dep_launch();  // the next decode step's prologue may overlap this combine
-    if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 1] = ptx::global_timer_ns();
     const int vb = blockIdx.x / hg;
     const int h = blockIdx.x - vb * hg;
     const int g = vb / batch, b = vb - g * batch;  // head-group-major virtual sequences
-    const int s0 = __ldg(split_off + vb);
-    const int ns = __ldg(split_off + vb + 1) - s0;
+    int s0, ns;
+    if (seqlens != nullptr) {
+        // The decode used the in-kernel schedule on a line of <= 32 entries: this sequence's
+        // split offset / count follow in closed form from seqlens (the same formula as
+        // inkernel_schedule_warp), computed before the grid dependency resolves so the
+        // partial loads go out right after it. seqlens are final here: the decode kernel
+        // triggered this launch only after its own grid_dep_wait.
+        __shared__ int s_info[2];
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            const LineShape ls = line_shape(batch, gridDim.x / hg / batch, parts, lanes_on != 0);
+            const int n = ls.line_n;
+            const int lv = vb / n, pos = vb - lv * n;
+            const int len = lane < n ? max(0, __ldg(seqlens + lane % batch)) : 0;
+            const int tiles = (len + TILE - 1) / TILE;
+            const int cost = tiles > 0 ? tiles + META_FIXED_COST : 0;
+            int incl = cost;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            const int pref = incl - cost;
+            const int T = max(1, (total + ls.p_line - 1) / ls.p_line);
+            const int nsi = (lane < n && tiles > 0) ? ((incl + T - 1) / T - 1) - (pref + META_FIXED_COST) / T + 1 : 0;
+            int so = nsi;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, so, o);
+                if (lane >= o) so += y;
+            }
+            const int ns_line = __shfl_sync(0xffffffffu, so, 31);
+            if (lane == pos) {
+                s_info[0] = lv * ns_line + so - nsi;
+                s_info[1] = nsi;
+            }
+        }
+        __syncthreads();
+        s0 = s_info[0];
+        ns = s_info[1];
+        ptx::grid_dep_wait();
+        ptx::grid_dep_launch();  // the next decode step's prologue may overlap this combine
+    } else {
+        ptx::grid_dep_wait();
+        ptx::grid_dep_launch();
+        s0 = __ldg(split_off + vb);
+        ns = __ldg(split_off + vb + 1) - s0;
+    }
+    if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 1] = ptx::global_timer_ns();
     if (ns == 1) {
         if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 2] = ptx::global_timer_ns();
         return;
@@ -1286,8 +1340,10 @@ OutMap local_outmap(int heads, float* out, float* lse) {
     return om;
 }
 
+// seqlens != null: the split offsets follow in closed form from seqlens (the decode ran the
+// in-kernel schedule on a line of <= 32 entries); otherwise K3 reads split_off
 int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_parts, void* workspace,
-                 const OutMap& om, void* stream) {
+                 const OutMap& om, void* stream, const int32_t* seqlens = nullptr) {
     const int hg = head_group_of(heads);
     const int groups = heads / hg;
     const size_t np = max_partials(batch, heads, num_sm_parts);
@@ -1305,7 +1361,8 @@ int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_part
     cfg2.numAttrs = 1;
     ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, static_cast<const float*>(ws_o),
                                  static_cast<const float*>(ws_lse), split_off, hg, batch, om,
-                                 static_cast<unsigned long long*>(g_combine_trace_buf)));
+                                 static_cast<unsigned long long*>(g_combine_trace_buf), seqlens, num_sm_parts,
+                                 lanes_enabled() ? 1 : 0));
     return ETAP_OK;
 }
 
@@ -1397,7 +1454,9 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     }
 
     if (flags & ETAP_FLAG_SKIP_COMBINE) return ETAP_OK;
-    return combine_impl(split_off, batch, heads, num_sm_parts, workspace, om, stream);
+    const bool closed_form = prm.inkernel_sched && ls.line_n <= 32;
+    return combine_impl(split_off, batch, heads, num_sm_parts, workspace, om, stream,
+                        closed_form ? seqlens : nullptr);
 }
 
 }  // namespace
