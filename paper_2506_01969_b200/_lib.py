@@ -11,6 +11,9 @@ from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "lib" / "libetap_mla.so"
+# experiments only (scripts/variant.sh builds A/B variants under lib/variants/)
+if os.environ.get("ETAP_LIB_VARIANT"):
+    LIB_PATH = _PKG / "lib" / "variants" / f"libetap_mla_{os.environ['ETAP_LIB_VARIANT']}.so"
 
 ETAP_OK = 0
 ETAP_ERR_SHAPE = 1

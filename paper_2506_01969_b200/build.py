@@ -79,6 +79,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> Path:
+    """An A/B variant of the library (lib/variants/libetap_mla_<name>.so, loaded with
+    ETAP_LIB_VARIANT=<name>): same sources, extra -D defines. Experiments only."""
+    out = LIBDIR / "variants" / f"libetap_mla_{name}.so"
+    out.parent.mkdir(parents=True, exist_ok=True)
+    vs = LIBDIR / "exports.map"
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", *map(str, SOURCES), "-o", str(out),
+           "-Xlinker", "--export-dynamic", "-Xlinker", f"--version-script={vs}"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("variant build failed")
+    return out
+
+
 def build_model() -> Path:
     """Host-only tool: the reference's `etaplab model` report for tcgen05 (no CUDA)."""
     src = CSRC / "etap_model.cpp"

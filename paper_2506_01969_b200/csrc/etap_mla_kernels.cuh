@@ -45,7 +45,10 @@ constexpr int SOFTMAX_WARP0 = 4;
 constexpr float LAZY_RESCALE_LOG2 = 8.0f;  // rescale O^T only when the max grows by > 2^8
 
 constexpr int SCHED_INTS = 8;
-constexpr int META_FIXED_COST = 3;  // per-split overhead in tile (page) units for the scheduler
+#ifndef ETAP_META_FIXED_COST
+#define ETAP_META_FIXED_COST 2
+#endif
+constexpr int META_FIXED_COST = ETAP_META_FIXED_COST;  // per-split overhead in tile units (scheduler)
 
 enum : unsigned {
     FLAG_NEGATE_RESCALE = 1u,
