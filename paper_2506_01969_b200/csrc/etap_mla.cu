@@ -375,8 +375,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     using C = Cfg<HG_>;
     constexpr int HG = C::HG, HH = C::HH;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smem = ptx::align_smem_1024(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
     const int warp = threadIdx.x >> 5;
@@ -761,26 +760,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_wait(&bars[BAR_G2_DONE + last % NTB], (last / NTB) & 1);
             ptx::tc_fence_after();
             if (tracer) ETAP_TRACE_G(prm, 10);
+            // BPW d-blocks per TMEM load wait (HG = 16: two blocks = 64 registers in flight)
+            constexpr int BPW = HG == 16 ? 2 : 1;
+            uint32_t o[BPW][2 * HG];
             const float wsum = halfwarp_reduce<false, HH>(l_part, lane);
             if (rwriter) red_sum[wq * HG + half * HH + rhead] = wsum;
             const int ns = soff[vb + 1] - soff[vb];
             const bool direct = ns == 1;  // one split: final O / L rows, else a split partial
             if (direct && wq == 0 && lane < HG) s_row[lane] = static_cast<int>(prm.om.row(sd.b, sd.g * HG + lane));
+            if (tracer) ETAP_TRACE(prm, last, 10);
+            ptx::named_bar_sync(2, 128);
+            if (tracer) ETAP_TRACE(prm, last, 11);
+            // one owner thread per head finishes l, 1/l and L in parallel (a serial per-head loop
+            // in every thread costs ~1.6k cycles); 1/l is broadcast through red_max, which no
+            // one reads between tiles
+            float L_own = 0.f;
+            float* s_inv = red_max;
+            if (wq == 0 && lane < HG) {
+                const float l = red_sum[lane] + red_sum[HG + lane] + red_sum[2 * HG + lane] + red_sum[3 * HG + lane];
+                s_inv[lane] = l > 0.f ? 1.f / l : 0.f;  // l = 0: column saw no row (O = 0, L = -inf)
+                L_own = (s_m[lane] + log2f(l)) * 0.69314718055994530942f;
+            }
             ptx::named_bar_sync(2, 128);
             float inv_l[HG];
 #pragma unroll
-            for (int h = 0; h < HG; ++h) {
-                const float l = red_sum[h] + red_sum[HG + h] + red_sum[2 * HG + h] + red_sum[3 * HG + h];
-                inv_l[h] = l > 0.f ? 1.f / l : 0.f;  // l = 0: column saw no row (O = 0, L = -inf)
+            for (int h = 0; h < HG; h += 4) {
+                const float4 v4 = *reinterpret_cast<const float4*>(s_inv + h);
+                inv_l[h] = v4.x; inv_l[h + 1] = v4.y; inv_l[h + 2] = v4.z; inv_l[h + 3] = v4.w;
             }
             const int idx = (vb == sch[0]) ? sch[4] : soff[vb] + idx_off;  // partial index (ns > 1)
             float* part_o = prm.ws_o + static_cast<size_t>(idx) * HG * D_V;
             const int drow = wq * 32 + lane;  // M=128 layout: d row = TMEM lane
-            // BPW d-blocks per TMEM load wait (HG = 16: two blocks = 64 registers in flight)
-            constexpr int BPW = HG == 16 ? 2 : 1;
 #pragma unroll 1
             for (int blk0 = 0; blk0 < 4; blk0 += BPW) {
-                uint32_t o[BPW][2 * HG];
 #pragma unroll
                 for (int bb = 0; bb < BPW; ++bb)
 #pragma unroll
@@ -788,6 +800,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         ptx::tmem_ld32(t_lane + C::TCOL_O + C::OBLK * (blk0 + bb) + 32 * part,
                                        *reinterpret_cast<uint32_t(*)[32]>(&o[bb][32 * part]));
                 ptx::tmem_wait_ld();
+                if (tracer && blk0 == 0) ETAP_TRACE(prm, last, 14);
 #pragma unroll
                 for (int bb = 0; bb < BPW; ++bb) {
                     const int d = (blk0 + bb) * 128 + drow;
@@ -808,10 +821,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         for (int h = 0; h < HG; ++h) part_o[h * D_V + d] = v[h];
                     }
                 }
+                if (tracer && blk0 == 0) ETAP_TRACE(prm, last, 15);
             }
+            if (tracer) ETAP_TRACE(prm, last, 12);
             if (wq == 0 && lane < HG) {
-                const float l = red_sum[lane] + red_sum[HG + lane] + red_sum[2 * HG + lane] + red_sum[3 * HG + lane];
-                const float L = (s_m[lane] + log2f(l)) * 0.69314718055994530942f;
+                const float L = L_own;
                 if (direct) {
                     for (int r = 0; r < prm.om.n_out; ++r) prm.om.lse[r][s_row[lane]] = L;
                 } else {
@@ -821,6 +835,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tc_fence_before();
             // red_sum / s_m are rewritten by the next split only after this barrier
             ptx::named_bar_sync(2, 128);
+            if (tracer) ETAP_TRACE(prm, last, 13);
         }
     }
 
@@ -980,8 +995,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                              float* s_out, float* o_out) {
     using C = Cfg<16>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smem = ptx::align_smem_1024(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1562,8 +1576,7 @@ int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* 
 namespace {
 __global__ void __launch_bounds__(128, 1) etap_umma_bench_kernel(int variant, int n, long long* out) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smem = ptx::align_smem_1024(smem_raw);
     __shared__ uint64_t bar;
     __shared__ uint32_t tslot;
     for (int i = threadIdx.x; i < 65536 / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
@@ -1638,8 +1651,7 @@ namespace {
 __global__ void __launch_bounds__(64, 1) etap_stream_bench_kernel(const __grid_constant__ CUtensorMap tm_kv,
                                                                    int pages_per_cta, int nslot) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smem = ptx::align_smem_1024(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + 200 * 1024);
     uint64_t* done = full + NTB;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -17,6 +17,20 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Dynamic shared memory aligned to 1024 B (SW128 atoms). The uintptr_t round trip makes
+// the compiler treat derived pointers as generic (LD/ST instead of LDS/STS). Measured on
+// B200: keeping the shared address space (raw + pad on the __shared__ array)
+// changes the softmax schedule and costs ~3 us/step at B=16 x 64K (189.7 vs 186.8 us), so
+// the generic form is kept; ETAP_SMEM_SHARED_AS selects the other one for A/B runs.
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* raw) {
+#ifdef ETAP_SMEM_SHARED_AS
+    const uint32_t a = smem_u32(raw);
+    return raw + ((1024u - (a & 1023u)) & 1023u);
+#else
+    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
+#endif
+}
+
 __device__ __forceinline__ uint32_t lane_id() {
     uint32_t l;
     asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
