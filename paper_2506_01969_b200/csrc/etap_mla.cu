@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int i = 0; i < NTB; ++i) {
             ptx::mbar_init(&bars[BAR_FULL_A + i], 1);
             ptx::mbar_init(&bars[BAR_FULL_B + i], 1);
+            ptx::mbar_init(&bars[BAR_FULL_C + i], 1);
             ptx::mbar_init(&bars[BAR_G2_DONE + i], 1);
             ptx::mbar_init(&bars[BAR_G2_HALF + i], 1);
         }
@@ -505,21 +506,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     __syncwarp();
                     ++nsplit;
                 }
-                // the remaining positions reuse tile gt-2's first 9 - SPLIT_POS positions: with
-                // the 24-slot ring those are {V0,V1,V2} or {rope,V0,V1}, free once GEMM2
-                // d-blocks 0-1 of tile gt-2 completed; otherwise wait for the whole GEMM2
-                if (gt >= 2)
-                    ptx::mbar_wait(&bars[(C::EARLY_HALF ? BAR_G2_HALF : BAR_G2_DONE) + (gt - 2) % NTB],
-                                   ((gt - 2) / NTB) & 1);
+                // positions [SPLIT_POS, SPLIT_POS2) reuse tile gt-2's first four positions: free
+                // once GEMM2 d-blocks 0-1 of gt-2 completed
+                if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_HALF + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
                 if (lane == 0) {
-                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_B + tb], (NCHUNK - C::SPLIT_POS) * SLOT_BYTES);
+                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_B + tb], (C::SPLIT_POS2 - C::SPLIT_POS) * SLOT_BYTES);
 #pragma unroll 1
-                    for (int pos = C::SPLIT_POS; pos < NCHUNK; ++pos) {
+                    for (int pos = C::SPLIT_POS; pos < C::SPLIT_POS2; ++pos) {
                         const uint32_t s = (pos0 + pos) % C::NSLOT;
                         ptx::tma_load_2d(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_B + tb],
                                          chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
                     }
-                    ETAP_TRACE(prm, gt, 1);
+                    if (!C::THIRD_GROUP) ETAP_TRACE(prm, gt, 1);
+                }
+                if constexpr (C::THIRD_GROUP) {
+                    // the rest reuse gt-2's positions [4, 9 - SPLIT_POS): the whole GEMM2 of gt-2
+                    __syncwarp();
+                    if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+                    if (lane == 0) {
+                        ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_C + tb], (NCHUNK - C::SPLIT_POS2) * SLOT_BYTES);
+#pragma unroll 1
+                        for (int pos = C::SPLIT_POS2; pos < NCHUNK; ++pos) {
+                            const uint32_t s = (pos0 + pos) % C::NSLOT;
+                            ptx::tma_load_2d(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_C + tb],
+                                             chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
+                        }
+                        ETAP_TRACE(prm, gt, 1);
+                    }
                 }
                 __syncwarp();
                 ++gt;
@@ -544,8 +557,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::mbar_wait(&bars[BAR_FULL_B + gt % NTB], (gt / NTB) & 1);
                 __syncwarp();
                 ptx::tc_fence_after();
-                ETAP_TRACE(prm, gt, 2);
-                issue_gemm1_tile<C, C::SPLIT_POS, NCHUNK>(s_tmem, ring_addr, q_addr, pos0, gt);
+                if (!C::THIRD_GROUP) ETAP_TRACE(prm, gt, 2);
+                issue_gemm1_tile<C, C::SPLIT_POS, C::SPLIT_POS2>(s_tmem, ring_addr, q_addr, pos0, gt);
+                if constexpr (C::THIRD_GROUP) {
+                    ptx::mbar_wait(&bars[BAR_FULL_C + gt % NTB], (gt / NTB) & 1);
+                    __syncwarp();
+                    ptx::tc_fence_after();
+                    ETAP_TRACE(prm, gt, 2);
+                    issue_gemm1_tile<C, C::SPLIT_POS2, NCHUNK>(s_tmem, ring_addr, q_addr, pos0, gt);
+                }
                 ptx::umma_commit_elect(&bars[BAR_S_FULL + buf]);
                 ETAP_TRACE(prm, gt, 3);
                 if (t == sd.t1 - 1) ptx::umma_commit_elect(&bars[BAR_Q_EMPTY]);

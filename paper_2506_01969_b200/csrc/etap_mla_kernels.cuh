@@ -34,7 +34,7 @@ constexpr int NCHUNK = 9;       // 576 / 64 column chunks (SW128 atoms are 64 bf
 constexpr int NVCHUNK = 8;      // 512 / 64 chunks that are also V
 constexpr int SLOT_BYTES = TILE * 128;  // 64 rows x 128 B = 8 KiB per ring slot
 constexpr int NTB = 4;          // tile-barrier ring depth (tiles in flight <= NSLOT/9 + 1)
-constexpr int NBAR = 4 * NTB + 8;
+constexpr int NBAR = 5 * NTB + 8;
 constexpr int MAX_FUSED_VB = 256;
 constexpr int SCHED_SMEM_INTS = 4 * MAX_FUSED_VB + 2 + 8 + 8;  // pref, soff, tiles, len, sched, wt
 
@@ -59,11 +59,12 @@ enum : unsigned {
 
 // barrier indices
 constexpr int BAR_FULL_A = 0;           // [NTB] ring positions [0, SPLIT_POS) of tile gt landed
-constexpr int BAR_FULL_B = NTB;         // [NTB] ring positions [SPLIT_POS, 9) of tile gt landed
+constexpr int BAR_FULL_B = NTB;         // [NTB] ring positions [SPLIT_POS, SPLIT_POS2) of tile gt landed
 constexpr int BAR_G2_DONE = 2 * NTB;    // [NTB] GEMM2 of tile gt complete: its 9 ring slots
                                         //       and its P buffer are free (gt % NTB)
 constexpr int BAR_G2_HALF = 3 * NTB;    // [NTB] GEMM2 d-blocks 0-1 of tile gt complete: the
                                         //       rope slot and V chunks 0-3 are free
+constexpr int BAR_FULL_C = 4 * NTB + 8;  // [NTB] ring positions [SPLIT_POS2, 9) of tile gt landed
 constexpr int BAR_Q_FULL = 4 * NTB + 0;
 constexpr int BAR_Q_EMPTY = 4 * NTB + 1;
 constexpr int BAR_S_FULL = 4 * NTB + 2;  // [2]
@@ -80,10 +81,14 @@ struct Cfg {
     static constexpr int HG = HG_;
     static constexpr int HH = HG / 2;                    // heads per softmax thread
     static constexpr int NSLOT = HG == 16 ? 24 : 20;     // ring depth in 8 KB chunk slots
-    // tile gt's ring positions [0, SPLIT_POS) reuse tile gt-3's slots, the rest tile gt-2's
+    // tile gt's ring positions [0, SPLIT_POS) reuse tile gt-3's last slots (free after its
+    // GEMM2), positions p >= SPLIT_POS reuse tile gt-2's position p - SPLIT_POS. Of those,
+    // gt-2's positions [0, 4) hold {V0..V3} or {rope, V0..V2}: free once GEMM2 d-blocks 0-1 of
+    // gt-2 completed (G2_HALF), so tile gt's positions [SPLIT_POS, SPLIT_POS2) go out then
+    // and only [SPLIT_POS2, 9) wait for the whole GEMM2 of gt-2 (an empty group for HG = 16).
     static constexpr int SPLIT_POS = NSLOT - 18;
-    // tile gt-2's reused positions [0, 9 - SPLIT_POS) are free after GEMM2 d-blocks 0-1
-    static constexpr bool EARLY_HALF = (9 - SPLIT_POS) <= 3;
+    static constexpr int SPLIT_POS2 = SPLIT_POS + 4 < NCHUNK ? SPLIT_POS + 4 : NCHUNK;
+    static constexpr bool THIRD_GROUP = SPLIT_POS2 < NCHUNK;
     static constexpr int Q_CHUNK_BYTES = HG * 128;
     static constexpr int Q_BYTES = NCHUNK * Q_CHUNK_BYTES;
     static constexpr int PN = 2 * HG;                    // GEMM2 N: HG heads hi | HG heads lo
