@@ -413,6 +413,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+#ifndef ETAP_NO_PREFETCH_HINT
+    if (warp == 0 && lane == 0 && prm.inkernel_sched) {
+        // While the previous kernel finishes: warm L2 with the first pages this CTA will most
+        // likely stream, guessed from its own range of the previous decode call (the fused
+        // schedule republishes it every call; a decode step moves it only when a sequence
+        // crosses a page). Hints only: every byte used is loaded after grid_dep_wait below,
+        // and a wrong or stale guess merely wastes a prefetch.
+        const int32_t* prev = prm.sched_out + blockIdx.x * SCHED_INTS;
+        const int p0 = prev[0], tb = prev[1], p1 = prev[2], off = prev[5];
+        const int vb = off + p0, nvb = prm.batch * prm.groups;
+        if (p1 >= p0 && p0 >= 0 && vb >= 0 && vb < nvb && tb >= 0 && tb < prm.max_pages) {
+            const int g = vb / prm.batch, b = vb - g * prm.batch;
+            const int32_t* bt = prm.block_table + static_cast<size_t>(b) * prm.max_pages;
+#pragma unroll 1
+            for (int k = 0; k < 2 && tb + k < prm.max_pages; ++k) {
+                const int page = bt[tb + k];
+                if (page >= 0 && page < prm.num_pages)
+                    ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) +
+                                              static_cast<size_t>(page) * PAGE * D_QK * 2,
+                                          PAGE * D_QK * 2);
+            }
+            ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.q) +
+                                      (static_cast<size_t>(b) * prm.heads + g * HG) * D_QK * 2,
+                                  HG * D_QK * 2);
+        }
+    }
+#endif
     ptx::grid_dep_wait();     // inputs / schedule written by earlier kernels in the stream
     ptx::grid_dep_launch();   // let the combine kernel get scheduled
     if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
@@ -1440,6 +1467,9 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     prm.om = om;
     prm.ws_o = static_cast<float*>(workspace);
     prm.ws_lse = prm.ws_o + np * hg * D_V;
+    prm.kv_pool = kv_pool;
+    prm.q = q;
+    prm.num_pages = num_pages;
     prm.max_pages = max_pages_per_seq;
     prm.batch = batch;
     prm.heads = heads;

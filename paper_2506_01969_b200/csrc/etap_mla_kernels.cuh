@@ -301,6 +301,9 @@ struct DecodeParams {
     OutMap om;               // final outputs (sequences finished by one split)
     float* ws_o;
     float* ws_lse;
+    const void* kv_pool;     // raw pool / Q (L2 prefetch hints before the grid dependency)
+    const void* q;
+    int64_t num_pages;
     int max_pages;
     int batch;
     int heads;            // query rows per sequence (all tokens folded)
