@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     uint32_t sa = pos0 + pos_of_chunk(2 * blk, gt);
                     sa = sa >= C::NSLOT ? sa - C::NSLOT : sa;
                     issue_gemm2_block<C>(tmem_base + C::TCOL_O + C::OBLK * blk, ring_addr + sa * SLOT_BYTES,
-                                         p_addr + buf * C::P_BYTES, t == sd.t0);
+                                         p_addr + (buf % C::P_BUFS) * C::P_BYTES, t == sd.t0);
                     if (blk == 1) ptx::umma_commit_elect(&bars[BAR_G2_HALF + gt % NTB]);
                 }
                 ptx::umma_commit_elect(&bars[BAR_G2_DONE + gt % NTB]);
@@ -754,8 +754,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     ptx::named_bar_sync(2, 128);
                 }
                 if (tracer) ETAP_TRACE(prm, gt, 8);
-                // the P buffer is reused every other tile: GEMM2(gt-2) must have read it
-                if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+                // the P buffer is reused every P_BUFS tiles: GEMM2(gt - P_BUFS) must have read it
+                if (gt >= C::P_BUFS)
+                    ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - C::P_BUFS) % NTB], ((gt - C::P_BUFS) / NTB) & 1);
                 if (tracer) ETAP_TRACE(prm, gt, 9);
                 if (need_rescale) {
                     // O^T must contain GEMM2(gt-1) before it is rescaled; s_alpha written above
@@ -780,7 +781,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                     ptx::tmem_wait_st();
                 }
-                write_p_hilo<C>(smem + C::OFF_P + buf * C::P_BYTES, row, half, pv);
+                write_p_hilo<C>(smem + C::OFF_P + (buf % C::P_BUFS) * C::P_BYTES, row, half, pv);
                 // rows of the last page past seqlen were loaded from HBM and may hold
                 // non-finite garbage; zero them in the V chunks (0 * NaN = NaN in the MMA)
                 if (grow >= sd.seqlen) {

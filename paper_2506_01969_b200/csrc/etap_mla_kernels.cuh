@@ -35,11 +35,14 @@ constexpr int NVCHUNK = 8;      // 512 / 64 chunks that are also V
 constexpr int SLOT_BYTES = TILE * 128;  // 64 rows x 128 B = 8 KiB per ring slot
 constexpr int NTB = 4;          // tile-barrier ring depth (tiles in flight <= NSLOT/9 + 1)
 constexpr int NBAR = 5 * NTB + 8;
-constexpr int MAX_FUSED_VB = 256;
+constexpr int MAX_FUSED_VB = 128;  // longer lines (batch * head groups) run K1 first
 constexpr int SCHED_SMEM_INTS = 4 * MAX_FUSED_VB + 2 + 8 + 8;  // pref, soff, tiles, len, sched, wt
 
 // warp 0 TMA producer, warp 1 GEMM1 issuer (+TMEM alloc), warp 2 GEMM2 issuer, warp 3 idle,
 // warps 4..7 softmax / epilogue (warp % 4 = TMEM lane quadrant)
+#ifndef ETAP_HG32_NSLOT
+#define ETAP_HG32_NSLOT 22
+#endif
 constexpr int NUM_THREADS = 256;
 constexpr int SOFTMAX_WARP0 = 4;
 constexpr float LAZY_RESCALE_LOG2 = 8.0f;  // rescale O^T only when the max grows by > 2^8
@@ -80,7 +83,10 @@ template <int HG_>
 struct Cfg {
     static constexpr int HG = HG_;
     static constexpr int HH = HG / 2;                    // heads per softmax thread
-    static constexpr int NSLOT = HG == 16 ? 24 : 20;     // ring depth in 8 KB chunk slots
+    // ring depth in 8 KB chunk slots; HG = 32 affords 22 with a single P buffer (the softmax
+    // writes P(gt) once GEMM2(gt-1) has read P(gt-1), which it has long done by then)
+    static constexpr int NSLOT = HG == 16 ? 24 : ETAP_HG32_NSLOT;
+    static constexpr int P_BUFS = (HG == 16 || NSLOT <= 20) ? 2 : 1;
     // tile gt's ring positions [0, SPLIT_POS) reuse tile gt-3's last slots (free after its
     // GEMM2), positions p >= SPLIT_POS reuse tile gt-2's position p - SPLIT_POS. Of those,
     // gt-2's positions [0, 4) hold {V0..V3} or {rope, V0..V2}: free once GEMM2 d-blocks 0-1 of
@@ -96,8 +102,8 @@ struct Cfg {
     static constexpr int P_BYTES = TILE * PN * 2;
     static constexpr int OFF_RING = 0;
     static constexpr int OFF_Q = OFF_RING + NSLOT * SLOT_BYTES;
-    static constexpr int OFF_P = OFF_Q + Q_BYTES;        // 2 buffers
-    static constexpr int OFF_RED = OFF_P + 2 * P_BYTES;  // red_max[2][4][HG], red_sum[4][HG], m[HG], alpha[HG], row[HG]
+    static constexpr int OFF_P = OFF_Q + Q_BYTES;        // P_BUFS buffers
+    static constexpr int OFF_RED = OFF_P + P_BUFS * P_BYTES;  // red_max[2][4][HG], red_sum[4][HG], m[HG], alpha[HG], row[HG]
     static constexpr int RED_FLOATS = 2 * 4 * HG + 4 * HG + HG + HG + HG;  // + output row per head
     static constexpr int OFF_BAR = align_up(OFF_RED + RED_FLOATS * 4, 16);
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
