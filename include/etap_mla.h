@@ -179,6 +179,28 @@ int etap_mla_host_decode(etap_mla_host_ctx* ctx, const void* q_host, const void*
                          float scale, unsigned flags, float* out_host, float* lse_host);
 void etap_mla_host_ctx_destroy(etap_mla_host_ctx* ctx);
 
+/* ---------------------------------------------------------------------------------------
+ * Serving-style decode steps (the caller side of the path: a paged latent-KV cache that
+ * stays resident in HBM, and one new latent row per sequence per step).
+ *
+ * etap_mla_append_kv: write the q_tokens new latent rows of every sequence into the paged
+ *   pool — row j of sequence b lands at token position seqlens[b] - q_tokens + j (seqlens
+ *   are the lengths AFTER the append), page block_table[b][pos / 64], row pos % 64. Device
+ *   pointers, stream-ordered; rows whose position or page is out of range are skipped.
+ *   kv_rows: [batch][q_tokens][576] bf16.
+ * etap_mla_host_ctx_load: upload the resident cache state (pool + block table) once.
+ * etap_mla_host_decode_step: one decode step from HOST buffers against the resident cache:
+ *   H2D of Q, the new rows and seqlens; append (above); K2 + K3; D2H of O / LSE; synchronize.
+ *   What `bench.py` reports as e2e_serving. */
+int etap_mla_append_kv(const void* kv_rows, void* kv_pool, int64_t num_pages,
+                       const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,
+                       int batch, int q_tokens, void* stream);
+int etap_mla_host_ctx_load(etap_mla_host_ctx* ctx, const void* kv_pool_host,
+                           const int32_t* block_table_host);
+int etap_mla_host_decode_step(etap_mla_host_ctx* ctx, const void* q_host, const void* kv_rows_host,
+                              const int32_t* seqlens_host, float scale, unsigned flags,
+                              float* out_host, float* lse_host);
+
 /* Reference-shaped entry (binary64 row-major matrices, exactly the storage of
  * etaplab::AttentionProblem, attention.hpp:15-25): rounds Q/K to bf16, checks the MLA
  * aliasing V == K[:, :512], runs the GPU path, widens O and L back to binary64.

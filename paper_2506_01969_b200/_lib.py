@@ -57,6 +57,9 @@ def _declare(lib: C.CDLL) -> None:
         "etap_mla_ipc_free": (i32, [vp]),
         "etap_mla_host_ctx_create": (i32, [i32, i32, i64, i32, P(vp)]),
         "etap_mla_host_decode": (i32, [vp, vp, vp, vp, vp, f32, u32, vp, vp]),
+        "etap_mla_host_ctx_load": (i32, [vp, vp, vp]),
+        "etap_mla_host_decode_step": (i32, [vp, vp, vp, vp, f32, u32, vp, vp]),
+        "etap_mla_append_kv": (i32, [vp, vp, i64, vp, i32, vp, i32, i32, vp]),
         "etap_mla_host_ctx_destroy": (None, [vp]),
         "etap_mla_run_etap_f64": (i32, [vp, i64, vp, i64, i64, vp, i64, f64, i64, i64, i64, u32,
                                         vp, vp]),

@@ -906,6 +906,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 // =============================================================================================
+// KV append (caller side of the path: the serving loop writes each step's new latent rows
+// into the paged cache before the decode reads them). One CTA of 72 threads per new row,
+// one 16 B vector each (576 bf16 = 1152 B). HBM-bound scatter of B * q_tokens rows.
+// =============================================================================================
+__global__ void __launch_bounds__(72)
+    etap_mla_append_kv_kernel(const uint4* __restrict__ rows, uint4* __restrict__ pool, int64_t num_pages,
+                              const int32_t* __restrict__ block_table, int max_pages,
+                              const int32_t* __restrict__ seqlens, int q_tokens) {
+    ptx::grid_dep_wait();
+    ptx::grid_dep_launch();
+    const int r = blockIdx.x;                 // b * q_tokens + j
+    const int b = r / q_tokens, j = r - b * q_tokens;
+    const int pos = __ldg(seqlens + b) - q_tokens + j;
+    if (pos < 0 || pos / PAGE >= max_pages) return;
+    const int page = __ldg(block_table + static_cast<size_t>(b) * max_pages + pos / PAGE);
+    if (page < 0 || page >= num_pages) return;
+    const size_t dst_row = static_cast<size_t>(page) * PAGE + pos % PAGE;
+    pool[dst_row * (D_QK * 2 / 16) + threadIdx.x] = rows[static_cast<size_t>(r) * (D_QK * 2 / 16) + threadIdx.x];
+}
+
+// =============================================================================================
 // K3: log-sum-exp combine of split partials (no reference analog: split-KV is a SPEC
 // non-goal; the math is pinned by L = m + log l, etap.cpp:144, and partition
 // invariance, acceptance.cpp:209-229). Grid: one CTA of 128 threads per (vb, head).
@@ -1576,6 +1597,29 @@ int etap_mla_decode_peer(const void* q, const void* kv_pool, int64_t num_pages,
                              workspace, om, flags, stream))
         return rc;
     return etap_b200::peer_signal_wait(pg, epoch, stream);
+}
+
+int etap_mla_append_kv(const void* kv_rows, void* kv_pool, int64_t num_pages, const int32_t* block_table,
+                       int max_pages_per_seq, const int32_t* seqlens, int batch, int q_tokens, void* stream) {
+    if (!kv_rows || !kv_pool || !block_table || !seqlens) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    if (batch < 1 || q_tokens < 1 || q_tokens > ETAP_MLA_MAX_Q_TOKENS || num_pages < 1 || max_pages_per_seq < 1)
+        return fail(ETAP_ERR_SHAPE, "batch, num_pages, max_pages_per_seq >= 1 and q_tokens in [1, 8] required");
+    if ((reinterpret_cast<uintptr_t>(kv_rows) | reinterpret_cast<uintptr_t>(kv_pool)) & 15)
+        return fail(ETAP_ERR_SHAPE, "kv_rows / kv_pool must be 16-byte aligned");
+    if (int rc = check_device()) return rc;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(batch * q_tokens);
+    cfg.blockDim = dim3(D_QK * 2 / 16);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_append_kv_kernel, static_cast<const uint4*>(kv_rows),
+                                 static_cast<uint4*>(kv_pool), num_pages, block_table, max_pages_per_seq,
+                                 seqlens, q_tokens));
+    return ETAP_OK;
 }
 
 int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_parts,

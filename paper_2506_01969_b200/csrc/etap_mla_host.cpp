@@ -64,7 +64,7 @@ struct etap_mla_host_ctx {
     int batch = 0, heads = 0, max_pages = 0, num_sm_parts = 0;
     int64_t num_pages = 0;
     cudaStream_t stream = nullptr;
-    DevBuf q, kv, bt, sl, out, lse, sched, split_off, ws;
+    DevBuf q, kv, bt, sl, out, lse, sched, split_off, ws, rows;
 };
 
 extern "C" {
@@ -96,6 +96,7 @@ int etap_mla_host_ctx_create(int batch, int heads, int64_t num_pages, int max_pa
             c->sl.alloc(static_cast<size_t>(batch) * 4) || c->out.alloc(rows * ETAP_MLA_D_V * 4) ||
             c->lse.alloc(rows * 4) || c->sched.alloc(sched_n * 4) ||
             c->split_off.alloc(so_n * 4) || c->ws.alloc(ws_n) ||
+            c->rows.alloc(static_cast<size_t>(batch) * ETAP_MLA_D_QK * 2) ||
             cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) ||
             cudaMemset(c->ws.p, 0, c->ws.n))  // combine flags / counters start at zero
             rc = host_fail(ETAP_ERR_CUDA, "device allocation failed");
@@ -129,6 +130,44 @@ int etap_mla_host_decode(etap_mla_host_ctx* c, const void* q_host, const void* k
                          scale, 1, static_cast<int32_t*>(c->sched.p),
                          static_cast<int32_t*>(c->split_off.p), c->num_sm_parts, c->ws.p,
                          static_cast<float*>(c->out.p), static_cast<float*>(c->lse.p), flags, s);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(out_host, c->out.p, c->out.n, cudaMemcpyDeviceToHost, s) ||
+        cudaMemcpyAsync(lse_host, c->lse.p, c->lse.n, cudaMemcpyDeviceToHost, s) ||
+        cudaStreamSynchronize(s))
+        return host_fail(ETAP_ERR_CUDA, "device->host copy / synchronize failed");
+    return ETAP_OK;
+}
+
+int etap_mla_host_ctx_load(etap_mla_host_ctx* c, const void* kv_pool_host, const int32_t* block_table_host) {
+    if (!c || !kv_pool_host || !block_table_host) return host_fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    if (cudaMemcpyAsync(c->kv.p, kv_pool_host, c->kv.n, cudaMemcpyHostToDevice, c->stream) ||
+        cudaMemcpyAsync(c->bt.p, block_table_host, c->bt.n, cudaMemcpyHostToDevice, c->stream) ||
+        cudaStreamSynchronize(c->stream))
+        return host_fail(ETAP_ERR_CUDA, "host->device copy of the cache failed");
+    return ETAP_OK;
+}
+
+// One serving decode step against the resident cache: the per-step inputs cross PCIe (Q, the
+// new latent row of every sequence, seqlens), the cache does not.
+int etap_mla_host_decode_step(etap_mla_host_ctx* c, const void* q_host, const void* kv_rows_host,
+                              const int32_t* seqlens_host, float scale, unsigned flags, float* out_host,
+                              float* lse_host) {
+    if (!c || !q_host || !kv_rows_host || !seqlens_host || !out_host || !lse_host)
+        return host_fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    cudaStream_t s = c->stream;
+    if (cudaMemcpyAsync(c->q.p, q_host, c->q.n, cudaMemcpyHostToDevice, s) ||
+        cudaMemcpyAsync(c->rows.p, kv_rows_host, c->rows.n, cudaMemcpyHostToDevice, s) ||
+        cudaMemcpyAsync(c->sl.p, seqlens_host, c->sl.n, cudaMemcpyHostToDevice, s))
+        return host_fail(ETAP_ERR_CUDA, "host->device copy failed");
+    int rc = etap_mla_append_kv(c->rows.p, c->kv.p, c->num_pages, static_cast<int32_t*>(c->bt.p), c->max_pages,
+                                static_cast<int32_t*>(c->sl.p), c->batch, 1, s);
+    if (rc) return rc;
+    // the schedule is computed inside the decode kernel (no K1 launch)
+    rc = etap_mla_decode(c->q.p, c->kv.p, c->num_pages, static_cast<int32_t*>(c->bt.p), c->max_pages,
+                         static_cast<int32_t*>(c->sl.p), c->batch, 1, c->heads, scale, 1,
+                         static_cast<int32_t*>(c->sched.p), static_cast<int32_t*>(c->split_off.p),
+                         c->num_sm_parts, c->ws.p, static_cast<float*>(c->out.p), static_cast<float*>(c->lse.p),
+                         flags, s);
     if (rc) return rc;
     if (cudaMemcpyAsync(out_host, c->out.p, c->out.n, cudaMemcpyDeviceToHost, s) ||
         cudaMemcpyAsync(lse_host, c->lse.p, c->lse.n, cudaMemcpyDeviceToHost, s) ||
