@@ -413,35 +413,48 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+    // (b, first tile) of this CTA's range in the previous call: a guess for this call
+    int hint_b = -1, hint_t0 = 0;
 #ifndef ETAP_NO_PREFETCH_HINT
-    if (warp == 0 && lane == 0 && prm.inkernel_sched) {
+    if (warp == 0 && prm.inkernel_sched) {
         // While the previous kernel finishes: warm L2 with the first pages this CTA will most
         // likely stream, guessed from its own range of the previous decode call (the fused
         // schedule republishes it every call; a decode step moves it only when a sequence
         // crosses a page). Hints only: every byte used is loaded after grid_dep_wait below,
         // and a wrong or stale guess merely wastes a prefetch.
-        const int32_t* prev = prm.sched_out + blockIdx.x * SCHED_INTS;
-        const int p0 = prev[0], tb = prev[1], p1 = prev[2], off = prev[5];
-        const int vb = off + p0, nvb = prm.batch * prm.groups;
-        if (p1 >= p0 && p0 >= 0 && vb >= 0 && vb < nvb && tb >= 0 && tb < prm.max_pages) {
-            const int g = vb / prm.batch, b = vb - g * prm.batch;
-            const int32_t* bt = prm.block_table + static_cast<size_t>(b) * prm.max_pages;
+        if (lane == 0) {
+            const int32_t* prev = prm.sched_out + blockIdx.x * SCHED_INTS;
+            const int p0 = prev[0], tb = prev[1], p1 = prev[2], off = prev[5];
+            const int vb = off + p0, nvb = prm.batch * prm.groups;
+            if (p1 >= p0 && p0 >= 0 && vb >= 0 && vb < nvb && tb >= 0 && tb < prm.max_pages) {
+                const int g = vb / prm.batch, b = vb - g * prm.batch;
+                hint_b = b;
+                hint_t0 = tb;
+                const int32_t* bt = prm.block_table + static_cast<size_t>(b) * prm.max_pages;
 #pragma unroll 1
-            for (int k = 0; k < 2 && tb + k < prm.max_pages; ++k) {
-                const int page = bt[tb + k];
-                if (page >= 0 && page < prm.num_pages)
-                    ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) +
-                                              static_cast<size_t>(page) * PAGE * D_QK * 2,
-                                          PAGE * D_QK * 2);
+                for (int k = 0; k < 2 && tb + k < prm.max_pages; ++k) {
+                    const int page = bt[tb + k];
+                    if (page >= 0 && page < prm.num_pages)
+                        ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) +
+                                                  static_cast<size_t>(page) * PAGE * D_QK * 2,
+                                              PAGE * D_QK * 2);
+                }
+                ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.q) +
+                                          (static_cast<size_t>(b) * prm.heads + g * HG) * D_QK * 2,
+                                      HG * D_QK * 2);
             }
-            ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.q) +
-                                      (static_cast<size_t>(b) * prm.heads + g * HG) * D_QK * 2,
-                                  HG * D_QK * 2);
         }
+        hint_b = __shfl_sync(0xffffffffu, hint_b, 0);
+        hint_t0 = __shfl_sync(0xffffffffu, hint_t0, 0);
     }
 #endif
     ptx::grid_dep_wait();     // inputs / schedule written by earlier kernels in the stream
     ptx::grid_dep_launch();   // let the combine kernel get scheduled
+    // the producer's first page ids for the guessed range go out together with the seqlens
+    // loads of the schedule (used only if the schedule confirms the guess)
+    int hint_pg = 0;
+    if (warp == 0 && hint_b >= 0 && hint_t0 + lane < prm.max_pages)
+        hint_pg = prm.block_table[static_cast<size_t>(hint_b) * prm.max_pages + hint_t0 + lane];
     if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
     const int32_t* sch;
     const int32_t* soff;      // split offsets per virtual sequence
@@ -493,7 +506,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // the first KV boxes wait on them, Q (usually L2-resident) is issued after those
             const int32_t* bt = prm.block_table + static_cast<size_t>(sd.b) * prm.max_pages;
             int base = sd.t0;
-            int pg = (base + lane < sd.t1) ? __ldg(bt + base + lane) : 0;
+            int pg;
+            if (nsplit == 0 && sd.b == hint_b && sd.t0 == hint_t0) pg = hint_pg;  // loaded already
+            else pg = (base + lane < sd.t1) ? __ldg(bt + base + lane) : 0;
             bool q_pending = true;
             for (int t = sd.t0; t < sd.t1; ++t) {
                 if (t - base >= 32) {  // page ids of the next 32 tiles, one per lane
