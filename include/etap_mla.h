@@ -192,6 +192,29 @@ void etap_mla_host_ctx_destroy(etap_mla_host_ctx* ctx);
  * etap_mla_host_decode_step: one decode step from HOST buffers against the resident cache:
  *   H2D of Q, the new rows and seqlens; append (above); K2 + K3; D2H of O / LSE; synchronize.
  *   What `bench.py` reports as e2e_serving. */
+/* ---------------------------------------------------------------------------------------
+ * The steps on either side of the kernel in an absorbed-MLA (DeepSeek) decode layer
+ * (not in the reference). Per-head GEMMs with only B token rows, run
+ * transposed like the decode itself (weights on the UMMA M axis, tokens on N), bf16
+ * operands, fp32 accumulation. Device pointers, stream-ordered.
+ *
+ * etap_mla_head_proj: y[b,h,:n_out] = x[b,h,:k_dim] . w[h] with w [heads][k_dim][n_out] bf16;
+ *   x bf16 (x_fp32 = 0) or fp32 (rounded to bf16 on load); y bf16 or fp32; strides in elements.
+ *   1 <= batch <= 256, k_dim % 64 == 0, n_out % 128 == 0.
+ * etap_mla_absorb_q: Q[b,t,h,0:512] = q_nope[b,t,h,:128] . W_UK[h] ([heads][128][512]) and
+ *   Q[b,t,h,512:576] = RoPE(q_pe[b,t,h,:64]) with per-token cos/sin [batch*q_tokens][32]
+ *   (half rotation: out_i = x_i cos_i - x_{i+32} sin_i, out_{i+32} = x_{i+32} cos_i + x_i sin_i).
+ *   Q is the decode's bf16 [batch][q_tokens][heads][576] input.
+ * etap_mla_up_proj: out[b,t,h,:128] = O[b,t,h,:512] . W_UV[h] ([heads][512][128]) from the
+ *   decode's fp32 O; out bf16 or fp32. */
+int etap_mla_head_proj(const void* x, int x_fp32, int64_t x_stride_b, int64_t x_stride_h, const void* w,
+                       int batch, int heads, int k_dim, int n_out, void* y, int y_fp32, int64_t y_stride_b,
+                       int64_t y_stride_h, void* stream);
+int etap_mla_absorb_q(const void* q_nope, const void* q_pe, const float* cos_t, const float* sin_t,
+                      const void* w_uk, int batch, int q_tokens, int heads, void* q, void* stream);
+int etap_mla_up_proj(const float* o, const void* w_uv, int batch, int q_tokens, int heads, void* out,
+                     int out_fp32, void* stream);
+
 int etap_mla_append_kv(const void* kv_rows, void* kv_pool, int64_t num_pages,
                        const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,
                        int batch, int q_tokens, void* stream);

@@ -1289,6 +1289,43 @@ size_t max_partials(int batch, int heads, int num_sm_parts) {
 namespace etap_b200 {
 // error reporting for the host-buffer entry points in etap_mla_host.cpp
 int host_fail(int code, const char* msg) { return fail(code, msg); }
+
+// 2-D bf16 tensor map over a row-major [rows][cols] matrix, box {64 cols, box_rows}, SW128
+// (etap_proj.cu); cached per (base, shape) like the decode's maps.
+int encode_bf16_sw128(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+    struct Entry {
+        const void* base = nullptr;
+        uint64_t cols = 0, rows = 0;
+        uint32_t box_rows = 0;
+        CUtensorMap map;
+    };
+    thread_local Entry cache[8];
+    thread_local unsigned next = 0;
+    for (auto& e : cache)
+        if (e.base == base && e.cols == cols && e.rows == rows && e.box_rows == box_rows) {
+            *map = e.map;
+            return ETAP_OK;
+        }
+    auto enc = get_encode_fn();
+    if (!enc) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver)");
+    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (cols * 2) % 16 != 0)
+        return fail(ETAP_ERR_SHAPE, "tensor base / row pitch must be 16-byte aligned");
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    Entry& e = cache[next++ % 8];
+    e.base = base;
+    e.cols = cols;
+    e.rows = rows;
+    e.box_rows = box_rows;
+    e.map = *map;
+    return ETAP_OK;
+}
 }  // namespace etap_b200
 
 extern "C" {

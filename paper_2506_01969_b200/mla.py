@@ -189,3 +189,39 @@ def selftest_umma(k: torch.Tensor, q: torch.Tensor, p: torch.Tensor) -> tuple[to
     check(_lib.lib().etap_mla_selftest_umma(k.data_ptr(), q.data_ptr(), p.data_ptr(), s_t.data_ptr(),
                                             o_t.data_ptr(), _stream_ptr(None)), "etap_mla_selftest_umma")
     return s_t, o_t
+
+
+# ------------------------------------------------------------------ adjacent decode steps
+def absorb_q(q_nope: torch.Tensor, q_pe: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, w_uk: torch.Tensor,
+             out: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Absorbed-MLA query: Q[b,t,h] = [q_nope[b,t,h] . W_UK[h] | RoPE(q_pe[b,t,h])] as the decode's
+    bf16 [B, T, H, 576] input (etap_mla_absorb_q). q_nope [B,T,H,128], q_pe [B,T,H,64] bf16,
+    cos/sin [B,T,32] fp32, w_uk [H,128,512] bf16."""
+    B, T, H = q_nope.shape[:3]
+    _check_tensor(q_nope, torch.bfloat16, (B, T, H, 128), "q_nope")
+    _check_tensor(q_pe, torch.bfloat16, (B, T, H, 64), "q_pe")
+    _check_tensor(cos, torch.float32, (B, T, 32), "cos")
+    _check_tensor(sin, torch.float32, (B, T, 32), "sin")
+    _check_tensor(w_uk, torch.bfloat16, (H, 128, D_V), "w_uk")
+    if out is None:
+        out = torch.empty((B, T, H, D_QK), dtype=torch.bfloat16, device=q_nope.device)
+    _check_tensor(out, torch.bfloat16, (B, T, H, D_QK), "out")
+    check(_lib.lib().etap_mla_absorb_q(q_nope.data_ptr(), q_pe.data_ptr(), cos.data_ptr(), sin.data_ptr(),
+                                       w_uk.data_ptr(), B, T, H, out.data_ptr(), _stream_ptr(stream)),
+          "etap_mla_absorb_q")
+    return out
+
+
+def up_proj(o: torch.Tensor, w_uv: torch.Tensor, out_dtype: torch.dtype = torch.bfloat16,
+            stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Per-head value up-projection of the decode output: out[b,t,h] = O[b,t,h] . W_UV[h]
+    (etap_mla_up_proj). o [B,T,H,512] fp32, w_uv [H,512,128] bf16 -> [B,T,H,128]."""
+    B, T, H = o.shape[:3]
+    _check_tensor(o, torch.float32, (B, T, H, D_V), "o")
+    _check_tensor(w_uv, torch.bfloat16, (H, D_V, 128), "w_uv")
+    if out_dtype not in (torch.bfloat16, torch.float32):
+        raise _lib.EtapShapeError("out_dtype must be bfloat16 or float32")
+    out = torch.empty((B, T, H, 128), dtype=out_dtype, device=o.device)
+    check(_lib.lib().etap_mla_up_proj(o.data_ptr(), w_uv.data_ptr(), B, T, H, out.data_ptr(),
+                                      int(out_dtype == torch.float32), _stream_ptr(stream)), "etap_mla_up_proj")
+    return out

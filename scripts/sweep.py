@@ -63,7 +63,59 @@ def measure(seqlens, heads, label, iters=50, q_tokens=1):
     torch.cuda.empty_cache()
 
 
+def measure_layer(B=16, H=16, ctx=65536, iters=50):
+    """Absorbed-MLA attention step: absorb_q (q_nope . W_UK + RoPE) -> decode -> up_proj
+    (O . W_UV), device time per piece and for the chained step (CUDA events, stream launches)."""
+    import math
+    inp = inputs.make_mla_inputs([ctx] * B, heads=H, seed=42, pad_value=0.0)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    q_nope = torch.randn((B, 1, H, 128), generator=g, device="cuda").to(torch.bfloat16)
+    q_pe = torch.randn((B, 1, H, 64), generator=g, device="cuda").to(torch.bfloat16)
+    w_uk = (torch.randn((H, 128, 512), generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    w_uv = (torch.randn((H, 512, 128), generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    cos = torch.ones((B, 1, 32), device="cuda"); sin = torch.zeros((B, 1, 32), device="cuda")
+    plan = mla.MlaDecodePlan.create(B, H, "cuda")
+    q = torch.empty((B, 1, H, 576), dtype=torch.bfloat16, device="cuda")
+    o = torch.empty((B, 1, H, 512), dtype=torch.float32, device="cuda")
+    lse = torch.empty((B, 1, H), dtype=torch.float32, device="cuda")
+    scale = 1 / math.sqrt(192)
+
+    def t(fn):
+        # device time: 20 calls captured in one CUDA graph (no host launch gaps), replayed
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s), torch.cuda.graph(gr, stream=s):
+            for _ in range(20):
+                fn()
+        torch.cuda.synchronize()
+        gr.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(max(1, iters // 20)):
+            gr.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1000 / (max(1, iters // 20) * 20)
+    absorb = lambda: mla.absorb_q(q_nope, q_pe, cos, sin, w_uk, out=q)
+    dec = lambda: plan.decode(q, inp.kv_pool, inp.block_table, inp.seqlens, scale, out=o, lse=lse)
+    up = lambda: mla.up_proj(o, w_uv)
+    line = {"config": f"absorbed MLA layer step B={B} H={H} ctx={ctx}", "absorb_q_us": t(absorb),
+            "decode_us": t(dec), "up_proj_us": t(up),
+            "step_us": t(lambda: (absorb(), dec(), up())),
+            "weight_bytes": (w_uk.numel() + w_uv.numel()) * 2}
+    print(json.dumps(line), flush=True)
+
+
 if __name__ == "__main__":
+    if "--layer" in sys.argv:
+        measure_layer()
+        measure_layer(ctx=4096)
+        sys.exit(0)
     if "--mtp" in sys.argv:  # multi-token decode: T tokens per sequence against the same context
         for t in (1, 2, 4):
             measure([65536] * 16, 16, f"B=16 ctx=64K H=16 q_tokens={t}", iters=20, q_tokens=t)
