@@ -199,7 +199,7 @@ __device__ __forceinline__ int cta_excl_scan256(int v, int* s_wt, int& total) {
     __syncthreads();
     int pre = 0, tot = 0;
 #pragma unroll
-    for (int w = 0; w < NUM_THREADS / 32; ++w) {
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
         const int t = s_wt[w];
         pre += (w < warp) ? t : 0;
         tot += t;
@@ -350,7 +350,7 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
     if (tid == 0) s_soff[n] = nsplits;
     __syncthreads();
     if (tid == 0) schedule_own_range(prm, ls, s_pref, s_soff, s_tiles, s_sched, total, T);
-    if (blockIdx.x == 0) publish_split_off(prm, ls, s_soff, tid, NUM_THREADS);
+    if (blockIdx.x == 0) publish_split_off(prm, ls, s_soff, tid, blockDim.x);
     __syncthreads();
 }
 
@@ -369,7 +369,7 @@ __device__ __forceinline__ bool split_at(const int32_t* sch, int seqlen, int bat
 }
 
 template <int HG_>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
     etap_mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv,
                            const __grid_constant__ CUtensorMap tm_q, const DecodeParams prm) {
     using C = Cfg<HG_>;
@@ -400,8 +400,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_init(&bars[BAR_Q_EMPTY], 1);
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&bars[BAR_S_FULL + i], 1);
-            ptx::mbar_init(&bars[BAR_S_FREE + i], 128);
-            ptx::mbar_init(&bars[BAR_P_FULL + i], 128);
+            ptx::mbar_init(&bars[BAR_S_FREE + i], 128 * C::NWG);
+            ptx::mbar_init(&bars[BAR_P_FULL + i], 128 * C::NWG);
         }
         ptx::fence_mbar_init();
     }
@@ -642,8 +642,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
         }
     } else if (warp >= SOFTMAX_WARP0) {
-        // ===================================================== softmax + epilogue (128 threads)
-        // thread = (KV row, head half): lane l of warp q owns row 16q + l%16, heads HH*(l/16)..
+        // ===================================================== softmax + epilogue (NWG x 128 threads)
+        // warpgroup wg owns heads [hoff, hoff + HW); thread = (KV row, head half): lane l of
+        // warp q owns row 16q + l%16, heads hoff + HH*(l/16)..; warpgroups synchronise only
+        // among themselves (named barriers 1+2wg, 2+2wg)
+        constexpr int HW = C::HW;
+        const int wg = (warp - SOFTMAX_WARP0) >> 2;
+        const int hoff = wg * HW;
+        const uint32_t bar_a = 1 + 2 * wg, bar_b = 2 + 2 * wg;
         const int wq = warp & 3;               // TMEM lane quadrant accessible by this warp
         const int half = lane >> 4;
         const int row = s_row_of(wq, lane);    // KV row in the tile
@@ -658,6 +664,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const float thresh = eager ? 0.f : LAZY_RESCALE_LOG2;
         const bool tracer = (threadIdx.x == SOFTMAX_WARP0 * 32);
         const bool head_owner = wq == 0 && (lane & 15) == 0;  // writes s_m / s_alpha of its half
+        const bool lane_head = wq == 0 && lane < HW;           // owner of head hoff + lane
         const bool mtp = prm.q_tokens > 1;
         const int rhead = halfwarp_reduce_head<HH>(lane);   // head (of the half) a reduction leaves here
         const bool rwriter = HH == 16 || (lane & 1) == 0;
@@ -673,12 +680,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < HH; ++j) {
                 m_own[j] = -INFINITY;
                 l_part[j] = 0.f;
-                const int tok = (sd.g * HG + half * HH + j) / prm.heads_per_token;
+                const int tok = (sd.g * HG + hoff + half * HH + j) / prm.heads_per_token;
                 row_lim[j] = sd.seqlen - (prm.causal ? prm.q_tokens - 1 - tok : 0);
                 // a split whose first tile shows no row to any column skips the max exchange
                 // (bar.red.or is false), so s_m must already read -inf for the epilogue
                 // (the previous split's epilogue released s_m with its final barrier)
-                if (head_owner) s_m[half * HH + j] = -INFINITY;
+                if (head_owner) s_m[hoff + half * HH + j] = -INFINITY;
             }
 
             for (int t = sd.t0; t < sd.t1; ++t) {
@@ -687,7 +694,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::tc_fence_after();
                 if (tracer) ETAP_TRACE(prm, gt, 4);
                 uint32_t sr[HH];
-                ptx::tmem_ld16x2<HH>(t_lane + C::TCOL_S + HG * buf, sr);
+                ptx::tmem_ld16x2<HH>(t_lane + C::TCOL_S + HG * buf + hoff, sr);
                 ptx::tmem_wait_ld();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&bars[BAR_S_FREE + buf]);
@@ -702,9 +709,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
                 const bool first = (t == sd.t0);
                 const bool debug = prm.state != nullptr && t < prm.state_tiles;
-                const float dbg_m_old = (debug && wq == 0 && lane < HG && !first) ? s_m[lane] : -INFINITY;
+                const float dbg_m_old = (debug && lane_head && !first) ? s_m[hoff + lane] : -INFINITY;
                 // one barrier decides, CTA-uniformly, whether any running max must move
-                const bool any = ptx::bar_red_or(1, 128, exceed || (negate && !first));
+                const bool any = ptx::bar_red_or(bar_a, 128, exceed || (negate && !first));
                 bool need_rescale = false;
                 float alpha_own[HH];
 #pragma unroll
@@ -712,12 +719,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (any) {
                     const float wm = halfwarp_reduce<true, HH>(x, lane);
                     float* rm = red_max + (gt & 1) * 4 * HG;
-                    if (rwriter) rm[wq * HG + half * HH + rhead] = wm;
-                    ptx::named_bar_sync(2, 128);
+                    if (rwriter) rm[wq * HG + hoff + half * HH + rhead] = wm;
+                    ptx::named_bar_sync(bar_b, 128);
                     bool upd = false;
 #pragma unroll
                     for (int j = 0; j < HH; ++j) {
-                        const int h = half * HH + j;
+                        const int h = hoff + half * HH + j;
                         const float mt = fmaxf(fmaxf(rm[h], rm[HG + h]), fmaxf(rm[2 * HG + h], rm[3 * HG + h]));
                         if (first) {
                             m_own[j] = mt;
@@ -731,12 +738,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         }
                     }
                     // CTA-uniform decision (also orders all reads of s_m before the writes below)
-                    need_rescale = ptx::bar_red_or(2, 128, upd) || (negate && !first);
+                    need_rescale = ptx::bar_red_or(bar_b, 128, upd) || (negate && !first);
                     if (head_owner) {
 #pragma unroll
                         for (int j = 0; j < HH; ++j) {
-                            s_m[half * HH + j] = m_own[j];
-                            s_alpha[half * HH + j] = alpha_own[j];
+                            s_m[hoff + half * HH + j] = m_own[j];
+                            s_alpha[hoff + half * HH + j] = alpha_own[j];
                         }
                     }
                 }
@@ -752,21 +759,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     // BlockHook replay: column sums of this tile's P, running l, m, rescale in
                     // natural-log units, as BlockStepInfo carries them (tiled_standard.hpp:32-40)
                     const float cs = halfwarp_reduce<false, HH>(pv, lane);
-                    if (rwriter) red_sum[wq * HG + half * HH + rhead] = cs;
-                    ptx::named_bar_sync(2, 128);
-                    if (wq == 0 && lane < HG) {
-                        const float colsum = red_sum[lane] + red_sum[HG + lane] + red_sum[2 * HG + lane] +
-                                             red_sum[3 * HG + lane];
-                        const float mn = s_m[lane];
-                        const float al = first ? 0.f : (any ? s_alpha[lane] : 1.f);
+                    if (rwriter) red_sum[wq * HG + hoff + half * HH + rhead] = cs;
+                    ptx::named_bar_sync(bar_b, 128);
+                    if (lane_head) {
+                        const int h = hoff + lane;
+                        const float colsum = red_sum[h] + red_sum[HG + h] + red_sum[2 * HG + h] + red_sum[3 * HG + h];
+                        const float mn = s_m[h];
+                        const float al = first ? 0.f : (any ? s_alpha[h] : 1.f);
                         dbg_l = first ? colsum : fmaf(dbg_l, al, colsum);
                         float* st = prm.state + (static_cast<size_t>(sd.vb) * prm.state_tiles + t) * 4 * HG;
-                        st[lane] = dbg_m_old * 0.69314718055994530942f;
-                        st[HG + lane] = mn * 0.69314718055994530942f;
-                        st[2 * HG + lane] = al;
-                        st[3 * HG + lane] = dbg_l;
+                        st[h] = dbg_m_old * 0.69314718055994530942f;
+                        st[HG + h] = mn * 0.69314718055994530942f;
+                        st[2 * HG + h] = al;
+                        st[3 * HG + h] = dbg_l;
                     }
-                    ptx::named_bar_sync(2, 128);
+                    ptx::named_bar_sync(bar_b, 128);
                 }
                 if (tracer) ETAP_TRACE(prm, gt, 8);
                 // the P buffer is reused every P_BUFS tiles: GEMM2(gt - P_BUFS) must have read it
@@ -775,34 +782,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (tracer) ETAP_TRACE(prm, gt, 9);
                 if (need_rescale) {
                     // O^T must contain GEMM2(gt-1) before it is rescaled; s_alpha written above
-                    ptx::named_bar_sync(2, 128);
+                    ptx::named_bar_sync(bar_b, 128);
                     ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 1) % NTB], ((gt - 1) / NTB) & 1);
                     ptx::tc_fence_after();
+                    // this warpgroup's heads: the hi columns [hoff, hoff+HW) and lo [HG+hoff, ...)
 #pragma unroll 1
                     for (int blk = 0; blk < 4; ++blk) {
 #pragma unroll
-                        for (int part = 0; part < static_cast<int>(C::OBLK) / 32; ++part) {
-                            uint32_t o[32];
-                            const uint32_t ta = t_lane + C::TCOL_O + C::OBLK * blk + 32 * part;
-                            ptx::tmem_ld32(ta, o);
+                        for (int seg = 0; seg < 2; ++seg) {
+                            uint32_t o[16];
+                            const uint32_t ta = t_lane + C::TCOL_O + C::OBLK * blk + seg * HG + hoff;
+                            ptx::tmem_ld16(ta, o);
                             ptx::tmem_wait_ld();
 #pragma unroll
-                            for (int c = 0; c < 32; ++c) {
-                                const float a = s_alpha[(32 * part + c) % HG];
+                            for (int c = 0; c < 16; ++c) {
+                                const float a = s_alpha[hoff + c];
                                 o[c] = __float_as_uint(__uint_as_float(o[c]) * (negate ? -a : a));
                             }
-                            ptx::tmem_st32(ta, o);
+                            ptx::tmem_st16(ta, o);
                         }
                     }
                     ptx::tmem_wait_st();
                 }
-                write_p_hilo<C>(smem + C::OFF_P + (buf % C::P_BUFS) * C::P_BYTES, row, half, pv);
+                write_p_hilo<C>(smem + C::OFF_P + (buf % C::P_BUFS) * C::P_BYTES, row, half, pv, hoff);
                 // rows of the last page past seqlen were loaded from HBM and may hold
                 // non-finite garbage; zero them in the V chunks (0 * NaN = NaN in the MMA)
                 if (grow >= sd.seqlen) {
                     const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
+                    constexpr int ZC = 8 / (2 * C::NWG);  // V chunks zeroed per thread
 #pragma unroll 1
-                    for (int c = half * 4; c < half * 4 + 4; ++c) {
+                    for (int c = (wg * 2 + half) * ZC; c < (wg * 2 + half + 1) * ZC; ++c) {
                         const uint32_t s = (pos0 + pos_of_chunk(c, gt)) % C::NSLOT;
                         uint4* dst = reinterpret_cast<uint4*>(smem + C::OFF_RING + s * SLOT_BYTES + row * 128);
 #pragma unroll
@@ -823,32 +832,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_wait(&bars[BAR_G2_DONE + last % NTB], (last / NTB) & 1);
             ptx::tc_fence_after();
             if (tracer) ETAP_TRACE_G(prm, 10);
-            // BPW d-blocks per TMEM load wait (HG = 16: two blocks = 64 registers in flight)
-            constexpr int BPW = HG == 16 ? 2 : 1;
-            uint32_t o[BPW][2 * HG];
+            // two d-blocks per TMEM load wait: this warpgroup's 16 hi + 16 lo columns each
+            constexpr int BPW = 2;
+            uint32_t o[BPW][2 * HW];
             const float wsum = halfwarp_reduce<false, HH>(l_part, lane);
-            if (rwriter) red_sum[wq * HG + half * HH + rhead] = wsum;
+            if (rwriter) red_sum[wq * HG + hoff + half * HH + rhead] = wsum;
             const int ns = soff[vb + 1] - soff[vb];
             const bool direct = ns == 1;  // one split: final O / L rows, else a split partial
-            if (direct && wq == 0 && lane < HG) s_row[lane] = static_cast<int>(prm.om.row(sd.b, sd.g * HG + lane));
+            if (direct && lane_head) s_row[hoff + lane] = static_cast<int>(prm.om.row(sd.b, sd.g * HG + hoff + lane));
             if (tracer) ETAP_TRACE(prm, last, 10);
-            ptx::named_bar_sync(2, 128);
+            ptx::named_bar_sync(bar_b, 128);
             if (tracer) ETAP_TRACE(prm, last, 11);
             // one owner thread per head finishes l, 1/l and L in parallel (a serial per-head loop
             // in every thread costs ~1.6k cycles); 1/l is broadcast through red_max, which no
             // one reads between tiles
             float L_own = 0.f;
             float* s_inv = red_max;
-            if (wq == 0 && lane < HG) {
-                const float l = red_sum[lane] + red_sum[HG + lane] + red_sum[2 * HG + lane] + red_sum[3 * HG + lane];
-                s_inv[lane] = l > 0.f ? 1.f / l : 0.f;  // l = 0: column saw no row (O = 0, L = -inf)
-                L_own = (s_m[lane] + log2f(l)) * 0.69314718055994530942f;
+            if (lane_head) {
+                const int h = hoff + lane;
+                const float l = red_sum[h] + red_sum[HG + h] + red_sum[2 * HG + h] + red_sum[3 * HG + h];
+                s_inv[h] = l > 0.f ? 1.f / l : 0.f;  // l = 0: column saw no row (O = 0, L = -inf)
+                L_own = (s_m[h] + log2f(l)) * 0.69314718055994530942f;
             }
-            ptx::named_bar_sync(2, 128);
-            float inv_l[HG];
+            ptx::named_bar_sync(bar_b, 128);
+            float inv_l[HW];
 #pragma unroll
-            for (int h = 0; h < HG; h += 4) {
-                const float4 v4 = *reinterpret_cast<const float4*>(s_inv + h);
+            for (int h = 0; h < HW; h += 4) {
+                const float4 v4 = *reinterpret_cast<const float4*>(s_inv + hoff + h);
                 inv_l[h] = v4.x; inv_l[h + 1] = v4.y; inv_l[h + 2] = v4.z; inv_l[h + 3] = v4.w;
             }
             const int idx = (vb == sch[0]) ? sch[4] : soff[vb] + idx_off;  // partial index (ns > 1)
@@ -859,45 +869,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int bb = 0; bb < BPW; ++bb)
 #pragma unroll
-                    for (int part = 0; part < 2 * HG / 32; ++part)
-                        ptx::tmem_ld32(t_lane + C::TCOL_O + C::OBLK * (blk0 + bb) + 32 * part,
-                                       *reinterpret_cast<uint32_t(*)[32]>(&o[bb][32 * part]));
+                    for (int seg = 0; seg < 2; ++seg)
+                        ptx::tmem_ld16(t_lane + C::TCOL_O + C::OBLK * (blk0 + bb) + seg * HG + hoff,
+                                       *reinterpret_cast<uint32_t(*)[16]>(&o[bb][16 * seg]));
                 ptx::tmem_wait_ld();
                 if (tracer && blk0 == 0) ETAP_TRACE(prm, last, 14);
 #pragma unroll
                 for (int bb = 0; bb < BPW; ++bb) {
                     const int d = (blk0 + bb) * 128 + drow;
-                    float v[HG];
+                    float v[HW];
 #pragma unroll
-                    for (int h = 0; h < HG; ++h)
-                        v[h] = (__uint_as_float(o[bb][h]) + __uint_as_float(o[bb][HG + h])) * inv_l[h];
+                    for (int h = 0; h < HW; ++h)
+                        v[h] = (__uint_as_float(o[bb][h]) + __uint_as_float(o[bb][HW + h])) * inv_l[h];
                     if (direct) {
                         // every output copy (peer gather: each rank's buffer over NVLink)
 #pragma unroll 1
                         for (int r = 0; r < prm.om.n_out; ++r) {
                             float* dst = prm.om.out[r] + d;
 #pragma unroll
-                            for (int h = 0; h < HG; ++h) dst[static_cast<size_t>(s_row[h]) * D_V] = v[h];
+                            for (int h = 0; h < HW; ++h) dst[static_cast<size_t>(s_row[hoff + h]) * D_V] = v[h];
                         }
                     } else {
 #pragma unroll
-                        for (int h = 0; h < HG; ++h) part_o[h * D_V + d] = v[h];
+                        for (int h = 0; h < HW; ++h) part_o[(hoff + h) * D_V + d] = v[h];
                     }
                 }
                 if (tracer && blk0 == 0) ETAP_TRACE(prm, last, 15);
             }
             if (tracer) ETAP_TRACE(prm, last, 12);
-            if (wq == 0 && lane < HG) {
+            if (lane_head) {
                 const float L = L_own;
                 if (direct) {
-                    for (int r = 0; r < prm.om.n_out; ++r) prm.om.lse[r][s_row[lane]] = L;
+                    for (int r = 0; r < prm.om.n_out; ++r) prm.om.lse[r][s_row[hoff + lane]] = L;
                 } else {
-                    prm.ws_lse[static_cast<size_t>(idx) * HG + lane] = L;
+                    prm.ws_lse[static_cast<size_t>(idx) * HG + hoff + lane] = L;
                 }
             }
             ptx::tc_fence_before();
             // red_sum / s_m are rewritten by the next split only after this barrier
-            ptx::named_bar_sync(2, 128);
+            ptx::named_bar_sync(bar_b, 128);
             if (tracer) ETAP_TRACE(prm, last, 13);
         }
     }
@@ -1575,17 +1585,18 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(num_sm_parts);
-    cfg.blockDim = dim3(NUM_THREADS);
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (hg == 32) {
         cfg.dynamicSmemBytes = Cfg<32>::SMEM_ALLOC;
+        cfg.blockDim = dim3(Cfg<32>::THREADS);
         static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<32>, Cfg<32>::SMEM_ALLOC);
         if (attr_rc) return attr_rc;
         ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel<32>, tm_kv, tm_q, prm));
     } else {
         cfg.dynamicSmemBytes = Cfg<16>::SMEM_ALLOC;
+        cfg.blockDim = dim3(Cfg<16>::THREADS);
         static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<16>, Cfg<16>::SMEM_ALLOC);
         if (attr_rc) return attr_rc;
         ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel<16>, tm_kv, tm_q, prm));

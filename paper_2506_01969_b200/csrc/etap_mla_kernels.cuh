@@ -36,7 +36,7 @@ constexpr int SLOT_BYTES = TILE * 128;  // 64 rows x 128 B = 8 KiB per ring slot
 constexpr int NTB = 4;          // tile-barrier ring depth (tiles in flight <= NSLOT/9 + 1)
 constexpr int NBAR = 5 * NTB + 8;
 constexpr int MAX_FUSED_VB = 128;  // longer lines (batch * head groups) run K1 first
-constexpr int SCHED_SMEM_INTS = 4 * MAX_FUSED_VB + 2 + 8 + 8;  // pref, soff, tiles, len, sched, wt
+constexpr int SCHED_SMEM_INTS = 4 * MAX_FUSED_VB + 2 + 8 + 16;  // pref, soff, tiles, len, sched, wt (<= 16 warps)
 
 // warp 0 TMA producer, warp 1 GEMM1 issuer (+TMEM alloc), warp 2 GEMM2 issuer, warp 3 idle,
 // warps 4..7 softmax / epilogue (warp % 4 = TMEM lane quadrant)
@@ -82,7 +82,12 @@ __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / 
 template <int HG_>
 struct Cfg {
     static constexpr int HG = HG_;
-    static constexpr int HH = HG / 2;                    // heads per softmax thread
+    // softmax warpgroups: HG = 32 splits its heads over two warpgroups (16 heads each), so a
+    // thread handles 8 heads either way and the per-tile softmax time does not double
+    static constexpr int NWG = HG == 32 ? 2 : 1;
+    static constexpr int HW = HG / NWG;                  // heads per softmax warpgroup
+    static constexpr int HH = HW / 2;                    // heads per softmax thread
+    static constexpr int THREADS = 128 * (1 + NWG);      // warps 0-3 roles, then the warpgroups
     // ring depth in 8 KB chunk slots; HG = 32 affords 22 with a single P buffer (the softmax
     // writes P(gt) once GEMM2(gt-1) has read P(gt-1), which it has long done by then)
     static constexpr int NSLOT = HG == 16 ? 24 : ETAP_HG32_NSLOT;
@@ -196,7 +201,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo_elem, float hi_elem) {
 // P (fp32, HH heads [HH*half, HH*half+HH) of KV row r) -> bf16 hi and lo parts, written into
 // row r of [P_hi | P_lo]^T: hi heads at columns HH*half.., lo heads at HG + HH*half..
 template <class C>
-__device__ __forceinline__ void write_p_hilo(uint8_t* p, int r, int half, const float (&pv)[C::HH]) {
+__device__ __forceinline__ void write_p_hilo(uint8_t* p, int r, int half, const float (&pv)[C::HH], int hoff = 0) {
     uint32_t hi[C::HH / 2], lo[C::HH / 2];
 #pragma unroll
     for (int i = 0; i < C::HH / 2; ++i) {
@@ -211,7 +216,7 @@ __device__ __forceinline__ void write_p_hilo(uint8_t* p, int r, int half, const 
     uint8_t* row = p + (r >> 3) * C::P_ROWGRP + (r & 7) * 16;
 #pragma unroll
     for (int c = 0; c < C::HH / 8; ++c) {  // 8 heads = one 16 B core-matrix row
-        const int n_hi = half * C::HH + 8 * c, n_lo = C::HG + n_hi;
+        const int n_hi = hoff + half * C::HH + 8 * c, n_lo = C::HG + n_hi;
         *reinterpret_cast<uint4*>(row + (n_hi >> 3) * 128) =
             make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
         *reinterpret_cast<uint4*>(row + (n_lo >> 3) * 128) =
