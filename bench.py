@@ -366,8 +366,20 @@ def e2e_host(inp, steps: int, dev) -> dict:
         L.etap_mla_host_ctx_destroy(ctx)
     h2d = q.numel() * 2 + kv.numel() * 2 + bt.numel() * 4 + sl.numel() * 4
     d2h = out.numel() * 4 + lse.numel() * 4
+    # the bound of this path: a plain pinned host->device copy of the same bytes
+    dst = torch.empty_like(kv, device=dev)
+    dst.copy_(kv, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(2):
+        dst.copy_(kv, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    h2d_gbs = 2 * kv.numel() * 2 / (time.perf_counter() - t0) / 1e9
+    del dst
     return {"value": dt * 1e6, "unit": "us/step", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "api": "etap_mla_host_decode (C-ABI, pinned host buffers, synchronous)", "steps": steps}
+            "api": "etap_mla_host_decode (C-ABI, pinned host buffers, synchronous)", "steps": steps,
+            "bound": {"kind": "pcie_h2d", "measured_h2d_gbs": h2d_gbs,
+                      "bound_us": (h2d + d2h) / h2d_gbs / 1e3, "frac": (h2d + d2h) / h2d_gbs / 1e3 / (dt * 1e6)}}
 
 
 def e2e_serving_host(inp, steps: int, dev) -> dict:
