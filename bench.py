@@ -233,7 +233,31 @@ def run_ours(args) -> None:
         if gather == "peer":
             from paper_2506_01969_b200 import peer
 
-            pg = peer.PeerGather(BATCH, HEADS, world, rank, device=dev)
+            # every rank must take the same path: if the IPC setup fails anywhere (or the
+            # first fused step does not verify against the NCCL gather), all fall back to NCCL
+            ok = 1
+            try:
+                pg = peer.PeerGather(BATCH, HEADS, world, rank, device=dev)
+            except Exception as e:  # noqa: BLE001
+                log(f"[bench] rank {rank}: peer gather setup failed ({e})")
+                pg, ok = None, 0
+            fdev = dev if backend == "nccl" else "cpu"
+            flag = torch.tensor([ok], device=fdev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 1:
+                o_p, l_p = pg.decode(plan, inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
+                plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, out=out, lse=lse)
+                o_n, l_n = sharding.gather_heads(out), sharding.gather_heads(lse)
+                torch.cuda.synchronize(dev)
+                same = int(torch.equal(o_p.reshape(o_n.shape), o_n) and torch.equal(l_p.reshape(l_n.shape), l_n))
+                flag = torch.tensor([same], device=fdev)
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+                if int(flag.item()) != 1:
+                    log("[bench] fused peer gather differs from the NCCL gather: falling back to NCCL")
+            if int(flag.item()) != 1:
+                if pg is not None:
+                    pg.close()
+                gather = "nccl"
 
     def step():
         # K2 computes the split schedule in its prologue (same partition as K1, which is the
