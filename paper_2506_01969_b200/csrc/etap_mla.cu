@@ -395,6 +395,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
             ptx::mbar_init(&bars[BAR_FULL_C + i], 1);
             ptx::mbar_init(&bars[BAR_G2_DONE + i], 1);
             ptx::mbar_init(&bars[BAR_G2_HALF + i], 1);
+            ptx::mbar_init(&bars[BAR_G2_3Q + i], 1);
         }
         ptx::mbar_init(&bars[BAR_Q_FULL], 1);
         ptx::mbar_init(&bars[BAR_Q_EMPTY], 1);
@@ -562,9 +563,12 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     if (!C::THIRD_GROUP) ETAP_TRACE(prm, gt, 1);
                 }
                 if constexpr (C::THIRD_GROUP) {
-                    // the rest reuse gt-2's positions [4, 9 - SPLIT_POS): the whole GEMM2 of gt-2
+                    // the rest reuse gt-2's positions [4, 9 - SPLIT_POS): free after GEMM2 d-blocks
+                    // 0-2 of gt-2 (22-slot ring) or the whole GEMM2
                     __syncwarp();
-                    if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+                    if (gt >= 2)
+                        ptx::mbar_wait(&bars[(C::G3_AFTER_3Q ? BAR_G2_3Q : BAR_G2_DONE) + (gt - 2) % NTB],
+                                       ((gt - 2) / NTB) & 1);
                     if (lane == 0) {
                         ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_C + tb], (NCHUNK - C::SPLIT_POS2) * SLOT_BYTES);
 #pragma unroll 1
@@ -635,6 +639,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     issue_gemm2_block<C>(tmem_base + C::TCOL_O + C::OBLK * blk, ring_addr + sa * SLOT_BYTES,
                                          p_addr + (buf % C::P_BUFS) * C::P_BYTES, t == sd.t0);
                     if (blk == 1) ptx::umma_commit_elect(&bars[BAR_G2_HALF + gt % NTB]);
+                    if (C::G3_AFTER_3Q && C::THIRD_GROUP && blk == 2) ptx::umma_commit_elect(&bars[BAR_G2_3Q + gt % NTB]);
                 }
                 ptx::umma_commit_elect(&bars[BAR_G2_DONE + gt % NTB]);
                 ETAP_TRACE(prm, gt, 7);

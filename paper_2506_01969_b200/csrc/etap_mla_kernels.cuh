@@ -34,7 +34,7 @@ constexpr int NCHUNK = 9;       // 576 / 64 column chunks (SW128 atoms are 64 bf
 constexpr int NVCHUNK = 8;      // 512 / 64 chunks that are also V
 constexpr int SLOT_BYTES = TILE * 128;  // 64 rows x 128 B = 8 KiB per ring slot
 constexpr int NTB = 4;          // tile-barrier ring depth (tiles in flight <= NSLOT/9 + 1)
-constexpr int NBAR = 5 * NTB + 8;
+constexpr int NBAR = 6 * NTB + 8;
 constexpr int MAX_FUSED_VB = 128;  // longer lines (batch * head groups) run K1 first
 constexpr int SCHED_SMEM_INTS = 4 * MAX_FUSED_VB + 2 + 8 + 16;  // pref, soff, tiles, len, sched, wt (<= 16 warps)
 
@@ -68,6 +68,7 @@ constexpr int BAR_G2_DONE = 2 * NTB;    // [NTB] GEMM2 of tile gt complete: its 
 constexpr int BAR_G2_HALF = 3 * NTB;    // [NTB] GEMM2 d-blocks 0-1 of tile gt complete: the
                                         //       rope slot and V chunks 0-3 are free
 constexpr int BAR_FULL_C = 4 * NTB + 8;  // [NTB] ring positions [SPLIT_POS2, 9) of tile gt landed
+constexpr int BAR_G2_3Q = 5 * NTB + 8;   // [NTB] GEMM2 d-blocks 0-2 of tile gt complete (V0..V5 free)
 constexpr int BAR_Q_FULL = 4 * NTB + 0;
 constexpr int BAR_Q_EMPTY = 4 * NTB + 1;
 constexpr int BAR_S_FULL = 4 * NTB + 2;  // [2]
@@ -100,6 +101,9 @@ struct Cfg {
     static constexpr int SPLIT_POS = NSLOT - 18;
     static constexpr int SPLIT_POS2 = SPLIT_POS + 4 < NCHUNK ? SPLIT_POS + 4 : NCHUNK;
     static constexpr bool THIRD_GROUP = SPLIT_POS2 < NCHUNK;
+    // the third group reuses gt-2's positions [4, 9 - SPLIT_POS): V chunks up to V(8 - SPLIT_POS),
+    // free after GEMM2 d-blocks 0-2 (G2_3Q) when that is at most V5
+    static constexpr bool G3_AFTER_3Q = SPLIT_POS >= 3;
     static constexpr int Q_CHUNK_BYTES = HG * 128;
     static constexpr int Q_BYTES = NCHUNK * Q_CHUNK_BYTES;
     static constexpr int PN = 2 * HG;                    // GEMM2 N: HG heads hi | HG heads lo
