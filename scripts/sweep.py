@@ -112,6 +112,12 @@ def measure_layer(B=16, H=16, ctx=65536, iters=50):
 
 
 if __name__ == "__main__":
+    if "--serving" in sys.argv:  # serving-style batches: many sequences, short-to-medium contexts
+        import random
+        for B, lo, hi in ((64, 2048, 8192), (128, 1024, 4096), (256, 512, 4096), (128, 4096, 32768)):
+            rnd = random.Random(B * 7 + lo)
+            measure([rnd.randint(lo, hi) for _ in range(B)], 16, f"serving B={B} ctx {lo}-{hi}", iters=20)
+        sys.exit(0)
     if "--layer" in sys.argv:
         measure_layer()
         measure_layer(ctx=4096)
