@@ -243,6 +243,11 @@ int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t
 int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* s_t, float* o_t,
                            void* stream);
 
+/* FP8 (e4m3) UMMA self-test (kind::f8f6f4), the FP8 latent-KV layouts: k8 [64][576], q8 [48][576]
+ * (three fp8 terms x 16 heads), p8 [64][48] e4m3 bytes; outputs s_t [64][48] = k8 q8^T and
+ * o_t [512][48] = k8[:, :512]^T p8, fp32. */
+int etap_mla_selftest_fp8(const void* k8, const void* q8, const void* p8, float* s_t, float* o_t, void* stream);
+
 /* Debug: when device_buf is non-NULL, subsequent decode launches record per-tile %clock64
  * stamps of the pipeline events into it: [cta][256][16] uint64, row = tile (< 255): 0/1 first /
  * last chunk TMA issued, 2 last chunk landed, 3 S^T committed, 4 softmax saw S^T, 5 P^T

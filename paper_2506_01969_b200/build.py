@@ -22,7 +22,8 @@ LIB = LIBDIR / "libetap_mla.so"
 BENCH = LIBDIR / "etap_bench"
 MODEL = LIBDIR / "etap_model"
 
-SOURCES = [CSRC / "etap_mla.cu", CSRC / "etap_peer.cu", CSRC / "etap_proj.cu", CSRC / "etap_mla_host.cpp"]
+SOURCES = [CSRC / "etap_mla.cu", CSRC / "etap_peer.cu", CSRC / "etap_proj.cu", CSRC / "etap_fp8.cu",
+           CSRC / "etap_mla_host.cpp"]
 DEPS = SOURCES + [CSRC / "etap_bench.cpp", CSRC / "sm100_ptx.cuh", CSRC / "etap_mla_kernels.cuh", ROOT / "include" / "etap_mla.h"]
 
 NVCC_FLAGS = [
