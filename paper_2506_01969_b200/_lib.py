@@ -64,6 +64,8 @@ def _declare(lib: C.CDLL) -> None:
         "etap_mla_absorb_q": (i32, [vp, vp, vp, vp, vp, i32, i32, i32, vp, vp]),
         "etap_mla_up_proj": (i32, [vp, vp, i32, i32, i32, vp, i32, vp]),
         "etap_mla_selftest_fp8": (i32, [vp, vp, vp, vp, vp, vp]),
+        "etap_mla_decode_fp8": (i32, [vp, vp, f32, i64, vp, i32, vp, i32, i32, i32, f32, i32, vp, vp, i32, vp, vp, vp,
+                                      u32, vp]),
         "etap_mla_host_ctx_destroy": (None, [vp]),
         "etap_mla_run_etap_f64": (i32, [vp, i64, vp, i64, i64, vp, i64, f64, i64, i64, i64, u32,
                                         vp, vp]),

@@ -1,103 +1,18 @@
 // SPDX-License-Identifier: Apache-2.0
-// FP8 (e4m3) latent-KV path of the ETAP MLA decode: operand layouts and their UMMA check.
-//
-// A page of the FP8 latent cache is [64 rows][576 B]. In shared memory one tile (page) is
-//   4 V chunks of 128 columns: 64 rows x 128 B, SW128, K-major for GEMM1 / MN-major (V^T)
-//     for GEMM2 (128 fp8 = one 128 B swizzle row, so a d-block of 128 is one chunk);
-//   1 rope chunk of 64 columns: 64 rows x 64 B, SW64, K-major (GEMM1 only).
-// GEMM1 (kind::f8f6f4, M = 64, N = 48, K = 32 per MMA) multiplies the page with three fp8
-// terms of Q (q = q0 + q1/16 + q2/256, exact for bf16 q in the normal range); GEMM2
-// (M = 128, N = 48) multiplies V^T with three fp8 terms of P (P = p0 + p1/16 + p2/256, about
-// 12 significant bits). Both read the fp8 page straight from shared memory: no dequantising
-// pass over the KV bytes.
+// FP8 (e4m3) latent-KV path: the kind::f8f6f4 UMMA self-test of the operand layouts in
+// etap_fp8.cuh (one tile, operands staged by plain loads).
 #include <cuda.h>
-#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "../../include/etap_mla.h"
-#include "sm100_ptx.cuh"
+#include "etap_fp8.cuh"
 
 namespace etap_b200 {
 int host_fail(int code, const char* msg);  // etap_mla.cu
 }
 
-namespace etap_b200 {
-namespace fp8 {
-
-constexpr int ROWS = 64;                  // KV rows per tile
-constexpr int VCH = 4;                    // V chunks of 128 fp8 columns
-constexpr int VCH_BYTES = ROWS * 128;     // 8 KB
-constexpr int ROPE_OFF = VCH * VCH_BYTES; // rope chunk: 64 rows x 64 B (SW64)
-constexpr int TILE_BYTES = ROPE_OFF + ROWS * 64;  // 36 KB
-constexpr int NT = 3;                     // fp8 terms of Q and of P
-constexpr int HGF = 16;                   // heads per work unit
-constexpr int NQ = NT * HGF;              // UMMA N of both GEMMs (48)
-constexpr int Q_VBLK = NQ * 128;          // Q^T V block: 48 rows x 128 B
-constexpr int Q_BYTES = VCH * Q_VBLK + NQ * 64;
-constexpr int P_ROWGRP = (NQ / 16) * 128; // P^T (MN-major, no swizzle): bytes per 8-row group
-constexpr int P_BYTES = ROWS / 8 * P_ROWGRP;
-
-// instruction descriptor, kind::f8f6f4: E4M3 A and B, f32 D
-__host__ __device__ constexpr uint32_t idesc_e4m3_f32(uint32_t m, uint32_t n, uint32_t a_mn, uint32_t b_mn) {
-    return (1u << 4) | (0u << 7) | (0u << 10) | (a_mn << 15) | (b_mn << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
-}
-
-__device__ __forceinline__ void umma_f8_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                              uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-
-// byte offset of (row, byte b) in a swizzled K-major / MN-major block with 128 B rows (SW128)
-// or 64 B rows (SW64): 16-byte units XOR-permuted within 1024 B / 512 B atoms
-__host__ __device__ inline uint32_t sw128_off(uint32_t row, uint32_t b) {
-    return row * 128 + ((((b >> 4) ^ (row & 7)) << 4) | (b & 15));
-}
-__host__ __device__ inline uint32_t sw64_off(uint32_t row, uint32_t b) {
-    return row * 64 + ((((b >> 4) ^ ((row >> 1) & 3)) << 4) | (b & 15));
-}
-// P^T element (KV row r, column n = term * 16 + head), MN-major without swizzle
-__host__ __device__ inline uint32_t p_off(uint32_t r, uint32_t n) {
-    return (r >> 3) * P_ROWGRP + (n >> 4) * 128 + (r & 7) * 16 + (n & 15);
-}
-
-// GEMM1: S^T[64 x 48] = K[64 x 576] . Q3^T (18 MMAs of K = 32). Whole-warp call.
-__device__ __forceinline__ void issue_gemm1(uint32_t s_tmem, uint32_t tile, uint32_t q) {
-    constexpr uint32_t idesc = idesc_e4m3_f32(64, NQ, 0, 0);
-#pragma unroll
-    for (int c = 0; c < VCH; ++c) {
-        const uint64_t a0 = ptx::smem_desc(tile + c * VCH_BYTES, 16, 1024, ptx::LAYOUT_SW128);
-        const uint64_t b0 = ptx::smem_desc(q + c * Q_VBLK, 16, 1024, ptx::LAYOUT_SW128);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // +32 B (32 fp8) along K inside the 128 B row
-            umma_f8_elect(s_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, (c == 0 && kk == 0) ? 0u : 1u);
-    }
-    const uint64_t a0 = ptx::smem_desc(tile + ROPE_OFF, 16, 512, ptx::LAYOUT_SW64);
-    const uint64_t b0 = ptx::smem_desc(q + VCH * Q_VBLK, 16, 512, ptx::LAYOUT_SW64);
-#pragma unroll
-    for (int kk = 0; kk < 2; ++kk) umma_f8_elect(s_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, 1u);
-}
-
-// GEMM2 for d-block c (128 latent columns = V chunk c): O^T[128 x 48] (+)= V^T[128 x 64] . P3^T
-__device__ __forceinline__ void issue_gemm2(uint32_t o_tmem, uint32_t vchunk, uint32_t p, bool zero_init) {
-    constexpr uint32_t idesc = idesc_e4m3_f32(128, NQ, 1, 1);
-    const uint64_t a0 = ptx::smem_desc(vchunk, VCH_BYTES, 1024, ptx::LAYOUT_SW128);
-    const uint64_t b0 = ptx::smem_desc(p, P_ROWGRP, 128, ptx::LAYOUT_NONE);
-#pragma unroll
-    for (int kk = 0; kk < ROWS / 32; ++kk)  // 32 KV rows per MMA: 4 swizzle atoms of V^T, 4 row groups of P^T
-        umma_f8_elect(o_tmem, a0 + kk * (4096 >> 4), b0 + kk * ((4 * P_ROWGRP) >> 4), idesc,
-                      (zero_init && kk == 0) ? 0u : 1u);
-}
-
-}  // namespace fp8
-}  // namespace etap_b200
 
 namespace {
 

@@ -23,6 +23,7 @@
 
 #include "../../include/etap_mla.h"
 #include "etap_mla_kernels.cuh"
+#include "etap_fp8.cuh"
 
 using namespace etap_b200;
 
@@ -936,6 +937,435 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
 }
 
 // =============================================================================================
+// K2-FP8: the transposed pipeline on an FP8 (e4m3) latent cache (etap_fp8.cuh for the operand
+// layouts). Same roles, schedule, softmax and split partials as the bf16 kernel (HG = 16), but
+//   * a tile is one 36 KB fp8 page in a ring of 5 page slots (5 pages in flight: the bytes per
+//     page halve, the latency to hide does not), loaded by 4 SW128 boxes + 1 SW64 box;
+//   * GEMM1 is 18 kind::f8f6f4 MMAs (K = 32) against three fp8 terms of Q (N = 48), GEMM2 is
+//     8 MMAs per tile of V^T against three fp8 terms of P (N = 48), both straight from the
+//     fp8 page: no dequantising pass; the KV scale folds into the softmax scale and 1/l.
+// =============================================================================================
+namespace kfp8 {
+constexpr int NPS = 5;                               // page slots in the ring
+constexpr int NTB8 = 8;                              // tile-barrier ring depth (>= NPS + 1)
+constexpr int OFF_RING = 0;
+constexpr int OFF_Q = NPS * fp8::TILE_BYTES;         // 180 KB
+constexpr int OFF_P = OFF_Q + fp8::Q_BYTES;          // 2 buffers
+constexpr int OFF_RED = OFF_P + 2 * fp8::P_BYTES;
+constexpr int HG8 = fp8::HGF, HH8 = HG8 / 2;
+constexpr int RED_FLOATS = 8 * HG8 + 4 * HG8 + 3 * HG8;
+constexpr int BAR_FULL = 0;                          // [NTB8] page of tile gt landed
+constexpr int BAR_G2D = NTB8;                        // [NTB8] GEMM2 of tile gt complete
+constexpr int BAR_QF = 2 * NTB8, BAR_QE = 2 * NTB8 + 1;
+constexpr int BAR_SF = 2 * NTB8 + 2, BAR_SR = 2 * NTB8 + 4, BAR_PF = 2 * NTB8 + 6;  // [2] each
+constexpr int NBAR8 = 2 * NTB8 + 8;
+constexpr int OFF_BAR = align_up(OFF_RED + RED_FLOATS * 4, 16);
+constexpr int OFF_TMEM = OFF_BAR + NBAR8 * 8;
+constexpr int OFF_SCHED = OFF_TMEM + 16;
+constexpr int SMEM_USED = OFF_SCHED + SCHED_SMEM_INTS * 4;
+constexpr int SMEM_ALLOC = SMEM_USED + 1024;
+constexpr uint32_t TCOL_S = 0;                       // S^T: 2 buffers x 48 columns
+constexpr uint32_t TCOL_O = 2 * fp8::NQ;             // O^T: 4 d-blocks x 48 columns
+constexpr uint32_t TMEM_COLS = 512;
+static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
+static_assert(OFF_Q % 1024 == 0 && OFF_P % 1024 == 0, "alignment");
+}  // namespace kfp8
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    etap_mla_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_kv128, const __grid_constant__ CUtensorMap tm_kv64,
+                               const __grid_constant__ CUtensorMap tm_q128, const __grid_constant__ CUtensorMap tm_q64,
+                               const DecodeParams prm, float kv_scale) {
+    using namespace kfp8;
+    constexpr int HG = HG8, HH = HH8, NQ = fp8::NQ;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = ptx::align_smem_1024(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tm_kv128);
+        ptx::prefetch_tmap(&tm_kv64);
+        ptx::prefetch_tmap(&tm_q128);
+        ptx::prefetch_tmap(&tm_q64);
+        for (int i = 0; i < NTB8; ++i) {
+            ptx::mbar_init(&bars[BAR_FULL + i], 1);
+            ptx::mbar_init(&bars[BAR_G2D + i], 1);
+        }
+        ptx::mbar_init(&bars[BAR_QF], 1);
+        ptx::mbar_init(&bars[BAR_QE], 1);
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&bars[BAR_SF + i], 1);
+            ptx::mbar_init(&bars[BAR_SR + i], 128);
+            ptx::mbar_init(&bars[BAR_PF + i], 128);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    ptx::grid_dep_wait();
+    ptx::grid_dep_launch();
+
+    int* s_pref = reinterpret_cast<int*>(smem + OFF_SCHED);
+    int* s_soff = s_pref + MAX_FUSED_VB + 1;
+    int* s_tiles = s_soff + MAX_FUSED_VB + 1;
+    int* s_len = s_tiles + MAX_FUSED_VB;
+    int* s_sched = s_len + MAX_FUSED_VB;
+    const bool fused = prm.inkernel_sched != 0;
+    const int32_t* sch;
+    const int32_t* soff;
+    int idx_off = 0;
+    if (fused) {
+        const LineShape ls = line_shape(prm.batch, prm.groups, gridDim.x, prm.lanes_on != 0);
+        if (ls.line_n <= 32) {
+            if (warp == 0) inkernel_schedule_warp(prm, ls, s_soff, s_len, s_sched);
+            __syncthreads();
+        } else {
+            inkernel_schedule(prm, ls, s_pref, s_soff, s_tiles, s_len, s_sched, s_sched + 8);
+        }
+        sch = s_sched;
+        soff = s_soff;
+        idx_off = sch[6];
+    } else {
+        sch = prm.sched + blockIdx.x * SCHED_INTS;
+        soff = prm.split_off + sch[5];
+    }
+    const int vb_begin = sch[0], vb_end = sch[2];
+    const int B = prm.batch;
+    const uint32_t ring_addr = ptx::smem_u32(smem + OFF_RING);
+    const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q);
+    const uint32_t p_addr = ptx::smem_u32(smem + OFF_P);
+    auto seqlen_of = [&](int i) { return fused ? s_len[i] : max(0, prm.seqlens[(sch[5] + i) % B]); };
+
+    if (warp == 0) {
+        // ===================================================== TMA producer
+        const bool kv_shared = line_shape(B, prm.groups, gridDim.x, prm.lanes_on != 0).lanes > 1;
+        const uint64_t pol_kv = kv_shared ? ptx::policy_evict_normal() : ptx::policy_evict_first();
+        const uint64_t pol_q = ptx::policy_evict_last();
+        uint32_t gt = 0, nsplit = 0;
+        for (int vb = vb_begin; vb <= vb_end; ++vb) {
+            SplitDesc sd;
+            if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
+            const int32_t* bt = prm.block_table + static_cast<size_t>(sd.b) * prm.max_pages;
+            int base = sd.t0;
+            int pg = (base + lane < sd.t1) ? __ldg(bt + base + lane) : 0;
+            bool q_pending = true;
+            for (int t = sd.t0; t < sd.t1; ++t) {
+                if (t - base >= 32) {
+                    base = t;
+                    pg = (base + lane < sd.t1) ? __ldg(bt + base + lane) : 0;
+                }
+                const int page = __shfl_sync(0xffffffffu, pg, t - base);
+                if (gt >= NPS) ptx::mbar_wait(&bars[BAR_G2D + (gt - NPS) % NTB8], ((gt - NPS) / NTB8) & 1);
+                if (lane == 0) {
+                    uint8_t* slot = smem + OFF_RING + (gt % NPS) * fp8::TILE_BYTES;
+                    uint64_t* full = &bars[BAR_FULL + gt % NTB8];
+                    ptx::mbar_arrive_expect_tx(full, fp8::TILE_BYTES);
+#pragma unroll 1
+                    for (int c = 0; c < fp8::VCH; ++c)
+                        ptx::tma_load_2d(slot + c * fp8::VCH_BYTES, &tm_kv128, full, c * 128, page * PAGE, pol_kv);
+                    ptx::tma_load_2d(slot + fp8::ROPE_OFF, &tm_kv64, full, 512, page * PAGE, pol_kv);
+                }
+                __syncwarp();
+                if (q_pending) {
+                    q_pending = false;
+                    if (nsplit > 0) ptx::mbar_wait(&bars[BAR_QE], (nsplit - 1) & 1);
+                    if (lane == 0) {
+                        ptx::mbar_arrive_expect_tx(&bars[BAR_QF], fp8::Q_BYTES);
+                        const int qrow = (sd.b * prm.groups + sd.g) * NQ;  // three-term Q of (b, g)
+#pragma unroll 1
+                        for (int c = 0; c < fp8::VCH; ++c)
+                            ptx::tma_load_2d(smem + OFF_Q + c * fp8::Q_VBLK, &tm_q128, &bars[BAR_QF], c * 128, qrow,
+                                             pol_q);
+                        ptx::tma_load_2d(smem + OFF_Q + fp8::VCH * fp8::Q_VBLK, &tm_q64, &bars[BAR_QF], 512, qrow, pol_q);
+                    }
+                    __syncwarp();
+                    ++nsplit;
+                }
+                ++gt;
+            }
+        }
+    } else if (warp == 1) {
+        // ===================================================== GEMM1 issuer
+        uint32_t gt = 0, nsplit = 0;
+        for (int vb = vb_begin; vb <= vb_end; ++vb) {
+            SplitDesc sd;
+            if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
+            ptx::mbar_wait(&bars[BAR_QF], nsplit & 1);
+            for (int t = sd.t0; t < sd.t1; ++t) {
+                const uint32_t buf = gt & 1;
+                if (gt >= 2) ptx::mbar_wait(&bars[BAR_SR + buf], ((gt >> 1) - 1) & 1);
+                ptx::mbar_wait(&bars[BAR_FULL + gt % NTB8], (gt / NTB8) & 1);
+                __syncwarp();
+                ptx::tc_fence_after();
+                fp8::issue_gemm1(tmem_base + TCOL_S + NQ * buf, ring_addr + (gt % NPS) * fp8::TILE_BYTES, q_addr);
+                ptx::umma_commit_elect(&bars[BAR_SF + buf]);
+                if (t == sd.t1 - 1) ptx::umma_commit_elect(&bars[BAR_QE]);
+                ++gt;
+            }
+            ++nsplit;
+        }
+    } else if (warp == 2) {
+        // ===================================================== GEMM2 issuer
+        uint32_t gt = 0;
+        for (int vb = vb_begin; vb <= vb_end; ++vb) {
+            SplitDesc sd;
+            if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
+            for (int t = sd.t0; t < sd.t1; ++t) {
+                const uint32_t buf = gt & 1;
+                ptx::mbar_wait(&bars[BAR_PF + buf], (gt >> 1) & 1);
+                __syncwarp();
+                ptx::tc_fence_after();
+                const uint32_t slot = ring_addr + (gt % NPS) * fp8::TILE_BYTES;
+#pragma unroll
+                for (int c = 0; c < fp8::VCH; ++c)
+                    fp8::issue_gemm2(tmem_base + TCOL_O + c * NQ, slot + c * fp8::VCH_BYTES, p_addr + buf * fp8::P_BYTES,
+                                     t == sd.t0);
+                ptx::umma_commit_elect(&bars[BAR_G2D + gt % NTB8]);
+                ++gt;
+            }
+        }
+    } else if (warp >= SOFTMAX_WARP0) {
+        // ===================================================== softmax + epilogue (128 threads)
+        const int wq = warp & 3;
+        const int half = lane >> 4;
+        const int row = s_row_of(wq, lane);
+        const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
+        float* red_max = reinterpret_cast<float*>(smem + OFF_RED);  // [2][4][HG]
+        float* red_sum = red_max + 8 * HG;
+        float* s_m = red_sum + 4 * HG;
+        float* s_alpha = s_m + HG;
+        int* s_row = reinterpret_cast<int*>(s_alpha + HG);
+        const float thresh = (prm.flags & FLAG_EAGER_RESCALE) ? 0.f : LAZY_RESCALE_LOG2;
+        const bool head_owner = wq == 0 && (lane & 15) == 0;
+        const bool lane_head = wq == 0 && lane < HG;
+        const bool mtp = prm.q_tokens > 1;
+        const int rhead = halfwarp_reduce_head<HH>(lane);
+        const bool rwriter = (lane & 1) == 0;
+        uint32_t gt = 0;
+        for (int vb = vb_begin; vb <= vb_end; ++vb) {
+            SplitDesc sd;
+            if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
+            float m_own[HH], l_part[HH];
+            int row_lim[HH];
+#pragma unroll
+            for (int j = 0; j < HH; ++j) {
+                m_own[j] = -INFINITY;
+                l_part[j] = 0.f;
+                const int tok = (sd.g * HG + half * HH + j) / prm.heads_per_token;
+                row_lim[j] = sd.seqlen - (prm.causal ? prm.q_tokens - 1 - tok : 0);
+                if (head_owner) s_m[half * HH + j] = -INFINITY;
+            }
+            for (int t = sd.t0; t < sd.t1; ++t) {
+                const uint32_t buf = gt & 1;
+                ptx::mbar_wait(&bars[BAR_SF + buf], (gt >> 1) & 1);
+                ptx::tc_fence_after();
+                uint32_t s0[HH], s1[HH], s2[HH];
+                ptx::tmem_ld16x2<HH>(t_lane + TCOL_S + NQ * buf, s0);
+                ptx::tmem_ld16x2<HH>(t_lane + TCOL_S + NQ * buf + 16, s1);
+                ptx::tmem_ld16x2<HH>(t_lane + TCOL_S + NQ * buf + 32, s2);
+                ptx::tmem_wait_ld();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&bars[BAR_SR + buf]);
+
+                const int grow = t * TILE + row;
+                float x[HH];
+                bool exceed = false;
+#pragma unroll
+                for (int j = 0; j < HH; ++j) {
+                    // S = S_q0 + S_q1 / 16 + S_q2 / 256 (the three fp8 terms of Q)
+                    const float sv = __uint_as_float(s0[j]) +
+                                     (__uint_as_float(s1[j]) * 0.0625f + __uint_as_float(s2[j]) * 0.00390625f);
+                    x[j] = grow < row_lim[j] ? sv * prm.scale_log2 : -INFINITY;
+                    exceed |= x[j] > m_own[j] + thresh;
+                }
+                const bool first = (t == sd.t0);
+                const bool any = ptx::bar_red_or(1, 128, exceed);
+                bool need_rescale = false;
+                float alpha_own[HH];
+#pragma unroll
+                for (int j = 0; j < HH; ++j) alpha_own[j] = first ? 0.f : 1.f;
+                if (any) {
+                    const float wm = halfwarp_reduce<true, HH>(x, lane);
+                    float* rm = red_max + (gt & 1) * 4 * HG;
+                    if (rwriter) rm[wq * HG + half * HH + rhead] = wm;
+                    ptx::named_bar_sync(2, 128);
+                    bool upd = false;
+#pragma unroll
+                    for (int j = 0; j < HH; ++j) {
+                        const int h = half * HH + j;
+                        const float mt = fmaxf(fmaxf(rm[h], rm[HG + h]), fmaxf(rm[2 * HG + h], rm[3 * HG + h]));
+                        if (first) {
+                            m_own[j] = mt;
+                        } else {
+                            const float mn = fmaxf(m_own[j], mt);
+                            if (mn > m_own[j] + thresh) {
+                                alpha_own[j] = exp2f(m_own[j] - mn);
+                                m_own[j] = mn;
+                                upd = true;
+                            }
+                        }
+                    }
+                    need_rescale = ptx::bar_red_or(2, 128, upd);
+                    if (head_owner) {
+#pragma unroll
+                        for (int j = 0; j < HH; ++j) {
+                            s_m[half * HH + j] = m_own[j];
+                            s_alpha[half * HH + j] = alpha_own[j];
+                        }
+                    }
+                }
+                float pv[HH];
+#pragma unroll
+                for (int j = 0; j < HH; ++j) {
+                    const float mu = (mtp && m_own[j] == -INFINITY) ? 0.f : m_own[j];
+                    pv[j] = exp2f(x[j] - mu);
+                    l_part[j] = first ? pv[j] : fmaf(l_part[j], alpha_own[j], pv[j]);
+                }
+                // the P buffer is reused every other tile: GEMM2(gt-2) must have read it
+                if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2D + (gt - 2) % NTB8], ((gt - 2) / NTB8) & 1);
+                if (need_rescale) {
+                    ptx::named_bar_sync(2, 128);
+                    ptx::mbar_wait(&bars[BAR_G2D + (gt - 1) % NTB8], ((gt - 1) / NTB8) & 1);
+                    ptx::tc_fence_after();
+#pragma unroll 1
+                    for (int c = 0; c < fp8::VCH; ++c) {
+#pragma unroll
+                        for (int term = 0; term < fp8::NT; ++term) {
+                            uint32_t o[16];
+                            const uint32_t ta = t_lane + TCOL_O + c * NQ + term * 16;
+                            ptx::tmem_ld16(ta, o);
+                            ptx::tmem_wait_ld();
+#pragma unroll
+                            for (int h = 0; h < 16; ++h) o[h] = __float_as_uint(__uint_as_float(o[h]) * s_alpha[h]);
+                            ptx::tmem_st16(ta, o);
+                        }
+                    }
+                    ptx::tmem_wait_st();
+                }
+                // P -> three e4m3 terms, this row's 8 heads per term: one 8-byte store each
+                {
+                    uint16_t tt[4][fp8::NT];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) fp8::split3(pv[2 * i], pv[2 * i + 1], tt[i]);
+                    uint8_t* pb = smem + OFF_P + buf * fp8::P_BYTES;
+#pragma unroll
+                    for (int term = 0; term < fp8::NT; ++term) {
+                        const uint32_t lo = static_cast<uint32_t>(tt[0][term]) | (static_cast<uint32_t>(tt[1][term]) << 16);
+                        const uint32_t hi = static_cast<uint32_t>(tt[2][term]) | (static_cast<uint32_t>(tt[3][term]) << 16);
+                        *reinterpret_cast<uint2*>(pb + fp8::p_off(row, term * 16 + half * HH)) = make_uint2(lo, hi);
+                    }
+                }
+                // rows past seqlen may hold non-finite bytes: zero them in the V chunks
+                if (grow >= sd.seqlen) {
+                    uint8_t* slot = smem + OFF_RING + (gt % NPS) * fp8::TILE_BYTES;
+#pragma unroll 1
+                    for (int c = half * 2; c < half * 2 + 2; ++c) {
+                        uint4* dst = reinterpret_cast<uint4*>(slot + c * fp8::VCH_BYTES + row * 128);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) dst[j] = make_uint4(0, 0, 0, 0);
+                    }
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&bars[BAR_PF + buf]);
+                ++gt;
+            }
+
+            // ---- epilogue: O = kv_scale * (O_0 + O_1/16 + O_2/256) / l, L = m + log l
+            const uint32_t last = gt - 1;
+            ptx::mbar_wait(&bars[BAR_G2D + last % NTB8], (last / NTB8) & 1);
+            ptx::tc_fence_after();
+            const float wsum = halfwarp_reduce<false, HH>(l_part, lane);
+            if (rwriter) red_sum[wq * HG + half * HH + rhead] = wsum;
+            const int ns = soff[vb + 1] - soff[vb];
+            const bool direct = ns == 1;
+            if (direct && lane_head) s_row[lane] = static_cast<int>(prm.om.row(sd.b, sd.g * HG + lane));
+            ptx::named_bar_sync(2, 128);
+            float L_own = 0.f;
+            float* s_inv = red_max;
+            if (lane_head) {
+                const float l = red_sum[lane] + red_sum[HG + lane] + red_sum[2 * HG + lane] + red_sum[3 * HG + lane];
+                s_inv[lane] = l > 0.f ? kv_scale / l : 0.f;
+                L_own = (s_m[lane] + log2f(l)) * 0.69314718055994530942f;
+            }
+            ptx::named_bar_sync(2, 128);
+            float inv_l[HG];
+#pragma unroll
+            for (int h = 0; h < HG; h += 4) {
+                const float4 v4 = *reinterpret_cast<const float4*>(s_inv + h);
+                inv_l[h] = v4.x; inv_l[h + 1] = v4.y; inv_l[h + 2] = v4.z; inv_l[h + 3] = v4.w;
+            }
+            const int idx = (vb == sch[0]) ? sch[4] : soff[vb] + idx_off;
+            float* part_o = prm.ws_o + static_cast<size_t>(idx) * HG * D_V;
+            const int drow = wq * 32 + lane;
+#pragma unroll 1
+            for (int c = 0; c < fp8::VCH; ++c) {
+                uint32_t o[fp8::NT][16];
+#pragma unroll
+                for (int term = 0; term < fp8::NT; ++term) ptx::tmem_ld16(t_lane + TCOL_O + c * NQ + term * 16, o[term]);
+                ptx::tmem_wait_ld();
+                const int d = c * 128 + drow;
+                float v[HG];
+#pragma unroll
+                for (int h = 0; h < HG; ++h)
+                    v[h] = (__uint_as_float(o[0][h]) + (__uint_as_float(o[1][h]) * 0.0625f +
+                                                       __uint_as_float(o[2][h]) * 0.00390625f)) * inv_l[h];
+                if (direct) {
+#pragma unroll 1
+                    for (int r = 0; r < prm.om.n_out; ++r) {
+                        float* dst = prm.om.out[r] + d;
+#pragma unroll
+                        for (int h = 0; h < HG; ++h) dst[static_cast<size_t>(s_row[h]) * D_V] = v[h];
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < HG; ++h) part_o[h * D_V + d] = v[h];
+                }
+            }
+            if (lane_head) {
+                if (direct) {
+                    for (int r = 0; r < prm.om.n_out; ++r) prm.om.lse[r][s_row[lane]] = L_own;
+                } else {
+                    prm.ws_lse[static_cast<size_t>(idx) * HG + lane] = L_own;
+                }
+            }
+            ptx::tc_fence_before();
+            ptx::named_bar_sync(2, 128);
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    }
+}
+
+// Three fp8 terms of every head's query row: Q3[(b * groups + g) * 48 + term * 16 + h][c]
+// from Q[b][g * 16 + h][c] (bf16); one thread per (row pair element).
+__global__ void __launch_bounds__(256) etap_fp8_quant_q_kernel(const __nv_bfloat16* __restrict__ q, uint8_t* __restrict__ q3,
+                                                               int rows_total, int groups) {
+    ptx::grid_dep_wait();
+    ptx::grid_dep_launch();
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (row, column pair)
+    if (i >= static_cast<int64_t>(rows_total) * (D_QK / 2)) return;
+    const int r = static_cast<int>(i / (D_QK / 2)), c = static_cast<int>(i % (D_QK / 2)) * 2;
+    const int b = r / (groups * 16), rem = r % (groups * 16), g = rem / 16, h = rem % 16;
+    const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(q + static_cast<size_t>(r) * D_QK + c);
+    uint16_t t[fp8::NT];
+    fp8::split3(__bfloat162float(v.x), __bfloat162float(v.y), t);
+    const size_t base = static_cast<size_t>(b * groups + g) * fp8::NQ;
+#pragma unroll
+    for (int term = 0; term < fp8::NT; ++term)
+        *reinterpret_cast<uint16_t*>(q3 + (base + term * 16 + h) * D_QK + c) = t[term];
+}
+
+// =============================================================================================
 // KV append (caller side of the path: the serving loop writes each step's new latent rows
 // into the paged cache before the decode reads them). One CTA of 72 threads per new row,
 // one 16 B vector each (576 bf16 = 1152 B). HBM-bound scatter of B * q_tokens rows.
@@ -1272,6 +1702,44 @@ int cached_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_r
     return ETAP_OK;
 }
 
+// 2-D uint8 tensor map over a row-major [rows][576] byte matrix (FP8 pool / three-term Q),
+// box {box_cols, box_rows}, SW128 (box_cols 128) or SW64 (box_cols 64); cached
+int cached_map_u8(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_cols, uint32_t box_rows) {
+    struct Entry {
+        const void* base = nullptr;
+        uint64_t rows = 0;
+        uint32_t bc = 0, br = 0;
+        CUtensorMap map;
+    };
+    thread_local Entry cache[8];
+    thread_local unsigned next = 0;
+    for (auto& e : cache)
+        if (e.base == base && e.rows == rows && e.bc == box_cols && e.br == box_rows) {
+            *map = e.map;
+            return ETAP_OK;
+        }
+    auto enc = get_encode_fn();
+    if (!enc) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver)");
+    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
+        return fail(ETAP_ERR_SHAPE, "tensor base address must be 16-byte aligned");
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(D_QK), rows};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(D_QK)};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     box_cols == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled (u8) failed: " + std::to_string(r));
+    Entry& e = cache[next++ % 8];
+    e.base = base;
+    e.rows = rows;
+    e.bc = box_cols;
+    e.br = box_rows;
+    e.map = *map;
+    return ETAP_OK;
+}
+
 // Heads per CTA work unit: 32 when the head count allows it (N = 32 / 64 UMMAs halve the
 // tensor-pipe issue count per KV byte, which is what bounds 64+ heads on one GPU), else 16.
 // ETAP_HEAD_GROUP=16 in the environment forces 16 (A/B runs); read once per process.
@@ -1297,6 +1765,18 @@ bool lanes_enabled() {
 
 size_t max_partials(int batch, int heads, int num_sm_parts) {
     return static_cast<size_t>(num_sm_parts) + static_cast<size_t>(batch) * (heads / head_group_of(heads));
+}
+
+// workspace layout: partial O [np][hg][512] fp32, partial LSE [np][hg] fp32, then (1 KB
+// aligned) the three fp8 terms of Q for the FP8 path, [batch * heads / 16][48][576] bytes.
+// A work unit of 16 heads needs no more partial space than one of 32 (np * hg grows with hg).
+size_t q3_offset(int batch, int heads, int num_sm_parts) {
+    const size_t np = max_partials(batch, heads, num_sm_parts);
+    const size_t hg = head_group_of(heads);
+    return (np * hg * D_V * sizeof(float) + np * hg * sizeof(float) + 1023) / 1024 * 1024;
+}
+size_t q3_bytes(int batch, int heads) {
+    return static_cast<size_t>(batch) * (heads / 16) * fp8::NQ * D_QK;
 }
 
 }  // namespace
@@ -1369,16 +1849,15 @@ int etap_mla_sched_ints(int batch, int heads, int num_sm_parts, size_t* sched_in
     if (batch < 1 || !heads_ok(heads) || num_sm_parts < 1)
         return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
     if (sched_ints) *sched_ints = static_cast<size_t>(num_sm_parts) * SCHED_INTS;
-    if (split_off_ints) *split_off_ints = static_cast<size_t>(batch) * (heads / head_group_of(heads)) + 1;
+    // sized for work units of 16 heads (the FP8 path), enough for 32 as well
+    if (split_off_ints) *split_off_ints = static_cast<size_t>(batch) * (heads / 16) + 1;
     return ETAP_OK;
 }
 
 int etap_mla_workspace_bytes(int batch, int heads, int num_sm_parts, size_t* bytes) {
     if (batch < 1 || !heads_ok(heads) || num_sm_parts < 1 || !bytes)
         return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
-    const size_t np = max_partials(batch, heads, num_sm_parts);
-    const size_t hg = head_group_of(heads);
-    *bytes = np * hg * D_V * sizeof(float) + np * hg * sizeof(float);
+    *bytes = q3_offset(batch, heads, num_sm_parts) + q3_bytes(batch, heads);
     return ETAP_OK;
 }
 
@@ -1449,12 +1928,19 @@ int etap_mla_metadata_host(const int32_t* seqlens, int batch, int heads, int num
     return ETAP_OK;
 }
 
+int metadata_launch(const int32_t* seqlens, int batch, int groups, int num_sm_parts, int32_t* sched,
+                    int32_t* split_off, void* stream);
+
 int etap_mla_metadata(const int32_t* seqlens, int batch, int heads, int num_sm_parts,
                       int32_t* sched, int32_t* split_off, void* stream) {
     if (!seqlens || !sched || !split_off) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
     if (batch < 1 || !heads_ok(heads))
         return fail(ETAP_ERR_SHAPE, "batch >= 1 and heads a multiple of 16 required");
-    const int groups = heads / head_group_of(heads);
+    return metadata_launch(seqlens, batch, heads / head_group_of(heads), num_sm_parts, sched, split_off, stream);
+}
+
+int metadata_launch(const int32_t* seqlens, int batch, int groups, int num_sm_parts, int32_t* sched,
+                    int32_t* split_off, void* stream) {
     if (batch * groups > META_MAX_VB)
         return fail(ETAP_ERR_SHAPE, "batch * head groups exceeds " + std::to_string(META_MAX_VB));
     if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
@@ -1492,13 +1978,17 @@ OutMap local_outmap(int heads, float* out, float* lse) {
 
 // seqlens != null: the split offsets follow in closed form from seqlens (the decode ran the
 // in-kernel schedule on a line of <= 32 entries); otherwise K3 reads split_off
+// hg_unit: heads per work unit of the decode that wrote the partials (the FP8 kernel uses 16
+// whatever the head count); the partial / LSE areas keep the allocation layout of
+// etap_mla_workspace_bytes either way
 int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_parts, void* workspace,
-                 const OutMap& om, void* stream, const int32_t* seqlens = nullptr) {
-    const int hg = head_group_of(heads);
+                 const OutMap& om, void* stream, const int32_t* seqlens = nullptr, int hg_unit = 0) {
+    const int hg_alloc = head_group_of(heads);
+    const int hg = hg_unit > 0 ? hg_unit : hg_alloc;
     const int groups = heads / hg;
     const size_t np = max_partials(batch, heads, num_sm_parts);
     float* ws_o = static_cast<float*>(workspace);
-    float* ws_lse = ws_o + np * hg * D_V;
+    float* ws_lse = ws_o + np * hg_alloc * D_V;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -1620,6 +2110,121 @@ int peer_signal_wait(const etap_mla_peer_gather* pg, uint32_t epoch, void* strea
 }
 
 extern "C" {
+
+// FP8 (e4m3) latent cache: quantise Q into three fp8 terms (workspace), K2-FP8, K3 (16 heads
+// per work unit). kv_scale: the per-tensor dequantisation scale of the cache.
+int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t num_pages, const int32_t* block_table,
+                    int max_pages_per_seq, const int32_t* seqlens, int batch, int q_tokens, int heads_per_token,
+                    float scale, int causal, const int32_t* sched, const int32_t* split_off, int num_sm_parts,
+                    void* workspace, const OutMap& om, unsigned flags, void* stream) {
+    if (!q || !kv_pool8 || !block_table || !seqlens || !sched || !split_off || !workspace)
+        return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    if (q_tokens < 1 || q_tokens > ETAP_MLA_MAX_Q_TOKENS)
+        return fail(ETAP_ERR_SHAPE, "q_tokens must be in [1, " + std::to_string(ETAP_MLA_MAX_Q_TOKENS) + "]");
+    if (heads_per_token < 1) return fail(ETAP_ERR_SHAPE, "heads must be >= 1");
+    const int heads = q_tokens * heads_per_token;
+    if (batch < 1 || !heads_ok(heads))
+        return fail(ETAP_ERR_SHAPE, "batch >= 1 and q_tokens * heads a multiple of 16 required");
+    if (num_pages < 1 || max_pages_per_seq < 1 || num_pages * PAGE > (int64_t)0x7fffffff)
+        return fail(ETAP_ERR_SHAPE, "num_pages and max_pages_per_seq must be >= 1, pool below 2^31 rows");
+    if (!(scale >= 0.f) || !std::isfinite(scale) || !(kv_scale > 0.f) || !std::isfinite(kv_scale))
+        return fail(ETAP_ERR_SHAPE, "scale must be finite and >= 0, kv_scale finite and > 0");
+    if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
+        return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
+    if (flags & (ETAP_FLAG_EXTERNAL_SCHEDULE | ETAP_FLAG_NEGATE_RESCALE))
+        return fail(ETAP_ERR_SHAPE, "FP8 path: external schedules and the rescale fault are not supported");
+    if (g_state_buf) return fail(ETAP_ERR_SHAPE, "FP8 path: the softmax-state dump is not supported");
+    if (int rc = check_device()) return rc;
+
+    constexpr int hg = fp8::HGF;
+    const int groups = heads / hg;
+    const size_t np = max_partials(batch, heads, num_sm_parts);
+    uint8_t* q3 = static_cast<uint8_t*>(workspace) + q3_offset(batch, heads, num_sm_parts);
+    CUtensorMap tm_kv128, tm_kv64, tm_q128, tm_q64;
+    const uint64_t pool_rows = static_cast<uint64_t>(num_pages) * PAGE;
+    const uint64_t q3_rows = static_cast<uint64_t>(batch) * groups * fp8::NQ;
+    if (int rc = cached_map_u8(&tm_kv128, kv_pool8, pool_rows, 128, PAGE)) return rc;
+    if (int rc = cached_map_u8(&tm_kv64, kv_pool8, pool_rows, 64, PAGE)) return rc;
+    if (int rc = cached_map_u8(&tm_q128, q3, q3_rows, 128, fp8::NQ)) return rc;
+    if (int rc = cached_map_u8(&tm_q64, q3, q3_rows, 64, fp8::NQ)) return rc;
+
+    DecodeParams prm;
+    prm.block_table = block_table;
+    prm.seqlens = seqlens;
+    prm.sched = sched;
+    prm.split_off = split_off;
+    prm.om = om;
+    prm.ws_o = static_cast<float*>(workspace);
+    prm.ws_lse = prm.ws_o + np * head_group_of(heads) * D_V;  // allocation layout
+    prm.kv_pool = kv_pool8;
+    prm.q = q;
+    prm.num_pages = num_pages;
+    prm.max_pages = max_pages_per_seq;
+    prm.batch = batch;
+    prm.heads = heads;
+    prm.groups = groups;
+    prm.q_tokens = q_tokens;
+    prm.heads_per_token = heads_per_token;
+    prm.causal = causal ? 1 : 0;
+    prm.sched_out = const_cast<int32_t*>(sched);
+    prm.split_off_out = const_cast<int32_t*>(split_off);
+    prm.lanes_on = lanes_enabled() ? 1 : 0;
+    const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
+    prm.inkernel_sched = ls.line_n <= MAX_FUSED_VB ? 1 : 0;
+    prm.scale_log2 = scale * kv_scale * 1.4426950408889634f;
+    prm.flags = flags;
+    prm.trace = nullptr;
+    prm.state = nullptr;
+    prm.state_tiles = 0;
+
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    // three fp8 terms of Q into the workspace
+    {
+        cudaLaunchConfig_t cfg = {};
+        const int64_t n = static_cast<int64_t>(batch) * heads * (D_QK / 2);
+        cfg.gridDim = dim3(static_cast<unsigned>((n + 255) / 256));
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_fp8_quant_q_kernel, static_cast<const __nv_bfloat16*>(q), q3,
+                                     batch * heads, groups));
+    }
+    if (!prm.inkernel_sched)
+        if (int rc = metadata_launch(seqlens, batch, groups, num_sm_parts, const_cast<int32_t*>(sched),
+                                     const_cast<int32_t*>(split_off), stream))
+            return rc;
+    {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(num_sm_parts);
+        cfg.blockDim = dim3(NUM_THREADS);
+        cfg.dynamicSmemBytes = kfp8::SMEM_ALLOC;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        static int attr_rc = ensure_smem_attr(etap_mla_decode_fp8_kernel, kfp8::SMEM_ALLOC);
+        if (attr_rc) return attr_rc;
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_fp8_kernel, tm_kv128, tm_kv64, tm_q128, tm_q64, prm, kv_scale));
+    }
+    if (flags & ETAP_FLAG_SKIP_COMBINE) return ETAP_OK;
+    const bool closed_form = prm.inkernel_sched && ls.line_n <= 32;
+    return combine_impl(split_off, batch, heads, num_sm_parts, workspace, om, stream, closed_form ? seqlens : nullptr,
+                        hg);
+}
+
+int etap_mla_decode_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t num_pages,
+                        const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens, int batch,
+                        int q_tokens, int heads_per_token, float scale, int causal, const int32_t* sched,
+                        const int32_t* split_off, int num_sm_parts, void* workspace, float* out, float* lse,
+                        unsigned flags, void* stream) {
+    if (!out || !lse) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    const OutMap om = local_outmap(q_tokens * heads_per_token, out, lse);
+    return decode_impl_fp8(q, kv_pool8, kv_scale, num_pages, block_table, max_pages_per_seq, seqlens, batch, q_tokens,
+                           heads_per_token, scale, causal, sched, split_off, num_sm_parts, workspace, om, flags, stream);
+}
 
 int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
                     const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,

@@ -136,6 +136,37 @@ class MlaDecodePlan:
             _stream_ptr(stream)), "etap_mla_decode")
         return out, lse
 
+    def decode_fp8(self, q: torch.Tensor, kv_pool8: torch.Tensor, block_table: torch.Tensor,
+                   seqlens: torch.Tensor, scale: float, kv_scale: float, out: torch.Tensor | None = None,
+                   lse: torch.Tensor | None = None, flags: int = 0, causal: bool = True,
+                   stream: torch.cuda.Stream | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+        """K2-FP8 + K3 on an FP8 (e4m3) latent cache: kv_pool8 [pages,64,576] float8_e4m3fn (or
+        its uint8 bytes), dequantised value = kv_scale * e4m3. Same q / block_table / seqlens /
+        outputs as decode()."""
+        B, H, T = self.batch, self.heads, self.q_tokens
+        if q.dim() == 3 and T == 1:
+            q = q.unsqueeze(1)
+        _check_tensor(q, torch.bfloat16, (B, T, H, D_QK), "q")
+        if kv_pool8.dim() != 3 or kv_pool8.shape[1:] != (PAGE_ROWS, D_QK) or \
+                kv_pool8.dtype not in (torch.float8_e4m3fn, torch.uint8) or not kv_pool8.is_contiguous():
+            raise _lib.EtapShapeError(f"kv_pool8 must be contiguous [pages,64,576] float8_e4m3fn, got "
+                                      f"{tuple(kv_pool8.shape)} {kv_pool8.dtype}")
+        if block_table.dim() != 2 or block_table.shape[0] != B or block_table.dtype != torch.int32 \
+                or not block_table.is_contiguous():
+            raise _lib.EtapShapeError("block_table must be contiguous [B, max_pages] int32")
+        _check_tensor(seqlens, torch.int32, (B,), "seqlens")
+        if out is None:
+            out = torch.empty((B, T, H, D_V), dtype=torch.float32, device=q.device)
+        if lse is None:
+            lse = torch.empty((B, T, H), dtype=torch.float32, device=q.device)
+        check(_lib.lib().etap_mla_decode_fp8(
+            q.data_ptr(), kv_pool8.data_ptr(), float(kv_scale), kv_pool8.shape[0], block_table.data_ptr(),
+            block_table.shape[1], seqlens.data_ptr(), B, T, H, float(scale), int(causal),
+            self.sched.data_ptr(), self.split_off.data_ptr(), self.num_sm_parts,
+            self.workspace.data_ptr(), out.data_ptr(), lse.data_ptr(), int(flags),
+            _stream_ptr(stream)), "etap_mla_decode_fp8")
+        return out, lse
+
     def capture(self, q: torch.Tensor, kv_pool: torch.Tensor, block_table: torch.Tensor,
                 seqlens: torch.Tensor, scale: float, out: torch.Tensor, lse: torch.Tensor,
                 flags: int = 0, with_metadata: bool = True) -> torch.cuda.CUDAGraph:

