@@ -92,7 +92,7 @@ class MlaDecodePlan:
         return cls(
             batch=batch, heads=heads, device=device, num_sm_parts=nparts, q_tokens=q_tokens,
             sched=torch.empty(n_sched.value, dtype=torch.int32, device=device),
-            split_off=torch.empty(n_so.value, dtype=torch.int32, device=device),
+            split_off=torch.zeros(n_so.value, dtype=torch.int32, device=device),
             # zero-filled once: the tail holds the combine's ready flags / counters, which every
             # decode call leaves at zero again
             workspace=torch.zeros(ws.value, dtype=torch.uint8, device=device),

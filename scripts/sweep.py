@@ -111,7 +111,59 @@ def measure_layer(B=16, H=16, ctx=65536, iters=50):
     print(json.dumps(line), flush=True)
 
 
+def measure_fp8(seqlens, heads, label, iters=50, q_tokens=1):
+    """FP8 (e4m3) latent cache: device time per step (stream launches), bytes of the fp8 pool."""
+    kv_bytes = sum(seqlens) * 576
+    ncopies = max(1, min(8, (2 * L2_BYTES) // max(1, kv_bytes) + 1))
+    B = len(seqlens)
+    sets = []
+    for i in range(ncopies):
+        inp = inputs.make_mla_inputs(seqlens, heads=heads, seed=42 + i, pad_value=0.0, q_tokens=q_tokens)
+        kv8 = (inp.kv_pool.float() / 0.125).to(torch.float8_e4m3fn)
+        inp.kv_pool = None
+        sets.append((inp, kv8))
+        torch.cuda.empty_cache()
+    plan = mla.MlaDecodePlan.create(B, heads, "cuda", q_tokens=q_tokens)
+    out = torch.empty((B, q_tokens, heads, 512), dtype=torch.float32, device="cuda")
+    lse = torch.empty((B, q_tokens, heads), dtype=torch.float32, device="cuda")
+
+    def step(j):
+        inp, kv8 = sets[j % ncopies]
+        plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 0.125, out=out, lse=lse)
+
+    for j in range(5):
+        step(j)
+    torch.cuda.synchronize()
+    res = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for j in range(iters):
+            step(j)
+        e1.record()
+        torch.cuda.synchronize()
+        res.append(e0.elapsed_time(e1) * 1000 / iters)
+    us = sorted(res)[1]
+    H = heads * q_tokens
+    nbytes = (kv_bytes + B * H * 576 * 2 + B * H * 512 * 4 + B * H * 4
+              + sum((s + 63) // 64 for s in seqlens) * 4 + 4 * B)
+    line = {"config": label, "kv": "fp8 e4m3", "batch": B, "heads": heads, "ctx_total": sum(seqlens),
+            "us_per_step_stream": us, "hbm_gbs": nbytes / us / 1e3,
+            "tflops": inputs.flops(seqlens, H) / us / 1e6, "algorithmic_bytes": nbytes,
+            "l2_rotation_copies": ncopies}
+    print(json.dumps(line), flush=True)
+    del sets
+    torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
+    if "--fp8" in sys.argv:
+        measure_fp8([1024], 16, "fp8 config1 B=1 H=16 ctx=1K")
+        for ctx in (1024, 4096, 16384, 65536):
+            measure_fp8([ctx] * 16, 16, f"fp8 config3 B=16 H=16 ctx={ctx}")
+        measure_fp8(inputs.varlen_seqlens(32), 16, "fp8 config4 B=32 varlen 4K-128K")
+        measure_fp8([65536] * 16, 16, "fp8 B=16 ctx=64K H=16 q_tokens=2", iters=20, q_tokens=2)
+        sys.exit(0)
     if "--serving" in sys.argv:  # serving-style batches: many sequences, short-to-medium contexts
         import random
         for B, lo, hi in ((64, 2048, 8192), (128, 1024, 4096), (256, 512, 4096), (128, 4096, 32768)):
