@@ -94,7 +94,7 @@ __device__ void block_scan_array(const int* a, int* out, int n, int* warp_tot) {
 __global__ void __launch_bounds__(META_THREADS, 1)
     etap_mla_metadata_kernel(const int32_t* __restrict__ seqlens, int batch, int groups,
                              int num_parts, int lanes_on, int32_t* __restrict__ sched,
-                             int32_t* __restrict__ split_off) {
+                             int32_t* __restrict__ split_off, int fixed_cost) {
     ptx::grid_dep_launch();
     __shared__ int s_tiles[META_MAX_VB];
     __shared__ int s_pref[META_MAX_VB + 1];
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(META_THREADS, 1)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const int len = max(0, seqlens[i % batch]);
         s_tiles[i] = (len + TILE - 1) / TILE;
-        s_ns[i] = s_tiles[i] > 0 ? s_tiles[i] + META_FIXED_COST : 0;  // cost, reused below
+        s_ns[i] = s_tiles[i] > 0 ? s_tiles[i] + fixed_cost : 0;  // cost, reused below
         s_first[i] = 0x7fffffff;
     }
     __syncthreads();
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(META_THREADS, 1)
         // skip zero-cost sequences that share the same prefix value
         while (lo + 1 < n && s_pref[lo + 1] <= x) ++lo;
         vb = lo;
-        t = min(max(0, x - s_pref[lo] - META_FIXED_COST), s_tiles[lo]);
+        t = min(max(0, x - s_pref[lo] - fixed_cost), s_tiles[lo]);
     };
 
     // line CTA kl's range [kl*T, (kl+1)*T) in (line index, tile) coordinates
@@ -226,7 +226,7 @@ __device__ void schedule_own_range(const DecodeParams& prm, const LineShape& ls,
         }
         while (lo + 1 < n && s_pref[lo + 1] <= x) ++lo;
         vb = lo;
-        t = min(max(0, x - s_pref[lo] - META_FIXED_COST), s_tiles[lo]);
+        t = min(max(0, x - s_pref[lo] - prm.fixed_cost), s_tiles[lo]);
     };
     const int x0 = k * T, x1 = min(total, (k + 1) * T);
     int b0 = 0, tb = 0, b1 = -1, te = 0, first = 0;
@@ -234,7 +234,7 @@ __device__ void schedule_own_range(const DecodeParams& prm, const LineShape& ls,
         map(x0, b0, tb);
         if (x1 >= total) { b1 = n - 1; te = s_tiles[n - 1]; }
         else map(x1, b1, te);
-        if (b1 >= b0) first = lane * s_soff[n] + s_soff[b0] + (k - (s_pref[b0] + META_FIXED_COST) / T);
+        if (b1 >= b0) first = lane * s_soff[n] + s_soff[b0] + (k - (s_pref[b0] + prm.fixed_cost) / T);
     }
     s_sched[0] = b0; s_sched[1] = tb; s_sched[2] = b1; s_sched[3] = te; s_sched[4] = first;
     s_sched[5] = min(lane, ls.lanes - 1) * n;         // virtual-sequence offset of the lane
@@ -265,7 +265,7 @@ __device__ void inkernel_schedule_warp(const DecodeParams& prm, const LineShape&
     const bool live = lane < n;
     const int len = live ? max(0, prm.seqlens[lane % prm.batch]) : 0;
     const int tiles = (len + TILE - 1) / TILE;
-    const int cost = tiles > 0 ? tiles + META_FIXED_COST : 0;
+    const int cost = tiles > 0 ? tiles + prm.fixed_cost : 0;
     int incl = cost;  // inclusive prefix = P[lane + 1]
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -276,7 +276,7 @@ __device__ void inkernel_schedule_warp(const DecodeParams& prm, const LineShape&
     if (lane == 0) { ETAP_TRACE_G(prm, 8); ETAP_TRACE_CLK(prm, 13); }
     const int pref = incl - cost;
     const int T = max(1, (total + ls.p_line - 1) / ls.p_line);
-    const int ns = (live && tiles > 0) ? ((incl + T - 1) / T - 1) - (pref + META_FIXED_COST) / T + 1 : 0;
+    const int ns = (live && tiles > 0) ? ((incl + T - 1) / T - 1) - (pref + prm.fixed_cost) / T + 1 : 0;
     int so = ns;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -299,10 +299,10 @@ __device__ void inkernel_schedule_warp(const DecodeParams& prm, const LineShape&
         int sb0 = 0, stb = 0, sb1 = -1, ste = 0, first = 0;
         if (cl < ls.lanes && x0 < total) {
             sb0 = b0;
-            stb = min(max(0, x0 - p0 - META_FIXED_COST), t0n);
+            stb = min(max(0, x0 - p0 - prm.fixed_cost), t0n);
             if (x1 >= total) { sb1 = n - 1; ste = tiles_last; }
-            else { sb1 = b1m; ste = min(max(0, x1 - p1 - META_FIXED_COST), t1n); }
-            if (sb1 >= sb0) first = cl * ns_line + so0 + (k - (p0 + META_FIXED_COST) / T);
+            else { sb1 = b1m; ste = min(max(0, x1 - p1 - prm.fixed_cost), t1n); }
+            if (sb1 >= sb0) first = cl * ns_line + so0 + (k - (p0 + prm.fixed_cost) / T);
         }
         const int lc = min(cl, ls.lanes - 1);
         s_sched[0] = sb0; s_sched[1] = stb; s_sched[2] = sb1; s_sched[3] = ste; s_sched[4] = first;
@@ -329,7 +329,7 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
     if (tid < n) {
         const int len = max(0, prm.seqlens[tid % prm.batch]);
         tiles = (len + TILE - 1) / TILE;
-        cost = tiles > 0 ? tiles + META_FIXED_COST : 0;
+        cost = tiles > 0 ? tiles + prm.fixed_cost : 0;
         s_tiles[tid] = tiles;
         s_len[tid] = len;
     }
@@ -341,7 +341,7 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
     const int T = max(1, (total + ls.p_line - 1) / ls.p_line);
     int ns = 0;
     if (tid < n && tiles > 0) {
-        const int kf = (pref + META_FIXED_COST) / T;
+        const int kf = (pref + prm.fixed_cost) / T;
         const int kl = (s_pref[tid + 1] + T - 1) / T - 1;
         ns = kl - kf + 1;
     }
@@ -369,11 +369,12 @@ __device__ __forceinline__ bool split_at(const int32_t* sch, int seqlen, int bat
     return d.t0 < d.t1;
 }
 
-template <int HG_>
+template <int HG_, bool DBG>
 __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
     etap_mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv,
                            const __grid_constant__ CUtensorMap tm_q, const DecodeParams prm) {
     using C = Cfg<HG_>;
+    constexpr bool kDebug = DBG;  // debug stamps / state dump (see etap_mla_kernels.cuh)
     constexpr int HG = C::HG, HH = C::HH;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = ptx::align_smem_1024(smem_raw);
@@ -714,7 +715,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     exceed |= x[j] > m_own[j] + thresh;
                 }
                 const bool first = (t == sd.t0);
-                const bool debug = prm.state != nullptr && t < prm.state_tiles;
+                const bool debug = kDebug && prm.state != nullptr && t < prm.state_tiles;
                 const float dbg_m_old = (debug && lane_head && !first) ? s_m[hoff + lane] : -INFINITY;
                 // one barrier decides, CTA-uniformly, whether any running max must move
                 const bool any = ptx::bar_red_or(bar_a, 128, exceed || (negate && !first));
@@ -971,11 +972,13 @@ static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
 static_assert(OFF_Q % 1024 == 0 && OFF_P % 1024 == 0, "alignment");
 }  // namespace kfp8
 
+template <bool DBG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     etap_mla_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_kv128, const __grid_constant__ CUtensorMap tm_kv64,
                                const __grid_constant__ CUtensorMap tm_q128, const __grid_constant__ CUtensorMap tm_q64,
                                const DecodeParams prm, float kv_scale) {
     using namespace kfp8;
+    constexpr bool kDebug = DBG;
     constexpr int HG = HG8, HH = HH8, NQ = fp8::NQ;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = ptx::align_smem_1024(smem_raw);
@@ -983,6 +986,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        ETAP_TRACE_G(prm, 0);
+        ETAP_TRACE_CLK(prm, 5);
+    }
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tm_kv128);
         ptx::prefetch_tmap(&tm_kv64);
@@ -1008,6 +1015,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
     ptx::grid_dep_wait();
     ptx::grid_dep_launch();
+    if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
 
     int* s_pref = reinterpret_cast<int*>(smem + OFF_SCHED);
     int* s_soff = s_pref + MAX_FUSED_VB + 1;
@@ -1033,6 +1041,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sch = prm.sched + blockIdx.x * SCHED_INTS;
         soff = prm.split_off + sch[5];
     }
+    if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 1); ETAP_TRACE_CLK(prm, 14); }
     const int vb_begin = sch[0], vb_end = sch[2];
     const int B = prm.batch;
     const uint32_t ring_addr = ptx::smem_u32(smem + OFF_RING);
@@ -1061,6 +1070,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const int page = __shfl_sync(0xffffffffu, pg, t - base);
                 if (gt >= NPS) ptx::mbar_wait(&bars[BAR_G2D + (gt - NPS) % NTB8], ((gt - NPS) / NTB8) & 1);
                 if (lane == 0) {
+                    if (gt == 0) { ETAP_TRACE_G(prm, 9); ETAP_TRACE_CLK(prm, 15); }
+                    ETAP_TRACE(prm, gt, 0);
                     uint8_t* slot = smem + OFF_RING + (gt % NPS) * fp8::TILE_BYTES;
                     uint64_t* full = &bars[BAR_FULL + gt % NTB8];
                     ptx::mbar_arrive_expect_tx(full, fp8::TILE_BYTES);
@@ -1068,6 +1079,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     for (int c = 0; c < fp8::VCH; ++c)
                         ptx::tma_load_2d(slot + c * fp8::VCH_BYTES, &tm_kv128, full, c * 128, page * PAGE, pol_kv);
                     ptx::tma_load_2d(slot + fp8::ROPE_OFF, &tm_kv64, full, 512, page * PAGE, pol_kv);
+                    ETAP_TRACE(prm, gt, 1);
                 }
                 __syncwarp();
                 if (q_pending) {
@@ -1101,8 +1113,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::mbar_wait(&bars[BAR_FULL + gt % NTB8], (gt / NTB8) & 1);
                 __syncwarp();
                 ptx::tc_fence_after();
+                ETAP_TRACE(prm, gt, 2);
                 fp8::issue_gemm1(tmem_base + TCOL_S + NQ * buf, ring_addr + (gt % NPS) * fp8::TILE_BYTES, q_addr);
                 ptx::umma_commit_elect(&bars[BAR_SF + buf]);
+                ETAP_TRACE(prm, gt, 3);
                 if (t == sd.t1 - 1) ptx::umma_commit_elect(&bars[BAR_QE]);
                 ++gt;
             }
@@ -1119,12 +1133,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::mbar_wait(&bars[BAR_PF + buf], (gt >> 1) & 1);
                 __syncwarp();
                 ptx::tc_fence_after();
+                ETAP_TRACE(prm, gt, 6);
                 const uint32_t slot = ring_addr + (gt % NPS) * fp8::TILE_BYTES;
 #pragma unroll
                 for (int c = 0; c < fp8::VCH; ++c)
                     fp8::issue_gemm2(tmem_base + TCOL_O + c * NQ, slot + c * fp8::VCH_BYTES, p_addr + buf * fp8::P_BYTES,
                                      t == sd.t0);
                 ptx::umma_commit_elect(&bars[BAR_G2D + gt % NTB8]);
+                ETAP_TRACE(prm, gt, 7);
                 ++gt;
             }
         }
@@ -1145,6 +1161,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool mtp = prm.q_tokens > 1;
         const int rhead = halfwarp_reduce_head<HH>(lane);
         const bool rwriter = (lane & 1) == 0;
+        const bool tracer = threadIdx.x == SOFTMAX_WARP0 * 32;
         uint32_t gt = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
@@ -1163,6 +1180,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint32_t buf = gt & 1;
                 ptx::mbar_wait(&bars[BAR_SF + buf], (gt >> 1) & 1);
                 ptx::tc_fence_after();
+                if (tracer) ETAP_TRACE(prm, gt, 4);
                 uint32_t s0[HH], s1[HH], s2[HH];
                 ptx::tmem_ld16x2<HH>(t_lane + TCOL_S + NQ * buf, s0);
                 ptx::tmem_ld16x2<HH>(t_lane + TCOL_S + NQ * buf + 16, s1);
@@ -1226,7 +1244,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     l_part[j] = first ? pv[j] : fmaf(l_part[j], alpha_own[j], pv[j]);
                 }
                 // the P buffer is reused every other tile: GEMM2(gt-2) must have read it
+                if (tracer) ETAP_TRACE(prm, gt, 8);
                 if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2D + (gt - 2) % NTB8], ((gt - 2) / NTB8) & 1);
+                if (tracer) ETAP_TRACE(prm, gt, 9);
                 if (need_rescale) {
                     ptx::named_bar_sync(2, 128);
                     ptx::mbar_wait(&bars[BAR_G2D + (gt - 1) % NTB8], ((gt - 1) / NTB8) & 1);
@@ -1271,6 +1291,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
                 ptx::fence_proxy_async_smem();
                 ptx::tc_fence_before();
+                if (tracer) ETAP_TRACE(prm, gt, 5);
                 ptx::mbar_arrive(&bars[BAR_PF + buf]);
                 ++gt;
             }
@@ -1279,6 +1300,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t last = gt - 1;
             ptx::mbar_wait(&bars[BAR_G2D + last % NTB8], (last / NTB8) & 1);
             ptx::tc_fence_after();
+            if (tracer) { ETAP_TRACE_G(prm, 10); ETAP_TRACE(prm, last, 10); }
             const float wsum = halfwarp_reduce<false, HH>(l_part, lane);
             if (rwriter) red_sum[wq * HG + half * HH + rhead] = wsum;
             const int ns = soff[vb + 1] - soff[vb];
@@ -1335,11 +1357,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             ptx::tc_fence_before();
             ptx::named_bar_sync(2, 128);
+            if (tracer) ETAP_TRACE(prm, last, 11);
         }
     }
 
+    if (tracer_exit(warp, lane)) ETAP_TRACE_G(prm, 11);
     ptx::tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) {
+        ETAP_TRACE_G(prm, 2);
+        ETAP_TRACE_CLK(prm, 6);
+    }
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, TMEM_COLS);
@@ -1398,7 +1426,7 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
     etap_mla_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
                             const int32_t* __restrict__ split_off, int hg, int batch,
                             const __grid_constant__ OutMap om, unsigned long long* trace,
-                            const int32_t* __restrict__ seqlens, int parts, int lanes_on) {
+                            const int32_t* __restrict__ seqlens, int parts, int lanes_on, int fixed_cost) {
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 0] = ptx::global_timer_ns();
     const int vb = blockIdx.x / hg;
     const int h = blockIdx.x - vb * hg;
@@ -1418,7 +1446,7 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
             const int lv = vb / n, pos = vb - lv * n;
             const int len = lane < n ? max(0, __ldg(seqlens + lane % batch)) : 0;
             const int tiles = (len + TILE - 1) / TILE;
-            const int cost = tiles > 0 ? tiles + META_FIXED_COST : 0;
+            const int cost = tiles > 0 ? tiles + fixed_cost : 0;
             int incl = cost;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -1428,7 +1456,7 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
             const int total = __shfl_sync(0xffffffffu, incl, 31);
             const int pref = incl - cost;
             const int T = max(1, (total + ls.p_line - 1) / ls.p_line);
-            const int nsi = (lane < n && tiles > 0) ? ((incl + T - 1) / T - 1) - (pref + META_FIXED_COST) / T + 1 : 0;
+            const int nsi = (lane < n && tiles > 0) ? ((incl + T - 1) / T - 1) - (pref + fixed_cost) / T + 1 : 0;
             int so = nsi;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -1929,7 +1957,7 @@ int etap_mla_metadata_host(const int32_t* seqlens, int batch, int heads, int num
 }
 
 int metadata_launch(const int32_t* seqlens, int batch, int groups, int num_sm_parts, int32_t* sched,
-                    int32_t* split_off, void* stream);
+                    int32_t* split_off, void* stream, int fixed_cost = META_FIXED_COST);
 
 int etap_mla_metadata(const int32_t* seqlens, int batch, int heads, int num_sm_parts,
                       int32_t* sched, int32_t* split_off, void* stream) {
@@ -1940,7 +1968,7 @@ int etap_mla_metadata(const int32_t* seqlens, int batch, int heads, int num_sm_p
 }
 
 int metadata_launch(const int32_t* seqlens, int batch, int groups, int num_sm_parts, int32_t* sched,
-                    int32_t* split_off, void* stream) {
+                    int32_t* split_off, void* stream, int fixed_cost) {
     if (batch * groups > META_MAX_VB)
         return fail(ETAP_ERR_SHAPE, "batch * head groups exceeds " + std::to_string(META_MAX_VB));
     if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
@@ -1956,7 +1984,7 @@ int metadata_launch(const int32_t* seqlens, int batch, int groups, int num_sm_pa
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_metadata_kernel, seqlens, batch, groups,
-                                 num_sm_parts, lanes_enabled() ? 1 : 0, sched, split_off));
+                                 num_sm_parts, lanes_enabled() ? 1 : 0, sched, split_off, fixed_cost));
     return ETAP_OK;
 }
 
@@ -1982,7 +2010,8 @@ OutMap local_outmap(int heads, float* out, float* lse) {
 // whatever the head count); the partial / LSE areas keep the allocation layout of
 // etap_mla_workspace_bytes either way
 int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_parts, void* workspace,
-                 const OutMap& om, void* stream, const int32_t* seqlens = nullptr, int hg_unit = 0) {
+                 const OutMap& om, void* stream, const int32_t* seqlens = nullptr, int hg_unit = 0,
+                 int fixed_cost = META_FIXED_COST) {
     const int hg_alloc = head_group_of(heads);
     const int hg = hg_unit > 0 ? hg_unit : hg_alloc;
     const int groups = heads / hg;
@@ -2002,7 +2031,7 @@ int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_part
     ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, static_cast<const float*>(ws_o),
                                  static_cast<const float*>(ws_lse), split_off, hg, batch, om,
                                  static_cast<unsigned long long*>(g_combine_trace_buf), seqlens, num_sm_parts,
-                                 lanes_enabled() ? 1 : 0));
+                                 lanes_enabled() ? 1 : 0, fixed_cost));
     return ETAP_OK;
 }
 
@@ -2061,6 +2090,7 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     prm.lanes_on = lanes_enabled() ? 1 : 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
     prm.inkernel_sched = (ls.line_n <= MAX_FUSED_VB && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
+    prm.fixed_cost = META_FIXED_COST;
     if (!prm.inkernel_sched && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) {
         // too many virtual sequences for the fused prologue: run K1 first on the same stream
         if (int rc = etap_mla_metadata(seqlens, batch, heads, num_sm_parts, const_cast<int32_t*>(sched),
@@ -2072,6 +2102,7 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     prm.trace = static_cast<unsigned long long*>(g_trace_buf);
     prm.state = static_cast<float*>(g_state_buf);
     prm.state_tiles = g_state_tiles;
+    const bool dbg = prm.trace != nullptr || prm.state != nullptr;  // debug instantiation
 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaLaunchAttribute attr[1];
@@ -2086,15 +2117,19 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     if (hg == 32) {
         cfg.dynamicSmemBytes = Cfg<32>::SMEM_ALLOC;
         cfg.blockDim = dim3(Cfg<32>::THREADS);
-        static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<32>, Cfg<32>::SMEM_ALLOC);
+        auto kern = dbg ? etap_mla_decode_kernel<32, true> : etap_mla_decode_kernel<32, false>;
+        static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<32, false>, Cfg<32>::SMEM_ALLOC) |
+                             ensure_smem_attr(etap_mla_decode_kernel<32, true>, Cfg<32>::SMEM_ALLOC);
         if (attr_rc) return attr_rc;
-        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel<32>, tm_kv, tm_q, prm));
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, kern, tm_kv, tm_q, prm));
     } else {
         cfg.dynamicSmemBytes = Cfg<16>::SMEM_ALLOC;
         cfg.blockDim = dim3(Cfg<16>::THREADS);
-        static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<16>, Cfg<16>::SMEM_ALLOC);
+        auto kern = dbg ? etap_mla_decode_kernel<16, true> : etap_mla_decode_kernel<16, false>;
+        static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<16, false>, Cfg<16>::SMEM_ALLOC) |
+                             ensure_smem_attr(etap_mla_decode_kernel<16, true>, Cfg<16>::SMEM_ALLOC);
         if (attr_rc) return attr_rc;
-        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_kernel<16>, tm_kv, tm_q, prm));
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, kern, tm_kv, tm_q, prm));
     }
 
     if (flags & ETAP_FLAG_SKIP_COMBINE) return ETAP_OK;
@@ -2171,9 +2206,10 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     prm.lanes_on = lanes_enabled() ? 1 : 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
     prm.inkernel_sched = ls.line_n <= MAX_FUSED_VB ? 1 : 0;
+    prm.fixed_cost = FP8_FIXED_COST;
     prm.scale_log2 = scale * kv_scale * 1.4426950408889634f;
     prm.flags = flags;
-    prm.trace = nullptr;
+    prm.trace = static_cast<unsigned long long*>(g_trace_buf);
     prm.state = nullptr;
     prm.state_tiles = 0;
 
@@ -2195,7 +2231,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     }
     if (!prm.inkernel_sched)
         if (int rc = metadata_launch(seqlens, batch, groups, num_sm_parts, const_cast<int32_t*>(sched),
-                                     const_cast<int32_t*>(split_off), stream))
+                                     const_cast<int32_t*>(split_off), stream, FP8_FIXED_COST))
             return rc;
     {
         cudaLaunchConfig_t cfg = {};
@@ -2205,14 +2241,17 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
         cfg.stream = st;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        static int attr_rc = ensure_smem_attr(etap_mla_decode_fp8_kernel, kfp8::SMEM_ALLOC);
+        const bool dbg = prm.trace != nullptr;
+        auto kern = dbg ? etap_mla_decode_fp8_kernel<true> : etap_mla_decode_fp8_kernel<false>;
+        static int attr_rc = ensure_smem_attr(etap_mla_decode_fp8_kernel<false>, kfp8::SMEM_ALLOC) |
+                             ensure_smem_attr(etap_mla_decode_fp8_kernel<true>, kfp8::SMEM_ALLOC);
         if (attr_rc) return attr_rc;
-        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_fp8_kernel, tm_kv128, tm_kv64, tm_q128, tm_q64, prm, kv_scale));
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, kern, tm_kv128, tm_kv64, tm_q128, tm_q64, prm, kv_scale));
     }
     if (flags & ETAP_FLAG_SKIP_COMBINE) return ETAP_OK;
     const bool closed_form = prm.inkernel_sched && ls.line_n <= 32;
     return combine_impl(split_off, batch, heads, num_sm_parts, workspace, om, stream, closed_form ? seqlens : nullptr,
-                        hg);
+                        hg, FP8_FIXED_COST);
 }
 
 int etap_mla_decode_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t num_pages,

@@ -52,6 +52,12 @@ constexpr int SCHED_INTS = 8;
 #define ETAP_META_FIXED_COST 2
 #endif
 constexpr int META_FIXED_COST = ETAP_META_FIXED_COST;  // per-split overhead in tile units (scheduler)
+// The FP8 path's tiles stream half the bytes in about half the time, while a split's fixed
+// work (epilogue, the next split's first-tile latency) stays: about 2.4 us, 3-4 FP8 tiles
+#ifndef ETAP_FP8_FIXED_COST
+#define ETAP_FP8_FIXED_COST 4
+#endif
+constexpr int FP8_FIXED_COST = ETAP_FP8_FIXED_COST;
 
 enum : unsigned {
     FLAG_NEGATE_RESCALE = 1u,
@@ -327,6 +333,7 @@ struct DecodeParams {
     int heads_per_token;
     int causal;           // q_tokens > 1: token j sees KV rows [0, seqlen - q_tokens + j]
     int inkernel_sched;  // 1: compute the split schedule in the prologue (and publish it)
+    int fixed_cost;      // per-split overhead in tile units of the split schedule
     int lanes_on;        // head-group lanes enabled (line_shape)
     float scale_log2;
     unsigned flags;
@@ -335,6 +342,12 @@ struct DecodeParams {
     int state_tiles;
 };
 
+// Debug stamps and the softmax-state dump are compiled into the DBG instantiations of the
+// decode kernels only (selected at launch when a debug buffer is registered): in the product
+// instantiation kDebug is false and every stamp vanishes, so the hot loops keep their schedule
+// (the runtime-checked stamps cost ~1% of the step, 10% on the MTP FP8 path). Helpers outside
+// the kernels see this namespace-scope value and keep the runtime check.
+constexpr bool kDebug = true;
 constexpr int TRACE_TILES = 256;
 constexpr int TRACE_SLOTS = 16;
 // Debug stamps: [cta][TRACE_TILES][TRACE_SLOTS]. Tile rows hold %clock64 (SM cycles, fine
@@ -342,19 +355,19 @@ constexpr int TRACE_SLOTS = 16;
 // across SMs) plus %clock64 at entry and exit (slots 5, 6) to convert cycles to ns.
 #define ETAP_TRACE(prm, gt, slot)                                                                   \
     do {                                                                                            \
-        if ((prm).trace != nullptr && (gt) < TRACE_TILES - 1)                                       \
+        if (kDebug && (prm).trace != nullptr && (gt) < TRACE_TILES - 1)                             \
             (prm).trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + (gt)) * TRACE_SLOTS + (slot)] = \
                 clock64();                                                                          \
     } while (0)
 #define ETAP_TRACE_G(prm, slot)                                                                     \
     do {                                                                                            \
-        if ((prm).trace != nullptr)                                                                 \
+        if (kDebug && (prm).trace != nullptr)                                                       \
             (prm).trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + TRACE_TILES - 1) * TRACE_SLOTS + \
                         (slot)] = ptx::global_timer_ns();                                           \
     } while (0)
 #define ETAP_TRACE_CLK(prm, slot)                                                                   \
     do {                                                                                            \
-        if ((prm).trace != nullptr)                                                                 \
+        if (kDebug && (prm).trace != nullptr)                                                       \
             (prm).trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + TRACE_TILES - 1) * TRACE_SLOTS + \
                         (slot)] = clock64();                                                        \
     } while (0)

@@ -14,6 +14,9 @@ k2 = [torch.zeros(n * TT * 16, dtype=torch.int64, device="cuda") for _ in range(
 k3 = [torch.zeros(B * 16 * 4, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
 L = _lib.lib()
 f = lambda: plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
+if os.environ.get("FP8"):  # FP8 (e4m3) latent cache
+    kv8 = (inp.kv_pool.float() / 0.125).to(torch.float8_e4m3fn)
+    f = lambda: plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 0.125)
 for _ in range(5): f()
 torch.cuda.synchronize()
 for i in range(STEPS):  # back to back, a different trace buffer per step
@@ -38,6 +41,8 @@ for i in range(STEPS):
     m = lambda j: r(np.median(ex[:, j]))
     print(f"        dep-wait done med {m(0):7.2f} (min {r(ex[:,0].min()):7.2f})  seqlens-in med {m(1):7.2f}  "
           f"first-KV-TMA med {m(2):7.2f}  last-epilogue med {m(3):7.2f}  softmax-done med {m(4):7.2f}")
+    if os.environ.get("FP8"):
+        print(f"        first Q terms published med {r(np.median((g[:, 4] - gbase).astype(np.float64))):7.2f}")
     ck = g[:, 12:16].astype(np.int64)
     d = np.median(ck[:, 1:] - ck[:, :1], axis=0)
     print(f"        clock64 after dep-wait: seqlens-in +{d[0]:.0f}  sched-done +{d[1]:.0f}  first-KV-TMA +{d[2]:.0f} cycles")

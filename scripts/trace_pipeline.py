@@ -27,9 +27,13 @@ def main() -> None:
     ap.add_argument("--ctx", type=int, default=65536)
     ap.add_argument("--runs", type=int, default=3)
     ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--fp8", action="store_true", help="FP8 (e4m3) latent cache (decode_fp8)")
     a = ap.parse_args()
     inp = inputs.make_mla_inputs([a.ctx] * a.batch, heads=a.heads, pad_value=0.0)
     plan = mla.MlaDecodePlan.create(a.batch, a.heads, "cuda")
+    if a.fp8:
+        kv8 = (inp.kv_pool.float() / 0.125).to(torch.float8_e4m3fn)
+        plan.decode = lambda q, kv, bt, sl, sc: mla.MlaDecodePlan.decode_fp8(plan, q, kv8, bt, sl, sc, 0.125)
     nparts = plan.num_sm_parts
     buf = torch.zeros(nparts * TRACE_TILES * 16, dtype=torch.int64, device="cuda")
     for _ in range(2):

@@ -113,3 +113,37 @@ def test_fp8_mtp_and_errors(cuda_device):
         check(o[:, j], l[:, j], o_ref[:, j], l_ref[:, j], vis.tolist())
     with pytest.raises(_lib.EtapShapeError):
         plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 0.0)  # kv_scale must be > 0
+
+
+def test_fp8_many_splits_per_cta(cuda_device):
+    """Q of each split is quantised in-kernel: the first split's straight into shared memory,
+    the next three staged in TMEM, later ones quantised at the boundary. 3 CTAs over 40 short
+    sequences walk all three paths (about 14 splits per CTA)."""
+    import random
+    rnd = random.Random(5)
+    seqlens = [rnd.randint(1, 700) for _ in range(40)]
+    inp, kv8, deq = fp8_inputs(seqlens, 16, seed=21)
+    plan = mla.MlaDecodePlan.create(len(seqlens), 16, "cuda", num_parts=3)
+    out, lse = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 2.0 ** -3)
+    torch.cuda.synchronize()
+    o_ref, l_ref = oracle_fp8(inp, deq)
+    check(out.double().cpu().numpy()[:, 0], lse.double().cpu().numpy()[:, 0], o_ref, l_ref, seqlens)
+    ref = mla.MlaDecodePlan.create(len(seqlens), 16, "cuda")  # 148 CTAs: at most a few splits each
+    o2, l2 = ref.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 2.0 ** -3)
+    torch.cuda.synchronize()
+    # P is split into fp8 terms relative to the running max of each split: different split
+    # boundaries quantise P differently (~1e-5 on O of magnitude ~0.1)
+    assert (o2 - out).abs().max().item() <= 1e-4 and (l2 - lse).abs().max().item() <= 1e-5
+
+
+def test_fp8_long_line_runs_k1(cuda_device):
+    """More than 128 work units: the split schedule comes from K1 (with the FP8 fixed cost)."""
+    import random
+    rnd = random.Random(8)
+    seqlens = [rnd.randint(0, 300) for _ in range(140)]
+    inp, kv8, deq = fp8_inputs(seqlens, 16, seed=4)
+    plan = mla.MlaDecodePlan.create(len(seqlens), 16, "cuda")
+    out, lse = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 2.0 ** -3)
+    torch.cuda.synchronize()
+    o_ref, l_ref = oracle_fp8(inp, deq)
+    check(out.double().cpu().numpy()[:, 0], lse.double().cpu().numpy()[:, 0], o_ref, l_ref, seqlens)
