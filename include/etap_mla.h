@@ -262,12 +262,14 @@ int etap_mla_selftest_umma(const void* k, const void* q, const float* p, float* 
  * o_t [512][48] = k8[:, :512]^T p8, fp32. */
 int etap_mla_selftest_fp8(const void* k8, const void* q8, const void* p8, float* s_t, float* o_t, void* stream);
 
-/* Debug: when device_buf is non-NULL, subsequent decode launches record per-tile %clock64
- * stamps of the pipeline events into it: [cta][256][16] uint64, row = tile (< 255): 0/1 first /
- * last chunk TMA issued, 2 last chunk landed, 3 S^T committed, 4 softmax saw S^T, 5 P^T
- * written, 6 MMA saw P^T, 7 O^T update committed, 8 softmax exp done, 9 P buffer free.
- * Row 255: %globaltimer ns at 0 entry, 1 schedule done, 2 exit; 3 SM id; %clock64 at 5 entry,
- * 6 exit. NULL disables (the default). */
+/* Debug: when device_buf is non-NULL, subsequent decode launches (bf16 and FP8) run the
+ * debug instantiation of the decode kernel, which records per-tile %clock64 stamps of the
+ * pipeline events into it: [cta][256][16] uint64, row = tile (< 255): 0/1 first / last chunk
+ * TMA issued, 2 last chunk landed, 3 S^T committed, 4 softmax saw S^T, 5 P^T written, 6 MMA saw
+ * P^T, 7 O^T update committed, 8 softmax exp done, 9 P buffer free (FP8: 10/11 split epilogue
+ * start / end on a split's last tile). Row 255: %globaltimer ns at 0 entry, 1 schedule done,
+ * 2 exit; 3 SM id; %clock64 at 5 entry, 6 exit. NULL disables (the default, and the product
+ * instantiation carries no stamps at all). */
 int etap_mla_debug_trace(void* device_buf);
 
 /* Debug: combine-kernel stamps [block][4] (entry, after grid-dependency wait, exit) or NULL. */

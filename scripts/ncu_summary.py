@@ -43,7 +43,9 @@ def raw(rep: str) -> dict:
 
 
 def main() -> None:
-    rep, launches, tag = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None, sys.argv[3] if len(sys.argv) > 3 else "r01"
+    fp8 = "--fp8" in sys.argv  # FP8 kernel capture: profiles/<tag>/ncu_fp8_kernel.md only
+    args = [a for a in sys.argv[1:] if a != "--fp8"]
+    rep, launches, tag = args[0], args[1] if len(args) > 1 and args[1] != "-" else None, args[2] if len(args) > 2 else "r01"
     from paper_2506_01969_b200 import inputs
 
     d = raw(rep)
@@ -51,6 +53,8 @@ def main() -> None:
     wr = d["dram__bytes_write.sum"][0] * SCALE[d["dram__bytes_write.sum"][1]]
     dur = d["gpu__time_duration.sum"][0] * SCALE[d["gpu__time_duration.sum"][1]]
     alg = inputs.algorithmic_bytes([65536] * 16, 16)
+    if fp8:  # the latent cache is one byte per element
+        alg -= 65536 * 16 * 576
     summary = {
         "workload": "mla_decode_b16_ctx64k_h16_per_gpu", "tag": tag, "source": rep,
         "decode_kernel": {
@@ -75,10 +79,12 @@ def main() -> None:
         tot = sum(sum(v) for v in ks.values())
         summary["launch_list"] = {k: {"launches": len(v), "avg_us": sum(v) / len(v) * 1e6,
                                       "share": sum(v) / tot} for k, v in ks.items()}
-    (ROOT / "profiles" / "ncu_summary.json").write_text(json.dumps(summary, indent=1) + "\n")
+    if not fp8:
+        (ROOT / "profiles" / "ncu_summary.json").write_text(json.dumps(summary, indent=1) + "\n")
     tagdir = ROOT / "profiles" / tag
     tagdir.mkdir(parents=True, exist_ok=True)
-    lines = [f"# ncu — etap_mla_decode_kernel (K2), B=16 x 64K, 16 heads ({tag})", "",
+    kname = "etap_mla_decode_fp8_kernel (K2-FP8, e4m3 latent cache)" if fp8 else "etap_mla_decode_kernel (K2)"
+    lines = [f"# ncu — {kname}, B=16 x 64K, 16 heads ({tag})", "",
              f"source: `{rep}` (`ncu --set full --clock-control none --import-source on`, one launch)", "",
              "| metric | value |", "|---|---|"]
     for k, v in summary["decode_kernel"].items():
@@ -88,7 +94,7 @@ def main() -> None:
                   "|---|---|---|---|"]
         for k, v in summary["launch_list"].items():
             lines.append(f"| {k} | {v['launches']} | {v['avg_us']:.2f} | {v['share']:.3f} |")
-    (tagdir / "ncu_decode_kernel.md").write_text("\n".join(lines) + "\n")
+    (tagdir / ("ncu_fp8_kernel.md" if fp8 else "ncu_decode_kernel.md")).write_text("\n".join(lines) + "\n")
     print(json.dumps(summary, indent=1))
 
 
