@@ -355,6 +355,42 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
     __syncthreads();
 }
 
+// Before the grid dependency (while the previous kernel finishes): warm L2 with the first pages
+// this CTA will most likely stream, guessed from its own range of the previous decode call (the
+// fused schedule republishes it every call; a decode step moves it only when a sequence crosses
+// a page), and return that guess (b, first tile). Hints only: every byte used is loaded after
+// the grid dependency, and a wrong or stale guess merely wastes a prefetch. Whole warp.
+__device__ __forceinline__ void prev_range_hint(const DecodeParams& prm, int hg, uint32_t page_bytes, bool q_rows,
+                                                int lane, int& hint_b, int& hint_t0) {
+#ifndef ETAP_NO_PREFETCH_HINT
+    if (!prm.inkernel_sched) return;
+    if (lane == 0) {
+        const int32_t* prev = prm.sched_out + blockIdx.x * SCHED_INTS;
+        const int p0 = prev[0], tb = prev[1], p1 = prev[2], off = prev[5];
+        const int vb = off + p0, nvb = prm.batch * prm.groups;
+        if (p1 >= p0 && p0 >= 0 && vb >= 0 && vb < nvb && tb >= 0 && tb < prm.max_pages) {
+            const int g = vb / prm.batch, b = vb - g * prm.batch;
+            hint_b = b;
+            hint_t0 = tb;
+            const int32_t* bt = prm.block_table + static_cast<size_t>(b) * prm.max_pages;
+#pragma unroll 1
+            for (int k = 0; k < 2 && tb + k < prm.max_pages; ++k) {
+                const int page = bt[tb + k];
+                if (page >= 0 && page < prm.num_pages)
+                    ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) + static_cast<size_t>(page) * page_bytes,
+                                          page_bytes);
+            }
+            if (q_rows)
+                ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.q) +
+                                          (static_cast<size_t>(b) * prm.heads + g * hg) * D_QK * 2,
+                                      hg * D_QK * 2);
+        }
+    }
+    hint_b = __shfl_sync(0xffffffffu, hint_b, 0);
+    hint_t0 = __shfl_sync(0xffffffffu, hint_t0, 0);
+#endif
+}
+
 // Split i of the CTA's range along the line: virtual sequence vb = lane_off + i (head-group
 // major: b = vb % batch, g = vb / batch) and the tile interval this CTA owns of it.
 __device__ __forceinline__ bool split_at(const int32_t* sch, int seqlen, int batch, int i,
@@ -418,39 +454,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
 
     // (b, first tile) of this CTA's range in the previous call: a guess for this call
     int hint_b = -1, hint_t0 = 0;
-#ifndef ETAP_NO_PREFETCH_HINT
-    if (warp == 0 && prm.inkernel_sched) {
-        // While the previous kernel finishes: warm L2 with the first pages this CTA will most
-        // likely stream, guessed from its own range of the previous decode call (the fused
-        // schedule republishes it every call; a decode step moves it only when a sequence
-        // crosses a page). Hints only: every byte used is loaded after grid_dep_wait below,
-        // and a wrong or stale guess merely wastes a prefetch.
-        if (lane == 0) {
-            const int32_t* prev = prm.sched_out + blockIdx.x * SCHED_INTS;
-            const int p0 = prev[0], tb = prev[1], p1 = prev[2], off = prev[5];
-            const int vb = off + p0, nvb = prm.batch * prm.groups;
-            if (p1 >= p0 && p0 >= 0 && vb >= 0 && vb < nvb && tb >= 0 && tb < prm.max_pages) {
-                const int g = vb / prm.batch, b = vb - g * prm.batch;
-                hint_b = b;
-                hint_t0 = tb;
-                const int32_t* bt = prm.block_table + static_cast<size_t>(b) * prm.max_pages;
-#pragma unroll 1
-                for (int k = 0; k < 2 && tb + k < prm.max_pages; ++k) {
-                    const int page = bt[tb + k];
-                    if (page >= 0 && page < prm.num_pages)
-                        ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) +
-                                                  static_cast<size_t>(page) * PAGE * D_QK * 2,
-                                              PAGE * D_QK * 2);
-                }
-                ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.q) +
-                                          (static_cast<size_t>(b) * prm.heads + g * HG) * D_QK * 2,
-                                      HG * D_QK * 2);
-            }
-        }
-        hint_b = __shfl_sync(0xffffffffu, hint_b, 0);
-        hint_t0 = __shfl_sync(0xffffffffu, hint_t0, 0);
-    }
-#endif
+    if (warp == 0) prev_range_hint(prm, HG, PAGE * D_QK * 2, true, lane, hint_b, hint_t0);
     ptx::grid_dep_wait();     // inputs / schedule written by earlier kernels in the stream
     ptx::grid_dep_launch();   // let the combine kernel get scheduled
     // the producer's first page ids for the guessed range go out together with the seqlens
@@ -1013,8 +1017,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    int hint_b = -1, hint_t0 = 0;  // guessed from the previous call, see prev_range_hint
+    if (warp == 0) prev_range_hint(prm, HG, PAGE * D_QK, false, lane, hint_b, hint_t0);
     ptx::grid_dep_wait();
     ptx::grid_dep_launch();
+    int hint_pg = 0;  // the producer's first page ids of the guessed range, beside the seqlens loads
+    if (warp == 0 && hint_b >= 0 && hint_t0 + lane < prm.max_pages)
+        hint_pg = prm.block_table[static_cast<size_t>(hint_b) * prm.max_pages + hint_t0 + lane];
     if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
 
     int* s_pref = reinterpret_cast<int*>(smem + OFF_SCHED);
@@ -1060,7 +1069,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
             const int32_t* bt = prm.block_table + static_cast<size_t>(sd.b) * prm.max_pages;
             int base = sd.t0;
-            int pg = (base + lane < sd.t1) ? __ldg(bt + base + lane) : 0;
+            int pg;
+            if (nsplit == 0 && sd.b == hint_b && sd.t0 == hint_t0) pg = hint_pg;  // loaded already
+            else pg = (base + lane < sd.t1) ? __ldg(bt + base + lane) : 0;
             bool q_pending = true;
             for (int t = sd.t0; t < sd.t1; ++t) {
                 if (t - base >= 32) {
