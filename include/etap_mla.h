@@ -89,9 +89,10 @@ int etap_mla_head_group(int heads, int* head_group);
 int etap_mla_num_sm_parts(int device, int* num_sm_parts);
 
 /* Sizes of the caller-owned scratch buffers.
- *   sched     : num_sm_parts * ETAP_MLA_SCHED_INTS int32
+ *   sched     : num_sm_parts * ETAP_MLA_SCHED_INTS int32 (zero it once after allocation: the
+ *               decode reads the previous call's ranges from it as an L2 prefetch hint)
  *   split_off : batch * heads/head_group + 1 int32
- *   workspace : bytes for split-KV partial O / LSE */
+ *   workspace : bytes for split-KV partial O / LSE (zero it once after allocation) */
 int etap_mla_sched_ints(int batch, int heads, int num_sm_parts, size_t* sched_ints,
                         size_t* split_off_ints);
 int etap_mla_workspace_bytes(int batch, int heads, int num_sm_parts, size_t* bytes);

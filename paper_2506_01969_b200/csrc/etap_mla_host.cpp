@@ -98,7 +98,8 @@ int etap_mla_host_ctx_create(int batch, int heads, int64_t num_pages, int max_pa
             c->split_off.alloc(so_n * 4) || c->ws.alloc(ws_n) ||
             c->rows.alloc(static_cast<size_t>(batch) * ETAP_MLA_D_QK * 2) ||
             cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) ||
-            cudaMemset(c->ws.p, 0, c->ws.n))  // combine flags / counters start at zero
+            cudaMemset(c->ws.p, 0, c->ws.n) ||  // combine flags / counters start at zero
+            cudaMemset(c->sched.p, 0, c->sched.n))  // read as a prefetch hint before the first decode
             rc = host_fail(ETAP_ERR_CUDA, "device allocation failed");
     }
     if (rc) {

@@ -91,7 +91,9 @@ class MlaDecodePlan:
         check(L.etap_mla_workspace_bytes(batch, rows, nparts, C.byref(ws)), "etap_mla_workspace_bytes")
         return cls(
             batch=batch, heads=heads, device=device, num_sm_parts=nparts, q_tokens=q_tokens,
-            sched=torch.empty(n_sched.value, dtype=torch.int32, device=device),
+            # zero-filled once: the decode reads its previous-call range from it as an L2
+            # prefetch hint before the schedule of this call is known
+            sched=torch.zeros(n_sched.value, dtype=torch.int32, device=device),
             split_off=torch.zeros(n_so.value, dtype=torch.int32, device=device),
             # zero-filled once: the tail holds the combine's ready flags / counters, which every
             # decode call leaves at zero again
