@@ -355,6 +355,9 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
     __syncthreads();
 }
 
+#ifndef ETAP_HINT_PAGES
+#define ETAP_HINT_PAGES 2
+#endif
 // Before the grid dependency (while the previous kernel finishes): warm L2 with the first pages
 // this CTA will most likely stream, guessed from its own range of the previous decode call (the
 // fused schedule republishes it every call; a decode step moves it only when a sequence crosses
@@ -374,7 +377,7 @@ __device__ __forceinline__ void prev_range_hint(const DecodeParams& prm, int hg,
             hint_t0 = tb;
             const int32_t* bt = prm.block_table + static_cast<size_t>(b) * prm.max_pages;
 #pragma unroll 1
-            for (int k = 0; k < 2 && tb + k < prm.max_pages; ++k) {
+            for (int k = 0; k < ETAP_HINT_PAGES && tb + k < prm.max_pages; ++k) {
                 const int page = bt[tb + k];
                 if (page >= 0 && page < prm.num_pages)
                     ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) + static_cast<size_t>(page) * page_bytes,

@@ -147,3 +147,26 @@ def test_fp8_long_line_runs_k1(cuda_device):
     torch.cuda.synchronize()
     o_ref, l_ref = oracle_fp8(inp, deq)
     check(out.double().cpu().numpy()[:, 0], lse.double().cpu().numpy()[:, 0], o_ref, l_ref, seqlens)
+
+
+def test_fp8_arbitrary_kv_scale_vs_fp64_torch(cuda_device):
+    """A kv_scale that is not a power of two (dequantised values not representable in bf16):
+    compare against a float64 softmax-attention over exactly kv_scale * e4m3 (V = first 512
+    latent columns), per sequence and head."""
+    seqlens, heads, kv_scale = [777, 64, 1500], 16, 0.37
+    inp = inputs.make_mla_inputs(seqlens, heads=heads, seed=17, pad_value=float("nan"))
+    kv8 = (inp.kv_pool.float() / kv_scale).to(torch.float8_e4m3fn)
+    plan = mla.MlaDecodePlan.create(len(seqlens), heads, "cuda")
+    out, lse = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, kv_scale)
+    torch.cuda.synchronize()
+    pool = kv8.double() * kv_scale
+    for b, n in enumerate(seqlens):
+        pages = inp.block_table[b, : (n + 63) // 64].long()
+        kv = pool[pages].reshape(-1, 576)[:n]
+        q = inp.q[b, 0].double()
+        s = (q @ kv.T) * inp.scale
+        l_ref = torch.logsumexp(s, dim=1)
+        o_ref = torch.softmax(s, dim=1) @ kv[:, :512]
+        rmse = (out[b, 0].double() - o_ref).pow(2).mean().sqrt().item()
+        assert rmse <= RMSE_TOL, (b, rmse)
+        assert (lse[b, 0].double() - l_ref).abs().max().item() <= LSE_TOL
