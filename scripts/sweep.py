@@ -163,6 +163,9 @@ if __name__ == "__main__":
             measure_fp8([ctx] * 16, 16, f"fp8 config3 B=16 H=16 ctx={ctx}")
         measure_fp8(inputs.varlen_seqlens(32), 16, "fp8 config4 B=32 varlen 4K-128K")
         measure_fp8([65536] * 16, 16, "fp8 B=16 ctx=64K H=16 q_tokens=2", iters=20, q_tokens=2)
+        if "--heads" in sys.argv:
+            for h in (32, 64, 128):
+                measure_fp8([65536] * 16, h, f"fp8 B=16 ctx=64K H={h}", iters=10)
         sys.exit(0)
     if "--serving" in sys.argv:  # serving-style batches: many sequences, short-to-medium contexts
         import random
