@@ -114,5 +114,46 @@ __device__ __forceinline__ void split3(float a, float b, uint16_t (&t)[NT]) {
     t[2] = to_e4m3x2((ra - f.x * 0.0625f) * 256.f, (rb - f.y * 0.0625f) * 256.f);
 }
 
+// The three fp8 terms of 8 consecutive bf16 query values (one 16-byte vector): term t as 8
+// bytes (x = t0 + t1/16 + t2/256, exact for bf16 values in the normal range).
+__device__ __forceinline__ void quant_q_vec(const uint4 v, uint2 (&t)[NT]) {
+    const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+    uint16_t tt[4][NT];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) split3(__uint_as_float(x[k] << 16), __uint_as_float(x[k] & 0xffff0000u), tt[k]);
+#pragma unroll
+    for (int term = 0; term < NT; ++term)
+        t[term] = make_uint2(static_cast<uint32_t>(tt[0][term]) | (static_cast<uint32_t>(tt[1][term]) << 16),
+                             static_cast<uint32_t>(tt[2][term]) | (static_cast<uint32_t>(tt[3][term]) << 16));
+}
+
+// Byte offset of the 8-byte group (GEMM1 B-operand row n = term * 16 + head, vector cv of the
+// 72 per query row) in the shared-memory Q buffer: V blocks of 48 rows x 128 B (SW128), then
+// the rope block of 48 rows x 64 B (SW64).
+__device__ __forceinline__ uint32_t q_smem_off(uint32_t n, int cv) {
+    return cv < 64 ? (cv >> 4) * Q_VBLK + sw128_off(n, (cv & 15) * 8) : VCH * Q_VBLK + sw64_off(n, (cv - 64) * 8);
+}
+
+// One warp: the three terms of a work unit's 16 query rows into a global scratch slot,
+// row-major [48][576] bytes (the layout the Q3 tensor maps read); nine loads in flight.
+__device__ __forceinline__ void quant_q_global_warp(const void* __restrict__ q16, uint8_t* __restrict__ q3, int lane) {
+    constexpr int VPR = 576 / 8, PER_LANE = HGF * VPR / 32;  // 36
+#pragma unroll 1
+    for (int i0 = 0; i0 < PER_LANE; i0 += 9) {
+        uint4 v[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) v[i] = __ldg(static_cast<const uint4*>(q16) + lane + 32 * (i0 + i));
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+            const int vi = lane + 32 * (i0 + i), h = vi / VPR, cv = vi - h * VPR;
+            uint2 t[NT];
+            quant_q_vec(v[i], t);
+#pragma unroll
+            for (int term = 0; term < NT; ++term)
+                *reinterpret_cast<uint2*>(q3 + (term * HGF + h) * 576 + cv * 8) = t[term];
+        }
+    }
+}
+
 }  // namespace fp8
 }  // namespace etap_b200

@@ -966,7 +966,13 @@ constexpr int BAR_FULL = 0;                          // [NTB8] page of tile gt l
 constexpr int BAR_G2D = NTB8;                        // [NTB8] GEMM2 of tile gt complete
 constexpr int BAR_QF = 2 * NTB8, BAR_QE = 2 * NTB8 + 1;
 constexpr int BAR_SF = 2 * NTB8 + 2, BAR_SR = 2 * NTB8 + 4, BAR_PF = 2 * NTB8 + 6;  // [2] each
-constexpr int NBAR8 = 2 * NTB8 + 8;
+constexpr int NSCR = 3;                              // per-CTA scratch slots: Q terms of later splits
+constexpr int BAR_SCF = 2 * NTB8 + 8;                // [NSCR] slot written
+constexpr int BAR_SCE = BAR_SCF + NSCR;              // [NSCR] slot read (its Q landed in smem)
+constexpr int NBAR8 = BAR_SCE + NSCR;
+constexpr int QPRO_THREADS = NUM_THREADS - 64;       // warps 2..7 quantise Q in the prologue
+constexpr int QPRO_VEC = fp8::HGF * (D_QK / 8) / QPRO_THREADS;  // 16-byte vectors per thread per split
+static_assert(fp8::HGF * (D_QK / 8) % QPRO_THREADS == 0, "prologue Q split");
 constexpr int OFF_BAR = align_up(OFF_RED + RED_FLOATS * 4, 16);
 constexpr int OFF_TMEM = OFF_BAR + NBAR8 * 8;
 constexpr int OFF_SCHED = OFF_TMEM + 16;
@@ -983,7 +989,7 @@ template <bool DBG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     etap_mla_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_kv128, const __grid_constant__ CUtensorMap tm_kv64,
                                const __grid_constant__ CUtensorMap tm_q128, const __grid_constant__ CUtensorMap tm_q64,
-                               const DecodeParams prm, float kv_scale) {
+                               const DecodeParams prm, float kv_scale, uint8_t* __restrict__ q3s) {
     using namespace kfp8;
     constexpr bool kDebug = DBG;
     constexpr int HG = HG8, HH = HH8, NQ = fp8::NQ;
@@ -1012,6 +1018,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_init(&bars[BAR_SF + i], 1);
             ptx::mbar_init(&bars[BAR_SR + i], 128);
             ptx::mbar_init(&bars[BAR_PF + i], 128);
+        }
+        for (int i = 0; i < NSCR; ++i) {
+            ptx::mbar_init(&bars[BAR_SCF + i], 1);
+            ptx::mbar_init(&bars[BAR_SCE + i], 1);
         }
         ptx::fence_mbar_init();
     }
@@ -1060,12 +1070,65 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q);
     const uint32_t p_addr = ptx::smem_u32(smem + OFF_P);
     auto seqlen_of = [&](int i) { return fused ? s_len[i] : max(0, prm.seqlens[(sch[5] + i) % B]); };
+    auto q_rows = [&](const SplitDesc& sd) {
+        return static_cast<const uint4*>(prm.q) + (static_cast<size_t>(sd.b) * prm.heads + sd.g * HG) * (D_QK / 8);
+    };
+    auto scratch = [&](uint32_t slot_q) { return q3s + (static_cast<size_t>(blockIdx.x) * NSCR + slot_q) * NQ * D_QK; };
+
+    if (warp >= 2) {
+        // ---- Q terms of the CTA's first 1 + NSCR splits, while the first pages load: warps 2..7
+        // quantise the first split's Q straight into the shared-memory operand and the next
+        // NSCR splits' into this CTA's scratch slots, from which the producer loads them like
+        // any operand (there is no separate quantisation kernel in front of the decode)
+        const int pt = threadIdx.x - 64;
+        int nq = 0;
+        uint4 v[1 + NSCR][QPRO_VEC];
+        {
+            int vb = vb_begin;
+#pragma unroll
+            for (int j = 0; j < 1 + NSCR; ++j) {  // the next split with tiles, loads in flight
+                SplitDesc sd;
+                bool found = false;
+                for (; vb <= vb_end && !found; ++vb) found = split_at(sch, seqlen_of(vb), B, vb, sd);
+                if (found) {
+                    nq = j + 1;
+                    const uint4* src = q_rows(sd);
+#pragma unroll
+                    for (int i = 0; i < QPRO_VEC; ++i) v[j][i] = __ldg(src + pt + QPRO_THREADS * i);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 1 + NSCR; ++j) {
+            if (j >= nq) break;
+#pragma unroll
+            for (int i = 0; i < QPRO_VEC; ++i) {
+                const int vi = pt + QPRO_THREADS * i, h = vi / (D_QK / 8), cv = vi - h * (D_QK / 8);
+                uint2 t[fp8::NT];
+                fp8::quant_q_vec(v[j][i], t);
+#pragma unroll
+                for (int term = 0; term < fp8::NT; ++term) {
+                    if (j == 0)
+                        *reinterpret_cast<uint2*>(smem + OFF_Q + fp8::q_smem_off(term * HG + h, cv)) = t[term];
+                    else
+                        *reinterpret_cast<uint2*>(scratch(j - 1) + (term * HG + h) * D_QK + cv * 8) = t[term];
+                }
+            }
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::fence_proxy_async_global();
+        ptx::named_bar_sync(5, QPRO_THREADS);
+        if (pt == 0) {
+            if (nq > 0) ptx::mbar_arrive(&bars[BAR_QF]);
+            for (int j = 1; j < nq; ++j) ptx::mbar_arrive(&bars[BAR_SCF + j - 1]);
+        }
+    }
 
     if (warp == 0) {
         // ===================================================== TMA producer
         const bool kv_shared = line_shape(B, prm.groups, gridDim.x, prm.lanes_on != 0).lanes > 1;
         const uint64_t pol_kv = kv_shared ? ptx::policy_evict_normal() : ptx::policy_evict_first();
-        const uint64_t pol_q = ptx::policy_evict_last();
+        const uint64_t pol_q = ptx::policy_evict_first();
         uint32_t gt = 0, nsplit = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
@@ -1075,7 +1138,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int pg;
             if (nsplit == 0 && sd.b == hint_b && sd.t0 == hint_t0) pg = hint_pg;  // loaded already
             else pg = (base + lane < sd.t1) ? __ldg(bt + base + lane) : 0;
-            bool q_pending = true;
+            bool q_pending = nsplit > 0;  // the first split's Q terms come from the prologue
             for (int t = sd.t0; t < sd.t1; ++t) {
                 if (t - base >= 32) {
                     base = t;
@@ -1097,11 +1160,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
                 __syncwarp();
                 if (q_pending) {
+                    // a later split's Q terms from the scratch slot the prologue (or warp 3) filled,
+                    // once GEMM1 of the previous split's last tile released the buffer
                     q_pending = false;
-                    if (nsplit > 0) ptx::mbar_wait(&bars[BAR_QE], (nsplit - 1) & 1);
+                    const uint32_t slot_q = (nsplit - 1) % NSCR;
+                    ptx::mbar_wait(&bars[BAR_QE], (nsplit - 1) & 1);
+                    ptx::mbar_wait(&bars[BAR_SCF + slot_q], ((nsplit - 1) / NSCR) & 1);
                     if (lane == 0) {
                         ptx::mbar_arrive_expect_tx(&bars[BAR_QF], fp8::Q_BYTES);
-                        const int qrow = (sd.b * prm.groups + sd.g) * NQ;  // three-term Q of (b, g)
+                        const int qrow = (blockIdx.x * NSCR + slot_q) * NQ;
 #pragma unroll 1
                         for (int c = 0; c < fp8::VCH; ++c)
                             ptx::tma_load_2d(smem + OFF_Q + c * fp8::Q_VBLK, &tm_q128, &bars[BAR_QF], c * 128, qrow,
@@ -1109,10 +1176,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         ptx::tma_load_2d(smem + OFF_Q + fp8::VCH * fp8::Q_VBLK, &tm_q64, &bars[BAR_QF], 512, qrow, pol_q);
                     }
                     __syncwarp();
-                    ++nsplit;
                 }
                 ++gt;
             }
+            ++nsplit;
         }
     } else if (warp == 1) {
         // ===================================================== GEMM1 issuer
@@ -1121,6 +1188,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             SplitDesc sd;
             if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
             ptx::mbar_wait(&bars[BAR_QF], nsplit & 1);
+            if (nsplit > 0 && lane == 0) ptx::mbar_arrive(&bars[BAR_SCE + (nsplit - 1) % NSCR]);  // slot read
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
                 if (gt >= 2) ptx::mbar_wait(&bars[BAR_SR + buf], ((gt >> 1) - 1) & 1);
@@ -1157,6 +1225,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ETAP_TRACE(prm, gt, 7);
                 ++gt;
             }
+        }
+    } else if (warp == 3) {
+        // ===================================================== Q terms of splits past 1 + NSCR
+        // (many short sequences per CTA): into scratch slot (j-1) % NSCR once GEMM1 saw the Q
+        // that slot held land in shared memory
+        uint32_t j = 0;
+        for (int vb = vb_begin; vb <= vb_end; ++vb) {
+            SplitDesc sd;
+            if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
+            if (j > NSCR) {
+                const uint32_t slot_q = (j - 1) % NSCR, u = (j - 1) / NSCR;
+                ptx::mbar_wait(&bars[BAR_SCE + slot_q], (u - 1) & 1);
+                fp8::quant_q_global_warp(q_rows(sd), scratch(slot_q), lane);
+                ptx::fence_proxy_async_global();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&bars[BAR_SCF + slot_q]);
+            }
+            ++j;
         }
     } else if (warp >= SOFTMAX_WARP0) {
         // ===================================================== softmax + epilogue (128 threads)
@@ -1386,25 +1472,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, TMEM_COLS);
     }
-}
-
-// Three fp8 terms of every head's query row: Q3[(b * groups + g) * 48 + term * 16 + h][c]
-// from Q[b][g * 16 + h][c] (bf16); one thread per (row pair element).
-__global__ void __launch_bounds__(256) etap_fp8_quant_q_kernel(const __nv_bfloat16* __restrict__ q, uint8_t* __restrict__ q3,
-                                                               int rows_total, int groups) {
-    ptx::grid_dep_wait();
-    ptx::grid_dep_launch();
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (row, column pair)
-    if (i >= static_cast<int64_t>(rows_total) * (D_QK / 2)) return;
-    const int r = static_cast<int>(i / (D_QK / 2)), c = static_cast<int>(i % (D_QK / 2)) * 2;
-    const int b = r / (groups * 16), rem = r % (groups * 16), g = rem / 16, h = rem % 16;
-    const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(q + static_cast<size_t>(r) * D_QK + c);
-    uint16_t t[fp8::NT];
-    fp8::split3(__bfloat162float(v.x), __bfloat162float(v.y), t);
-    const size_t base = static_cast<size_t>(b * groups + g) * fp8::NQ;
-#pragma unroll
-    for (int term = 0; term < fp8::NT; ++term)
-        *reinterpret_cast<uint16_t*>(q3 + (base + term * 16 + h) * D_QK + c) = t[term];
 }
 
 // =============================================================================================
@@ -1810,15 +1877,16 @@ size_t max_partials(int batch, int heads, int num_sm_parts) {
 }
 
 // workspace layout: partial O [np][hg][512] fp32, partial LSE [np][hg] fp32, then (1 KB
-// aligned) the three fp8 terms of Q for the FP8 path, [batch * heads / 16][48][576] bytes.
-// A work unit of 16 heads needs no more partial space than one of 32 (np * hg grows with hg).
+// aligned) the FP8 path's per-CTA scratch for the three fp8 terms of Q of later splits,
+// [num_sm_parts][NSCR][48][576] bytes. A work unit of 16 heads needs no more partial space
+// than one of 32 (np * hg grows with hg).
 size_t q3_offset(int batch, int heads, int num_sm_parts) {
     const size_t np = max_partials(batch, heads, num_sm_parts);
     const size_t hg = head_group_of(heads);
     return (np * hg * D_V * sizeof(float) + np * hg * sizeof(float) + 1023) / 1024 * 1024;
 }
-size_t q3_bytes(int batch, int heads) {
-    return static_cast<size_t>(batch) * (heads / 16) * fp8::NQ * D_QK;
+size_t q3_bytes(int num_sm_parts) {
+    return static_cast<size_t>(num_sm_parts) * kfp8::NSCR * fp8::NQ * D_QK;
 }
 
 }  // namespace
@@ -1899,7 +1967,7 @@ int etap_mla_sched_ints(int batch, int heads, int num_sm_parts, size_t* sched_in
 int etap_mla_workspace_bytes(int batch, int heads, int num_sm_parts, size_t* bytes) {
     if (batch < 1 || !heads_ok(heads) || num_sm_parts < 1 || !bytes)
         return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
-    *bytes = q3_offset(batch, heads, num_sm_parts) + q3_bytes(batch, heads);
+    *bytes = q3_offset(batch, heads, num_sm_parts) + q3_bytes(num_sm_parts);
     return ETAP_OK;
 }
 
@@ -2191,7 +2259,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     uint8_t* q3 = static_cast<uint8_t*>(workspace) + q3_offset(batch, heads, num_sm_parts);
     CUtensorMap tm_kv128, tm_kv64, tm_q128, tm_q64;
     const uint64_t pool_rows = static_cast<uint64_t>(num_pages) * PAGE;
-    const uint64_t q3_rows = static_cast<uint64_t>(batch) * groups * fp8::NQ;
+    const uint64_t q3_rows = static_cast<uint64_t>(num_sm_parts) * kfp8::NSCR * fp8::NQ;
     if (int rc = cached_map_u8(&tm_kv128, kv_pool8, pool_rows, 128, PAGE)) return rc;
     if (int rc = cached_map_u8(&tm_kv64, kv_pool8, pool_rows, 64, PAGE)) return rc;
     if (int rc = cached_map_u8(&tm_q128, q3, q3_rows, 128, fp8::NQ)) return rc;
@@ -2231,18 +2299,6 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    // three fp8 terms of Q into the workspace
-    {
-        cudaLaunchConfig_t cfg = {};
-        const int64_t n = static_cast<int64_t>(batch) * heads * (D_QK / 2);
-        cfg.gridDim = dim3(static_cast<unsigned>((n + 255) / 256));
-        cfg.blockDim = dim3(256);
-        cfg.stream = st;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_fp8_quant_q_kernel, static_cast<const __nv_bfloat16*>(q), q3,
-                                     batch * heads, groups));
-    }
     if (!prm.inkernel_sched)
         if (int rc = metadata_launch(seqlens, batch, groups, num_sm_parts, const_cast<int32_t*>(sched),
                                      const_cast<int32_t*>(split_off), stream, FP8_FIXED_COST))
@@ -2260,7 +2316,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
         static int attr_rc = ensure_smem_attr(etap_mla_decode_fp8_kernel<false>, kfp8::SMEM_ALLOC) |
                              ensure_smem_attr(etap_mla_decode_fp8_kernel<true>, kfp8::SMEM_ALLOC);
         if (attr_rc) return attr_rc;
-        ETAP_CUDA(cudaLaunchKernelEx(&cfg, kern, tm_kv128, tm_kv64, tm_q128, tm_q64, prm, kv_scale));
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, kern, tm_kv128, tm_kv64, tm_q128, tm_q64, prm, kv_scale, q3));
     }
     if (flags & ETAP_FLAG_SKIP_COMBINE) return ETAP_OK;
     const bool closed_form = prm.inkernel_sched && ls.line_n <= 32;
