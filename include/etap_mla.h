@@ -123,12 +123,13 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
 
 /* K2-FP8 + K3 — the same decode on an FP8 (e4m3) latent cache: kv_pool8 [pages][64][576]
  * e4m3 bytes, dequantised value = kv_scale * e4m3 (per-tensor scale > 0). q stays bf16; the
- * kernel splits it into three fp8 terms (exact for bf16 values in the normal range) and P
- * into three fp8 terms (about 12 significant bits), so both contractions run as
- * kind::f8f6f4 UMMAs straight on the fp8 page (no dequantising pass); fp32 accumulation, fp32
- * O / LSE. Same sizing, schedule and workspace as etap_mla_decode (16 heads per work unit;
- * the workspace also holds the fp8 terms of Q). External schedules (ETAP_FLAG_EXTERNAL_SCHEDULE)
- * and the rescale fault flag are not supported here. */
+ * kernel itself splits it into three fp8 terms (exact for bf16 values in the normal range)
+ * and P into three fp8 terms (about 12 significant bits), so both contractions run as
+ * kind::f8f6f4 UMMAs straight on the fp8 page (no dequantising pass, no extra kernel); fp32
+ * accumulation, fp32 O / LSE. Same sizing, schedule and workspace as etap_mla_decode (16 heads
+ * per work unit; the workspace also holds per-CTA scratch for the fp8 terms of later splits'
+ * Q). External schedules (ETAP_FLAG_EXTERNAL_SCHEDULE) and the rescale fault flag are not
+ * supported here. */
 int etap_mla_decode_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t num_pages,
                         const int32_t* block_table, int max_pages_per_seq, const int32_t* seqlens,
                         int batch, int q_tokens, int heads, float scale, int causal,
