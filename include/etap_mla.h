@@ -73,6 +73,16 @@ extern "C" {
                                        batch*heads/head_group <= 256 (K1 off the per-step
                                        critical path); above 256 virtual sequences
                                        etap_mla_decode launches K1 itself first. */
+#define ETAP_FLAG_DEP_METADATA 16u  /* seqlens / block_table are written by the kernel launched
+                                       immediately before this decode on the stream. By default
+                                       the decode kernels launch with programmatic dependent
+                                       launch and read seqlens and block_table (never KV or Q)
+                                       BEFORE that kernel has finished, so the split schedule
+                                       and the first page ids are ready when it does; the
+                                       preceding kernel must therefore not write them (host
+                                       copies, kernels without programmatic launch and all of
+                                       this library's kernels satisfy this). With this flag
+                                       both are read only after the dependency resolves. */
 
 /* Thread-local description of the last error. Never NULL. */
 const char* etap_mla_last_error(void);

@@ -22,6 +22,7 @@ FLAG_NEGATE_RESCALE = 1
 FLAG_EAGER_RESCALE = 2
 FLAG_SKIP_COMBINE = 4
 FLAG_EXTERNAL_SCHEDULE = 8
+FLAG_DEP_METADATA = 16  # seqlens / block_table come from the preceding kernel (etap_mla.h)
 
 _lib = None
 

@@ -215,7 +215,8 @@ __device__ __forceinline__ int cta_excl_scan256(int v, int* s_wt, int& total) {
 // iff (k+1)T > P[i]+F and kT < P[i+1]) -> split offsets -> this CTA's range. Identical output
 // to K1 (GPU test); CTA 0 publishes split_off for the combine kernel, every CTA its sched row.
 __device__ void schedule_own_range(const DecodeParams& prm, const LineShape& ls, const int* s_pref,
-                                   const int* s_soff, const int* s_tiles, int* s_sched, int total, int T) {
+                                   const int* s_soff, const int* s_tiles, int* s_sched, int total, int T,
+                                   bool publish) {
     const int n = ls.line_n;
     const int lane = blockIdx.x / ls.p_line, k = blockIdx.x - lane * ls.p_line;
     auto map = [&](int x, int& vb, int& t) {
@@ -240,6 +241,7 @@ __device__ void schedule_own_range(const DecodeParams& prm, const LineShape& ls,
     s_sched[5] = min(lane, ls.lanes - 1) * n;         // virtual-sequence offset of the lane
     s_sched[6] = min(lane, ls.lanes - 1) * s_soff[n];  // partial-index offset of the lane
     s_sched[7] = 0;
+    if (!publish) return;
     int32_t* g = prm.sched_out + blockIdx.x * SCHED_INTS;
     for (int i = 0; i < SCHED_INTS; ++i) g[i] = s_sched[i];
 }
@@ -259,7 +261,7 @@ __device__ __forceinline__ void publish_split_off(const DecodeParams& prm, const
 // searches, so the producer can issue its first loads a few hundred cycles earlier.
 // Same output as schedule_own_range / K1 (GPU test).
 __device__ void inkernel_schedule_warp(const DecodeParams& prm, const LineShape& ls, int* s_soff,
-                                       int* s_len, int* s_sched) {
+                                       int* s_len, int* s_sched, bool publish) {
     const int n = ls.line_n;
     const int lane = threadIdx.x & 31;
     const bool live = lane < n;
@@ -317,12 +319,21 @@ __device__ void inkernel_schedule_warp(const DecodeParams& prm, const LineShape&
     if (lane == 31) s_soff[n] = so;
     __syncwarp();
     // published for the combine kernel and external readers (not read back by this CTA)
+    if (!publish) return;
     if (lane < SCHED_INTS) prm.sched_out[blockIdx.x * SCHED_INTS + lane] = s_sched[lane];
     if (blockIdx.x == 0) publish_split_off(prm, ls, s_soff, lane, 32);
 }
 
+// The schedule computed before the grid dependency (DecodeParams::early_meta) is published
+// only after it: the previous step's combine may still read split_off until then.
+__device__ __forceinline__ void publish_schedule(const DecodeParams& prm, const LineShape& ls, const int* s_soff,
+                                                 const int* s_sched, int tid, int nthreads) {
+    if (tid < SCHED_INTS) prm.sched_out[blockIdx.x * SCHED_INTS + tid] = s_sched[tid];
+    if (blockIdx.x == 0) publish_split_off(prm, ls, s_soff, tid, nthreads);
+}
+
 __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, int* s_pref, int* s_soff,
-                                  int* s_tiles, int* s_len, int* s_sched, int* s_wt) {
+                                  int* s_tiles, int* s_len, int* s_sched, int* s_wt, bool publish) {
     const int n = ls.line_n;
     const int tid = threadIdx.x;
     int tiles = 0, cost = 0;
@@ -350,8 +361,8 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
     if (tid < n) s_soff[tid] = so;
     if (tid == 0) s_soff[n] = nsplits;
     __syncthreads();
-    if (tid == 0) schedule_own_range(prm, ls, s_pref, s_soff, s_tiles, s_sched, total, T);
-    if (blockIdx.x == 0) publish_split_off(prm, ls, s_soff, tid, blockDim.x);
+    if (tid == 0) schedule_own_range(prm, ls, s_pref, s_soff, s_tiles, s_sched, total, T, publish);
+    if (publish && blockIdx.x == 0) publish_split_off(prm, ls, s_soff, tid, blockDim.x);
     __syncthreads();
 }
 
@@ -408,6 +419,114 @@ __device__ __forceinline__ bool split_at(const int32_t* sch, int seqlen, int bat
     return d.t0 < d.t1;
 }
 
+// Split schedule and the producer's first page ids, around the grid dependency (all threads).
+// With early_meta (default; ETAP_FLAG_DEP_METADATA turns it off) seqlens and block_table are
+// read BEFORE griddepcontrol.wait: the API requires that the kernel immediately before the
+// decode in the stream does not write them (none of this library's kernels does; host copies
+// and kernels without programmatic launch are ordered anyway). The dependency then gates only
+// the KV / Q loads and every global write: the schedule is published after it (the previous
+// step's combine may still read split_off), and the producer's first TMA goes out right after
+// it with its page ids already in registers. Without early_meta the previous call's range
+// serves as an L2 prefetch guess and the schedule is computed after the dependency.
+struct Prologue {
+    const int32_t* sch;
+    const int32_t* soff;
+    const int* s_len;
+    int idx_off;
+    int hint_b, hint_t0, hint_pg;  // (b, first tile) of the producer's first split, its first 32 page ids
+    bool late_wait;                // warp 0 has not waited for the grid dependency yet
+};
+
+// The producer's grid-dependency wait when decode_prologue deferred it (whole warp 0).
+template <bool kDebug>
+__device__ __forceinline__ void dep_wait_producer(const DecodeParams& prm) {
+    ptx::grid_dep_wait();
+    ptx::grid_dep_launch();
+    if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
+}
+
+template <bool kDebug>
+__device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uint8_t* sched_smem, int hg,
+                                                    uint32_t page_bytes, bool q_rows, int warp, int lane) {
+    int* s_pref = reinterpret_cast<int*>(sched_smem);
+    int* s_soff = s_pref + MAX_FUSED_VB + 1;
+    int* s_tiles = s_soff + MAX_FUSED_VB + 1;
+    int* s_len = s_tiles + MAX_FUSED_VB;
+    int* s_sched = s_len + MAX_FUSED_VB;
+    const bool fused = prm.inkernel_sched != 0;
+    const bool early = fused && prm.early_meta != 0;
+    Prologue r{};
+    r.s_len = s_len;
+    r.hint_b = -1;
+    LineShape ls{};
+    if (fused) ls = line_shape(prm.batch, prm.groups, gridDim.x, prm.lanes_on != 0);
+    auto schedule = [&](bool publish) {
+        if (ls.line_n <= 32) {
+            if (warp == 0) inkernel_schedule_warp(prm, ls, s_soff, s_len, s_sched, publish);
+            __syncthreads();
+        } else {
+            inkernel_schedule(prm, ls, s_pref, s_soff, s_tiles, s_len, s_sched, s_sched + 8, publish);
+        }
+    };
+    if (early) {
+        schedule(false);
+        if (warp == 0) {
+            for (int vb = s_sched[0]; vb <= s_sched[2]; ++vb) {
+                SplitDesc sd;
+                if (!split_at(s_sched, s_len[vb], prm.batch, vb, sd)) continue;
+                r.hint_b = sd.b;
+                r.hint_t0 = sd.t0;
+                r.hint_pg = (sd.t0 + lane < sd.t1) ? __ldg(prm.block_table + static_cast<size_t>(sd.b) * prm.max_pages +
+                                                           sd.t0 + lane) : 0;
+#ifndef ETAP_NO_PREFETCH_HINT
+                // L2 warm-up only: the bytes used are loaded by TMA after the dependency
+                if (lane < ETAP_HINT_PAGES && sd.t0 + lane < sd.t1 && r.hint_pg >= 0 && r.hint_pg < prm.num_pages)
+                    ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) +
+                                              static_cast<size_t>(r.hint_pg) * page_bytes, page_bytes);
+                if (q_rows && lane == 0)
+                    ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.q) +
+                                              (static_cast<size_t>(sd.b) * prm.heads + sd.g * hg) * D_QK * 2,
+                                          hg * D_QK * 2);
+#endif
+                break;
+            }
+        }
+    } else if (warp == 0) {
+        prev_range_hint(prm, hg, page_bytes, q_rows, lane, r.hint_b, r.hint_t0);
+    }
+    // With early_meta the producer warp (warp 0) has nothing left to do before its first TMA:
+    // it waits for the dependency itself, right before issuing it (dep_wait_producer), with
+    // the issue path already fetched and its page ids in registers.
+    r.late_wait = early;
+    if (!(early && warp == 0)) {
+        ptx::grid_dep_wait();     // KV / Q and the outputs of earlier kernels in the stream
+        ptx::grid_dep_launch();   // let the combine kernel get scheduled
+    }
+    if (!early) {
+        // the first page ids for the guessed range go out together with the seqlens loads of
+        // the schedule (used only if the schedule confirms the guess)
+        if (warp == 0 && r.hint_b >= 0 && r.hint_t0 + lane < prm.max_pages)
+            r.hint_pg = prm.block_table[static_cast<size_t>(r.hint_b) * prm.max_pages + r.hint_t0 + lane];
+    }
+    if (threadIdx.x == 0 && !early) { ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
+    if (fused) {
+        if (early) {
+            if (warp == 3) publish_schedule(prm, ls, s_soff, s_sched, lane, 32);
+        } else {
+            schedule(true);
+        }
+        r.sch = s_sched;
+        r.soff = s_soff;  // line-local split offsets
+        r.idx_off = s_sched[6];
+    } else {
+        r.sch = prm.sched + blockIdx.x * SCHED_INTS;
+        r.soff = prm.split_off + r.sch[5];  // indexed by line position like the fused copy
+        r.idx_off = 0;
+    }
+    if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 1); ETAP_TRACE_CLK(prm, 14); }
+    return r;
+}
+
 template <int HG_, bool DBG>
 __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
     etap_mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv,
@@ -455,42 +574,14 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    // (b, first tile) of this CTA's range in the previous call: a guess for this call
-    int hint_b = -1, hint_t0 = 0;
-    if (warp == 0) prev_range_hint(prm, HG, PAGE * D_QK * 2, true, lane, hint_b, hint_t0);
-    ptx::grid_dep_wait();     // inputs / schedule written by earlier kernels in the stream
-    ptx::grid_dep_launch();   // let the combine kernel get scheduled
-    // the producer's first page ids for the guessed range go out together with the seqlens
-    // loads of the schedule (used only if the schedule confirms the guess)
-    int hint_pg = 0;
-    if (warp == 0 && hint_b >= 0 && hint_t0 + lane < prm.max_pages)
-        hint_pg = prm.block_table[static_cast<size_t>(hint_b) * prm.max_pages + hint_t0 + lane];
-    if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
-    const int32_t* sch;
-    const int32_t* soff;      // split offsets per virtual sequence
-    int* s_pref = reinterpret_cast<int*>(smem + C::OFF_SCHED);
-    int* s_soff = s_pref + MAX_FUSED_VB + 1;
-    int* s_tiles = s_soff + MAX_FUSED_VB + 1;
-    int* s_len = s_tiles + MAX_FUSED_VB;
-    int* s_sched = s_len + MAX_FUSED_VB;
+    // split schedule + the producer's first page ids, around the grid dependency
+    const Prologue pro = decode_prologue<kDebug>(prm, smem + C::OFF_SCHED, HG, PAGE * D_QK * 2, true, warp, lane);
+    const int32_t* sch = pro.sch;
+    const int32_t* soff = pro.soff;  // split offsets per virtual sequence
+    const int idx_off = pro.idx_off; // partial-index offset of this CTA's lane (fused schedule)
+    const int hint_b = pro.hint_b, hint_t0 = pro.hint_t0, hint_pg = pro.hint_pg;
     const bool fused = prm.inkernel_sched != 0;
-    int idx_off = 0;          // partial-index offset of this CTA's lane (fused schedule)
-    if (fused) {
-        const LineShape ls = line_shape(prm.batch, prm.groups, gridDim.x, prm.lanes_on != 0);
-        if (ls.line_n <= 32) {
-            if (warp == 0) inkernel_schedule_warp(prm, ls, s_soff, s_len, s_sched);
-            __syncthreads();
-        } else {
-            inkernel_schedule(prm, ls, s_pref, s_soff, s_tiles, s_len, s_sched, s_sched + 8);
-        }
-        sch = s_sched;
-        soff = s_soff;        // line-local split offsets
-        idx_off = sch[6];
-    } else {
-        sch = prm.sched + blockIdx.x * SCHED_INTS;
-        soff = prm.split_off + sch[5];  // indexed by line position like the fused copy
-    }
-    if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 1); ETAP_TRACE_CLK(prm, 14); }
+    const int* s_len = pro.s_len;
 
     const int vb_begin = sch[0], vb_end = sch[2];  // line positions (vb = sch[5] + position)
     const int B = prm.batch;
@@ -529,6 +620,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 const int page = __shfl_sync(0xffffffffu, pg, t - base);
                 const uint32_t tb = gt % NTB;
                 const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
+                if (gt == 0 && pro.late_wait) dep_wait_producer<kDebug>(prm);
                 if (gt >= 3) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 3) % NTB], ((gt - 3) / NTB) & 1);
                 if (lane == 0) {
                     if (gt == 0) { ETAP_TRACE_G(prm, 9); ETAP_TRACE_CLK(prm, 15); }
@@ -593,6 +685,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 ++gt;
             }
         }
+        if (gt == 0 && pro.late_wait) dep_wait_producer<kDebug>(prm);  // no tiles in this CTA's range
     } else if (warp == 1) {
         // ===================================================== GEMM1 issuer (whole warp, elect)
         uint32_t gt = 0, nsplit = 0;
@@ -1030,40 +1123,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    int hint_b = -1, hint_t0 = 0;  // guessed from the previous call, see prev_range_hint
-    if (warp == 0) prev_range_hint(prm, HG, PAGE * D_QK, false, lane, hint_b, hint_t0);
-    ptx::grid_dep_wait();
-    ptx::grid_dep_launch();
-    int hint_pg = 0;  // the producer's first page ids of the guessed range, beside the seqlens loads
-    if (warp == 0 && hint_b >= 0 && hint_t0 + lane < prm.max_pages)
-        hint_pg = prm.block_table[static_cast<size_t>(hint_b) * prm.max_pages + hint_t0 + lane];
-    if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
-
-    int* s_pref = reinterpret_cast<int*>(smem + OFF_SCHED);
-    int* s_soff = s_pref + MAX_FUSED_VB + 1;
-    int* s_tiles = s_soff + MAX_FUSED_VB + 1;
-    int* s_len = s_tiles + MAX_FUSED_VB;
-    int* s_sched = s_len + MAX_FUSED_VB;
+    const Prologue pro = decode_prologue<kDebug>(prm, smem + OFF_SCHED, HG, PAGE * D_QK, false, warp, lane);
+    const int32_t* sch = pro.sch;
+    const int32_t* soff = pro.soff;
+    const int idx_off = pro.idx_off;
+    const int hint_b = pro.hint_b, hint_t0 = pro.hint_t0, hint_pg = pro.hint_pg;
     const bool fused = prm.inkernel_sched != 0;
-    const int32_t* sch;
-    const int32_t* soff;
-    int idx_off = 0;
-    if (fused) {
-        const LineShape ls = line_shape(prm.batch, prm.groups, gridDim.x, prm.lanes_on != 0);
-        if (ls.line_n <= 32) {
-            if (warp == 0) inkernel_schedule_warp(prm, ls, s_soff, s_len, s_sched);
-            __syncthreads();
-        } else {
-            inkernel_schedule(prm, ls, s_pref, s_soff, s_tiles, s_len, s_sched, s_sched + 8);
-        }
-        sch = s_sched;
-        soff = s_soff;
-        idx_off = sch[6];
-    } else {
-        sch = prm.sched + blockIdx.x * SCHED_INTS;
-        soff = prm.split_off + sch[5];
-    }
-    if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 1); ETAP_TRACE_CLK(prm, 14); }
+    const int* s_len = pro.s_len;
     const int vb_begin = sch[0], vb_end = sch[2];
     const int B = prm.batch;
     const uint32_t ring_addr = ptx::smem_u32(smem + OFF_RING);
@@ -1145,6 +1211,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     pg = (base + lane < sd.t1) ? __ldg(bt + base + lane) : 0;
                 }
                 const int page = __shfl_sync(0xffffffffu, pg, t - base);
+                if (gt == 0 && pro.late_wait) dep_wait_producer<kDebug>(prm);
                 if (gt >= NPS) ptx::mbar_wait(&bars[BAR_G2D + (gt - NPS) % NTB8], ((gt - NPS) / NTB8) & 1);
                 if (lane == 0) {
                     if (gt == 0) { ETAP_TRACE_G(prm, 9); ETAP_TRACE_CLK(prm, 15); }
@@ -1181,6 +1248,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             ++nsplit;
         }
+        if (gt == 0 && pro.late_wait) dep_wait_producer<kDebug>(prm);  // no tiles in this CTA's range
     } else if (warp == 1) {
         // ===================================================== GEMM1 issuer
         uint32_t gt = 0, nsplit = 0;
@@ -1872,6 +1940,16 @@ bool lanes_enabled() {
     return on;
 }
 
+// Schedule before the grid dependency (DecodeParams::early_meta); ETAP_EARLY_META=0 in the
+// environment disables it for A/B runs (same as ETAP_FLAG_DEP_METADATA on every call).
+bool early_meta_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("ETAP_EARLY_META");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 size_t max_partials(int batch, int heads, int num_sm_parts) {
     return static_cast<size_t>(num_sm_parts) + static_cast<size_t>(batch) * (heads / head_group_of(heads));
 }
@@ -2172,6 +2250,7 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     prm.lanes_on = lanes_enabled() ? 1 : 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
     prm.inkernel_sched = (ls.line_n <= MAX_FUSED_VB && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
+    prm.early_meta = (early_meta_enabled() && !(flags & ETAP_FLAG_DEP_METADATA)) ? 1 : 0;
     prm.fixed_cost = META_FIXED_COST;
     if (!prm.inkernel_sched && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) {
         // too many virtual sequences for the fused prologue: run K1 first on the same stream
@@ -2288,6 +2367,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     prm.lanes_on = lanes_enabled() ? 1 : 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
     prm.inkernel_sched = ls.line_n <= MAX_FUSED_VB ? 1 : 0;
+    prm.early_meta = (early_meta_enabled() && !(flags & ETAP_FLAG_DEP_METADATA)) ? 1 : 0;
     prm.fixed_cost = FP8_FIXED_COST;
     prm.scale_log2 = scale * kv_scale * 1.4426950408889634f;
     prm.flags = flags;

@@ -333,6 +333,7 @@ struct DecodeParams {
     int heads_per_token;
     int causal;           // q_tokens > 1: token j sees KV rows [0, seqlen - q_tokens + j]
     int inkernel_sched;  // 1: compute the split schedule in the prologue (and publish it)
+    int early_meta;      // 1: read seqlens / block_table before the grid dependency (decode_prologue)
     int fixed_cost;      // per-split overhead in tile units of the split schedule
     int lanes_on;        // head-group lanes enabled (line_shape)
     float scale_log2;

@@ -12,8 +12,8 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import (FLAG_EAGER_RESCALE, FLAG_EXTERNAL_SCHEDULE, FLAG_NEGATE_RESCALE,  # noqa: F401
-                   FLAG_SKIP_COMBINE, check)
+from ._lib import (FLAG_DEP_METADATA, FLAG_EAGER_RESCALE, FLAG_EXTERNAL_SCHEDULE,  # noqa: F401
+                   FLAG_NEGATE_RESCALE, FLAG_SKIP_COMBINE, check)
 
 D_QK = 576
 D_V = 512

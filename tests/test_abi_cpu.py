@@ -35,6 +35,18 @@ def test_library_exports_every_declared_symbol():
     assert set(syms) <= exported
 
 
+def test_python_constants_match_the_header():
+    text = (ROOT / "include" / "etap_mla.h").read_text()
+    consts = {k: int(v) for k, v in re.findall(r"#define (ETAP_(?:FLAG|ERR|OK)\w*)\s+(\d+)u?", text)}
+    assert consts["ETAP_OK"] == _lib.ETAP_OK
+    assert consts["ETAP_ERR_SHAPE"] == _lib.ETAP_ERR_SHAPE and consts["ETAP_ERR_CUDA"] == _lib.ETAP_ERR_CUDA
+    flags = {k[len("ETAP_FLAG_"):]: v for k, v in consts.items() if k.startswith("ETAP_FLAG_")}
+    assert len(flags) >= 5
+    for name, v in flags.items():
+        assert getattr(_lib, "FLAG_" + name) == v, name
+    assert len(set(flags.values())) == len(flags)
+
+
 def test_library_targets_sm100a_only():
     out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True)
     if out.returncode != 0:
