@@ -469,6 +469,13 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
         }
     };
     if (early) {
+        // warp 2 (idle until the first tile) warms L2 with the previous call's first pages while
+        // warp 0 computes this call's schedule (matters when nothing overlaps the prologue,
+        // e.g. the first node of a CUDA graph replay)
+        if (warp == 2) {
+            int gb = -1, gt0 = 0;
+            prev_range_hint(prm, hg, page_bytes, q_rows, lane, gb, gt0);
+        }
         schedule(false);
         if (warp == 0) {
             for (int vb = s_sched[0]; vb <= s_sched[2]; ++vb) {
