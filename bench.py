@@ -8,7 +8,9 @@ Workload (BASELINE.json configs[1]): MLA decode, B=16 sequences x 64K latent-KV 
 16 heads per GPU, d_qk=576 / d_v=512, bf16 paged KV (64-row pages), fp32 O + LSE.
 A step = K2 (transposed tcgen05 pipeline; it computes the K1 split-KV schedule in its
 prologue) + K3 (LSE combine) on inputs resident in HBM; with N > 1 GPUs every rank owns 16 of the 16*N heads (KV replicated)
-and the step ends with an NCCL all-gather of O (weak scaling).
+and the step ends with the all-gather of O, fused into K2/K3 stores over NVLink peer memory (NCCL
+all-gather when peer access is missing); weak scaling, SURVEY.md §8e. `e2e` is the same step with
+host buffers: the C-ABI etap_mla_host_decode at N=1, the Python API on every rank at N > 1.
 Inputs (1.2 GB of KV) exceed the 126 MB L2, so no flush is needed between steps.
 """
 from __future__ import annotations
@@ -314,11 +316,21 @@ def run_ours(args) -> None:
     achieved = nbytes / (k2_avg_ms * 1e-3) / 1e9
     traffic = ncu_traffic()
 
+    # N > 1 e2e: every rank, through the Python API, with host buffers (all ranks take part)
+    e2e_multi = None
+    if world > 1 and args.e2e_steps > 0:
+        def run_step(q, kv, bt, sl):
+            if gather == "peer":
+                return pg.decode(plan, q, kv, bt, sl, inp.scale)
+            plan.decode(q, kv, bt, sl, inp.scale, out=out, lse=lse)
+            return sharding.gather_heads(out), sharding.gather_heads(lse)
+        e2e_multi = e2e_ranks(inp, args.e2e_steps, dev, run_step, barrier, world)
+
     result = {}
     if rank == 0:
         clocks = clk.summary()
         # e2e: the reference-facing C-ABI call with HOST buffers (H2D + K1/K2/K3 + D2H per step)
-        e2e = e2e_serving = None
+        e2e, e2e_serving = e2e_multi, None
         if world == 1 and args.e2e_steps > 0:
             e2e = e2e_host(inp, args.e2e_steps, dev)
             # serving-style step (cache resident in HBM): reported beside e2e, not instead
@@ -404,6 +416,47 @@ def e2e_host(inp, steps: int, dev) -> dict:
             "api": "etap_mla_host_decode (C-ABI, pinned host buffers, synchronous)", "steps": steps,
             "bound": {"kind": "pcie_h2d", "measured_h2d_gbs": h2d_gbs,
                       "bound_us": (h2d + d2h) / h2d_gbs / 1e3, "frac": (h2d + d2h) / h2d_gbs / 1e3 / (dt * 1e6)}}
+
+
+def e2e_ranks(inp, steps: int, dev, run_step, barrier, world: int) -> dict:
+    """N > 1: the same step end to end on every rank through the Python API (head-sharded
+    decode + all-gather of O): per step each rank copies its Q shard, the replicated latent
+    cache, the block table and seqlens from pinned host buffers, runs the step and reads the
+    gathered O / LSE (all 16*N heads) back into pinned host memory. Wall clock per rank between
+    barriers, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    host = [t.cpu().pin_memory() for t in (inp.q, inp.kv_pool, inp.block_table, inp.seqlens)]
+    devb = [torch.empty_like(t) for t in (inp.q, inp.kv_pool, inp.block_table, inp.seqlens)]
+    res_h = []
+
+    def one():
+        for d, h in zip(devb, host):
+            d.copy_(h, non_blocking=True)
+        o, l = run_step(*devb)
+        if not res_h:
+            res_h.extend([torch.empty(o.shape, dtype=o.dtype).pin_memory(), torch.empty(l.shape, dtype=l.dtype).pin_memory()])
+        res_h[0].copy_(o, non_blocking=True)
+        res_h[1].copy_(l, non_blocking=True)
+        torch.cuda.synchronize(dev)
+
+    one()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    dt = (time.perf_counter() - t0) / steps
+    t = torch.tensor([dt], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    h2d = sum(h.numel() * h.element_size() for h in host)
+    d2h = sum(r.numel() * r.element_size() for r in res_h)
+    del devb
+    return {"value": float(t.item()) * 1e6, "unit": "us/step", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "api": f"paper_2506_01969_b200 Python API on each of {world} ranks (pinned host buffers in: Q shard + "
+                   "replicated latent cache + block table + seqlens; head-sharded decode + all-gather of O; "
+                   "all heads' O / LSE out), wall clock, max over ranks"}
 
 
 def e2e_serving_host(inp, steps: int, dev) -> dict:
