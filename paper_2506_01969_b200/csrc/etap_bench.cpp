@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -83,6 +84,11 @@ int main(int argc, char** argv) {
     };
     for (int i = 0; i < 10; ++i) step();
     CK(cudaStreamSynchronize(st));
+    // host cost of one decode call (C-ABI entry + K2/K3 launches), enqueue only
+    const auto h0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < iters; ++i) step();
+    const double us_host = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count() / iters;
+    CK(cudaStreamSynchronize(st));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -116,7 +122,7 @@ int main(int argc, char** argv) {
     const double kv_bytes = static_cast<double>(B) * ctx * ETAP_MLA_D_QK * 2;
     const double best = us_graph > 0 ? std::min(us_stream, us_graph) : us_stream;
     std::printf("{\"batch\": %d, \"ctx\": %d, \"heads\": %d, \"us_per_step_stream\": %.2f, "
-                "\"us_per_step_graph\": %.2f, \"kv_gbs_best\": %.1f, \"pages\": \"%s\"}\n",
-                B, ctx, H, us_stream, us_graph, kv_bytes / best / 1e3, contiguous ? "contiguous" : "shuffled");
+                "\"us_per_step_graph\": %.2f, \"host_enqueue_us\": %.2f, \"kv_gbs_best\": %.1f, \"pages\": \"%s\"}\n",
+                B, ctx, H, us_stream, us_graph, us_host, kv_bytes / best / 1e3, contiguous ? "contiguous" : "shuffled");
     return 0;
 }

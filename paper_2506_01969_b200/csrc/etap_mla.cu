@@ -1947,6 +1947,16 @@ bool lanes_enabled() {
     return on;
 }
 
+// Programmatic dependent launch on every launch of this library; ETAP_PDL=0 in the
+// environment launches without it (A/B: stream launches vs CUDA graphs). Read once.
+unsigned pdl_attrs() {
+    static const unsigned n = [] {
+        const char* e = std::getenv("ETAP_PDL");
+        return (e && e[0] == '0') ? 0u : 1u;
+    }();
+    return n;
+}
+
 // Schedule before the grid dependency (DecodeParams::early_meta); ETAP_EARLY_META=0 in the
 // environment disables it for A/B runs (same as ETAP_FLAG_DEP_METADATA on every call).
 bool early_meta_enabled() {
@@ -2149,7 +2159,7 @@ int metadata_launch(const int32_t* seqlens, int batch, int groups, int num_sm_pa
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_attrs();
     ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_metadata_kernel, seqlens, batch, groups,
                                  num_sm_parts, lanes_enabled() ? 1 : 0, sched, split_off, fixed_cost));
     return ETAP_OK;
@@ -2194,7 +2204,7 @@ int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_part
     cfg2.dynamicSmemBytes = 0;
     cfg2.stream = static_cast<cudaStream_t>(stream);
     cfg2.attrs = attr;
-    cfg2.numAttrs = 1;
+    cfg2.numAttrs = pdl_attrs();
     ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, static_cast<const float*>(ws_o),
                                  static_cast<const float*>(ws_lse), split_off, hg, batch, om,
                                  static_cast<unsigned long long*>(g_combine_trace_buf), seqlens, num_sm_parts,
@@ -2281,7 +2291,7 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     cfg.gridDim = dim3(num_sm_parts);
     cfg.stream = st;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_attrs();
     if (hg == 32) {
         cfg.dynamicSmemBytes = Cfg<32>::SMEM_ALLOC;
         cfg.blockDim = dim3(Cfg<32>::THREADS);
@@ -2397,7 +2407,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
         cfg.dynamicSmemBytes = kfp8::SMEM_ALLOC;
         cfg.stream = st;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = pdl_attrs();
         const bool dbg = prm.trace != nullptr;
         auto kern = dbg ? etap_mla_decode_fp8_kernel<true> : etap_mla_decode_fp8_kernel<false>;
         static int attr_rc = ensure_smem_attr(etap_mla_decode_fp8_kernel<false>, kfp8::SMEM_ALLOC) |
@@ -2484,7 +2494,7 @@ int etap_mla_append_kv(const void* kv_rows, void* kv_pool, int64_t num_pages, co
     cfg.blockDim = dim3(D_QK * 2 / 16);
     cfg.stream = static_cast<cudaStream_t>(stream);
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_attrs();
     ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_append_kv_kernel, static_cast<const uint4*>(kv_rows),
                                  static_cast<uint4*>(kv_pool), num_pages, block_table, max_pages_per_seq,
                                  seqlens, q_tokens));

@@ -50,8 +50,11 @@ def _ptr(t: torch.Tensor | None) -> int | None:
 
 
 def _stream_ptr(stream: torch.cuda.Stream | None) -> int:
-    s = torch.cuda.current_stream() if stream is None else stream
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    # the current device's current stream without building a Stream object (~0.3 us instead
+    # of ~3 us per call: at 1K contexts the host-side cost of a decode call is the step)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 @dataclass
@@ -194,11 +197,11 @@ class MlaDecodePlan:
 
 
 def _check_tensor(t: torch.Tensor, dtype: torch.dtype, shape: tuple, name: str) -> None:
-    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+    if isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dtype and t.shape == shape and t.is_contiguous():
+        return
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise _lib.EtapShapeError(f"{name} must be a CUDA tensor")
-    if t.dtype != dtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous():
-        raise _lib.EtapShapeError(
-            f"{name} must be contiguous {tuple(shape)} {dtype}, got {tuple(t.shape)} {t.dtype}")
+    raise _lib.EtapShapeError(f"{name} must be contiguous {tuple(shape)} {dtype}, got {tuple(t.shape)} {t.dtype}")
 
 
 def mla_decode(q: torch.Tensor, kv_pool: torch.Tensor, block_table: torch.Tensor,
