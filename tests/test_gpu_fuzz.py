@@ -2,9 +2,11 @@
 """Randomised decode configurations against the binary64 oracle (bf16 and FP8 latent caches):
 batch, ragged / empty / page-aligned context lengths, heads (16..64), query tokens (MTP),
 CTA counts 1..148 (the split schedule, lanes, K1 vs in-kernel schedule, combine). Fixed seeds,
-so every run checks the same 40 cases."""
+so every run checks the same 40 cases (ETAP_FUZZ_CASES=N draws N per cache type instead).
+Every case is also decoded with FLAG_DEP_METADATA and must be bitwise the same."""
 from __future__ import annotations
 
+import os
 import random
 
 import numpy as np
@@ -18,6 +20,7 @@ pytestmark = pytest.mark.gpu
 
 RMSE_TOL = 2e-5
 LSE_TOL = 1e-4
+N_CASES = int(os.environ.get("ETAP_FUZZ_CASES", 20))
 
 
 def bits(t):
@@ -67,18 +70,20 @@ def check(out, lse, o_ref, l_ref, lens, q_tokens):
             assert (o[~ne, j] == 0).all() and np.isneginf(l[~ne, j]).all()
 
 
-@pytest.mark.parametrize("case", range(20))
+@pytest.mark.parametrize("case", range(N_CASES))
 def test_fuzz_bf16(cuda_device, case):
     lens, heads, q_tokens, parts = draw(case)
     inp = inputs.make_mla_inputs(lens, heads=heads, seed=case, pad_value=float("nan"), q_tokens=q_tokens)
     plan = mla.MlaDecodePlan.create(len(lens), heads, "cuda", parts, q_tokens=q_tokens)
     out, lse = plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
+    o2, l2 = plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, flags=mla.FLAG_DEP_METADATA)
     torch.cuda.synchronize()
+    assert torch.equal(out, o2) and torch.equal(lse, l2)
     o_ref, l_ref = reference(inp, q_tokens, bits(inp.kv_pool))
     check(out, lse, o_ref, l_ref, lens, q_tokens)
 
 
-@pytest.mark.parametrize("case", range(20, 40))
+@pytest.mark.parametrize("case", range(N_CASES, 2 * N_CASES))
 def test_fuzz_fp8(cuda_device, case):
     lens, heads, q_tokens, parts = draw(case)
     inp = inputs.make_mla_inputs(lens, heads=heads, seed=case, pad_value=float("nan"), q_tokens=q_tokens)
@@ -87,6 +92,8 @@ def test_fuzz_fp8(cuda_device, case):
     deq = (kv8.float() * kv_scale).to(torch.bfloat16)
     plan = mla.MlaDecodePlan.create(len(lens), heads, "cuda", parts, q_tokens=q_tokens)
     out, lse = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, kv_scale)
+    o2, l2 = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, kv_scale, flags=mla.FLAG_DEP_METADATA)
     torch.cuda.synchronize()
+    assert torch.equal(out, o2) and torch.equal(lse, l2)
     o_ref, l_ref = reference(inp, q_tokens, bits(deq))
     check(out, lse, o_ref, l_ref, lens, q_tokens)
