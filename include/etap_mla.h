@@ -216,8 +216,10 @@ void etap_mla_host_ctx_destroy(etap_mla_host_ctx* ctx);
  *   kv_rows: [batch][q_tokens][576] bf16.
  * etap_mla_host_ctx_load: upload the resident cache state (pool + block table) once.
  * etap_mla_host_decode_step: one decode step from HOST buffers against the resident cache:
- *   H2D of Q, the new rows and seqlens; append (above); K2 + K3; D2H of O / LSE; synchronize.
- *   What `bench.py` reports as e2e_serving. */
+ *   Q, the new rows and seqlens in; append (above); K2 + K3; O / LSE out; synchronize. With
+ *   page-locked buffers (cudaHostAlloc / cudaHostRegister) the inputs are read in place over
+ *   PCIe by one ingest kernel and O / LSE are stored straight into the host buffers; pageable
+ *   buffers go through H2D / D2H staging copies. What `bench.py` reports as e2e_serving. */
 /* ---------------------------------------------------------------------------------------
  * The steps on either side of the kernel in an absorbed-MLA (DeepSeek) decode layer
  * (not in the reference). Per-head GEMMs with only B token rows, run

@@ -1570,6 +1570,36 @@ __global__ void __launch_bounds__(72)
     pool[dst_row * (D_QK * 2 / 16) + threadIdx.x] = rows[static_cast<size_t>(r) * (D_QK * 2 / 16) + threadIdx.x];
 }
 
+// Serving-step ingest (etap_mla_host_decode_step with page-locked host buffers): one kernel
+// reads this step's Q, new latent rows and seqlens straight from mapped host memory over PCIe,
+// writes Q and seqlens to their device buffers and appends the rows into the paged pool —
+// instead of three host->device copies and the append kernel. Blocks [0, nq) copy one Q row
+// (1152 B) each, blocks [nq, nq + B*T) append one latent row. It never triggers its dependents
+// early: the decode launched after it reads seqlens before its own grid dependency.
+__global__ void __launch_bounds__(72)
+    etap_mla_ingest_kernel(const uint4* __restrict__ q_src, uint4* __restrict__ q_dst, int nq,
+                           const uint4* __restrict__ rows, uint4* __restrict__ pool, int64_t num_pages,
+                           const int32_t* __restrict__ block_table, int max_pages,
+                           const int32_t* __restrict__ seqlens_src, int32_t* __restrict__ seqlens_dst,
+                           int batch, int q_tokens) {
+    constexpr int V = D_QK * 2 / 16;  // 16-byte vectors per row
+    const int r = blockIdx.x;
+    if (r < nq) {
+        q_dst[static_cast<size_t>(r) * V + threadIdx.x] = q_src[static_cast<size_t>(r) * V + threadIdx.x];
+        if (r == 0)
+            for (int i = threadIdx.x; i < batch; i += blockDim.x) seqlens_dst[i] = seqlens_src[i];
+        return;
+    }
+    const int rr = r - nq;  // b * q_tokens + j
+    const int b = rr / q_tokens, j = rr - b * q_tokens;
+    const int pos = seqlens_src[b] - q_tokens + j;
+    if (pos < 0 || pos / PAGE >= max_pages) return;
+    const int page = block_table[static_cast<size_t>(b) * max_pages + pos / PAGE];
+    if (page < 0 || page >= num_pages) return;
+    const size_t dst_row = static_cast<size_t>(page) * PAGE + pos % PAGE;
+    pool[dst_row * V + threadIdx.x] = rows[static_cast<size_t>(rr) * V + threadIdx.x];
+}
+
 // =============================================================================================
 // K3: log-sum-exp combine of split partials (no reference analog: split-KV is a SPEC
 // non-goal; the math is pinned by L = m + log l, etap.cpp:144, and partition
@@ -2024,6 +2054,21 @@ int encode_bf16_sw128(CUtensorMap* map, const void* base, uint64_t cols, uint64_
     e.rows = rows;
     e.box_rows = box_rows;
     e.map = *map;
+    return ETAP_OK;
+}
+// Launch of the serving-step ingest (etap_mla_host.cpp): q_src / rows / seqlens_src are
+// device pointers of page-locked host memory.
+int ingest_step(const void* q_src, void* q_dst, int nq_rows, const void* rows, void* pool, int64_t num_pages,
+                const int32_t* block_table, int max_pages, const int32_t* seqlens_src, int32_t* seqlens_dst,
+                int batch, int q_tokens, void* stream) {
+    if ((reinterpret_cast<uintptr_t>(q_src) | reinterpret_cast<uintptr_t>(q_dst) | reinterpret_cast<uintptr_t>(rows) |
+         reinterpret_cast<uintptr_t>(pool)) & 15)
+        return fail(ETAP_ERR_SHAPE, "ingest: 16-byte alignment required");
+    // a plain launch: no programmatic serialisation with the kernel before it either
+    etap_mla_ingest_kernel<<<nq_rows + batch * q_tokens, D_QK * 2 / 16, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(q_src), static_cast<uint4*>(q_dst), nq_rows, static_cast<const uint4*>(rows),
+        static_cast<uint4*>(pool), num_pages, block_table, max_pages, seqlens_src, seqlens_dst, batch, q_tokens);
+    ETAP_CUDA(cudaGetLastError());
     return ETAP_OK;
 }
 }  // namespace etap_b200

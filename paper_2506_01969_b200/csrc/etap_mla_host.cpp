@@ -17,6 +17,9 @@
 
 namespace etap_b200 {
 int host_fail(int code, const char* msg);  // etap_mla.cu: sets etap_mla_last_error()
+int ingest_step(const void* q_src, void* q_dst, int nq_rows, const void* rows, void* pool, int64_t num_pages,
+                const int32_t* block_table, int max_pages, const int32_t* seqlens_src, int32_t* seqlens_dst,
+                int batch, int q_tokens, void* stream);  // etap_mla.cu
 }
 using etap_b200::host_fail;
 
@@ -56,6 +59,17 @@ uint16_t bf16_bits_rne(double x) {
     uint32_t u;
     std::memcpy(&u, &f, 4);
     return static_cast<uint16_t>(u >> 16);
+}
+
+// Device address of page-locked (cudaHostAlloc / cudaHostRegister) host memory, or nullptr
+// for pageable memory: the serving step then reads / writes it directly over PCIe.
+void* mapped(const void* host) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return (a.type == cudaMemoryTypeHost && a.devicePointer) ? a.devicePointer : nullptr;
 }
 
 }  // namespace
@@ -156,24 +170,41 @@ int etap_mla_host_decode_step(etap_mla_host_ctx* c, const void* q_host, const vo
     if (!c || !q_host || !kv_rows_host || !seqlens_host || !out_host || !lse_host)
         return host_fail(ETAP_ERR_SHAPE, "NULL pointer argument");
     cudaStream_t s = c->stream;
-    if (cudaMemcpyAsync(c->q.p, q_host, c->q.n, cudaMemcpyHostToDevice, s) ||
-        cudaMemcpyAsync(c->rows.p, kv_rows_host, c->rows.n, cudaMemcpyHostToDevice, s) ||
-        cudaMemcpyAsync(c->sl.p, seqlens_host, c->sl.n, cudaMemcpyHostToDevice, s))
-        return host_fail(ETAP_ERR_CUDA, "host->device copy failed");
-    int rc = etap_mla_append_kv(c->rows.p, c->kv.p, c->num_pages, static_cast<int32_t*>(c->bt.p), c->max_pages,
+    int rc;
+    // Page-locked host buffers are read / written in place over PCIe: one ingest kernel for Q,
+    // the new rows and seqlens, and the decode's O / LSE stores go straight to host memory
+    // (no copy engine round trips). Pageable buffers take the copy path.
+    const void* q_m = mapped(q_host);
+    const void* rows_m = mapped(kv_rows_host);
+    const void* sl_m = mapped(seqlens_host);
+    float* out_m = static_cast<float*>(mapped(out_host));
+    float* lse_m = static_cast<float*>(mapped(lse_host));
+    if (q_m && rows_m && sl_m) {
+        rc = etap_b200::ingest_step(q_m, c->q.p, c->batch * c->heads, rows_m, c->kv.p, c->num_pages,
+                                    static_cast<int32_t*>(c->bt.p), c->max_pages, static_cast<const int32_t*>(sl_m),
+                                    static_cast<int32_t*>(c->sl.p), c->batch, 1, s);
+        if (rc) return rc;
+    } else {
+        if (cudaMemcpyAsync(c->q.p, q_host, c->q.n, cudaMemcpyHostToDevice, s) ||
+            cudaMemcpyAsync(c->rows.p, kv_rows_host, c->rows.n, cudaMemcpyHostToDevice, s) ||
+            cudaMemcpyAsync(c->sl.p, seqlens_host, c->sl.n, cudaMemcpyHostToDevice, s))
+            return host_fail(ETAP_ERR_CUDA, "host->device copy failed");
+        rc = etap_mla_append_kv(c->rows.p, c->kv.p, c->num_pages, static_cast<int32_t*>(c->bt.p), c->max_pages,
                                 static_cast<int32_t*>(c->sl.p), c->batch, 1, s);
-    if (rc) return rc;
+        if (rc) return rc;
+    }
+    const bool direct_out = out_m && lse_m;
     // the schedule is computed inside the decode kernel (no K1 launch)
     rc = etap_mla_decode(c->q.p, c->kv.p, c->num_pages, static_cast<int32_t*>(c->bt.p), c->max_pages,
                          static_cast<int32_t*>(c->sl.p), c->batch, 1, c->heads, scale, 1,
                          static_cast<int32_t*>(c->sched.p), static_cast<int32_t*>(c->split_off.p),
-                         c->num_sm_parts, c->ws.p, static_cast<float*>(c->out.p), static_cast<float*>(c->lse.p),
-                         flags, s);
+                         c->num_sm_parts, c->ws.p, direct_out ? out_m : static_cast<float*>(c->out.p),
+                         direct_out ? lse_m : static_cast<float*>(c->lse.p), flags, s);
     if (rc) return rc;
-    if (cudaMemcpyAsync(out_host, c->out.p, c->out.n, cudaMemcpyDeviceToHost, s) ||
-        cudaMemcpyAsync(lse_host, c->lse.p, c->lse.n, cudaMemcpyDeviceToHost, s) ||
-        cudaStreamSynchronize(s))
-        return host_fail(ETAP_ERR_CUDA, "device->host copy / synchronize failed");
+    if (!direct_out && (cudaMemcpyAsync(out_host, c->out.p, c->out.n, cudaMemcpyDeviceToHost, s) ||
+                        cudaMemcpyAsync(lse_host, c->lse.p, c->lse.n, cudaMemcpyDeviceToHost, s)))
+        return host_fail(ETAP_ERR_CUDA, "device->host copy failed");
+    if (cudaStreamSynchronize(s)) return host_fail(ETAP_ERR_CUDA, "synchronize failed");
     return ETAP_OK;
 }
 
