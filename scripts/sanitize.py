@@ -1,6 +1,7 @@
 # SPDX-License-Identifier: Apache-2.0
 """Small decodes for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
-bf16 with head groups of 16 and 32, MTP, the FP8 path, the combine and K1 paths.
+bf16 with head groups of 16 and 32, MTP, the FP8 path, the combine and K1 paths, and the
+serving step from page-locked host buffers (ingest kernel, O / LSE stored to host memory).
     compute-sanitizer --tool memcheck python scripts/sanitize.py"""
 from __future__ import annotations
 
@@ -28,6 +29,25 @@ def run() -> None:
     plan = mla.MlaDecodePlan.create(len(seqlens), 16, "cuda")
     plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
     torch.cuda.synchronize()
+    # serving step from page-locked host buffers: ingest kernel + O / LSE stored to host memory
+    import ctypes as C
+
+    from paper_2506_01969_b200 import _lib
+    L = _lib.lib()
+    seqlens = [300, 1, 129]
+    inp = inputs.make_mla_inputs(seqlens, heads=16, seed=7, pad_value=0.0)
+    last = inp.seqlens.long() - 1
+    pages = inp.block_table.gather(1, (last // 64).unsqueeze(1)).squeeze(1).long()
+    rows = inp.kv_pool[pages, last % 64].contiguous().cpu().pin_memory()
+    q_h, sl_h = inp.q.cpu().pin_memory(), inp.seqlens.cpu().pin_memory()
+    o_h, l_h = torch.empty((3, 16, 512)).pin_memory(), torch.empty((3, 16)).pin_memory()
+    kv_h, bt_h = inp.kv_pool.cpu(), inp.block_table.cpu()
+    ctx = C.c_void_p()
+    _lib.check(L.etap_mla_host_ctx_create(3, 16, inp.kv_pool.shape[0], inp.block_table.shape[1], C.byref(ctx)), "ctx")
+    _lib.check(L.etap_mla_host_ctx_load(ctx, kv_h.data_ptr(), bt_h.data_ptr()), "load")
+    _lib.check(L.etap_mla_host_decode_step(ctx, q_h.data_ptr(), rows.data_ptr(), sl_h.data_ptr(), inp.scale, 0,
+                                           o_h.data_ptr(), l_h.data_ptr()), "step")
+    L.etap_mla_host_ctx_destroy(ctx)
     print("sanitize cases done")
 
 
