@@ -28,7 +28,8 @@
  *              attention.cpp:38-40, and callers build V = K[:, :512] with col_block)
  *   block_table[batch][max_pages]               int32 page ids
  *   seqlens    [batch]                          int32 context lengths (varlen; 0 allowed)
- *   out        [batch][q_tokens][heads][512]    fp32  O = softmax(scale * Q K^T) V
+ *   out        [batch][q_tokens][heads][512]    fp32  O = softmax(scale * Q K^T) V (16-byte
+ *              aligned, like q, kv_pool and the workspace; ETAP_ERR_SHAPE otherwise)
  *   lse        [batch][q_tokens][heads]         fp32  L = m + log l, natural log (etap.cpp:144)
  *   q_tokens > 1 (multi-token / MTP decode, no reference analog: SPEC.md:12,146,249 put it out
  *   of scope) folds the tokens into the head axis, n_q = q_tokens * heads rows per sequence

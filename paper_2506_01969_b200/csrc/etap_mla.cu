@@ -2214,6 +2214,9 @@ int metadata_launch(const int32_t* seqlens, int batch, int groups, int num_sm_pa
 
 namespace {
 
+// O rows are stored (K3) and split partials loaded as float4
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 OutMap local_outmap(int heads, float* out, float* lse) {
     OutMap om = {};
     om.q_tokens = 1;
@@ -2472,6 +2475,7 @@ int etap_mla_decode_fp8(const void* q, const void* kv_pool8, float kv_scale, int
                         const int32_t* split_off, int num_sm_parts, void* workspace, float* out, float* lse,
                         unsigned flags, void* stream) {
     if (!out || !lse) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    if (!aligned16(out) || !aligned16(workspace)) return fail(ETAP_ERR_SHAPE, "out / workspace must be 16-byte aligned");
     const OutMap om = local_outmap(q_tokens * heads_per_token, out, lse);
     return decode_impl_fp8(q, kv_pool8, kv_scale, num_pages, block_table, max_pages_per_seq, seqlens, batch, q_tokens,
                            heads_per_token, scale, causal, sched, split_off, num_sm_parts, workspace, om, flags, stream);
@@ -2483,6 +2487,7 @@ int etap_mla_decode(const void* q, const void* kv_pool, int64_t num_pages,
                     const int32_t* sched, const int32_t* split_off, int num_sm_parts,
                     void* workspace, float* out, float* lse, unsigned flags, void* stream) {
     if (!out || !lse) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    if (!aligned16(out) || !aligned16(workspace)) return fail(ETAP_ERR_SHAPE, "out / workspace must be 16-byte aligned");
     const OutMap om = local_outmap(q_tokens * heads_per_token, out, lse);
     return decode_impl(q, kv_pool, num_pages, block_table, max_pages_per_seq, seqlens, batch, q_tokens,
                        heads_per_token, scale, causal, sched, split_off, num_sm_parts, workspace, om,
@@ -2549,6 +2554,7 @@ int etap_mla_append_kv(const void* kv_rows, void* kv_pool, int64_t num_pages, co
 int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_parts,
                      void* workspace, float* out, float* lse, void* stream) {
     if (!split_off || !workspace || !out || !lse) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    if (!aligned16(out) || !aligned16(workspace)) return fail(ETAP_ERR_SHAPE, "out / workspace must be 16-byte aligned");
     if (batch < 1 || !heads_ok(heads) || num_sm_parts < 1)
         return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
     return combine_impl(split_off, batch, heads, num_sm_parts, workspace, local_outmap(heads, out, lse), stream);

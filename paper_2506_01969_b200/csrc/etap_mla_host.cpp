@@ -179,7 +179,8 @@ int etap_mla_host_decode_step(etap_mla_host_ctx* c, const void* q_host, const vo
     const void* sl_m = mapped(seqlens_host);
     float* out_m = static_cast<float*>(mapped(out_host));
     float* lse_m = static_cast<float*>(mapped(lse_host));
-    if (q_m && rows_m && sl_m) {
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (q_m && rows_m && sl_m && al16(q_m) && al16(rows_m)) {
         rc = etap_b200::ingest_step(q_m, c->q.p, c->batch * c->heads, rows_m, c->kv.p, c->num_pages,
                                     static_cast<int32_t*>(c->bt.p), c->max_pages, static_cast<const int32_t*>(sl_m),
                                     static_cast<int32_t*>(c->sl.p), c->batch, 1, s);
@@ -193,7 +194,7 @@ int etap_mla_host_decode_step(etap_mla_host_ctx* c, const void* q_host, const vo
                                 static_cast<int32_t*>(c->sl.p), c->batch, 1, s);
         if (rc) return rc;
     }
-    const bool direct_out = out_m && lse_m;
+    const bool direct_out = out_m && lse_m && al16(out_m);
     // the schedule is computed inside the decode kernel (no K1 launch)
     rc = etap_mla_decode(c->q.p, c->kv.p, c->num_pages, static_cast<int32_t*>(c->bt.p), c->max_pages,
                          static_cast<int32_t*>(c->sl.p), c->batch, 1, c->heads, scale, 1,

@@ -77,14 +77,19 @@ def test_sizes_and_shape_validation():
     assert L.etap_mla_head_group(24, C.byref(hg)) == _lib.ETAP_ERR_SHAPE
     # decode rejects q_tokens outside [1, 8], q_tokens * heads not a multiple of 16 and a bad
     # scale before touching the device
-    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 9, 16, 1.0, 1, 1, 1, 148, 1, 1, 1, 0, None)
+    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 9, 16, 1.0, 1, 1, 1, 148, 16, 16, 16, 0, None)
     assert rc == _lib.ETAP_ERR_SHAPE and "q_tokens" in _lib.last_error()
-    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 0, 16, 1.0, 1, 1, 1, 148, 1, 1, 1, 0, None)
+    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 0, 16, 1.0, 1, 1, 1, 148, 16, 16, 16, 0, None)
     assert rc == _lib.ETAP_ERR_SHAPE and "q_tokens" in _lib.last_error()
-    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 3, 8, 1.0, 1, 1, 1, 148, 1, 1, 1, 0, None)
+    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 3, 8, 1.0, 1, 1, 1, 148, 16, 16, 16, 0, None)
     assert rc == _lib.ETAP_ERR_SHAPE and "multiple of 16" in _lib.last_error()
-    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 1, 16, float("nan"), 1, 1, 1, 148, 1, 1, 1, 0, None)
+    rc = L.etap_mla_decode(1, 1, 1, 1, 1, 1, 1, 1, 16, float("nan"), 1, 1, 1, 148, 16, 16, 16, 0, None)
     assert rc == _lib.ETAP_ERR_SHAPE and "scale" in _lib.last_error()
+    # O rows are stored and split partials loaded as float4: out / workspace must be 16-byte aligned
+    rc = L.etap_mla_decode(16, 16, 1, 16, 1, 16, 1, 1, 16, 1.0, 1, 16, 16, 148, 16, 20, 16, 0, None)
+    assert rc == _lib.ETAP_ERR_SHAPE and "aligned" in _lib.last_error()
+    rc = L.etap_mla_decode_fp8(16, 16, 1.0, 1, 16, 1, 16, 1, 1, 16, 1.0, 1, 16, 16, 148, 24, 16, 16, 0, None)
+    assert rc == _lib.ETAP_ERR_SHAPE and "aligned" in _lib.last_error()
 
 
 def test_reference_error_behaviour_mirrored():
