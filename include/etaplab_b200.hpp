@@ -17,15 +17,26 @@
 //   * d_qk != 576, d_v != 512, or V not equal to K[:, :512] (MLA latent aliasing)
 //                                -> std::invalid_argument (outside the GPU path's scope)
 //   * CUDA failure / no B200     -> std::runtime_error (there is no CPU fallback)
-//   * BlockHook                  -> not observable on the GPU; a non-empty hook throws
+//   * BlockHook                  -> the device cannot call back per KV block: the kernel records
+//                                   the softmax state of every 64-row tile (one split, the
+//                                   reference's serial block order, eager rescale) and the hook
+//                                   is replayed in order after the run with BlockStepInfo
+//                                   {query_block (16-row groups), kv_block, m_old,
+//                                   SoftmaxState{m, l}, rescale} (tiled_standard.hpp:32-40)
 //   * EtapFaults::negate_rescale -> ETAP_FLAG_NEGATE_RESCALE (same fault, on the device)
 // Q/K are rounded to bf16 (RNE) on the way in, O and L are widened from fp32 on the way out;
 // the reference's oracle (attention_ref) evaluated on the same rounded operands is the
 // parity target (RMSE <= 2e-5).
 #pragma once
 
+#include <algorithm>
+#include <cstddef>
+#include <functional>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "etap_mla.h"
 
@@ -50,11 +61,52 @@ Output run_etap(const Problem& p, const Tiles& tiles, const Faults& faults) {
     return out;
 }
 
+namespace detail {
+// BlockStepInfo from the hook's signature (etaplab::BlockHook = std::function<void(const BlockStepInfo&)>)
+template <class F>
+struct hook_arg;
+template <class R, class A>
+struct hook_arg<std::function<R(A)>> {
+    using type = std::remove_cv_t<std::remove_reference_t<A>>;
+};
+}  // namespace detail
+
 // Reference-signature form: drop-in for etaplab::run_etap(problem, tiles, hook, faults).
 template <class Output, class Problem, class Tiles, class Hook, class Faults>
 Output run_etap(const Problem& p, const Tiles& tiles, const Hook& hook, const Faults& faults) {
-    if (hook) throw std::invalid_argument("BlockHook is not observable on the GPU path");
-    return run_etap<Output>(p, tiles, faults);
+    if (!hook) return run_etap<Output>(p, tiles, faults);
+    using Info = typename detail::hook_arg<Hook>::type;
+    using State = std::remove_cv_t<std::remove_reference_t<decltype(std::declval<const Info&>().state)>>;
+    if (tiles.b_r < 1 || tiles.b_c < 1 || tiles.stages < 1)
+        throw std::invalid_argument("tile config fields must be >= 1");
+    using MatrixT = decltype(Output{}.o);
+    Output out;
+    out.o = MatrixT(p.n_q, p.d_v);
+    out.l.assign(p.n_q, 0.0);
+    const std::size_t rows = (p.n_q + 15) / 16 * 16, t_c = (p.n_kv + 63) / 64;
+    std::vector<double> state(t_c * 4 * rows);
+    // the reference's per-block rescale order (etap.cpp:40-47) so every step's factor is observable
+    const unsigned flags = ETAP_FLAG_EAGER_RESCALE | (faults.negate_rescale ? ETAP_FLAG_NEGATE_RESCALE : 0u);
+    const int rc = etap_mla_run_etap_f64_state(
+        p.q.data(), static_cast<int64_t>(p.n_q), p.k.data(), static_cast<int64_t>(p.n_kv),
+        static_cast<int64_t>(p.d_qk), p.v.data(), static_cast<int64_t>(p.d_v), p.scale, flags, out.o.data(),
+        out.l.data(), state.data());
+    if (rc == ETAP_ERR_SHAPE) throw std::invalid_argument(etap_mla_last_error());
+    if (rc != ETAP_OK) throw std::runtime_error(std::string("etap_b200: ") + etap_mla_last_error());
+    // state[j][0..3][row]: m_old, m, rescale, l after KV block j (include/etap_mla.h)
+    for (std::size_t h0 = 0, qb = 0; h0 < p.n_q; h0 += 16, ++qb) {
+        const std::size_t h1 = std::min<std::size_t>(p.n_q, h0 + 16);
+        for (std::size_t j = 0; j < t_c; ++j) {
+            auto row = [&](int r) {
+                const double* b = state.data() + (j * 4 + r) * rows;
+                return std::vector<double>(b + h0, b + h1);
+            };
+            const std::vector<double> m_old = row(0), rescale = row(2);
+            const State st{row(1), row(3)};
+            hook(Info{qb, j, m_old, st, rescale});
+        }
+    }
+    return out;
 }
 
 }  // namespace etaplab_b200

@@ -91,5 +91,37 @@ int main() {
         ++mirrored;
     }
     std::printf("{\"invalid_argument_mirrored\": %d}\n", mirrored);
-    return (failures == 0 && mirrored == 2) ? 0 : 1;
+
+    // BlockHook through the adapter: the GPU's per-tile softmax state replayed into the
+    // reference's own observer type, checked with the rules of the reference's StateChecker
+    // (cli.cpp:43-70: m never decreases, l > 0, rescale 0 on first touch else in (0, 1]). The
+    // negate_rescale fault (EtapFaults, etap.hpp:39-41, etap.cpp:62) flips the factor applied to
+    // the accumulator, not the reported state: as in the reference, the invariants still hold
+    // and the fault shows in the output (the verifier's equivalence check, cli.cpp:147-160).
+    int hook_ok = 0;
+    for (int fault = 0; fault < 2; ++fault) {
+        const AttentionProblem hp = mla_problem(7, 32, 1000);
+        std::size_t calls = 0, violations = 0;
+        BlockHook hook = [&](const BlockStepInfo& info) {
+            ++calls;
+            for (std::size_t i = 0; i < info.m_old.size(); ++i) {
+                const bool first_touch = std::isinf(info.m_old[i]) && info.m_old[i] < 0;
+                if (info.state.m[i] < info.m_old[i]) ++violations;
+                else if (!(info.state.l[i] > 0.0)) ++violations;
+                else if (first_touch ? info.rescale[i] != 0.0 : !(info.rescale[i] > 0.0 && info.rescale[i] <= 1.0))
+                    ++violations;
+            }
+        };
+        EtapFaults faults{};
+        faults.negate_rescale = fault != 0;
+        const AttentionOutput g = etaplab_b200::run_etap<AttentionOutput>(hp, TileConfig{64, 64, 2}, hook, faults);
+        const double e = rmse(g.o, attention_ref(hp).o);
+        const std::size_t want = ((hp.n_q + 15) / 16) * ((hp.n_kv + 63) / 64);
+        const bool ok = violations == 0 && calls == want && (fault ? e > 100 * 2e-5 : e <= 2e-5);
+        hook_ok += ok;
+        std::printf("{\"block_hook\": {\"negate_rescale\": %s, \"calls\": %zu, \"expected_calls\": %zu, "
+                    "\"violations\": %zu, \"rmse\": %.3e, \"ok\": %s}}\n", fault ? "true" : "false", calls, want,
+                    violations, e, ok ? "true" : "false");
+    }
+    return (failures == 0 && mirrored == 2 && hook_ok == 2) ? 0 : 1;
 }
