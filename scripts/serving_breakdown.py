@@ -1,7 +1,9 @@
 # SPDX-License-Identifier: Apache-2.0
-"""Where a serving decode step's time goes beyond the device step (bench.py's e2e_serving):
-the same sequence as etap_mla_host_decode_step (H2D of Q / new rows / seqlens, append, decode,
-D2H of O / LSE, synchronize), with CUDA events between the pieces, plus the wall time."""
+"""Where a serving decode step's time goes beyond the device step, on the COPY path of
+etap_mla_host_decode_step (pageable host buffers: H2D of Q / new rows / seqlens, append, decode,
+D2H of O / LSE, synchronize), with CUDA events between the pieces, plus the wall time. This
+breakdown is what motivated the page-locked path (one ingest kernel, O / LSE stored to host
+memory); scripts/serving_step.py times both paths through the C-ABI."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
