@@ -69,7 +69,10 @@ void* mapped(const void* host) {
         cudaGetLastError();
         return nullptr;
     }
-    return (a.type == cudaMemoryTypeHost && a.devicePointer) ? a.devicePointer : nullptr;
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    // page-locked memory of another device's context may not be mapped here: copy path then
+    return (a.type == cudaMemoryTypeHost && a.devicePointer && a.device == dev) ? a.devicePointer : nullptr;
 }
 
 }  // namespace
