@@ -445,14 +445,14 @@ __device__ __forceinline__ void dep_wait_producer(const DecodeParams& prm) {
     if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
 }
 
-template <bool kDebug>
+template <bool kDebug, int MAXVB>
 __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uint8_t* sched_smem, int hg,
                                                     uint32_t page_bytes, bool q_rows, int warp, int lane) {
     int* s_pref = reinterpret_cast<int*>(sched_smem);
-    int* s_soff = s_pref + MAX_FUSED_VB + 1;
-    int* s_tiles = s_soff + MAX_FUSED_VB + 1;
-    int* s_len = s_tiles + MAX_FUSED_VB;
-    int* s_sched = s_len + MAX_FUSED_VB;
+    int* s_soff = s_pref + MAXVB + 1;
+    int* s_tiles = s_soff + MAXVB + 1;
+    int* s_len = s_tiles + MAXVB;
+    int* s_sched = s_len + MAXVB;
     const bool fused = prm.inkernel_sched != 0;
     const bool early = fused && prm.early_meta != 0;
     Prologue r{};
@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     // split schedule + the producer's first page ids, around the grid dependency
-    const Prologue pro = decode_prologue<kDebug>(prm, smem + C::OFF_SCHED, HG, PAGE * D_QK * 2, true, warp, lane);
+    const Prologue pro = decode_prologue<kDebug, C::MAX_VB>(prm, smem + C::OFF_SCHED, HG, PAGE * D_QK * 2, true, warp, lane);
     const int32_t* sch = pro.sch;
     const int32_t* soff = pro.soff;  // split offsets per virtual sequence
     const int idx_off = pro.idx_off; // partial-index offset of this CTA's lane (fused schedule)
@@ -1076,7 +1076,7 @@ static_assert(fp8::HGF * (D_QK / 8) % QPRO_THREADS == 0, "prologue Q split");
 constexpr int OFF_BAR = align_up(OFF_RED + RED_FLOATS * 4, 16);
 constexpr int OFF_TMEM = OFF_BAR + NBAR8 * 8;
 constexpr int OFF_SCHED = OFF_TMEM + 16;
-constexpr int SMEM_USED = OFF_SCHED + SCHED_SMEM_INTS * 4;
+constexpr int SMEM_USED = OFF_SCHED + sched_smem_ints(MAX_FUSED_VB_WIDE) * 4;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;
 constexpr uint32_t TCOL_S = 0;                       // S^T: 2 buffers x 48 columns
 constexpr uint32_t TCOL_O = 2 * fp8::NQ;             // O^T: 4 d-blocks x 48 columns
@@ -1130,7 +1130,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const Prologue pro = decode_prologue<kDebug>(prm, smem + OFF_SCHED, HG, PAGE * D_QK, false, warp, lane);
+    const Prologue pro = decode_prologue<kDebug, MAX_FUSED_VB_WIDE>(prm, smem + OFF_SCHED, HG, PAGE * D_QK, false, warp, lane);
     const int32_t* sch = pro.sch;
     const int32_t* soff = pro.soff;
     const int idx_off = pro.idx_off;
@@ -2314,7 +2314,8 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     prm.split_off_out = const_cast<int32_t*>(split_off);
     prm.lanes_on = lanes_enabled() ? 1 : 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
-    prm.inkernel_sched = (ls.line_n <= MAX_FUSED_VB && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
+    const int max_vb = hg == 16 ? Cfg<16>::MAX_VB : Cfg<32>::MAX_VB;
+    prm.inkernel_sched = (ls.line_n <= max_vb && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
     prm.early_meta = (early_meta_enabled() && !(flags & ETAP_FLAG_DEP_METADATA)) ? 1 : 0;
     prm.fixed_cost = META_FIXED_COST;
     if (!prm.inkernel_sched && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) {
@@ -2431,7 +2432,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     prm.split_off_out = const_cast<int32_t*>(split_off);
     prm.lanes_on = lanes_enabled() ? 1 : 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
-    prm.inkernel_sched = ls.line_n <= MAX_FUSED_VB ? 1 : 0;
+    prm.inkernel_sched = ls.line_n <= MAX_FUSED_VB_WIDE ? 1 : 0;
     prm.early_meta = (early_meta_enabled() && !(flags & ETAP_FLAG_DEP_METADATA)) ? 1 : 0;
     prm.fixed_cost = FP8_FIXED_COST;
     prm.scale_log2 = scale * kv_scale * 1.4426950408889634f;

@@ -24,10 +24,11 @@ def run() -> None:
         if heads == 16:
             kv8 = (inp.kv_pool.float() / 0.125).to(torch.float8_e4m3fn)
             plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 0.125)
-    seqlens = [64] * 140  # > 128 work units: K1 + K2 + K3
-    inp = inputs.make_mla_inputs(seqlens, heads=16, seed=5, pad_value=0.0)
-    plan = mla.MlaDecodePlan.create(len(seqlens), 16, "cuda")
-    plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
+    for n in (140, 300):  # block-wide fused schedule (<= 256 work units), then K1 + K2 + K3
+        seqlens = [64] * n
+        inp = inputs.make_mla_inputs(seqlens, heads=16, seed=5, pad_value=0.0)
+        plan = mla.MlaDecodePlan.create(len(seqlens), 16, "cuda")
+        plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
     torch.cuda.synchronize()
     # serving step from page-locked host buffers: ingest kernel + O / LSE stored to host memory
     import ctypes as C

@@ -136,11 +136,13 @@ def test_fp8_many_splits_per_cta(cuda_device):
     assert (o2 - out).abs().max().item() <= 1e-4 and (l2 - lse).abs().max().item() <= 1e-5
 
 
-def test_fp8_long_line_runs_k1(cuda_device):
-    """More than 128 work units: the split schedule comes from K1 (with the FP8 fixed cost)."""
+@pytest.mark.parametrize("batch", [140, 300])
+def test_fp8_long_lines(cuda_device, batch):
+    """Long lines: up to 256 work units the decode computes the split schedule itself with the
+    block-wide scan (140), beyond that K1 runs first (300), both with the FP8 fixed cost."""
     import random
     rnd = random.Random(8)
-    seqlens = [rnd.randint(0, 300) for _ in range(140)]
+    seqlens = [rnd.randint(0, 300) for _ in range(batch)]
     inp, kv8, deq = fp8_inputs(seqlens, 16, seed=4)
     plan = mla.MlaDecodePlan.create(len(seqlens), 16, "cuda")
     out, lse = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 2.0 ** -3)
