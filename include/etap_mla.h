@@ -71,10 +71,9 @@ extern "C" {
 #define ETAP_FLAG_EXTERNAL_SCHEDULE 8u /* read sched / split_off produced by etap_mla_metadata.
                                        Without it K2 computes the same schedule in its
                                        prologue and writes it to sched / split_off when
-                                       the line (batch * head groups) has <= 256 entries
-                                       (head groups of 16, FP8) or <= 128 (head groups of
-                                       32): K1 off the per-step critical path; longer lines
-                                       make etap_mla_decode launch K1 itself first. */
+                                       the line (batch * head groups) has <= 256 entries:
+                                       K1 off the per-step critical path; longer lines make
+                                       etap_mla_decode launch K1 itself first. */
 #define ETAP_FLAG_DEP_METADATA 16u  /* seqlens / block_table are written by the kernel launched
                                        immediately before this decode on the stream. By default
                                        the decode kernels launch with programmatic dependent

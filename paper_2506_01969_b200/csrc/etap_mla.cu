@@ -215,7 +215,7 @@ __device__ __forceinline__ int cta_excl_scan256(int v, int* s_wt, int& total) {
 // iff (k+1)T > P[i]+F and kT < P[i+1]) -> split offsets -> this CTA's range. Identical output
 // to K1 (GPU test); CTA 0 publishes split_off for the combine kernel, every CTA its sched row.
 __device__ void schedule_own_range(const DecodeParams& prm, const LineShape& ls, const int* s_pref,
-                                   const int* s_soff, const int* s_tiles, int* s_sched, int total, int T,
+                                   const int* s_soff, const int* s_len, int* s_sched, int total, int T,
                                    bool publish) {
     const int n = ls.line_n;
     const int lane = blockIdx.x / ls.p_line, k = blockIdx.x - lane * ls.p_line;
@@ -227,13 +227,13 @@ __device__ void schedule_own_range(const DecodeParams& prm, const LineShape& ls,
         }
         while (lo + 1 < n && s_pref[lo + 1] <= x) ++lo;
         vb = lo;
-        t = min(max(0, x - s_pref[lo] - prm.fixed_cost), s_tiles[lo]);
+        t = min(max(0, x - s_pref[lo] - prm.fixed_cost), (s_len[lo] + TILE - 1) / TILE);
     };
     const int x0 = k * T, x1 = min(total, (k + 1) * T);
     int b0 = 0, tb = 0, b1 = -1, te = 0, first = 0;
     if (lane < ls.lanes && x0 < total) {
         map(x0, b0, tb);
-        if (x1 >= total) { b1 = n - 1; te = s_tiles[n - 1]; }
+        if (x1 >= total) { b1 = n - 1; te = (s_len[n - 1] + TILE - 1) / TILE; }
         else map(x1, b1, te);
         if (b1 >= b0) first = lane * s_soff[n] + s_soff[b0] + (k - (s_pref[b0] + prm.fixed_cost) / T);
     }
@@ -333,7 +333,7 @@ __device__ __forceinline__ void publish_schedule(const DecodeParams& prm, const 
 }
 
 __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, int* s_pref, int* s_soff,
-                                  int* s_tiles, int* s_len, int* s_sched, int* s_wt, bool publish) {
+                                  int* s_len, int* s_sched, int* s_wt, bool publish) {
     const int n = ls.line_n;
     const int tid = threadIdx.x;
     int tiles = 0, cost = 0;
@@ -341,7 +341,6 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
         const int len = max(0, prm.seqlens[tid % prm.batch]);
         tiles = (len + TILE - 1) / TILE;
         cost = tiles > 0 ? tiles + prm.fixed_cost : 0;
-        s_tiles[tid] = tiles;
         s_len[tid] = len;
     }
     int total;
@@ -361,7 +360,7 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
     if (tid < n) s_soff[tid] = so;
     if (tid == 0) s_soff[n] = nsplits;
     __syncthreads();
-    if (tid == 0) schedule_own_range(prm, ls, s_pref, s_soff, s_tiles, s_sched, total, T, publish);
+    if (tid == 0) schedule_own_range(prm, ls, s_pref, s_soff, s_len, s_sched, total, T, publish);
     if (publish && blockIdx.x == 0) publish_split_off(prm, ls, s_soff, tid, blockDim.x);
     __syncthreads();
 }
@@ -450,8 +449,7 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
                                                     uint32_t page_bytes, bool q_rows, int warp, int lane) {
     int* s_pref = reinterpret_cast<int*>(sched_smem);
     int* s_soff = s_pref + MAXVB + 1;
-    int* s_tiles = s_soff + MAXVB + 1;
-    int* s_len = s_tiles + MAXVB;
+    int* s_len = s_soff + MAXVB + 1;
     int* s_sched = s_len + MAXVB;
     const bool fused = prm.inkernel_sched != 0;
     const bool early = fused && prm.early_meta != 0;
@@ -465,7 +463,7 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
             if (warp == 0) inkernel_schedule_warp(prm, ls, s_soff, s_len, s_sched, publish);
             __syncthreads();
         } else {
-            inkernel_schedule(prm, ls, s_pref, s_soff, s_tiles, s_len, s_sched, s_sched + 8, publish);
+            inkernel_schedule(prm, ls, s_pref, s_soff, s_len, s_sched, s_sched + 8, publish);
         }
     };
     if (early) {
@@ -1076,7 +1074,7 @@ static_assert(fp8::HGF * (D_QK / 8) % QPRO_THREADS == 0, "prologue Q split");
 constexpr int OFF_BAR = align_up(OFF_RED + RED_FLOATS * 4, 16);
 constexpr int OFF_TMEM = OFF_BAR + NBAR8 * 8;
 constexpr int OFF_SCHED = OFF_TMEM + 16;
-constexpr int SMEM_USED = OFF_SCHED + sched_smem_ints(MAX_FUSED_VB_WIDE) * 4;
+constexpr int SMEM_USED = OFF_SCHED + sched_smem_ints(MAX_FUSED_VB) * 4;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;
 constexpr uint32_t TCOL_S = 0;                       // S^T: 2 buffers x 48 columns
 constexpr uint32_t TCOL_O = 2 * fp8::NQ;             // O^T: 4 d-blocks x 48 columns
@@ -1130,7 +1128,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const Prologue pro = decode_prologue<kDebug, MAX_FUSED_VB_WIDE>(prm, smem + OFF_SCHED, HG, PAGE * D_QK, false, warp, lane);
+    const Prologue pro = decode_prologue<kDebug, MAX_FUSED_VB>(prm, smem + OFF_SCHED, HG, PAGE * D_QK, false, warp, lane);
     const int32_t* sch = pro.sch;
     const int32_t* soff = pro.soff;
     const int idx_off = pro.idx_off;
@@ -2432,7 +2430,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     prm.split_off_out = const_cast<int32_t*>(split_off);
     prm.lanes_on = lanes_enabled() ? 1 : 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
-    prm.inkernel_sched = ls.line_n <= MAX_FUSED_VB_WIDE ? 1 : 0;
+    prm.inkernel_sched = ls.line_n <= MAX_FUSED_VB ? 1 : 0;
     prm.early_meta = (early_meta_enabled() && !(flags & ETAP_FLAG_DEP_METADATA)) ? 1 : 0;
     prm.fixed_cost = FP8_FIXED_COST;
     prm.scale_log2 = scale * kv_scale * 1.4426950408889634f;

@@ -36,12 +36,10 @@ constexpr int SLOT_BYTES = TILE * 128;  // 64 rows x 128 B = 8 KiB per ring slot
 constexpr int NTB = 4;          // tile-barrier ring depth (tiles in flight <= NSLOT/9 + 1)
 constexpr int NBAR = 6 * NTB + 8;
 // Longest line (batch * head groups, or batch with lanes) whose split schedule the decode
-// kernel computes itself; longer lines run K1 first. The block-wide scan takes one line entry
-// per thread: 256 for the 256-thread kernels (head groups of 16, FP8), 128 for head groups of
-// 32, whose shared memory has no room for the larger tables.
-constexpr int MAX_FUSED_VB = 128;
-constexpr int MAX_FUSED_VB_WIDE = 256;
-constexpr int sched_smem_ints(int max_vb) { return 4 * max_vb + 2 + 8 + 16; }  // pref, soff, tiles, len, sched, wt (<= 16 warps)
+// kernel computes itself (the block-wide scan takes one line entry per thread of the >= 256-
+// thread CTA); longer lines run K1 first.
+constexpr int MAX_FUSED_VB = 256;
+constexpr int sched_smem_ints(int max_vb) { return 3 * max_vb + 2 + 8 + 16; }  // pref, soff, len, sched, wt (<= 16 warps)
 
 // warp 0 TMA producer, warp 1 GEMM1 issuer (+TMEM alloc), warp 2 GEMM2 issuer, warp 3 idle,
 // warps 4..7 softmax / epilogue (warp % 4 = TMEM lane quadrant)
@@ -128,7 +126,7 @@ struct Cfg {
     static constexpr int OFF_BAR = align_up(OFF_RED + RED_FLOATS * 4, 16);
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr int OFF_SCHED = OFF_TMEM + 16;
-    static constexpr int MAX_VB = HG == 16 ? MAX_FUSED_VB_WIDE : MAX_FUSED_VB;  // fused-schedule line limit
+    static constexpr int MAX_VB = MAX_FUSED_VB;  // fused-schedule line limit
     static constexpr int SMEM_USED = OFF_SCHED + sched_smem_ints(MAX_VB) * 4;
     static constexpr int SMEM_ALLOC = SMEM_USED + 1024;  // slack for manual 1024 B alignment
     // TMEM columns (128 lanes x 32 bit): S^T double buffer [0, 2HG) (M=64 lane layout), then
