@@ -1603,7 +1603,11 @@ __global__ void __launch_bounds__(72)
 // non-goal; the math is pinned by L = m + log l, etap.cpp:144, and partition
 // invariance, acceptance.cpp:209-229). Grid: one CTA of 128 threads per (vb, head).
 // =============================================================================================
-constexpr int COMBINE_THREADS = 128;
+#ifndef ETAP_COMBINE_HPB
+#define ETAP_COMBINE_HPB 1
+#endif
+constexpr int COMBINE_HPB = ETAP_COMBINE_HPB;  // heads per CTA (128 threads each)
+constexpr int COMBINE_THREADS = 128 * COMBINE_HPB;
 constexpr int COMBINE_BATCH = 16;  // partial float4 loads in flight per thread
 
 __global__ void __launch_bounds__(COMBINE_THREADS)
@@ -1612,8 +1616,10 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
                             const __grid_constant__ OutMap om, unsigned long long* trace,
                             const int32_t* __restrict__ seqlens, int parts, int lanes_on, int fixed_cost) {
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 0] = ptx::global_timer_ns();
-    const int vb = blockIdx.x / hg;
-    const int h = blockIdx.x - vb * hg;
+    const int units = hg / COMBINE_HPB;           // CTAs per virtual sequence
+    const int vb = blockIdx.x / units;
+    const int h = (blockIdx.x - vb * units) * COMBINE_HPB + threadIdx.x / 128;
+    const int t = threadIdx.x % 128;              // float4 of the 512-wide O row
     const int g = vb / batch, b = vb - g * batch;  // head-group-major virtual sequences
     int s0, ns;
     if (seqlens != nullptr) {
@@ -1625,7 +1631,7 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
         __shared__ int s_info[2];
         if (threadIdx.x < 32) {
             const int lane = threadIdx.x;
-            const LineShape ls = line_shape(batch, gridDim.x / hg / batch, parts, lanes_on != 0);
+            const LineShape ls = line_shape(batch, gridDim.x / units / batch, parts, lanes_on != 0);
             const int n = ls.line_n;
             const int lv = vb / n, pos = vb - lv * n;
             const int len = lane < n ? max(0, __ldg(seqlens + lane % batch)) : 0;
@@ -1672,15 +1678,15 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
     const size_t orow = om.row(b, g * hg + h);
     if (ns <= 0) {  // empty context: O = 0, L = -inf
         for (int r = 0; r < om.n_out; ++r) {
-            reinterpret_cast<float4*>(om.out[r] + orow * D_V)[threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (threadIdx.x == 0) om.lse[r][orow] = -INFINITY;
+            reinterpret_cast<float4*>(om.out[r] + orow * D_V)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (t == 0) om.lse[r][orow] = -INFINITY;
         }
         return;
     }
     // One round trip after split_off: every thread issues all of its partial loads (one float4
     // per split, up to COMBINE_BATCH in flight) together with the split LSEs, then merges.
     const float* l_base = ws_lse + static_cast<size_t>(s0) * hg + h;
-    const float4* p4 = reinterpret_cast<const float4*>(ws_o + (static_cast<size_t>(s0) * hg + h) * D_V) + threadIdx.x;
+    const float4* p4 = reinterpret_cast<const float4*>(ws_o + (static_cast<size_t>(s0) * hg + h) * D_V) + t;
     const size_t stride4 = static_cast<size_t>(hg) * D_V / 4;
     float mx = -INFINITY, sum = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1720,8 +1726,8 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
     const float inv = sum > 0.f ? 1.f / sum : 0.f;
     acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
     for (int r = 0; r < om.n_out; ++r) {  // every output copy (peer gather: each rank's buffer)
-        if (threadIdx.x == 0) om.lse[r][orow] = mx + logf(sum);
-        reinterpret_cast<float4*>(om.out[r] + orow * D_V)[threadIdx.x] = acc;
+        if (t == 0) om.lse[r][orow] = mx + logf(sum);
+        reinterpret_cast<float4*>(om.out[r] + orow * D_V)[t] = acc;
     }
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 2] = ptx::global_timer_ns();
 }
@@ -2245,7 +2251,7 @@ int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_part
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg2 = {};
-    cfg2.gridDim = dim3(batch * groups * hg);
+    cfg2.gridDim = dim3(batch * groups * hg / COMBINE_HPB);
     cfg2.blockDim = dim3(COMBINE_THREADS);
     cfg2.dynamicSmemBytes = 0;
     cfg2.stream = static_cast<cudaStream_t>(stream);
