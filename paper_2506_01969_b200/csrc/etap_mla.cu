@@ -365,8 +365,10 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
     __syncthreads();
 }
 
-#ifndef ETAP_HINT_PAGES
-#define ETAP_HINT_PAGES 2
+// L2 prefetch depth before the grid dependency, in bytes of KV: 2 bf16 pages = 4 FP8 pages
+// (measured best for each kernel; deeper prefetch competes with the previous step's tail)
+#ifndef ETAP_HINT_BYTES
+#define ETAP_HINT_BYTES (2 * 64 * 576 * 2)
 #endif
 // Before the grid dependency (while the previous kernel finishes): warm L2 with the first pages
 // this CTA will most likely stream, guessed from its own range of the previous decode call (the
@@ -387,7 +389,7 @@ __device__ __forceinline__ void prev_range_hint(const DecodeParams& prm, int hg,
             hint_t0 = tb;
             const int32_t* bt = prm.block_table + static_cast<size_t>(b) * prm.max_pages;
 #pragma unroll 1
-            for (int k = 0; k < ETAP_HINT_PAGES && tb + k < prm.max_pages; ++k) {
+            for (int k = 0; k < static_cast<int>(ETAP_HINT_BYTES / page_bytes) && tb + k < prm.max_pages; ++k) {
                 const int page = bt[tb + k];
                 if (page >= 0 && page < prm.num_pages)
                     ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) + static_cast<size_t>(page) * page_bytes,
@@ -485,7 +487,8 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
                                                            sd.t0 + lane) : 0;
 #ifndef ETAP_NO_PREFETCH_HINT
                 // L2 warm-up only: the bytes used are loaded by TMA after the dependency
-                if (lane < ETAP_HINT_PAGES && sd.t0 + lane < sd.t1 && r.hint_pg >= 0 && r.hint_pg < prm.num_pages)
+                if (lane < static_cast<int>(ETAP_HINT_BYTES / page_bytes) && sd.t0 + lane < sd.t1 && r.hint_pg >= 0 &&
+                    r.hint_pg < prm.num_pages)
                     ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) +
                                               static_cast<size_t>(r.hint_pg) * page_bytes, page_bytes);
                 if (q_rows && lane == 0)
