@@ -74,16 +74,21 @@ extern "C" {
                                        the line (batch * head groups) has <= 256 entries:
                                        K1 off the per-step critical path; longer lines make
                                        etap_mla_decode launch K1 itself first. */
-#define ETAP_FLAG_DEP_METADATA 16u  /* seqlens / block_table are written by the kernel launched
-                                       immediately before this decode on the stream. By default
-                                       the decode kernels launch with programmatic dependent
-                                       launch and read seqlens and block_table (never KV or Q)
-                                       BEFORE that kernel has finished, so the split schedule
-                                       and the first page ids are ready when it does; the
-                                       preceding kernel must therefore not write them (host
-                                       copies, kernels without programmatic launch and all of
-                                       this library's kernels satisfy this). With this flag
-                                       both are read only after the dependency resolves. */
+#define ETAP_FLAG_DEP_METADATA 16u  /* the default since round 2, kept as a no-op for callers
+                                       that pass it: seqlens / block_table are read only after
+                                       the grid dependency on the preceding kernel resolved */
+#define ETAP_FLAG_EARLY_METADATA 32u /* opt-in fast path (~1-2 us per call): the decode kernels
+                                       launch with programmatic dependent launch and read
+                                       seqlens and block_table (never KV or Q) BEFORE the
+                                       kernel immediately before them on the stream has
+                                       finished, so the split schedule and the first page ids
+                                       are ready when it does. The caller guarantees that this
+                                       preceding kernel does not write seqlens / block_table
+                                       (host copies and this library's decode / combine kernels
+                                       satisfy this; a PDL producer kernel that writes them
+                                       and triggers its dependents early does not). Without
+                                       the flag (default) both are read after the dependency
+                                       resolves, which is safe whoever wrote them. */
 
 /* Thread-local description of the last error. Never NULL. */
 const char* etap_mla_last_error(void);
@@ -315,6 +320,11 @@ int etap_mla_umma_bench(int variant, int n, long long* out_dev, int grid);
  * (grid CTAs x pages_per_cta pages, ring of nslot 8 KB slots) — the attainable read rate. */
 int etap_mla_stream_bench(const void* kv_pool, int64_t num_pages, int pages_per_cta, int grid,
                           int nslot, void* stream);
+
+/* Debug / tests: a one-CTA kernel launched with programmatic dependent launch that triggers
+ * its dependents at entry, sleeps delay_ns, then copies n int32 from src to dst (device
+ * pointers) — a PDL producer writing seqlens or block_table right before a decode. */
+int etap_mla_debug_pdl_write(int32_t* dst, const int32_t* src, int n, int delay_ns, void* stream);
 
 #ifdef __cplusplus
 }

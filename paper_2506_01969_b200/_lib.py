@@ -22,7 +22,8 @@ FLAG_NEGATE_RESCALE = 1
 FLAG_EAGER_RESCALE = 2
 FLAG_SKIP_COMBINE = 4
 FLAG_EXTERNAL_SCHEDULE = 8
-FLAG_DEP_METADATA = 16  # seqlens / block_table come from the preceding kernel (etap_mla.h)
+FLAG_DEP_METADATA = 16  # no-op since round 2: seqlens / block_table are read after the grid dependency by default
+FLAG_EARLY_METADATA = 32  # opt-in: read seqlens / block_table before the grid dependency (etap_mla.h)
 
 _lib = None
 
@@ -77,6 +78,7 @@ def _declare(lib: C.CDLL) -> None:
         "etap_mla_debug_trace_combine": (i32, [vp]),
         "etap_mla_umma_bench": (i32, [i32, i32, vp, i32]),
         "etap_mla_stream_bench": (i32, [vp, i64, i32, i32, i32, vp]),
+        "etap_mla_debug_pdl_write": (i32, [vp, vp, i32, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

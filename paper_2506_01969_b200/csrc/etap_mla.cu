@@ -95,6 +95,9 @@ __global__ void __launch_bounds__(META_THREADS, 1)
     etap_mla_metadata_kernel(const int32_t* __restrict__ seqlens, int batch, int groups,
                              int num_parts, int lanes_on, int32_t* __restrict__ sched,
                              int32_t* __restrict__ split_off, int fixed_cost) {
+    // seqlens may come from the kernel before this one, and the previous step's combine may
+    // still read split_off: nothing is read or written before the grid dependency resolved
+    ptx::grid_dep_wait();
     ptx::grid_dep_launch();
     __shared__ int s_tiles[META_MAX_VB];
     __shared__ int s_pref[META_MAX_VB + 1];
@@ -421,10 +424,10 @@ __device__ __forceinline__ bool split_at(const int32_t* sch, int seqlen, int bat
 }
 
 // Split schedule and the producer's first page ids, around the grid dependency (all threads).
-// With early_meta (default; ETAP_FLAG_DEP_METADATA turns it off) seqlens and block_table are
-// read BEFORE griddepcontrol.wait: the API requires that the kernel immediately before the
-// decode in the stream does not write them (none of this library's kernels does; host copies
-// and kernels without programmatic launch are ordered anyway). The dependency then gates only
+// With early_meta (opt-in, ETAP_FLAG_EARLY_METADATA) seqlens and block_table are read BEFORE
+// griddepcontrol.wait: the caller guarantees that the kernel immediately before the decode in
+// the stream does not write them (this library's decode / combine kernels do not; host copies
+// are ordered anyway). By default both are read after the wait. The dependency then gates only
 // the KV / Q loads and every global write: the schedule is published after it (the previous
 // step's combine may still read split_off), and the producer's first TMA goes out right after
 // it with its page ids already in registers. Without early_meta the previous call's range
@@ -1994,8 +1997,8 @@ unsigned pdl_attrs() {
     return n;
 }
 
-// Schedule before the grid dependency (DecodeParams::early_meta); ETAP_EARLY_META=0 in the
-// environment disables it for A/B runs (same as ETAP_FLAG_DEP_METADATA on every call).
+// Schedule before the grid dependency (DecodeParams::early_meta, opt-in per call with
+// ETAP_FLAG_EARLY_METADATA); ETAP_EARLY_META=0 in the environment ignores that flag (A/B runs).
 bool early_meta_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("ETAP_EARLY_META");
@@ -2323,7 +2326,7 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
     const int max_vb = hg == 16 ? Cfg<16>::MAX_VB : Cfg<32>::MAX_VB;
     prm.inkernel_sched = (ls.line_n <= max_vb && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
-    prm.early_meta = (early_meta_enabled() && !(flags & ETAP_FLAG_DEP_METADATA)) ? 1 : 0;
+    prm.early_meta = (early_meta_enabled() && (flags & ETAP_FLAG_EARLY_METADATA)) ? 1 : 0;
     prm.fixed_cost = META_FIXED_COST;
     if (!prm.inkernel_sched && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) {
         // too many virtual sequences for the fused prologue: run K1 first on the same stream
@@ -2402,6 +2405,11 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
         return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
     if (flags & (ETAP_FLAG_EXTERNAL_SCHEDULE | ETAP_FLAG_NEGATE_RESCALE))
         return fail(ETAP_ERR_SHAPE, "FP8 path: external schedules and the rescale fault are not supported");
+    // the FP8 kernel leaves partials in 16-head units; etap_mla_combine assumes the bf16
+    // kernel's head group, which is 32 for these head counts
+    if ((flags & ETAP_FLAG_SKIP_COMBINE) && head_group_of(heads) != fp8::HGF)
+        return fail(ETAP_ERR_SHAPE, "FP8 path: SKIP_COMBINE needs a head count whose work unit is 16 heads "
+                                    "(heads not a multiple of 32)");
     if (g_state_buf) return fail(ETAP_ERR_SHAPE, "FP8 path: the softmax-state dump is not supported");
     if (int rc = check_device()) return rc;
 
@@ -2440,7 +2448,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     prm.lanes_on = lanes_enabled() ? 1 : 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
     prm.inkernel_sched = ls.line_n <= MAX_FUSED_VB ? 1 : 0;
-    prm.early_meta = (early_meta_enabled() && !(flags & ETAP_FLAG_DEP_METADATA)) ? 1 : 0;
+    prm.early_meta = (early_meta_enabled() && (flags & ETAP_FLAG_EARLY_METADATA)) ? 1 : 0;
     prm.fixed_cost = FP8_FIXED_COST;
     prm.scale_log2 = scale * kv_scale * 1.4426950408889634f;
     prm.flags = flags;
@@ -2515,6 +2523,7 @@ int etap_mla_decode_peer(const void* q, const void* kv_pool, int64_t num_pages,
         return fail(ETAP_ERR_SHAPE, "peer gather: head_offset + heads exceeds heads_total");
     if (flags & ETAP_FLAG_SKIP_COMBINE) return fail(ETAP_ERR_SHAPE, "peer gather: SKIP_COMBINE not allowed");
     if (epoch == 0) return fail(ETAP_ERR_SHAPE, "peer gather: epoch must be nonzero");
+    if (!aligned16(workspace)) return fail(ETAP_ERR_SHAPE, "workspace must be 16-byte aligned");
     OutMap om = {};
     om.q_tokens = q_tokens;
     om.heads_per_token = heads_per_token;
@@ -2524,6 +2533,7 @@ int etap_mla_decode_peer(const void* q, const void* kv_pool, int64_t num_pages,
     for (int r = 0; r < pg->world; ++r) {
         if (!pg->out[r] || !pg->lse[r] || !pg->flags[r])
             return fail(ETAP_ERR_SHAPE, "peer gather: NULL output / flag pointer");
+        if (!aligned16(pg->out[r])) return fail(ETAP_ERR_SHAPE, "peer gather: output buffers must be 16-byte aligned");
         // own copy first: the local rows are written before the remote ones
         const int src = (pg->rank + r) % pg->world;
         om.out[r] = pg->out[src];
@@ -2672,6 +2682,36 @@ extern "C" int etap_mla_umma_bench(int variant, int n, long long* out_dev, int g
     cudaFuncSetAttribute(etap_umma_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
     etap_umma_bench_kernel<<<grid, 128, 66 * 1024>>>(variant, n, out_dev);
     ETAP_CUDA(cudaGetLastError());
+    return ETAP_OK;
+}
+
+// =============================================================================================
+// PDL producer (tests): triggers its dependents at entry, then writes dst after a delay — the
+// shape of a serving-stack kernel that updates seqlens / block_table right before the decode.
+// =============================================================================================
+namespace {
+__global__ void etap_pdl_writer_kernel(int32_t* dst, const int32_t* src, int n, int delay_ns) {
+    ptx::grid_dep_wait();    // ordered after the kernel before it
+    ptx::grid_dep_launch();  // ... and lets the next kernel (the decode) start right away
+    const uint64_t t0 = ptx::global_timer_ns();
+    while (ptx::global_timer_ns() - t0 < static_cast<uint64_t>(delay_ns)) __nanosleep(500);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+}  // namespace
+
+extern "C" int etap_mla_debug_pdl_write(int32_t* dst, const int32_t* src, int n, int delay_ns, void* stream) {
+    if (!dst || !src || n < 0 || delay_ns < 0) return fail(ETAP_ERR_SHAPE, "bad argument");
+    if (int rc = check_device()) return rc;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(128);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_pdl_writer_kernel, dst, src, n, delay_ns));
     return ETAP_OK;
 }
 

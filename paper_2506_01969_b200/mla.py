@@ -12,8 +12,8 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import (FLAG_DEP_METADATA, FLAG_EAGER_RESCALE, FLAG_EXTERNAL_SCHEDULE,  # noqa: F401
-                   FLAG_NEGATE_RESCALE, FLAG_SKIP_COMBINE, check)
+from ._lib import (FLAG_DEP_METADATA, FLAG_EAGER_RESCALE, FLAG_EARLY_METADATA,  # noqa: F401
+                   FLAG_EXTERNAL_SCHEDULE, FLAG_NEGATE_RESCALE, FLAG_SKIP_COMBINE, check)
 
 D_QK = 576
 D_V = 512
@@ -117,25 +117,10 @@ class MlaDecodePlan:
         """K2 + K3. q [B,T,H,576] bf16 (T = q_tokens), kv_pool [pages,64,576] bf16, block_table
         [B,max_pages] int32, seqlens [B] int32 -> (out [B,T,H,512] fp32, lse [B,T,H] fp32, natural
         log). With T > 1 and ``causal`` token j sees KV rows [0, seqlen - T + j]."""
-        B, H, T = self.batch, self.heads, self.q_tokens
-        if q.dim() == 3 and T == 1:
-            q = q.unsqueeze(1)
-        _check_tensor(q, torch.bfloat16, (B, T, H, D_QK), "q")
-        if kv_pool.dim() != 3 or kv_pool.shape[1:] != (PAGE_ROWS, D_QK) or kv_pool.dtype != torch.bfloat16:
-            raise _lib.EtapShapeError(f"kv_pool must be [pages,64,576] bf16, got {tuple(kv_pool.shape)} {kv_pool.dtype}")
-        if not kv_pool.is_contiguous():
-            raise _lib.EtapShapeError("kv_pool must be contiguous")
-        if block_table.dim() != 2 or block_table.shape[0] != B or block_table.dtype != torch.int32 \
-                or not block_table.is_contiguous():
-            raise _lib.EtapShapeError("block_table must be contiguous [B, max_pages] int32")
-        _check_tensor(seqlens, torch.int32, (B,), "seqlens")
-        if out is None:
-            out = torch.empty((B, T, H, D_V), dtype=torch.float32, device=q.device)
-        if lse is None:
-            lse = torch.empty((B, T, H), dtype=torch.float32, device=q.device)
+        q, out, lse = self._check_io(q, kv_pool, block_table, seqlens, out, lse, (torch.bfloat16,), "kv_pool")
         check(_lib.lib().etap_mla_decode(
             q.data_ptr(), kv_pool.data_ptr(), kv_pool.shape[0], block_table.data_ptr(),
-            block_table.shape[1], seqlens.data_ptr(), B, T, H, float(scale), int(causal),
+            block_table.shape[1], seqlens.data_ptr(), self.batch, self.q_tokens, self.heads, float(scale), int(causal),
             self.sched.data_ptr(), self.split_off.data_ptr(), self.num_sm_parts,
             self.workspace.data_ptr(), out.data_ptr(), lse.data_ptr(), int(flags),
             _stream_ptr(stream)), "etap_mla_decode")
@@ -148,29 +133,51 @@ class MlaDecodePlan:
         """K2-FP8 + K3 on an FP8 (e4m3) latent cache: kv_pool8 [pages,64,576] float8_e4m3fn (or
         its uint8 bytes), dequantised value = kv_scale * e4m3. Same q / block_table / seqlens /
         outputs as decode()."""
-        B, H, T = self.batch, self.heads, self.q_tokens
-        if q.dim() == 3 and T == 1:
-            q = q.unsqueeze(1)
-        _check_tensor(q, torch.bfloat16, (B, T, H, D_QK), "q")
-        if kv_pool8.dim() != 3 or kv_pool8.shape[1:] != (PAGE_ROWS, D_QK) or \
-                kv_pool8.dtype not in (torch.float8_e4m3fn, torch.uint8) or not kv_pool8.is_contiguous():
-            raise _lib.EtapShapeError(f"kv_pool8 must be contiguous [pages,64,576] float8_e4m3fn, got "
-                                      f"{tuple(kv_pool8.shape)} {kv_pool8.dtype}")
-        if block_table.dim() != 2 or block_table.shape[0] != B or block_table.dtype != torch.int32 \
-                or not block_table.is_contiguous():
-            raise _lib.EtapShapeError("block_table must be contiguous [B, max_pages] int32")
-        _check_tensor(seqlens, torch.int32, (B,), "seqlens")
-        if out is None:
-            out = torch.empty((B, T, H, D_V), dtype=torch.float32, device=q.device)
-        if lse is None:
-            lse = torch.empty((B, T, H), dtype=torch.float32, device=q.device)
+        q, out, lse = self._check_io(q, kv_pool8, block_table, seqlens, out, lse,
+                                     (torch.float8_e4m3fn, torch.uint8), "kv_pool8")
         check(_lib.lib().etap_mla_decode_fp8(
             q.data_ptr(), kv_pool8.data_ptr(), float(kv_scale), kv_pool8.shape[0], block_table.data_ptr(),
-            block_table.shape[1], seqlens.data_ptr(), B, T, H, float(scale), int(causal),
+            block_table.shape[1], seqlens.data_ptr(), self.batch, self.q_tokens, self.heads, float(scale),
+            int(causal),
             self.sched.data_ptr(), self.split_off.data_ptr(), self.num_sm_parts,
             self.workspace.data_ptr(), out.data_ptr(), lse.data_ptr(), int(flags),
             _stream_ptr(stream)), "etap_mla_decode_fp8")
         return out, lse
+
+    def _check_io(self, q, pool, block_table, seqlens, out, lse, pool_dtypes, pool_name, outputs=True):
+        """Shape / dtype / device checks of one decode call (EtapShapeError, never a device fault);
+        allocates out / lse when they are not given."""
+        B, H, T = self.batch, self.heads, self.q_tokens
+        if isinstance(q, torch.Tensor) and q.dim() == 3 and T == 1:
+            q = q.unsqueeze(1)
+        _check_tensor(q, torch.bfloat16, (B, T, H, D_QK), "q")
+        if not isinstance(pool, torch.Tensor) or not pool.is_cuda:
+            raise _lib.EtapShapeError(f"{pool_name} must be a CUDA tensor")
+        if pool.dim() != 3 or pool.shape[1:] != (PAGE_ROWS, D_QK) or pool.dtype not in pool_dtypes \
+                or not pool.is_contiguous():
+            raise _lib.EtapShapeError(f"{pool_name} must be contiguous [pages,64,576] {pool_dtypes[0]}, got "
+                                      f"{tuple(pool.shape)} {pool.dtype}")
+        if not isinstance(block_table, torch.Tensor) or not block_table.is_cuda:
+            raise _lib.EtapShapeError("block_table must be a CUDA tensor")
+        if block_table.dim() != 2 or block_table.shape[0] != B or block_table.dtype != torch.int32 \
+                or not block_table.is_contiguous():
+            raise _lib.EtapShapeError("block_table must be contiguous [B, max_pages] int32")
+        _check_tensor(seqlens, torch.int32, (B,), "seqlens")
+        if not outputs:  # the caller owns the output buffers (peer gather)
+            out, lse = q, seqlens  # device checks only
+        if out is None:
+            out = torch.empty((B, T, H, D_V), dtype=torch.float32, device=q.device)
+        if lse is None:
+            lse = torch.empty((B, T, H), dtype=torch.float32, device=q.device)
+        if outputs:
+            _check_tensor(out, torch.float32, (B, T, H, D_V), "out")
+            _check_tensor(lse, torch.float32, (B, T, H), "lse")
+        dev = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        for name, t in (("q", q), (pool_name, pool), ("block_table", block_table), ("seqlens", seqlens),
+                        ("out", out), ("lse", lse)):
+            if t.device.index != dev:
+                raise _lib.EtapShapeError(f"{name} is on {t.device}, the plan on cuda:{dev}")
+        return q, out, lse
 
     def capture(self, q: torch.Tensor, kv_pool: torch.Tensor, block_table: torch.Tensor,
                 seqlens: torch.Tensor, scale: float, out: torch.Tensor, lse: torch.Tensor,

@@ -18,7 +18,7 @@ import torch
 
 from . import _lib
 from ._lib import check
-from .mla import D_V, MlaDecodePlan, _check_tensor, _stream_ptr
+from .mla import D_V, MlaDecodePlan, _stream_ptr
 
 MAX_PEERS = 8
 HANDLE_BYTES = 64
@@ -116,10 +116,9 @@ class PeerGather:
         B, H, T = plan.batch, plan.heads, plan.q_tokens
         if (B, H, T) != (self.batch, self.heads_local, self.q_tokens):
             raise _lib.EtapShapeError("plan shape does not match the PeerGather buffers")
-        if q.dim() == 3 and T == 1:
-            q = q.unsqueeze(1)
-        _check_tensor(q, torch.bfloat16, (B, T, H, 576), "q")
-        _check_tensor(seqlens, torch.int32, (B,), "seqlens")
+        # same checks as MlaDecodePlan.decode (out / lse are this object's own buffers)
+        q, _, _ = plan._check_io(q, kv_pool, block_table, seqlens, None, None, (torch.bfloat16,), "kv_pool",
+                                 outputs=False)
         self.epoch += 1
         s = self.epoch % self.nbuf
         check(_lib.lib().etap_mla_decode_peer(

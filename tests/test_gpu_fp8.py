@@ -172,3 +172,27 @@ def test_fp8_arbitrary_kv_scale_vs_fp64_torch(cuda_device):
         rmse = (out[b, 0].double() - o_ref).pow(2).mean().sqrt().item()
         assert rmse <= RMSE_TOL, (b, rmse)
         assert (lse[b, 0].double() - l_ref).abs().max().item() <= LSE_TOL
+
+
+def test_fp8_skip_combine_rejected_for_32_head_work_units(cuda_device):
+    """The FP8 kernel writes split partials in 16-head units, etap_mla_combine assumes the bf16
+    kernel's head group (32 for head counts that are multiples of 32): SKIP_COMBINE is rejected
+    there instead of merging with the wrong layout; at 16 / 48 heads skip + combine equals the
+    plain FP8 decode."""
+    for heads, ok in ((32, False), (64, False), (16, True), (48, True)):
+        inp = inputs.make_mla_inputs([3000, 70, 1000], heads=heads, seed=3, pad_value=0.0)
+        kv8 = (inp.kv_pool.float() / 0.125).to(torch.float8_e4m3fn)
+        plan = mla.MlaDecodePlan.create(3, heads, "cuda")
+        if not ok:
+            with pytest.raises(_lib.EtapShapeError):
+                plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 0.125, flags=mla.FLAG_SKIP_COMBINE)
+            continue
+        o_ref, l_ref = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 0.125)
+        o_ref, l_ref = o_ref.clone(), l_ref.clone()
+        out = torch.empty_like(o_ref)
+        lse = torch.empty_like(l_ref)
+        plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 0.125, out=out, lse=lse,
+                        flags=mla.FLAG_SKIP_COMBINE)
+        plan.combine(out, lse)
+        torch.cuda.synchronize()
+        assert torch.equal(out, o_ref) and torch.equal(lse, l_ref)

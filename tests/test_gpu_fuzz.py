@@ -3,7 +3,8 @@
 batch, ragged / empty / page-aligned context lengths, heads (16..64), query tokens (MTP),
 CTA counts 1..148 (the split schedule, lanes, K1 vs in-kernel schedule, combine). Fixed seeds,
 so every run checks the same 40 cases (ETAP_FUZZ_CASES=N draws N per cache type instead).
-Every case is also decoded with FLAG_DEP_METADATA and must be bitwise the same."""
+Every case is also decoded with FLAG_EARLY_METADATA (schedule read before the grid
+dependency) and must be bitwise the same."""
 from __future__ import annotations
 
 import os
@@ -76,7 +77,7 @@ def test_fuzz_bf16(cuda_device, case):
     inp = inputs.make_mla_inputs(lens, heads=heads, seed=case, pad_value=float("nan"), q_tokens=q_tokens)
     plan = mla.MlaDecodePlan.create(len(lens), heads, "cuda", parts, q_tokens=q_tokens)
     out, lse = plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
-    o2, l2 = plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, flags=mla.FLAG_DEP_METADATA)
+    o2, l2 = plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, flags=mla.FLAG_EARLY_METADATA)
     torch.cuda.synchronize()
     assert torch.equal(out, o2) and torch.equal(lse, l2)
     o_ref, l_ref = reference(inp, q_tokens, bits(inp.kv_pool))
@@ -92,7 +93,7 @@ def test_fuzz_fp8(cuda_device, case):
     deq = (kv8.float() * kv_scale).to(torch.bfloat16)
     plan = mla.MlaDecodePlan.create(len(lens), heads, "cuda", parts, q_tokens=q_tokens)
     out, lse = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, kv_scale)
-    o2, l2 = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, kv_scale, flags=mla.FLAG_DEP_METADATA)
+    o2, l2 = plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, kv_scale, flags=mla.FLAG_EARLY_METADATA)
     torch.cuda.synchronize()
     assert torch.equal(out, o2) and torch.equal(lse, l2)
     o_ref, l_ref = reference(inp, q_tokens, bits(deq))
