@@ -258,17 +258,38 @@ int etap_mla_host_decode_step(etap_mla_host_ctx* ctx, const void* q_host, const 
                               const int32_t* seqlens_host, float scale, unsigned flags,
                               float* out_host, float* lse_host);
 
+/* Precision of the reference's AttentionProblem (etaplab::Precision, matrix.hpp:22). The GPU
+ * path computes bf16 x bf16 -> fp32 on the stored operands, which is a mapping of exact64
+ * storage only; the fp32 / fp16emu emulation modes are rejected with ETAP_ERR_SHAPE (the
+ * adapter throws std::invalid_argument) rather than silently computed differently. */
+#define ETAP_PRECISION_EXACT64 0
+#define ETAP_PRECISION_FP32 1
+#define ETAP_PRECISION_FP16EMU 2
+
 /* Reference-shaped entry (binary64 row-major matrices, exactly the storage of
  * etaplab::AttentionProblem, attention.hpp:15-25): rounds Q/K to bf16, checks the MLA
  * aliasing V == K[:, :512], runs the GPU path, widens O and L back to binary64.
- * d_qk must be 576 and d_v 512; n_q is padded to a multiple of 16 heads internally.
- * b_r/b_c/stages mirror TileConfig (tiled_standard.hpp:11-15): validated (>= 1, as
- * run_etap does at etap.cpp:104-106) and otherwise ignored — the GPU tiling is fixed and the
- * result is partition invariant (acceptance.cpp:209-229). */
+ * d_qk must be 576, d_v 512 and precision ETAP_PRECISION_EXACT64; n_q is padded to a multiple
+ * of 16 heads internally. b_r/b_c/stages mirror TileConfig (tiled_standard.hpp:11-15):
+ * validated (>= 1, as run_etap does at etap.cpp:104-106) and otherwise without numeric effect
+ * — the GPU tiling is fixed and the result is partition invariant (acceptance.cpp:209-229). */
 int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t n_kv,
-                          int64_t d_qk, const double* v, int64_t d_v, double scale,
+                          int64_t d_qk, const double* v, int64_t d_v, double scale, int precision,
                           int64_t b_r, int64_t b_c, int64_t stages, unsigned flags, double* o,
                           double* l);
+
+/* Reference-shaped entry with the BlockHook stream (tiled_standard.hpp:32-40; run_etap calls
+ * the hook after every KV block of b_c rows, etap.cpp:122-129): state [t_c][4][n_q] host
+ * binary64, t_c = ceil(n_kv / b_c), holding after KV block j for every query row i
+ *   state[(j*4 + 0)*n_q + i] = m_old (-inf before the first block), [1] = m (running max of
+ *   scale*q.k), [2] = rescale exp(m_old - m) (0 on the first block), [3] = running sum l
+ * — the device's softmax state over exactly rows [0, min((j+1) b_c, n_kv)) with one split (the
+ * reference's serial block order), for any b_c: every block boundary that is not a 64-row tile
+ * boundary is observed as the final state of a prefix sequence sharing the same KV pages. */
+int etap_mla_run_etap_f64_state(const double* q, int64_t n_q, const double* k, int64_t n_kv,
+                                int64_t d_qk, const double* v, int64_t d_v, double scale,
+                                int precision, int64_t b_c, unsigned flags, double* o, double* l,
+                                double* state);
 
 /* UMMA descriptor self-test (one CTA, one tile): S^T = K Q^T and O^T = V^T P^T through the
  * same smem layouts as the 16-head decode kernel. Device pointers: k [64][576] bf16,
@@ -304,13 +325,6 @@ int etap_mla_debug_trace_combine(void* device_buf);
  * for head h of the head group (hg = etap_mla_head_group(heads), vb head-group major). Per-split state: run with one split per sequence
  * (num_sm_parts = 1 or a single sequence) to observe the reference's single chain. */
 int etap_mla_debug_state(void* device_buf, int max_tiles);
-
-/* Reference-shaped entry with the softmax state returned (one split, the reference's serial
- * block order with b_c = 64): state [n_tiles][4][n_q_padded16] host binary64, layout as above
- * with the head index running over n_q (padded to a multiple of 16). */
-int etap_mla_run_etap_f64_state(const double* q, int64_t n_q, const double* k, int64_t n_kv,
-                                int64_t d_qk, const double* v, int64_t d_v, double scale,
-                                unsigned flags, double* o, double* l, double* state);
 
 /* Debug: tensor-pipe microbenchmark — `grid` CTAs each issue n tcgen05.mma of one operand
  * layout variant; out_dev[0..1] (device, int64) = issue cycles, issue+completion cycles. */

@@ -23,6 +23,7 @@ FLAG_EAGER_RESCALE = 2
 FLAG_SKIP_COMBINE = 4
 FLAG_EXTERNAL_SCHEDULE = 8
 FLAG_DEP_METADATA = 16  # no-op since round 2: seqlens / block_table are read after the grid dependency by default
+PRECISION_EXACT64 = 0  # etaplab::Precision (matrix.hpp:22); fp32 = 1 / fp16emu = 2 are rejected
 FLAG_EARLY_METADATA = 32  # opt-in: read seqlens / block_table before the grid dependency (etap_mla.h)
 
 _lib = None
@@ -69,11 +70,11 @@ def _declare(lib: C.CDLL) -> None:
         "etap_mla_decode_fp8": (i32, [vp, vp, f32, i64, vp, i32, vp, i32, i32, i32, f32, i32, vp, vp, i32, vp, vp, vp,
                                       u32, vp]),
         "etap_mla_host_ctx_destroy": (None, [vp]),
-        "etap_mla_run_etap_f64": (i32, [vp, i64, vp, i64, i64, vp, i64, f64, i64, i64, i64, u32,
+        "etap_mla_run_etap_f64": (i32, [vp, i64, vp, i64, i64, vp, i64, f64, i32, i64, i64, i64, u32,
                                         vp, vp]),
         "etap_mla_selftest_umma": (i32, [vp, vp, vp, vp, vp, vp]),
         "etap_mla_debug_state": (i32, [vp, i32]),
-        "etap_mla_run_etap_f64_state": (i32, [vp, i64, vp, i64, i64, vp, i64, f64, u32, vp, vp, vp]),
+        "etap_mla_run_etap_f64_state": (i32, [vp, i64, vp, i64, i64, vp, i64, f64, i32, i64, u32, vp, vp, vp]),
         "etap_mla_debug_trace": (i32, [vp]),
         "etap_mla_debug_trace_combine": (i32, [vp]),
         "etap_mla_umma_bench": (i32, [i32, i32, vp, i32]),

@@ -7,6 +7,7 @@
 //     mirroring run_etap's argument meaning and error behaviour (etap.cpp:102-106).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -218,8 +219,16 @@ void etap_mla_host_ctx_destroy(etap_mla_host_ctx* c) {
     delete c;
 }
 
+// The reference's BlockHook stream (tiled_standard.hpp:32-40, called per (query block, KV
+// block) at etap.cpp:128) reconstructed from the device's softmax-state dump. One decode of a
+// batch of "prefix sequences" that share the KV pages through the block table: sequence j
+// sees rows [0, R_j), R_j = min((j+1) b_c, n_kv), and its last tile's state IS the state after
+// KV block j (the running max / sum over exactly those rows). When b_c is a multiple of 64
+// every R_j is a tile boundary of the full problem and one sequence suffices (its per-tile
+// states at the boundaries). num_sm_parts = 1: every sequence is one split, the reference's
+// serial chain of blocks.
 static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int64_t n_kv,
-                             int64_t d_qk, const double* v, int64_t d_v, double scale,
+                             int64_t d_qk, const double* v, int64_t d_v, double scale, int precision,
                              int64_t b_r, int64_t b_c, int64_t stages, unsigned flags, double* o,
                              double* l, double* state) {
     // argument validation mirrors run_etap / make_problem (etap.cpp:104-106,
@@ -228,6 +237,10 @@ static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int6
         return host_fail(ETAP_ERR_SHAPE, "tile config fields must be >= 1");
     if (!q || !k || !v || !o || !l || n_q < 1 || n_kv < 1)
         return host_fail(ETAP_ERR_SHAPE, "matrix dimensions must be >= 1");
+    if (precision != ETAP_PRECISION_EXACT64)
+        return host_fail(ETAP_ERR_SHAPE,
+                         "GPU ETAP path computes bf16 x bf16 -> fp32 on exact64-stored operands; the fp32 / "
+                         "fp16emu emulation modes (Precision, matrix.hpp:22) are not mapped");
     if (d_qk != ETAP_MLA_D_QK || d_v != ETAP_MLA_D_V)
         return host_fail(ETAP_ERR_SHAPE, "GPU ETAP path is MLA decode: d_qk=576, d_v=512");
     if (!(scale >= 0.0) || !std::isfinite(scale))
@@ -242,17 +255,28 @@ static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int6
                       ETAP_MLA_HEAD_GROUP;
     const int64_t pages = (n_kv + ETAP_MLA_PAGE_ROWS - 1) / ETAP_MLA_PAGE_ROWS;
     if (pages > 0x7fffffff) return host_fail(ETAP_ERR_SHAPE, "too many pages");
-    std::vector<uint16_t> qb(static_cast<size_t>(heads) * d_qk, 0);
+    const int64_t t_c = (n_kv + b_c - 1) / b_c;
+    // hook replay: prefix sequences unless every block boundary is a tile boundary
+    const bool prefixes = state && (b_c % ETAP_MLA_PAGE_ROWS) != 0 && t_c > 1;
+    const int64_t batch = prefixes ? t_c : 1;
+    if (prefixes && (batch * (heads / ETAP_MLA_HEAD_GROUP) > 2048 || batch * pages > ((int64_t)1 << 26)))
+        return host_fail(ETAP_ERR_SHAPE, "BlockHook replay with b_c not a multiple of 64 is limited to "
+                                         "2048 (KV blocks x 16-head groups) and 2^26 prefix tiles");
+    std::vector<uint16_t> qb(static_cast<size_t>(batch) * heads * d_qk, 0);
     std::vector<uint16_t> kvb(static_cast<size_t>(pages) * ETAP_MLA_PAGE_ROWS * d_qk, 0);
     for (int64_t i = 0; i < n_q * d_qk; ++i) qb[i] = bf16_bits_rne(q[i]);
+    for (int64_t b = 1; b < batch; ++b)
+        std::memcpy(qb.data() + b * heads * d_qk, qb.data(), sizeof(uint16_t) * heads * d_qk);
     for (int64_t i = 0; i < n_kv * d_qk; ++i) kvb[i] = bf16_bits_rne(k[i]);
-    std::vector<int32_t> bt(pages);
-    for (int64_t i = 0; i < pages; ++i) bt[i] = static_cast<int32_t>(i);
-    const int32_t seqlen = static_cast<int32_t>(n_kv);
-    std::vector<float> of(static_cast<size_t>(heads) * d_v), lf(heads);
+    std::vector<int32_t> bt(static_cast<size_t>(batch) * pages), sl(batch);
+    for (int64_t b = 0; b < batch; ++b) {
+        for (int64_t i = 0; i < pages; ++i) bt[b * pages + i] = static_cast<int32_t>(i);
+        sl[b] = static_cast<int32_t>(prefixes ? std::min((b + 1) * b_c, n_kv) : n_kv);
+    }
+    std::vector<float> of(static_cast<size_t>(batch) * heads * d_v), lf(static_cast<size_t>(batch) * heads);
 
     etap_mla_host_ctx* ctx = nullptr;
-    int rc = etap_mla_host_ctx_create(1, heads, pages, static_cast<int>(pages), &ctx);
+    int rc = etap_mla_host_ctx_create(static_cast<int>(batch), heads, pages, static_cast<int>(pages), &ctx);
     if (rc) return rc;
     float* st_dev = nullptr;
     int hg = ETAP_MLA_HEAD_GROUP;
@@ -261,9 +285,9 @@ static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int6
         return e;
     }
     const int groups = heads / hg;
-    const size_t st_n = static_cast<size_t>(groups) * pages * 4 * hg;
+    const size_t st_n = static_cast<size_t>(groups) * batch * pages * 4 * hg;
     if (state) {
-        ctx->num_sm_parts = 1;  // one split: the reference's serial chain of KV blocks
+        ctx->num_sm_parts = 1;  // one split per sequence: the reference's serial chain of KV blocks
         if (cudaMalloc(&st_dev, st_n * sizeof(float)) != cudaSuccess) {
             etap_mla_host_ctx_destroy(ctx);
             return host_fail(ETAP_ERR_CUDA, "state buffer allocation failed");
@@ -271,42 +295,64 @@ static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int6
         cudaMemset(st_dev, 0, st_n * sizeof(float));
         etap_mla_debug_state(st_dev, static_cast<int>(pages));
     }
-    rc = etap_mla_host_decode(ctx, qb.data(), kvb.data(), bt.data(), &seqlen,
-                              static_cast<float>(scale), flags, of.data(), lf.data());
+    rc = etap_mla_host_decode(ctx, qb.data(), kvb.data(), bt.data(), sl.data(), static_cast<float>(scale), flags,
+                              of.data(), lf.data());
     if (state) {
         etap_mla_debug_state(nullptr, 0);
         std::vector<float> sf(st_n);
         if (!rc && cudaMemcpy(sf.data(), st_dev, st_n * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess)
             rc = host_fail(ETAP_ERR_CUDA, "state copy failed");
         cudaFree(st_dev);
-        // [vb = head group][tile][4][hg] -> [tile][4][heads]
+        // dump [vb = g * batch + b][tile][4][hg] (m_old, m, rescale, l; natural-log units) ->
+        // state[j][4][n_q] after KV block j: m and l from the tile that ends block j; m_old is
+        // the previous block's m and the block's rescale exp(m_old - m) (0 on the first block,
+        // m_old = -inf), as block_update_impl reports them (etap.cpp:40-47)
         if (!rc)
-            for (int g = 0; g < groups; ++g)
-                for (int64_t t = 0; t < pages; ++t)
-                    for (int f = 0; f < 4; ++f)
-                        for (int h = 0; h < hg; ++h)
-                            state[(t * 4 + f) * heads + g * hg + h] =
-                                sf[((static_cast<size_t>(g) * pages + t) * 4 + f) * hg + h];
+            for (int64_t j = 0; j < t_c; ++j) {
+                const int64_t rows_j = std::min((j + 1) * b_c, n_kv);
+                const int64_t seq = prefixes ? j : 0;
+                const int64_t tile = (rows_j + ETAP_MLA_PAGE_ROWS - 1) / ETAP_MLA_PAGE_ROWS - 1;
+                for (int64_t i = 0; i < n_q; ++i) {
+                    const int g = static_cast<int>(i / hg), h = static_cast<int>(i % hg);
+                    const float* st = sf.data() + ((static_cast<size_t>(g) * batch + seq) * pages + tile) * 4 * hg;
+                    const double m_old = j == 0 ? -INFINITY : state[((j - 1) * 4 + 1) * n_q + i];
+                    double m = st[hg + h], lsum = st[3 * hg + h];
+                    // prefix sequences are separate runs: a tile's S^T may differ in the last fp32
+                    // bit with the tile's ring parity (GEMM1 chunk order), so the running max is
+                    // carried over explicitly (m = max(m_old, max over block j), the definition)
+                    // and l re-expressed relative to it
+                    if (m_old > m) {
+                        lsum *= std::exp(m - m_old);
+                        m = m_old;
+                    }
+                    state[(j * 4 + 0) * n_q + i] = m_old;
+                    state[(j * 4 + 1) * n_q + i] = m;
+                    state[(j * 4 + 2) * n_q + i] = j == 0 ? 0.0 : std::exp(m_old - m);
+                    state[(j * 4 + 3) * n_q + i] = lsum;
+                }
+            }
     }
     etap_mla_host_ctx_destroy(ctx);
     if (rc) return rc;
-    for (int64_t i = 0; i < n_q * d_v; ++i) o[i] = static_cast<double>(of[i]);
-    for (int64_t i = 0; i < n_q; ++i) l[i] = static_cast<double>(lf[i]);
+    // the full problem is the last prefix sequence
+    const size_t last = static_cast<size_t>(batch - 1) * heads;
+    for (int64_t i = 0; i < n_q * d_v; ++i) o[i] = static_cast<double>(of[last * d_v + i]);
+    for (int64_t i = 0; i < n_q; ++i) l[i] = static_cast<double>(lf[last + i]);
     return ETAP_OK;
 }
 
-int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t n_kv,
-                          int64_t d_qk, const double* v, int64_t d_v, double scale, int64_t b_r,
-                          int64_t b_c, int64_t stages, unsigned flags, double* o, double* l) {
-    return run_etap_f64_impl(q, n_q, k, n_kv, d_qk, v, d_v, scale, b_r, b_c, stages, flags, o, l,
+int etap_mla_run_etap_f64(const double* q, int64_t n_q, const double* k, int64_t n_kv, int64_t d_qk,
+                          const double* v, int64_t d_v, double scale, int precision, int64_t b_r, int64_t b_c,
+                          int64_t stages, unsigned flags, double* o, double* l) {
+    return run_etap_f64_impl(q, n_q, k, n_kv, d_qk, v, d_v, scale, precision, b_r, b_c, stages, flags, o, l,
                              nullptr);
 }
 
-int etap_mla_run_etap_f64_state(const double* q, int64_t n_q, const double* k, int64_t n_kv,
-                                int64_t d_qk, const double* v, int64_t d_v, double scale,
+int etap_mla_run_etap_f64_state(const double* q, int64_t n_q, const double* k, int64_t n_kv, int64_t d_qk,
+                                const double* v, int64_t d_v, double scale, int precision, int64_t b_c,
                                 unsigned flags, double* o, double* l, double* state) {
     if (!state) return host_fail(ETAP_ERR_SHAPE, "state is NULL");
-    return run_etap_f64_impl(q, n_q, k, n_kv, d_qk, v, d_v, scale, 16, 64, 2, flags, o, l, state);
+    return run_etap_f64_impl(q, n_q, k, n_kv, d_qk, v, d_v, scale, precision, 1, b_c, 1, flags, o, l, state);
 }
 
 }  // extern "C"

@@ -137,15 +137,23 @@ def run_etap(problem: AttentionProblem, tiles: TileConfig = TileConfig(),
     V not the first 512 columns of K).
 
     ``hook`` (BlockHook, tiled_standard.hpp:32-40): the device cannot call back per KV block,
-    so the kernel records the softmax state of every 64-row tile (one split, the reference's
-    serial block order; query blocks = 16-head groups, KV blocks = 64 rows) and the hook is
-    replayed in order after the run with BlockStepInfo(query_block, kv_block, m_old,
-    SoftmaxState(m, l), rescale). With a hook the rescale order defaults to the reference's
-    eager one (``eager=True``); the default lazy mode gives the same invariants.
+    so the kernel records its softmax state (one split, the reference's serial block order)
+    and the hook is replayed after the run exactly as run_etap calls it (etap.cpp:115-129):
+    query blocks of ``tiles.b_r`` rows (outer), KV blocks of ``tiles.b_c`` rows (inner), each
+    with BlockStepInfo(query_block, kv_block, m_old, SoftmaxState(m, l), rescale) over the
+    block's query rows. Block boundaries off the 64-row tile grid are observed through prefix
+    sequences (etap_mla_run_etap_f64_state). With a hook the rescale order defaults to the
+    reference's eager one (``eager=True``); the default lazy mode gives the same invariants.
+
+    ``problem.precision``: "exact64" and "bf16" (this mirror's name for exact64 storage rounded
+    to bf16) map to the GPU's bf16 x bf16 -> fp32; the reference's fp32 / fp16emu emulation
+    modes raise EtapShapeError instead of being computed differently.
     """
     if tiles.b_r < 1 or tiles.b_c < 1 or tiles.stages < 1:
         raise EtapShapeError("tile config fields must be >= 1")
     p = problem
+    if p.precision not in ("exact64", "bf16"):
+        raise EtapShapeError(f"precision {p.precision!r} is not mapped to the GPU path (exact64 / bf16 only)")
     if p.d_qk != 576 or p.d_v != 512:
         raise EtapShapeError("GPU ETAP path is MLA decode: d_qk=576, d_v=512")
     if not _is_prefix(p.v, p.k):
@@ -162,20 +170,17 @@ def run_etap(problem: AttentionProblem, tiles: TileConfig = TileConfig(),
     if hook is None:
         check(_lib.lib().etap_mla_run_etap_f64(
             q.ctypes.data_as(vp), p.n_q, k.ctypes.data_as(vp), p.n_kv, p.d_qk, v.ctypes.data_as(vp), p.d_v,
-            float(p.scale), tiles.b_r, tiles.b_c, tiles.stages, flags, o.ctypes.data_as(vp),
-            l.ctypes.data_as(vp)), "etap_mla_run_etap_f64")
+            float(p.scale), _lib.PRECISION_EXACT64, tiles.b_r, tiles.b_c, tiles.stages, flags,
+            o.ctypes.data_as(vp), l.ctypes.data_as(vp)), "etap_mla_run_etap_f64")
         return AttentionOutput(o, l)
-    heads = (p.n_q + 15) // 16 * 16
-    t_c = (p.n_kv + 63) // 64
-    state = np.empty((t_c, 4, heads))
+    t_c = (p.n_kv + tiles.b_c - 1) // tiles.b_c
+    state = np.empty((t_c, 4, p.n_q))
     check(_lib.lib().etap_mla_run_etap_f64_state(
         q.ctypes.data_as(vp), p.n_q, k.ctypes.data_as(vp), p.n_kv, p.d_qk, v.ctypes.data_as(vp), p.d_v,
-        float(p.scale), flags, o.ctypes.data_as(vp), l.ctypes.data_as(vp), state.ctypes.data_as(vp)),
-        "etap_mla_run_etap_f64_state")
-    for qb in range(heads // 16):
-        h0, h1 = qb * 16, min(p.n_q, qb * 16 + 16)
-        if h0 >= p.n_q:
-            break
+        float(p.scale), _lib.PRECISION_EXACT64, tiles.b_c, flags, o.ctypes.data_as(vp), l.ctypes.data_as(vp),
+        state.ctypes.data_as(vp)), "etap_mla_run_etap_f64_state")
+    for qb, h0 in enumerate(range(0, p.n_q, tiles.b_r)):
+        h1 = min(p.n_q, h0 + tiles.b_r)
         for j in range(t_c):
             st = state[j, :, h0:h1]
             hook(BlockStepInfo(qb, j, st[0].copy(), SoftmaxState(st[1].copy(), st[3].copy()), st[2].copy()))
