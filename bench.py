@@ -1,17 +1,22 @@
 # SPDX-License-Identifier: Apache-2.0
 """ETAP MLA decode benchmark (BASELINE.json metric) — prints ONE JSON line on rank 0.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--scaling strong]
     torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
 
 Workload (BASELINE.json configs[1]): MLA decode, B=16 sequences x 64K latent-KV rows,
 16 heads per GPU, d_qk=576 / d_v=512, bf16 paged KV (64-row pages), fp32 O + LSE.
 A step = K2 (transposed tcgen05 pipeline; it computes the K1 split-KV schedule in its
-prologue) + K3 (LSE combine) on inputs resident in HBM; with N > 1 GPUs every rank owns 16 of the 16*N heads (KV replicated)
-and the step ends with the all-gather of O, fused into K2/K3 stores over NVLink peer memory (NCCL
-all-gather when peer access is missing); weak scaling, SURVEY.md §8e. `e2e` is the same step with
-host buffers: the C-ABI etap_mla_host_decode at N=1, the Python API on every rank at N > 1.
+prologue) + K3 (LSE combine) on inputs resident in HBM. Scaling (SURVEY.md §8e, configs[4]):
+  * weak (default): every rank owns 16 heads, 16*N heads in total (KV replicated);
+  * strong (--scaling strong --total-heads 128): the 128-head DeepSeek-R1 decode split over N
+    ranks, 128/N heads each (N = 1: all 128 heads on one GPU).
+With N > 1 the step ends with the all-gather of O, fused into K2/K3 stores over NVLink peer
+memory (NCCL all-gather when peer access is missing). `e2e` is the same step with host
+buffers: the C-ABI etap_mla_host_decode at N=1, the Python API on every rank at N > 1.
 Inputs (1.2 GB of KV) exceed the 126 MB L2, so no flush is needed between steps.
+`--impl reference` times the reference's own run_etap (exact64, oracle/_ref compiled from the
+reference sources) on the full workload on the host cores.
 """
 from __future__ import annotations
 
@@ -31,6 +36,16 @@ METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"] if (ROOT / "
     "MLA decode µs/step & HBM GB/s (B=16, ctx 64K, 16 heads/GPU); RMSE vs CPU"
 BATCH, CTX, HEADS = 16, 65536, 16
 WORKLOAD = "mla_decode_b16_ctx64k_h16_per_gpu"
+SEED = 42
+
+
+def workload(scaling: str, total_heads: int, world: int) -> tuple[str, int, int]:
+    """(workload name, heads per rank, total heads) of a run."""
+    if scaling == "strong":
+        if total_heads % world or (total_heads // world) % 16:
+            raise SystemExit(f"--total-heads {total_heads} cannot be split into {world} shards of 16k heads")
+        return f"mla_decode_b16_ctx64k_h{total_heads}_strong", total_heads // world, total_heads
+    return WORKLOAD, HEADS, HEADS * world
 
 
 def log(*a):
@@ -114,6 +129,19 @@ def ncu_traffic() -> float | None:
         return None
 
 
+def tensor_peak() -> tuple[float, str]:
+    """Dense bf16 TF/s: the measured cuBLAS figure (MEASURED_PEAKS.json; sustained for a kernel
+    inside a long step), else the B200_PROFILING fallback."""
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d.get("bf16_tflops_sustained") or d["bf16_tflops"]), "measured (sustained)"
+        except Exception:
+            pass
+    return 2250.0, "fallback (nominal dense bf16)"
+
+
 def cpu_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -121,36 +149,32 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-def reference_cpu_sample(q_bits, kv_rows_bits, scale: float, nthreads: int):
-    """Time the reference's run_etap (oracle/_ref, the unmodified etaplab library) on the
-    given sample; returns seconds."""
-    import numpy as np
-
+def reference_full_step(heads: int, ctx: int, steps: int, warmup: int, threads: int) -> tuple[list[float], float]:
+    """The reference's run_etap (exact64, oracle/_ref = the unmodified etaplab library compiled
+    from source) on the FULL workload: B=16 problems of ctx rows x `heads` heads, generated once
+    outside the timed region with the reference generator (the same bf16 operands the GPU arm
+    reads), then `steps` timed steps (each all 16 problems, `threads` workers, like cmd_bench's
+    timed loop over its problems, cli.cpp:277-283). Returns (step seconds, generation seconds)."""
     import oracle
 
-    q = oracle.bf16_widen(q_bits)            # [B, H, 576]
-    kv = oracle.bf16_widen(kv_rows_bits)     # [B, rows, 576]
-    t, _, _ = oracle.ref_mla_run_etap_batch(np.ascontiguousarray(q), np.ascontiguousarray(kv), scale, nthreads)
-    return t
-
-
-def sample_inputs_cpu(inp, rows: int):
-    """Contiguous first `rows` latent rows of every sequence as bf16 bits [B, rows, 576]."""
-    import numpy as np
-    import torch
-
-    B = inp.batch
-    pages = rows // 64
-    idx = inp.block_table[:, :pages].long()                       # [B, pages]
-    kv = inp.kv_pool[idx].reshape(B, pages * 64, 576)             # gather on device
-    qb = inp.q[:, 0].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
-    kvb = kv.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
-    return qb, kvb
+    t0 = time.perf_counter()
+    rb = oracle.RefMlaBench(BATCH, heads, ctx, SEED, 1.0 / math.sqrt(576.0), threads)
+    gen = time.perf_counter() - t0
+    try:
+        times = []
+        for i in range(warmup + steps):
+            t = rb.step()
+            if i >= warmup:
+                times.append(t)
+    finally:
+        rb.close()
+    return times, gen
 
 
 # ------------------------------------------------------------------------ reference arm
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return  # rank 0 alone runs the CPU reference
     import numpy as np
@@ -160,30 +184,25 @@ def run_reference(args) -> None:
     if not oracle.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libetaplab_ref.so not built"}))
         return
-    rows = args.ref_rows
+    name, heads, total = workload(args.scaling, args.total_heads, world)
+    ctx = args.ref_ctx
     threads = cpu_threads()
-    # the same bf16 inputs as the GPU arm, generated on the host with the reference generator
-    seeds = [42 + 7919 * b for b in range(BATCH)]
-    q = np.stack([oracle.bf16_bits(oracle.ref_matrix_from_seed(HEADS, 576, 3 * s + 1)) for s in seeds])
-    kv = np.stack([oracle.bf16_bits(oracle.ref_matrix_from_seed(rows, 576, 3 * s + 2)) for s in seeds])
-    scale = 1.0 / math.sqrt(576.0)
-    times = []
-    for i in range(args.warmup + args.steps):
-        t = reference_cpu_sample(q, kv, scale, threads)
-        if i >= args.warmup:
-            times.append(t)
-    scale_up = CTX / rows
+    times, gen = reference_full_step(heads, ctx, args.steps, args.warmup, threads)
+    scale_up = CTX / ctx
     us = float(np.median(times)) * 1e6 * scale_up
-    sample = (f"run_etap exact64 (reference etaplab, compiled from source) on all {BATCH} sequences x "
-              f"{rows} of {CTX} KV rows x {HEADS} heads per step, {threads} host threads (one per "
-              f"sequence), median of {args.steps} steps scaled x{scale_up:.0f} to the full workload")
+    sample = (f"run_etap exact64 (reference etaplab, compiled from source by oracle/Makefile) on all {BATCH} "
+              f"sequences x {ctx} KV rows x {heads} heads per step (TileConfig 64/64/2, bf16-rounded operands "
+              f"from the reference generator, V = KV[:, :512]; {gen:.1f} s generation outside the timed region), "
+              f"{threads} host threads over the batch, median of {args.steps} steps after {args.warmup} warm-up"
+              + (f", scaled x{scale_up:g} from a reduced context" if ctx != CTX else " (full workload, not scaled)"))
     line = {"metric": METRIC, "value": us, "unit": "us/step", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "batch": BATCH, "ctx": CTX, "heads_per_gpu": HEADS,
-                       "d_qk": 576, "d_v": 512},
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name, "batch": BATCH, "ctx": CTX, "heads_per_gpu": heads, "total_heads": total,
+                       "d_qk": 576, "d_v": 512, "sample_ctx": ctx},
             "cpu_baseline": {"value": us, "unit": "us/step", "cores": threads, "kind": "reference", "sample": sample},
-            "e2e": {"value": us, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": us, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "step_times_s": times}
     print(json.dumps(line), flush=True)
 
 
@@ -193,7 +212,7 @@ def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
 
-    from paper_2506_01969_b200 import inputs, mla, sharding
+    from paper_2506_01969_b200 import _lib, inputs, mla, sharding
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -213,14 +232,14 @@ def run_ours(args) -> None:
         else:
             dist.init_process_group(backend)
 
-    total_heads = HEADS * world
+    name, heads, total_heads = workload(args.scaling, args.total_heads, world)
     seqlens = [CTX] * BATCH
     h0, _ = sharding.head_shard(total_heads, world, rank)
-    inp = inputs.make_mla_inputs(seqlens, heads=HEADS, seed=42, device=dev, pad_value=0.0,
+    inp = inputs.make_mla_inputs(seqlens, heads=heads, seed=SEED, device=dev, pad_value=0.0,
                                  head_offset=h0, total_heads=total_heads)
-    plan = mla.MlaDecodePlan.create(BATCH, HEADS, dev)
-    out = torch.empty((BATCH, 1, HEADS, 512), dtype=torch.float32, device=dev)
-    lse = torch.empty((BATCH, 1, HEADS), dtype=torch.float32, device=dev)
+    plan = mla.MlaDecodePlan.create(BATCH, heads, dev)
+    out = torch.empty((BATCH, 1, heads, 512), dtype=torch.float32, device=dev)
+    lse = torch.empty((BATCH, 1, heads), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     # N > 1: the all-gather of O is fused into the kernels over NVLink peer memory
     # (etap_mla_decode_peer) when every local GPU pair has peer access; ETAP_GATHER=nccl (or no
@@ -239,7 +258,7 @@ def run_ours(args) -> None:
             # first fused step does not verify against the NCCL gather), all fall back to NCCL
             ok = 1
             try:
-                pg = peer.PeerGather(BATCH, HEADS, world, rank, device=dev)
+                pg = peer.PeerGather(BATCH, heads, world, rank, device=dev)
             except Exception as e:  # noqa: BLE001
                 log(f"[bench] rank {rank}: peer gather setup failed ({e})")
                 pg, ok = None, 0
@@ -271,7 +290,7 @@ def run_ours(args) -> None:
         if gather == "peer":  # K2 + K3 store every rank's copy, K4 = arrival flags
             return pg.decode(plan, inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, flags=dflags)
         plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, out=out, lse=lse, flags=dflags)
-        if world > 1:  # head-sharded output -> all 16*N heads on every rank (NCCL all-gather)
+        if world > 1:  # head-sharded output -> all heads on every rank (NCCL all-gather)
             return sharding.gather_heads(out), sharding.gather_heads(lse)
         return out, lse
 
@@ -283,16 +302,23 @@ def run_ours(args) -> None:
                 dist.barrier()
         torch.cuda.synchronize(dev)
 
+    # K2's span per launch without touching programmatic launch (events around K2 would
+    # serialise it): the product kernel stamps %globaltimer per CTA when its grid dependency
+    # resolved and at exit (etap_mla_debug_span); one row of stamps per timed step
+    L = _lib.lib()
+    spans = torch.zeros((args.steps, plan.num_sm_parts, 2), dtype=torch.int64, device=dev)
     for _ in range(args.warmup):
         step()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            L.etap_mla_debug_span(spans[i].data_ptr())
             step()
         ev1.record(stream)
         torch.cuda.synchronize(dev)
+    L.etap_mla_debug_span(None)
     barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
@@ -300,25 +326,20 @@ def run_ours(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     us = ms * 1e3
+    sp = spans.cpu().numpy()
+    k2_us = (sp[:, :, 1].max(axis=1) - sp[:, :, 0].min(axis=1)) / 1e3  # per launch
+    k2_avg_us = float(k2_us.mean())
 
-    # roofline pass: the dominant kernel (K2) timed alone with events on its stream
-    k2_ms = []
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for a, b in evs:
-        a.record(stream)
-        plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, out=out, lse=lse,
-                    flags=mla.FLAG_SKIP_COMBINE)
-        b.record(stream)
-        plan.combine(out, lse)
-    torch.cuda.synchronize(dev)
-    k2_ms = sorted(a.elapsed_time(b) for a, b in evs)
-    k2_avg_ms = sum(k2_ms) / len(k2_ms)
-
-    nbytes = inputs.algorithmic_bytes(seqlens, HEADS)
-    nflops = inputs.flops(seqlens, HEADS)
+    nbytes = inputs.algorithmic_bytes(seqlens, heads)
+    nflops = inputs.flops(seqlens, heads)
     peak, peak_kind = peaks()
-    achieved = nbytes / (k2_avg_ms * 1e-3) / 1e9
-    traffic = ncu_traffic()
+    tpeak, tpeak_kind = tensor_peak()
+    achieved = nbytes / (k2_avg_us * 1e-6) / 1e9
+    achieved_tf = nflops / (k2_avg_us * 1e-6) / 1e12
+    # arithmetic intensity vs the ridge: 16 heads (30 FLOP/B) are HBM-bound, 128 heads (242) sit
+    # at the ridge (peak TF/s / peak GB/s ~ 251)
+    bound = "hbm" if nflops / nbytes < tpeak * 1e12 / (peak * 1e9) else "tensor"
+    traffic = ncu_traffic() if name == WORKLOAD else None
 
     # N > 1 e2e: every rank, through the Python API, with host buffers (all ranks take part)
     e2e_multi = None
@@ -341,13 +362,27 @@ def run_ours(args) -> None:
             e2e_serving = e2e_serving_host(inp, 50, dev)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(inp, args)
+            cpu = cpu_baseline(heads, args)
+        if bound == "hbm":
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "peak_kind": peak_kind, "tensor_frac": achieved_tf / tpeak}
+        else:
+            roof = {"bound": "tensor", "achieved": achieved_tf, "peak": tpeak, "unit": "TFLOP/s",
+                    "frac": achieved_tf / tpeak, "peak_kind": tpeak_kind, "hbm_frac": achieved / peak,
+                    "note": "useful FLOPs 2*H*ctx*(576+512); the bf16 hi+lo split of P doubles the issued GEMM2 "
+                            "FLOPs (1.47x useful) and is not credited"}
+        roof.update({"traffic": traffic, "kernel": "etap_mla_decode_kernel (K2)", "kernel_avg_us": k2_avg_us,
+                     "kernel_min_us": float(k2_us.min()), "kernel_max_us": float(k2_us.max()),
+                     "timing": (f"per-CTA %globaltimer span of the product K2 over the {args.steps} timed steps "
+                                "(max exit - min grid-dependency resolution per launch, etap_mla_debug_span), "
+                                "programmatic launch intact; mean over launches")})
         result = {
             "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "batch": BATCH, "ctx": CTX, "heads_per_gpu": HEADS,
-                       "total_heads": total_heads, "dist_backend": backend if world > 1 else None, "d_qk": 576, "d_v": 512, "page_rows": 64,
+            "config": {"workload": name, "batch": BATCH, "ctx": CTX, "heads_per_gpu": heads,
+                       "total_heads": total_heads, "dist_backend": backend if world > 1 else None, "d_qk": 576,
+                       "d_v": 512, "page_rows": 64, "head_group": mla.head_group(heads),
                        "kv_bytes_per_gpu": inp.kv_bytes(), "l2": "inputs (1.2 GB KV) > 126 MB L2, no flush",
                        "parallelism": (f"head-shard tp{world} (KV replicated, all-gather of O fused into K2/K3 "
                                        "over NVLink peer memory)" if gather == "peer" else
@@ -359,11 +394,9 @@ def run_ours(args) -> None:
             "throughput": {"hbm_gbs_aggregate": nbytes * world / (us * 1e-6) / 1e9,
                            "hbm_gbs_per_gpu": nbytes / (us * 1e-6) / 1e9,
                            "tflops_aggregate": nflops * world / (us * 1e-6) / 1e12,
-                           "algorithmic_bytes_per_step_per_gpu": nbytes},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "etap_mla_decode_kernel (K2)",
-                         "kernel_avg_us": k2_avg_ms * 1e3, "peak_kind": peak_kind,
-                         "timing": f"second timed pass of {args.steps} steps, CUDA events around each K2 launch"},
+                           "tflops_per_gpu": nflops / (us * 1e-6) / 1e12,
+                           "algorithmic_bytes_per_step_per_gpu": nbytes, "flops_per_step_per_gpu": nflops},
+            "roofline": roof,
             "clocks": clocks,
             "gpu_launches": (3 if gather == "peer" else 2) * args.steps,
             "e2e": e2e,
@@ -513,22 +546,24 @@ def e2e_serving_host(inp, steps: int, dev) -> dict:
                    "row per sequence + seqlens, append, decode, D2H of O/LSE, synchronous)", "steps": steps}
 
 
-def cpu_baseline(inp, args) -> dict | None:
+def cpu_baseline(heads: int, args) -> dict | None:
+    """The reference's CPU path on this box's host cores: one full step (all 16 sequences x 64K
+    rows) of run_etap exact64 after one warm-up step, on the same operands as the GPU arm."""
     try:
         import oracle
 
         if not oracle.ref_available():
             return None
-        rows = args.cpu_rows
         threads = cpu_threads()
-        qb, kvb = sample_inputs_cpu(inp, rows)
-        t = reference_cpu_sample(qb, kvb, inp.scale, threads)
-        scale_up = CTX / rows
-        us = t * 1e6 * scale_up
+        times, gen = reference_full_step(heads, args.cpu_ctx, 1, 1, threads)
+        scale_up = CTX / args.cpu_ctx
+        us = times[0] * 1e6 * scale_up
         return {"value": us, "unit": "us/step", "cores": threads, "kind": "reference",
-                "sample": (f"reference run_etap exact64 (oracle/_ref, etaplab compiled from source) on the same "
-                           f"bf16 inputs: {BATCH} sequences x first {rows} of {CTX} rows x {HEADS} heads, "
-                           f"{threads} threads, {t:.2f} s wall, scaled x{scale_up:.0f}")}
+                "sample": (f"reference run_etap exact64 (oracle/_ref, etaplab compiled from source) on {BATCH} "
+                           f"sequences x {args.cpu_ctx} rows x {heads} heads, the GPU arm's operands (reference "
+                           f"generator, bf16-rounded, V = KV[:, :512]; {gen:.1f} s generation untimed), {threads} "
+                           f"threads, one step after one warm-up step, {times[0]:.2f} s wall"
+                           + (f", scaled x{scale_up:g}" if args.cpu_ctx != CTX else " (full workload, not scaled)"))}
     except Exception as e:  # pragma: no cover
         log(f"[bench] cpu baseline failed: {e}")
         return None
@@ -540,9 +575,12 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: 16 heads per GPU (16*N total); strong: --total-heads split over N GPUs")
+    ap.add_argument("--total-heads", type=int, default=128, help="heads of the strong-scaling workload")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-rows", type=int, default=16384, help="KV rows per sequence in the CPU baseline sample")
-    ap.add_argument("--ref-rows", type=int, default=2048, help="KV rows per sequence per reference-arm step")
+    ap.add_argument("--cpu-ctx", type=int, default=CTX, help="KV rows per sequence of the CPU baseline step")
+    ap.add_argument("--ref-ctx", type=int, default=CTX, help="KV rows per sequence of each reference-arm step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

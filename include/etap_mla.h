@@ -313,6 +313,13 @@ int etap_mla_selftest_fp8(const void* k8, const void* q8, const void* p8, float*
  * instantiation carries no stamps at all). */
 int etap_mla_debug_trace(void* device_buf);
 
+/* Kernel span (bench timing that keeps programmatic dependent launch intact): when device_buf
+ * is non-NULL, the product decode kernels (bf16 and FP8) record per CTA [cta][2] uint64
+ * %globaltimer ns: 0 = its grid dependency resolved (the earliest moment it may read KV), 1 =
+ * exit. The launch reads the pointer at launch time, so a caller may point successive launches
+ * at successive rows. NULL (default) disables; two stores per CTA outside every loop. */
+int etap_mla_debug_span(void* device_buf);
+
 /* Debug: combine-kernel stamps [block][4] (entry, after grid-dependency wait, exit) or NULL. */
 int etap_mla_debug_trace_combine(void* device_buf);
 

@@ -100,6 +100,12 @@ def ref() -> C.CDLL:
         L.ref_load_matrix.argtypes = [C.c_char_p, vp, i64, C.POINTER(i64), C.POINTER(i64)]
         L.ref_mla_run_etap_batch.restype = f64
         L.ref_mla_run_etap_batch.argtypes = [vp, vp, i64, i64, i64, f64, i32, vp, vp]
+        L.ref_mla_bench_create.restype = vp
+        L.ref_mla_bench_create.argtypes = [i64, i64, i64, C.c_uint64, f64, i32]
+        L.ref_mla_bench_step.restype = f64
+        L.ref_mla_bench_step.argtypes = [vp, i32, vp, vp]
+        L.ref_mla_bench_destroy.restype = None
+        L.ref_mla_bench_destroy.argtypes = [vp]
         _ref = L
     return _ref
 
@@ -283,3 +289,28 @@ def ref_mla_run_etap_batch(q: np.ndarray, kv: np.ndarray, scale: float, nthreads
     if t < 0:
         raise RuntimeError("reference run_etap failed")
     return t, o, l
+
+
+class RefMlaBench:
+    """The bench's full-size CPU workload on the reference (oracle/_ref): B MLA problems of
+    ctx rows x H heads generated once with the reference generator (seeds seed0 + 7919 b,
+    bf16-rounded, V = KV[:, :512]); step() times run_etap (exact64) over all of them."""
+
+    def __init__(self, batch: int, heads: int, ctx: int, seed0: int, scale: float, nthreads: int):
+        self.batch, self.heads, self.nthreads = batch, heads, nthreads
+        self.h = ref().ref_mla_bench_create(batch, heads, ctx, seed0, float(scale), int(nthreads))
+        if not self.h:
+            raise RuntimeError("reference workload creation failed")
+
+    def step(self, outputs: bool = False):
+        o = np.empty((self.batch, self.heads, 512)) if outputs else None
+        l = np.empty((self.batch, self.heads)) if outputs else None
+        t = ref().ref_mla_bench_step(self.h, self.nthreads, _dp(o) if outputs else None, _dp(l) if outputs else None)
+        if t < 0:
+            raise RuntimeError("reference run_etap failed")
+        return (t, o, l) if outputs else t
+
+    def close(self) -> None:
+        if self.h:
+            ref().ref_mla_bench_destroy(self.h)
+            self.h = None

@@ -6,6 +6,7 @@
 // It only marshals plain arrays into etaplab::Matrix / AttentionProblem and calls the
 // reference's own functions; no reference code is copied here.
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -188,6 +189,85 @@ double ref_mla_run_etap_batch(const double* q, const double* kv, std::int64_t ba
         return -1.0;
     }
 }
+
+// Full-size CPU workload of the bench (BASELINE.json configs[1]: B sequences x ctx rows x H
+// heads): the B MLA problems are generated ONCE with the reference's own generator
+// (matrix_from_seed, seeds s_b = seed0 + 7919 b as cmd_bench, cli.cpp:239; Q from s*3+1, latent
+// KV from s*3+2, attention.cpp:38-39), rounded to bf16 (the operands the GPU reads, i.e. the
+// device inputs of inputs.make_mla_inputs, pinned equal by the tests), V = KV.col_block(0, 512).
+// Generation runs in parallel and outside every timed region; each step then times run_etap
+// (exact64, cmd_bench's TileConfig{64,64,2}) on all B problems, one std::thread per worker over
+// the batch, like ref_mla_run_etap_batch. Returns an opaque handle (nullptr on error).
+struct RefBench {
+    std::vector<AttentionProblem> probs;
+    std::vector<AttentionOutput> outs;
+};
+
+static double bf16_round_rne(double x) {
+    const double ax = std::fabs(x);
+    if (ax == 0.0 || !std::isfinite(x)) return x;
+    int e;
+    std::frexp(ax, &e);
+    return std::copysign(std::ldexp(std::nearbyint(std::ldexp(ax, 8 - e)), e - 8), x);
+}
+
+void* ref_mla_bench_create(std::int64_t batch, std::int64_t heads, std::int64_t ctx, std::uint64_t seed0,
+                           double scale, int nthreads) {
+    try {
+        auto* rb = new RefBench();
+        rb->probs.resize(batch);
+        rb->outs.resize(batch);
+        if (nthreads < 1) nthreads = 1;
+        std::vector<std::thread> th;
+        for (int w = 0; w < nthreads; ++w)
+            th.emplace_back([&, w] {
+                for (std::int64_t b = w; b < batch; b += nthreads) {
+                    const std::uint64_t s = seed0 + 7919ull * static_cast<std::uint64_t>(b);
+                    Matrix q = matrix_from_seed(heads, 576, s * 3 + 1, Dist::normal);
+                    Matrix kv = matrix_from_seed(ctx, 576, s * 3 + 2, Dist::normal);
+                    for (std::size_t i = 0; i < q.size(); ++i) q.data()[i] = bf16_round_rne(q.data()[i]);
+                    for (std::size_t i = 0; i < kv.size(); ++i) kv.data()[i] = bf16_round_rne(kv.data()[i]);
+                    Matrix v = kv.col_block(0, 512);
+                    rb->probs[b] = make_problem(std::move(q), std::move(kv), std::move(v), scale, Precision::exact64);
+                }
+            });
+        for (auto& t : th) t.join();
+        return rb;
+    } catch (const std::exception&) {
+        return nullptr;
+    }
+}
+
+// One timed step: run_etap on every problem (nthreads workers); seconds, or -1 on error.
+// o / l (optional, [B][H][512] / [B][H]) receive the outputs.
+double ref_mla_bench_step(void* h, int nthreads, double* o, double* l) {
+    auto* rb = static_cast<RefBench*>(h);
+    if (!rb) return -1.0;
+    try {
+        const std::int64_t batch = static_cast<std::int64_t>(rb->probs.size());
+        const TileConfig tiles{64, 64, 2};  // cmd_bench defaults (cli.hpp:30-63)
+        if (nthreads < 1) nthreads = 1;
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> th;
+        for (int w = 0; w < nthreads; ++w)
+            th.emplace_back([&, w] {
+                for (std::int64_t b = w; b < batch; b += nthreads) rb->outs[b] = run_etap(rb->probs[b], tiles);
+            });
+        for (auto& t : th) t.join();
+        const auto t1 = std::chrono::steady_clock::now();
+        if (o && l)
+            for (std::int64_t b = 0; b < batch; ++b) {
+                const std::size_t H = rb->outs[b].l.size();
+                std::memcpy(o + b * H * 512, rb->outs[b].o.data(), sizeof(double) * H * 512);
+                std::memcpy(l + b * H, rb->outs[b].l.data(), sizeof(double) * H);
+            }
+        return std::chrono::duration<double>(t1 - t0).count();
+    } catch (const std::exception&) {
+        return -1.0;
+    }
+}
+
+void ref_mla_bench_destroy(void* h) { delete static_cast<RefBench*>(h); }
 
 // utilization / predicted_speedup (wgmma_model.cpp:54-86) with the given WgmmaSpec.
 // out = {useful_macs, issued_macs, utilization, qk m-axis util, pv m-axis util, speedup}

@@ -76,6 +76,7 @@ def _declare(lib: C.CDLL) -> None:
         "etap_mla_debug_state": (i32, [vp, i32]),
         "etap_mla_run_etap_f64_state": (i32, [vp, i64, vp, i64, i64, vp, i64, f64, i32, i64, u32, vp, vp, vp]),
         "etap_mla_debug_trace": (i32, [vp]),
+        "etap_mla_debug_span": (i32, [vp]),
         "etap_mla_debug_trace_combine": (i32, [vp]),
         "etap_mla_umma_bench": (i32, [i32, i32, vp, i32]),
         "etap_mla_stream_bench": (i32, [vp, i64, i32, i32, i32, vp]),

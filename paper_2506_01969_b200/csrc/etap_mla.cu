@@ -442,11 +442,18 @@ struct Prologue {
 };
 
 // The producer's grid-dependency wait when decode_prologue deferred it (whole warp 0).
+// Kernel span (bench roofline timing without breaking programmatic launch): when prm.span is
+// set, thread 0 of every CTA records %globaltimer when its grid dependency resolved (the first
+// moment it may touch KV) and at exit: span[cta][0..1]. Two stores per CTA outside every loop.
+__device__ __forceinline__ void span_stamp(const DecodeParams& prm, int slot) {
+    if (prm.span != nullptr) prm.span[blockIdx.x * 2 + slot] = ptx::global_timer_ns();
+}
+
 template <bool kDebug>
 __device__ __forceinline__ void dep_wait_producer(const DecodeParams& prm) {
     ptx::grid_dep_wait();
     ptx::grid_dep_launch();
-    if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
+    if (threadIdx.x == 0) { span_stamp(prm, 0); ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
 }
 
 template <bool kDebug, int MAXVB>
@@ -519,7 +526,7 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
         if (warp == 0 && r.hint_b >= 0 && r.hint_t0 + lane < prm.max_pages)
             r.hint_pg = prm.block_table[static_cast<size_t>(r.hint_b) * prm.max_pages + r.hint_t0 + lane];
     }
-    if (threadIdx.x == 0 && !early) { ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
+    if (threadIdx.x == 0 && !early) { span_stamp(prm, 0); ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
     if (fused) {
         if (early) {
             if (warp == 3) publish_schedule(prm, ls, s_soff, s_sched, lane, 32);
@@ -1034,6 +1041,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
     ptx::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
+        span_stamp(prm, 1);
         ETAP_TRACE_G(prm, 2);
         ETAP_TRACE_CLK(prm, 6);
         if (prm.trace != nullptr) {
@@ -1544,6 +1552,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
+        span_stamp(prm, 1);
         ETAP_TRACE_G(prm, 2);
         ETAP_TRACE_CLK(prm, 6);
     }
@@ -1874,6 +1883,7 @@ int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_row
 }
 
 void* g_trace_buf = nullptr;  // debug tracing target (etap_mla_debug_trace)
+void* g_span_buf = nullptr;   // kernel-span stamps (etap_mla_debug_span)
 void* g_state_buf = nullptr;  // debug softmax-state dump target (etap_mla_debug_state)
 void* g_combine_trace_buf = nullptr;  // debug: [block][4] stamps of the combine kernel
 int g_state_tiles = 0;
@@ -2337,6 +2347,7 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.flags = flags;
     prm.trace = static_cast<unsigned long long*>(g_trace_buf);
+    prm.span = static_cast<unsigned long long*>(g_span_buf);
     prm.state = static_cast<float*>(g_state_buf);
     prm.state_tiles = g_state_tiles;
     const bool dbg = prm.trace != nullptr || prm.state != nullptr;  // debug instantiation
@@ -2453,6 +2464,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     prm.scale_log2 = scale * kv_scale * 1.4426950408889634f;
     prm.flags = flags;
     prm.trace = static_cast<unsigned long long*>(g_trace_buf);
+    prm.span = static_cast<unsigned long long*>(g_span_buf);
     prm.state = nullptr;
     prm.state_tiles = 0;
 
@@ -2586,6 +2598,11 @@ int etap_mla_debug_state(void* device_buf, int max_tiles) {
 
 int etap_mla_debug_trace(void* device_buf) {
     g_trace_buf = device_buf;
+    return ETAP_OK;
+}
+
+int etap_mla_debug_span(void* device_buf) {
+    g_span_buf = device_buf;
     return ETAP_OK;
 }
 

@@ -343,6 +343,7 @@ struct DecodeParams {
     float scale_log2;
     unsigned flags;
     unsigned long long* trace;  // debug: [cta][TRACE_TILES][TRACE_SLOTS] stamps (ETAP_TRACE), or null
+    unsigned long long* span;   // [cta][2] %globaltimer at grid-dependency resolution / exit, or null
     float* state;               // debug: per-tile softmax state [vb][state_tiles][4][16], or null
     int state_tiles;
 };

@@ -25,7 +25,7 @@ def test_reference_arm_json_line():
     if not oracle.ref_available():
         pytest.skip("oracle/_ref not built")
     res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "2",
-                          "--warmup", "3", "--ref-rows", "64"], capture_output=True, text=True, timeout=300,
+                          "--warmup", "3", "--ref-ctx", "256"], capture_output=True, text=True, timeout=300,
                          cwd=ROOT)
     assert res.returncode == 0, res.stderr
     lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
