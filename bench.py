@@ -244,13 +244,11 @@ def run_ours(args) -> None:
     # N > 1: the all-gather of O is fused into the kernels over NVLink peer memory
     # (etap_mla_decode_peer) when every local GPU pair has peer access; ETAP_GATHER=nccl (or no
     # peer access) uses decode + ncclAllGather instead
-    gather = None
+    gather, fallback = None, None
     if world > 1:
         gather = os.environ.get("ETAP_GATHER", "peer")
-        ndev = torch.cuda.device_count()
-        if gather == "peer" and not all(torch.cuda.can_device_access_peer(gpu, d) for d in range(ndev) if d != gpu):
-            log("[bench] no peer access between all GPUs: falling back to NCCL all-gather")
-            gather = "nccl"
+        if gather != "peer":
+            fallback = f"ETAP_GATHER={gather}"
         if gather == "peer":
             from paper_2506_01969_b200 import peer
 
@@ -259,9 +257,9 @@ def run_ours(args) -> None:
             ok = 1
             try:
                 pg = peer.PeerGather(BATCH, heads, world, rank, device=dev)
-            except Exception as e:  # noqa: BLE001
-                log(f"[bench] rank {rank}: peer gather setup failed ({e})")
-                pg, ok = None, 0
+            except Exception as e:  # noqa: BLE001  (peer.PeerAccessUnavailable: no P2P between some pair)
+                log(f"[bench] rank {rank}: peer gather setup failed ({e}); falling back to the NCCL all-gather")
+                pg, ok, fallback = None, 0, f"rank {rank}: {e}"
             fdev = dev if backend == "nccl" else "cpu"
             flag = torch.tensor([ok], device=fdev)
             dist.all_reduce(flag, op=dist.ReduceOp.MIN)
@@ -275,7 +273,9 @@ def run_ours(args) -> None:
                 dist.all_reduce(flag, op=dist.ReduceOp.MIN)
                 if int(flag.item()) != 1:
                     log("[bench] fused peer gather differs from the NCCL gather: falling back to NCCL")
+                    fallback = "fused peer gather differs from the NCCL gather"
             if int(flag.item()) != 1:
+                fallback = fallback or "peer gather setup failed on another rank"
                 if pg is not None:
                     pg.close()
                 gather = "nccl"
@@ -387,7 +387,7 @@ def run_ours(args) -> None:
                        "parallelism": (f"head-shard tp{world} (KV replicated, all-gather of O fused into K2/K3 "
                                        "over NVLink peer memory)" if gather == "peer" else
                                        f"head-shard tp{world} (KV replicated, NCCL all-gather of O)") if world > 1
-                       else "single GPU", "decode_flags": "ETAP_FLAG_EARLY_METADATA (seqlens / block_table read "
+                       else "single GPU", "gather_fallback_reason": fallback, "decode_flags": "ETAP_FLAG_EARLY_METADATA (seqlens / block_table read "
                        "before the grid dependency; opt-in, nothing in the step writes them)",
                        "step": "K2 decode (in-kernel split schedule) + K3 combine" +
                        ((" + K4 peer arrival" if gather == "peer" else " + NCCL all-gather(O)") if world > 1 else "")},

@@ -52,6 +52,27 @@ def _open(handle: bytes) -> int:
     return p.value
 
 
+class PeerAccessUnavailable(RuntimeError):
+    """Some rank pair cannot map each other's memory (no CUDA peer access between their GPUs,
+    or a peer GPU that is not visible to this process): the caller falls back to NCCL."""
+
+
+def _device_uuid(index: int) -> str:
+    return str(torch.cuda.get_device_properties(index).uuid)
+
+
+def check_peer_access(my_index: int, uuids: list[str]) -> None:
+    """Raise PeerAccessUnavailable unless this process can access every rank's GPU: the same
+    device (CUDA IPC within one GPU) or a peer that cudaDeviceCanAccessPeer allows."""
+    local = {_device_uuid(i): i for i in range(torch.cuda.device_count())}
+    for r, u in enumerate(uuids):
+        idx = local.get(u)
+        if idx is None:
+            raise PeerAccessUnavailable(f"rank {r}'s GPU {u} is not visible to this process")
+        if idx != my_index and not torch.cuda.can_device_access_peer(my_index, idx):
+            raise PeerAccessUnavailable(f"no CUDA peer access from GPU {my_index} to GPU {idx} (rank {r})")
+
+
 class PeerGather:
     """Full-head output buffers shared by ``world`` ranks (``nbuf`` sets used round robin by
     epoch, so a rank one call ahead never overwrites rows a slower rank still reads)."""
@@ -78,13 +99,24 @@ class PeerGather:
         own.append(pf)
         handles.append(hf)
         self._own = own
+        my_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        mine = (_device_uuid(my_index), handles)
         if world > 1:
             import torch.distributed as dist
 
-            allh = [None] * world
-            dist.all_gather_object(allh, handles, group=group)
+            alli = [None] * world
+            dist.all_gather_object(alli, mine, group=group)
         else:
-            allh = [handles]
+            alli = [mine]
+        allh = [h for _, h in alli]
+        # every peer pair is checked BEFORE any handle is mapped (cudaIpcOpenMemHandle with lazy
+        # peer enable would otherwise fail late, or fault in the kernel)
+        try:
+            check_peer_access(my_index, [u for u, _ in alli])
+        except PeerAccessUnavailable:
+            for p in own:
+                _lib.lib().etap_mla_ipc_free(C.c_void_p(p))
+            raise
         self._opened = []
         ptrs = []  # ptrs[r] = rank r's pointers mapped in this process
         for r in range(world):
