@@ -574,6 +574,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
             ptx::mbar_init(&bars[BAR_G2_DONE + i], 1);
             ptx::mbar_init(&bars[BAR_G2_HALF + i], 1);
             ptx::mbar_init(&bars[BAR_G2_3Q + i], 1);
+            ptx::mbar_init(&bars[BAR_G2_Q1 + i], 1);
         }
         ptx::mbar_init(&bars[BAR_Q_FULL], 1);
         ptx::mbar_init(&bars[BAR_Q_EMPTY], 1);
@@ -639,7 +640,9 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 const uint32_t tb = gt % NTB;
                 const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
                 if (gt == 0 && pro.late_wait) dep_wait_producer<kDebug>(prm);
-                if (gt >= 3) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 3) % NTB], ((gt - 3) / NTB) & 1);
+                // group A reuses slots of tile gt - A_LAG (all GEMM2 work of that tile done)
+                constexpr uint32_t A_LAG = C::RING16 ? 2 : 3;
+                if (gt >= A_LAG) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - A_LAG) % NTB], ((gt - A_LAG) / NTB) & 1);
                 if (lane == 0) {
                     if (gt == 0) { ETAP_TRACE_G(prm, 9); ETAP_TRACE_CLK(prm, 15); }
                     ETAP_TRACE(prm, gt, 0);
@@ -650,6 +653,14 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                         ptx::tma_load_2d(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_A + tb],
                                          chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
                     }
+#ifndef ETAP_NO_LATE_PREFETCH
+                    // 16-slot ring: the tile's last chunks can only load once GEMM2 of the
+                    // previous tile released its first positions; warm them in L2 now so that
+                    // load is an L2 hit on the critical path
+                    if constexpr (C::RING16)
+                        for (int pos = C::SPLIT_POS; pos < NCHUNK; ++pos)
+                            ptx::tma_prefetch_2d(&tm_kv, chunk_at(pos, gt) * 64, page * PAGE);
+#endif
                 }
                 __syncwarp();
                 if (q_pending) {
@@ -669,8 +680,13 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     ++nsplit;
                 }
                 // positions [SPLIT_POS, SPLIT_POS2) reuse tile gt-2's first four positions: free
-                // once GEMM2 d-blocks 0-1 of gt-2 completed
-                if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_HALF + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+                // once GEMM2 d-blocks 0-1 of gt-2 completed (16-slot ring: tile gt-1's first two
+                // positions, free once GEMM2 d-block 0 of gt-1 completed)
+                if constexpr (C::RING16) {
+                    if (gt >= 1) ptx::mbar_wait(&bars[BAR_G2_Q1 + (gt - 1) % NTB], ((gt - 1) / NTB) & 1);
+                } else {
+                    if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_HALF + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+                }
                 if (lane == 0) {
                     ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_B + tb], (C::SPLIT_POS2 - C::SPLIT_POS) * SLOT_BYTES);
 #pragma unroll 1
@@ -758,6 +774,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     sa = sa >= C::NSLOT ? sa - C::NSLOT : sa;
                     issue_gemm2_block<C>(tmem_base + C::TCOL_O + C::OBLK * blk, ring_addr + sa * SLOT_BYTES,
                                          p_addr + (buf % C::P_BUFS) * C::P_BYTES, t == sd.t0);
+                    if (C::RING16 && blk == 0) ptx::umma_commit_elect(&bars[BAR_G2_Q1 + gt % NTB]);
                     if (blk == 1) ptx::umma_commit_elect(&bars[BAR_G2_HALF + gt % NTB]);
                     if (C::G3_AFTER_3Q && C::THIRD_GROUP && blk == 2) ptx::umma_commit_elect(&bars[BAR_G2_3Q + gt % NTB]);
                 }
@@ -856,7 +873,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                         } else {
                             const float mn = fmaxf(m_own[j], mt);
                             if (mn > m_own[j] + thresh) {
-                                alpha_own[j] = exp2f(m_own[j] - mn);
+                                alpha_own[j] = ptx::exp2_ftz(m_own[j] - mn);
                                 m_own[j] = mn;
                                 upd = true;
                             }
@@ -877,7 +894,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 for (int j = 0; j < HH; ++j) {
                     // a column may have no visible row yet (multi-token causal mask): m = -inf
                     const float mu = (mtp && m_own[j] == -INFINITY) ? 0.f : m_own[j];
-                    pv[j] = exp2f(x[j] - mu);
+                    pv[j] = ptx::exp2_ftz(x[j] - mu);
                     l_part[j] = first ? pv[j] : fmaf(l_part[j], alpha_own[j], pv[j]);
                 }
                 if (debug) {
@@ -914,14 +931,16 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
 #pragma unroll 1
                     for (int blk = 0; blk < 4; ++blk) {
 #pragma unroll
-                        for (int seg = 0; seg < 2; ++seg) {
+                        for (int seg = 0; seg < C::OSEG * (HW / 16); ++seg) {  // SAME_D: one accumulator
                             uint32_t o[16];
-                            const uint32_t ta = t_lane + C::TCOL_O + C::OBLK * blk + seg * HG + hoff;
+                            const int sub = seg % (HW / 16);
+                            const uint32_t ta =
+                                t_lane + C::TCOL_O + C::OBLK * blk + (seg / (HW / 16)) * HG + hoff + 16 * sub;
                             ptx::tmem_ld16(ta, o);
                             ptx::tmem_wait_ld();
 #pragma unroll
                             for (int c = 0; c < 16; ++c) {
-                                const float a = s_alpha[hoff + c];
+                                const float a = s_alpha[hoff + 16 * sub + c];
                                 o[c] = __float_as_uint(__uint_as_float(o[c]) * (negate ? -a : a));
                             }
                             ptx::tmem_st16(ta, o);
@@ -959,7 +978,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
             if (tracer) ETAP_TRACE_G(prm, 10);
             // two d-blocks per TMEM load wait: this warpgroup's 16 hi + 16 lo columns each
             constexpr int BPW = 2;
-            uint32_t o[BPW][2 * HW];
+            uint32_t o[BPW][C::OSEG * HW];  // SAME_D: the HW summed columns only
             const float wsum = halfwarp_reduce<false, HH>(l_part, lane);
             if (rwriter) red_sum[wq * HG + hoff + half * HH + rhead] = wsum;
             const int ns = soff[vb + 1] - soff[vb];
@@ -994,9 +1013,11 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
 #pragma unroll
                 for (int bb = 0; bb < BPW; ++bb)
 #pragma unroll
-                    for (int seg = 0; seg < 2; ++seg)
-                        ptx::tmem_ld16(t_lane + C::TCOL_O + C::OBLK * (blk0 + bb) + seg * HG + hoff,
-                                       *reinterpret_cast<uint32_t(*)[16]>(&o[bb][16 * seg]));
+                    for (int seg = 0; seg < C::OSEG; ++seg)
+#pragma unroll
+                        for (int sub = 0; sub < HW / 16; ++sub)
+                            ptx::tmem_ld16(t_lane + C::TCOL_O + C::OBLK * (blk0 + bb) + seg * HG + hoff + 16 * sub,
+                                           *reinterpret_cast<uint32_t(*)[16]>(&o[bb][HW * seg + 16 * sub]));
                 ptx::tmem_wait_ld();
                 if (tracer && blk0 == 0) ETAP_TRACE(prm, last, 14);
 #pragma unroll
@@ -1005,7 +1026,8 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     float v[HW];
 #pragma unroll
                     for (int h = 0; h < HW; ++h)
-                        v[h] = (__uint_as_float(o[bb][h]) + __uint_as_float(o[bb][HW + h])) * inv_l[h];
+                        v[h] = (C::OSEG == 2 ? __uint_as_float(o[bb][h]) + __uint_as_float(o[bb][(C::OSEG - 1) * HW + h])
+                                             : __uint_as_float(o[bb][h])) * inv_l[h];
                     if (direct) {
                         // every output copy (peer gather: each rank's buffer over NVLink)
 #pragma unroll 1
@@ -1408,7 +1430,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         } else {
                             const float mn = fmaxf(m_own[j], mt);
                             if (mn > m_own[j] + thresh) {
-                                alpha_own[j] = exp2f(m_own[j] - mn);
+                                alpha_own[j] = ptx::exp2_ftz(m_own[j] - mn);
                                 m_own[j] = mn;
                                 upd = true;
                             }
@@ -1427,7 +1449,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < HH; ++j) {
                     const float mu = (mtp && m_own[j] == -INFINITY) ? 0.f : m_own[j];
-                    pv[j] = exp2f(x[j] - mu);
+                    pv[j] = ptx::exp2_ftz(x[j] - mu);
                     l_part[j] = first ? pv[j] : fmaf(l_part[j], alpha_own[j], pv[j]);
                 }
                 // the P buffer is reused every other tile: GEMM2(gt-2) must have read it
@@ -1983,7 +2005,8 @@ int head_group_of(int heads) {
         return e ? std::atoi(e) : 0;
     }();
     if (forced == 16) return 16;
-    return heads % 32 == 0 ? 32 : 16;
+    if (forced == 32) return heads % 32 == 0 ? 32 : 16;
+    return heads % 64 == 0 ? 64 : (heads % 32 == 0 ? 32 : 16);
 }
 
 bool heads_ok(int heads) { return heads >= 16 && heads % 16 == 0; }
@@ -2334,7 +2357,7 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     prm.split_off_out = const_cast<int32_t*>(split_off);
     prm.lanes_on = lanes_enabled() ? 1 : 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
-    const int max_vb = hg == 16 ? Cfg<16>::MAX_VB : Cfg<32>::MAX_VB;
+    const int max_vb = MAX_FUSED_VB;
     prm.inkernel_sched = (ls.line_n <= max_vb && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
     prm.early_meta = (early_meta_enabled() && (flags & ETAP_FLAG_EARLY_METADATA)) ? 1 : 0;
     prm.fixed_cost = META_FIXED_COST;
@@ -2362,7 +2385,15 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_attrs();
-    if (hg == 32) {
+    if (hg == 64) {
+        cfg.dynamicSmemBytes = Cfg<64>::SMEM_ALLOC;
+        cfg.blockDim = dim3(Cfg<64>::THREADS);
+        auto kern = dbg ? etap_mla_decode_kernel<64, true> : etap_mla_decode_kernel<64, false>;
+        static int attr_rc = ensure_smem_attr(etap_mla_decode_kernel<64, false>, Cfg<64>::SMEM_ALLOC) |
+                             ensure_smem_attr(etap_mla_decode_kernel<64, true>, Cfg<64>::SMEM_ALLOC);
+        if (attr_rc) return attr_rc;
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, kern, tm_kv, tm_q, prm));
+    } else if (hg == 32) {
         cfg.dynamicSmemBytes = Cfg<32>::SMEM_ALLOC;
         cfg.blockDim = dim3(Cfg<32>::THREADS);
         auto kern = dbg ? etap_mla_decode_kernel<32, true> : etap_mla_decode_kernel<32, false>;

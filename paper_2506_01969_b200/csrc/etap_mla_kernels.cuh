@@ -34,7 +34,7 @@ constexpr int NCHUNK = 9;       // 576 / 64 column chunks (SW128 atoms are 64 bf
 constexpr int NVCHUNK = 8;      // 512 / 64 chunks that are also V
 constexpr int SLOT_BYTES = TILE * 128;  // 64 rows x 128 B = 8 KiB per ring slot
 constexpr int NTB = 4;          // tile-barrier ring depth (tiles in flight <= NSLOT/9 + 1)
-constexpr int NBAR = 6 * NTB + 8;
+constexpr int NBAR = 7 * NTB + 8;
 // Longest line (batch * head groups, or batch with lanes) whose split schedule the decode
 // kernel computes itself (the block-wide scan takes one line entry per thread of the >= 256-
 // thread CTA); longer lines run K1 first.
@@ -78,6 +78,7 @@ constexpr int BAR_G2_HALF = 3 * NTB;    // [NTB] GEMM2 d-blocks 0-1 of tile gt c
                                         //       rope slot and V chunks 0-3 are free
 constexpr int BAR_FULL_C = 4 * NTB + 8;  // [NTB] ring positions [SPLIT_POS2, 9) of tile gt landed
 constexpr int BAR_G2_3Q = 5 * NTB + 8;   // [NTB] GEMM2 d-blocks 0-2 of tile gt complete (V0..V5 free)
+constexpr int BAR_G2_Q1 = 6 * NTB + 8;   // [NTB] GEMM2 d-block 0 of tile gt complete (its first two positions free)
 constexpr int BAR_Q_FULL = 4 * NTB + 0;
 constexpr int BAR_Q_EMPTY = 4 * NTB + 1;
 constexpr int BAR_S_FULL = 4 * NTB + 2;  // [2]
@@ -87,35 +88,48 @@ constexpr int BAR_P_FULL = 4 * NTB + 6;  // [2]
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
 // Everything that depends on the head-group width HG (the UMMA N of GEMM1; GEMM2 uses
-// N = 2*HG for the hi|lo parts of P). HG = 16 fits a 24-slot ring (2.67 pages in flight),
-// HG = 32 (twice the heads per KV byte, used for >= 32 heads) a 20-slot ring.
+// N = 2*HG for the hi|lo parts of P, or two N = HG MMAs into one accumulator for HG = 64).
+// HG = 16 fits a 24-slot ring (2.67 pages in flight), HG = 32 (twice the heads per KV byte,
+// used for 32 / 96 heads) a 22-slot ring, HG = 64 (64 / 128 heads: half the GEMM1 issue
+// cycles per head of HG = 32) a 16-slot ring beside its 72 KB of Q.
 template <int HG_>
 struct Cfg {
     static constexpr int HG = HG_;
-    // softmax warpgroups: HG = 32 splits its heads over two warpgroups (16 heads each), so a
-    // thread handles 8 heads either way and the per-tile softmax time does not double
-    static constexpr int NWG = HG == 32 ? 2 : 1;
+    // softmax warpgroups: HG >= 32 splits its heads over two warpgroups, so a thread handles 8
+    // (HG = 32) or 16 (HG = 64) heads
+#ifndef ETAP_HG64_NWG
+#define ETAP_HG64_NWG 4
+#endif
+    static constexpr int NWG = HG == 64 ? ETAP_HG64_NWG : (HG >= 32 ? 2 : 1);
     static constexpr int HW = HG / NWG;                  // heads per softmax warpgroup
     static constexpr int HH = HW / 2;                    // heads per softmax thread
     static constexpr int THREADS = 128 * (1 + NWG);      // warps 0-3 roles, then the warpgroups
     // ring depth in 8 KB chunk slots; HG = 32 affords 22 with a single P buffer (the softmax
     // writes P(gt) once GEMM2(gt-1) has read P(gt-1), which it has long done by then)
-    static constexpr int NSLOT = HG == 16 ? 24 : ETAP_HG32_NSLOT;
-    static constexpr int P_BUFS = (HG == 16 || NSLOT <= 20) ? 2 : 1;
-    // tile gt's ring positions [0, SPLIT_POS) reuse tile gt-3's last slots (free after its
-    // GEMM2), positions p >= SPLIT_POS reuse tile gt-2's position p - SPLIT_POS. Of those,
-    // gt-2's positions [0, 4) hold {V0..V3} or {rope, V0..V2}: free once GEMM2 d-blocks 0-1 of
-    // gt-2 completed (G2_HALF), so tile gt's positions [SPLIT_POS, SPLIT_POS2) go out then
-    // and only [SPLIT_POS2, 9) wait for the whole GEMM2 of gt-2 (an empty group for HG = 16).
-    static constexpr int SPLIT_POS = NSLOT - 18;
-    static constexpr int SPLIT_POS2 = SPLIT_POS + 4 < NCHUNK ? SPLIT_POS + 4 : NCHUNK;
+    static constexpr int NSLOT = HG == 16 ? 24 : (HG == 32 ? ETAP_HG32_NSLOT : 16);
+    static constexpr int P_BUFS = (HG == 16 || (HG == 32 && NSLOT <= 20)) ? 2 : 1;
+    // HG = 64: O^T for 64 heads with separate hi / lo columns would take all 512 TMEM columns;
+    // GEMM2 instead issues the hi and the lo part as two N = HG MMAs into the same accumulator
+    static constexpr bool SAME_D = HG == 64;
+    // 16-slot ring (HG = 64): tile gt's positions [0, 7) reuse tile gt-2's positions [2, 9)
+    // (free after GEMM2(gt-2)), positions 7, 8 reuse tile gt-1's positions 0, 1 (rope / V0 /
+    // V1: free once GEMM2 d-block 0 of gt-1 completed, G2_Q1)
+    static constexpr bool RING16 = NSLOT == 16;
+    // >= 18 slots: tile gt's ring positions [0, SPLIT_POS) reuse tile gt-3's last slots (free
+    // after its GEMM2), positions p >= SPLIT_POS reuse tile gt-2's position p - SPLIT_POS. Of
+    // those, gt-2's positions [0, 4) hold {V0..V3} or {rope, V0..V2}: free once GEMM2 d-blocks
+    // 0-1 of gt-2 completed (G2_HALF), so tile gt's positions [SPLIT_POS, SPLIT_POS2) go out
+    // then and only [SPLIT_POS2, 9) wait for the whole GEMM2 of gt-2 (an empty group for HG = 16).
+    static constexpr int SPLIT_POS = RING16 ? 7 : NSLOT - 18;
+    static constexpr int SPLIT_POS2 = RING16 ? NCHUNK : (SPLIT_POS + 4 < NCHUNK ? SPLIT_POS + 4 : NCHUNK);
     static constexpr bool THIRD_GROUP = SPLIT_POS2 < NCHUNK;
     // the third group reuses gt-2's positions [4, 9 - SPLIT_POS): V chunks up to V(8 - SPLIT_POS),
     // free after GEMM2 d-blocks 0-2 (G2_3Q) when that is at most V5
     static constexpr bool G3_AFTER_3Q = SPLIT_POS >= 3;
     static constexpr int Q_CHUNK_BYTES = HG * 128;
     static constexpr int Q_BYTES = NCHUNK * Q_CHUNK_BYTES;
-    static constexpr int PN = 2 * HG;                    // GEMM2 N: HG heads hi | HG heads lo
+    static constexpr int PN = 2 * HG;                    // P^T columns: HG heads hi | HG heads lo
+    static constexpr int GN = SAME_D ? HG : PN;          // GEMM2 MMA N
     static constexpr int P_ROWGRP = PN * 16;             // bytes per 8-row group of P^T
     static constexpr int P_BYTES = TILE * PN * 2;
     static constexpr int OFF_RING = 0;
@@ -130,14 +144,16 @@ struct Cfg {
     static constexpr int SMEM_USED = OFF_SCHED + sched_smem_ints(MAX_VB) * 4;
     static constexpr int SMEM_ALLOC = SMEM_USED + 1024;  // slack for manual 1024 B alignment
     // TMEM columns (128 lanes x 32 bit): S^T double buffer [0, 2HG) (M=64 lane layout), then
-    // four O^T d-blocks of 2HG columns (HG hi | HG lo)
+    // four O^T d-blocks of GN columns (HG hi | HG lo, or HG summed for SAME_D)
     static constexpr uint32_t TCOL_S = 0;
     static constexpr uint32_t TCOL_O = 2 * HG;
-    static constexpr uint32_t OBLK = 2 * HG;
+    static constexpr uint32_t OBLK = GN;
+    static constexpr int OSEG = SAME_D ? 1 : 2;          // accumulator segments per d-block (hi, lo)
     static constexpr uint32_t TMEM_COLS = (TCOL_O + 4 * OBLK) <= 256 ? 256 : 512;
     static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
-    static_assert(NSLOT % 2 == 0 && NSLOT >= 18 && NSLOT <= 27, "ring must hold two tiles, even slots");
+    static_assert(NSLOT % 2 == 0 && (NSLOT == 16 || (NSLOT >= 18 && NSLOT <= 27)), "ring must hold two tiles, even slots");
     static_assert(TCOL_O + 4 * OBLK <= 512, "TMEM budget");
+    static_assert(HW % 16 == 0, "a warpgroup handles whole 16-column TMEM loads");
 };
 
 // P^T operand (B of GEMM2): MN-major, no swizzle. Core matrices of 8 KV rows x 8 columns
@@ -193,18 +209,23 @@ __device__ __forceinline__ void issue_gemm1_tile(uint32_t s_tmem, uint32_t ring_
 }
 
 // GEMM2 part for one d-block (128 latent columns = chunks 2i, 2i+1 in slots s, s+1):
-// O^T[128 x 2HG] (+)= V^T[128 x 64] . [P_hi | P_lo]^T[64 x 2HG]. Whole-warp call.
+// O^T[128 x 2HG] (+)= V^T[128 x 64] . [P_hi | P_lo]^T[64 x 2HG], or for SAME_D
+// O^T[128 x HG] (+)= V^T . P_hi^T + V^T . P_lo^T (two N = HG MMAs, one accumulator). Whole-warp call.
 template <class C>
 __device__ __forceinline__ void issue_gemm2_block(uint32_t o_tmem, uint32_t slot_addr,
                                                   uint32_t p_addr, bool zero_init) {
-    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, C::PN, 1, 1);
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, C::GN, 1, 1);
     // MN-major SW128: LBO = stride between 64-wide MN atoms (next slot), SBO = 8-row group
     const uint64_t a0 = ptx::smem_desc(slot_addr, SLOT_BYTES, 1024, ptx::LAYOUT_SW128);
     const uint64_t b0 = p_desc<C>(p_addr);
 #pragma unroll
-    for (int kk = 0; kk < TILE / 16; ++kk)  // 16 KV rows = 2 row groups per MMA
+    for (int kk = 0; kk < TILE / 16; ++kk) {  // 16 KV rows = 2 row groups per MMA
         ptx::umma_f16_elect(o_tmem, a0 + kk * (2048 >> 4), b0 + kk * ((2 * C::P_ROWGRP) >> 4),
                             idesc, (zero_init && kk == 0) ? 0u : 1u);
+        if constexpr (C::SAME_D)  // P_lo: columns [HG, 2HG) of the P^T tile, 8-column groups of 128 B
+            ptx::umma_f16_elect(o_tmem, a0 + kk * (2048 >> 4),
+                                b0 + kk * ((2 * C::P_ROWGRP) >> 4) + ((C::HG / 8 * 128) >> 4), idesc, 1u);
+    }
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo_elem, float hi_elem) {
@@ -219,13 +240,11 @@ __device__ __forceinline__ void write_p_hilo(uint8_t* p, int r, int half, const 
     uint32_t hi[C::HH / 2], lo[C::HH / 2];
 #pragma unroll
     for (int i = 0; i < C::HH / 2; ++i) {
-        const __nv_bfloat16 h0 = __float2bfloat16_rn(pv[2 * i]);
-        const __nv_bfloat16 h1 = __float2bfloat16_rn(pv[2 * i + 1]);
-        __nv_bfloat162 hh;
-        hh.x = h0;
-        hh.y = h1;
-        hi[i] = *reinterpret_cast<uint32_t*>(&hh);
-        lo[i] = pack_bf16x2(pv[2 * i] - __bfloat162float(h0), pv[2 * i + 1] - __bfloat162float(h1));
+        // one packed RNE conversion per pair (F2FP) instead of two scalar F2F; widening a bf16
+        // back to fp32 is a 16-bit shift
+        hi[i] = pack_bf16x2(pv[2 * i], pv[2 * i + 1]);
+        const float h0 = __uint_as_float(hi[i] << 16), h1 = __uint_as_float(hi[i] & 0xffff0000u);
+        lo[i] = pack_bf16x2(pv[2 * i] - h0, pv[2 * i + 1] - h1);
     }
     uint8_t* row = p + (r >> 3) * C::P_ROWGRP + (r & 7) * 16;
 #pragma unroll
