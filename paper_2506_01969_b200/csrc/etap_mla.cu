@@ -575,6 +575,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
             ptx::mbar_init(&bars[BAR_G2_HALF + i], 1);
             ptx::mbar_init(&bars[BAR_G2_3Q + i], 1);
             ptx::mbar_init(&bars[BAR_G2_Q1 + i], 1);
+            ptx::mbar_init(&bars[BAR_G2_P1 + i], 1);
         }
         ptx::mbar_init(&bars[BAR_Q_FULL], 1);
         ptx::mbar_init(&bars[BAR_Q_EMPTY], 1);
@@ -582,6 +583,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
             ptx::mbar_init(&bars[BAR_S_FULL + i], 1);
             ptx::mbar_init(&bars[BAR_S_FREE + i], 128 * C::NWG);
             ptx::mbar_init(&bars[BAR_P_FULL + i], 128 * C::NWG);
+            ptx::mbar_init(&bars[BAR_P2_FULL + i], 128 * C::NWG);
         }
         ptx::fence_mbar_init();
     }
@@ -641,7 +643,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
                 if (gt == 0 && pro.late_wait) dep_wait_producer<kDebug>(prm);
                 // group A reuses slots of tile gt - A_LAG (all GEMM2 work of that tile done)
-                constexpr uint32_t A_LAG = C::RING16 ? 2 : 3;
+                constexpr uint32_t A_LAG = C::P_IN_ROPE ? 2 : 3;
                 if (gt >= A_LAG) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - A_LAG) % NTB], ((gt - A_LAG) / NTB) & 1);
                 if (lane == 0) {
                     if (gt == 0) { ETAP_TRACE_G(prm, 9); ETAP_TRACE_CLK(prm, 15); }
@@ -653,14 +655,6 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                         ptx::tma_load_2d(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_A + tb],
                                          chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
                     }
-#ifndef ETAP_NO_LATE_PREFETCH
-                    // 16-slot ring: the tile's last chunks can only load once GEMM2 of the
-                    // previous tile released its first positions; warm them in L2 now so that
-                    // load is an L2 hit on the critical path
-                    if constexpr (C::RING16)
-                        for (int pos = C::SPLIT_POS; pos < NCHUNK; ++pos)
-                            ptx::tma_prefetch_2d(&tm_kv, chunk_at(pos, gt) * 64, page * PAGE);
-#endif
                 }
                 __syncwarp();
                 if (q_pending) {
@@ -682,11 +676,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 // positions [SPLIT_POS, SPLIT_POS2) reuse tile gt-2's first four positions: free
                 // once GEMM2 d-blocks 0-1 of gt-2 completed (16-slot ring: tile gt-1's first two
                 // positions, free once GEMM2 d-block 0 of gt-1 completed)
-                if constexpr (C::RING16) {
-                    if (gt >= 1) ptx::mbar_wait(&bars[BAR_G2_Q1 + (gt - 1) % NTB], ((gt - 1) / NTB) & 1);
-                } else {
-                    if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_HALF + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
-                }
+                if (!C::P_IN_ROPE && gt >= 2) ptx::mbar_wait(&bars[BAR_G2_HALF + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
                 if (lane == 0) {
                     ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_B + tb], (C::SPLIT_POS2 - C::SPLIT_POS) * SLOT_BYTES);
 #pragma unroll 1
@@ -701,7 +691,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     // the rest reuse gt-2's positions [4, 9 - SPLIT_POS): free after GEMM2 d-blocks
                     // 0-2 of gt-2 (22-slot ring) or the whole GEMM2
                     __syncwarp();
-                    if (gt >= 2)
+                    if (!C::P_IN_ROPE && gt >= 2)
                         ptx::mbar_wait(&bars[(C::G3_AFTER_3Q ? BAR_G2_3Q : BAR_G2_DONE) + (gt - 2) % NTB],
                                        ((gt - 2) / NTB) & 1);
                     if (lane == 0) {
@@ -768,15 +758,36 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 ptx::tc_fence_after();
                 ETAP_TRACE(prm, gt, 6);
                 const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
+                if constexpr (C::P_IN_ROPE) {
+                    // pass 1: O^T += V^T P_hi^T (P in the tile's rope slot), then the softmax
+                    // replaces P_hi by P_lo in the same slot; pass 2: O^T += V^T P_lo^T
+                    const uint32_t pa = ring_addr + ((pos0 + pos_of_chunk(8, gt)) % C::NSLOT) * SLOT_BYTES;
 #pragma unroll
-                for (int blk = 0; blk < 4; ++blk) {
-                    uint32_t sa = pos0 + pos_of_chunk(2 * blk, gt);
-                    sa = sa >= C::NSLOT ? sa - C::NSLOT : sa;
-                    issue_gemm2_block<C>(tmem_base + C::TCOL_O + C::OBLK * blk, ring_addr + sa * SLOT_BYTES,
-                                         p_addr + (buf % C::P_BUFS) * C::P_BYTES, t == sd.t0);
-                    if (C::RING16 && blk == 0) ptx::umma_commit_elect(&bars[BAR_G2_Q1 + gt % NTB]);
-                    if (blk == 1) ptx::umma_commit_elect(&bars[BAR_G2_HALF + gt % NTB]);
-                    if (C::G3_AFTER_3Q && C::THIRD_GROUP && blk == 2) ptx::umma_commit_elect(&bars[BAR_G2_3Q + gt % NTB]);
+                    for (int pass = 0; pass < 2; ++pass) {
+                        if (pass == 1) {
+                            ptx::mbar_wait(&bars[BAR_P2_FULL + buf], (gt >> 1) & 1);
+                            __syncwarp();
+                            ptx::tc_fence_after();
+                        }
+#pragma unroll
+                        for (int blk = 0; blk < 4; ++blk) {
+                            uint32_t sa = pos0 + pos_of_chunk(2 * blk, gt);
+                            sa = sa >= C::NSLOT ? sa - C::NSLOT : sa;
+                            issue_gemm2_block<C>(tmem_base + C::TCOL_O + C::OBLK * blk, ring_addr + sa * SLOT_BYTES, pa,
+                                                 pass == 0 && t == sd.t0);
+                        }
+                        if (pass == 0) ptx::umma_commit_elect(&bars[BAR_G2_P1 + gt % NTB]);
+                    }
+                } else {
+#pragma unroll
+                    for (int blk = 0; blk < 4; ++blk) {
+                        uint32_t sa = pos0 + pos_of_chunk(2 * blk, gt);
+                        sa = sa >= C::NSLOT ? sa - C::NSLOT : sa;
+                        issue_gemm2_block<C>(tmem_base + C::TCOL_O + C::OBLK * blk, ring_addr + sa * SLOT_BYTES,
+                                             p_addr + (buf % C::P_BUFS) * C::P_BYTES, t == sd.t0);
+                        if (blk == 1) ptx::umma_commit_elect(&bars[BAR_G2_HALF + gt % NTB]);
+                        if (C::G3_AFTER_3Q && C::THIRD_GROUP && blk == 2) ptx::umma_commit_elect(&bars[BAR_G2_3Q + gt % NTB]);
+                    }
                 }
                 ptx::umma_commit_elect(&bars[BAR_G2_DONE + gt % NTB]);
                 ETAP_TRACE(prm, gt, 7);
@@ -918,8 +929,9 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     ptx::named_bar_sync(bar_b, 128);
                 }
                 if (tracer) ETAP_TRACE(prm, gt, 8);
-                // the P buffer is reused every P_BUFS tiles: GEMM2(gt - P_BUFS) must have read it
-                if (gt >= C::P_BUFS)
+                // the P buffer is reused every P_BUFS tiles: GEMM2(gt - P_BUFS) must have read it (P in
+                // the tile's own rope slot: free since GEMM1 of this tile completed)
+                if (C::P_BUFS > 0 && gt >= C::P_BUFS)
                     ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - C::P_BUFS) % NTB], ((gt - C::P_BUFS) / NTB) & 1);
                 if (tracer) ETAP_TRACE(prm, gt, 9);
                 if (need_rescale) {
@@ -948,7 +960,22 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     }
                     ptx::tmem_wait_st();
                 }
-                write_p_hilo<C>(smem + C::OFF_P + (buf % C::P_BUFS) * C::P_BYTES, row, half, pv, hoff);
+                uint32_t p_lo[HH / 2];  // two-pass GEMM2: written after pass 1
+                uint8_t* p_rope = nullptr;
+                if constexpr (C::P_IN_ROPE) {
+                    uint32_t p_hi[HH / 2];
+#pragma unroll
+                    for (int i = 0; i < HH / 2; ++i) {
+                        p_hi[i] = pack_bf16x2(pv[2 * i], pv[2 * i + 1]);
+                        p_lo[i] = pack_bf16x2(pv[2 * i] - __uint_as_float(p_hi[i] << 16),
+                                              pv[2 * i + 1] - __uint_as_float(p_hi[i] & 0xffff0000u));
+                    }
+                    const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
+                    p_rope = smem + C::OFF_RING + ((pos0 + pos_of_chunk(8, gt)) % C::NSLOT) * SLOT_BYTES;
+                    write_p_part<C>(p_rope, row, half, p_hi, hoff);
+                } else {
+                    write_p_hilo<C>(smem + C::OFF_P + (buf % C::P_BUFS) * C::P_BYTES, row, half, pv, hoff);
+                }
                 // rows of the last page past seqlen were loaded from HBM and may hold
                 // non-finite garbage; zero them in the V chunks (0 * NaN = NaN in the MMA)
                 if (grow >= sd.seqlen) {
@@ -966,6 +993,15 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 ptx::tc_fence_before();
                 if (tracer) ETAP_TRACE(prm, gt, 5);
                 ptx::mbar_arrive(&bars[BAR_P_FULL + buf]);
+                if constexpr (C::P_IN_ROPE) {
+                    // P_lo replaces P_hi once GEMM2 pass 1 of this tile has read it
+                    ptx::mbar_wait(&bars[BAR_G2_P1 + gt % NTB], (gt / NTB) & 1);
+                    ptx::tc_fence_after();
+                    write_p_part<C>(p_rope, row, half, p_lo, hoff);
+                    ptx::fence_proxy_async_smem();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&bars[BAR_P2_FULL + buf]);
+                }
                 ++gt;
             }
 

@@ -34,7 +34,7 @@ constexpr int NCHUNK = 9;       // 576 / 64 column chunks (SW128 atoms are 64 bf
 constexpr int NVCHUNK = 8;      // 512 / 64 chunks that are also V
 constexpr int SLOT_BYTES = TILE * 128;  // 64 rows x 128 B = 8 KiB per ring slot
 constexpr int NTB = 4;          // tile-barrier ring depth (tiles in flight <= NSLOT/9 + 1)
-constexpr int NBAR = 7 * NTB + 8;
+constexpr int NBAR = 8 * NTB + 10;
 // Longest line (batch * head groups, or batch with lanes) whose split schedule the decode
 // kernel computes itself (the block-wide scan takes one line entry per thread of the >= 256-
 // thread CTA); longer lines run K1 first.
@@ -79,6 +79,8 @@ constexpr int BAR_G2_HALF = 3 * NTB;    // [NTB] GEMM2 d-blocks 0-1 of tile gt c
 constexpr int BAR_FULL_C = 4 * NTB + 8;  // [NTB] ring positions [SPLIT_POS2, 9) of tile gt landed
 constexpr int BAR_G2_3Q = 5 * NTB + 8;   // [NTB] GEMM2 d-blocks 0-2 of tile gt complete (V0..V5 free)
 constexpr int BAR_G2_Q1 = 6 * NTB + 8;   // [NTB] GEMM2 d-block 0 of tile gt complete (its first two positions free)
+constexpr int BAR_G2_P1 = 7 * NTB + 8;   // [NTB] GEMM2 pass 1 (P_hi) of tile gt complete (two-pass GEMM2)
+constexpr int BAR_P2_FULL = 8 * NTB + 8; // [2] P_lo written (two-pass GEMM2), count 128 * NWG
 constexpr int BAR_Q_FULL = 4 * NTB + 0;
 constexpr int BAR_Q_EMPTY = 4 * NTB + 1;
 constexpr int BAR_S_FULL = 4 * NTB + 2;  // [2]
@@ -106,29 +108,32 @@ struct Cfg {
     static constexpr int THREADS = 128 * (1 + NWG);      // warps 0-3 roles, then the warpgroups
     // ring depth in 8 KB chunk slots; HG = 32 affords 22 with a single P buffer (the softmax
     // writes P(gt) once GEMM2(gt-1) has read P(gt-1), which it has long done by then)
-    static constexpr int NSLOT = HG == 16 ? 24 : (HG == 32 ? ETAP_HG32_NSLOT : 16);
-    static constexpr int P_BUFS = (HG == 16 || (HG == 32 && NSLOT <= 20)) ? 2 : 1;
-    // HG = 64: O^T for 64 heads with separate hi / lo columns would take all 512 TMEM columns;
-    // GEMM2 instead issues the hi and the lo part as two N = HG MMAs into the same accumulator
-    static constexpr bool SAME_D = HG == 64;
-    // 16-slot ring (HG = 64): tile gt's positions [0, 7) reuse tile gt-2's positions [2, 9)
-    // (free after GEMM2(gt-2)), positions 7, 8 reuse tile gt-1's positions 0, 1 (rope / V0 /
-    // V1: free once GEMM2 d-block 0 of gt-1 completed, G2_Q1)
-    static constexpr bool RING16 = NSLOT == 16;
-    // >= 18 slots: tile gt's ring positions [0, SPLIT_POS) reuse tile gt-3's last slots (free
+    static constexpr int NSLOT = HG == 16 ? 24 : (HG == 32 ? ETAP_HG32_NSLOT : 18);
+    // HG = 64: O^T for 64 heads with separate hi / lo columns would take all 512 TMEM columns,
+    // and 72 KB of Q leave room for only two whole tiles: P lives in the tile's own rope slot
+    // (free once GEMM1 of the tile completed; the rope chunk feeds GEMM1 only) and GEMM2 runs
+    // in two passes into one accumulator, O^T += V^T P_hi^T, then the softmax overwrites the
+    // slot with P_lo and O^T += V^T P_lo^T. Tile gt then occupies ring half gt % 2 and the next
+    // tile loads whole while GEMM2 of this one runs.
+    static constexpr bool P_IN_ROPE = HG == 64;
+    static constexpr bool SAME_D = P_IN_ROPE;
+    static constexpr int P_BUFS = P_IN_ROPE ? 0 : ((HG == 16 || (HG == 32 && NSLOT <= 20)) ? 2 : 1);
+    // >= 20 slots: tile gt's ring positions [0, SPLIT_POS) reuse tile gt-3's last slots (free
     // after its GEMM2), positions p >= SPLIT_POS reuse tile gt-2's position p - SPLIT_POS. Of
     // those, gt-2's positions [0, 4) hold {V0..V3} or {rope, V0..V2}: free once GEMM2 d-blocks
     // 0-1 of gt-2 completed (G2_HALF), so tile gt's positions [SPLIT_POS, SPLIT_POS2) go out
     // then and only [SPLIT_POS2, 9) wait for the whole GEMM2 of gt-2 (an empty group for HG = 16).
-    static constexpr int SPLIT_POS = RING16 ? 7 : NSLOT - 18;
-    static constexpr int SPLIT_POS2 = RING16 ? NCHUNK : (SPLIT_POS + 4 < NCHUNK ? SPLIT_POS + 4 : NCHUNK);
+    // 18 slots (P_IN_ROPE): tile gt reuses tile gt-2's slots, all free after GEMM2(gt-2); the
+    // three landing groups only let GEMM1 start on the first chunks while the rest stream in.
+    static constexpr int SPLIT_POS = P_IN_ROPE ? 3 : NSLOT - 18;
+    static constexpr int SPLIT_POS2 = P_IN_ROPE ? 6 : (SPLIT_POS + 4 < NCHUNK ? SPLIT_POS + 4 : NCHUNK);
     static constexpr bool THIRD_GROUP = SPLIT_POS2 < NCHUNK;
     // the third group reuses gt-2's positions [4, 9 - SPLIT_POS): V chunks up to V(8 - SPLIT_POS),
     // free after GEMM2 d-blocks 0-2 (G2_3Q) when that is at most V5
     static constexpr bool G3_AFTER_3Q = SPLIT_POS >= 3;
     static constexpr int Q_CHUNK_BYTES = HG * 128;
     static constexpr int Q_BYTES = NCHUNK * Q_CHUNK_BYTES;
-    static constexpr int PN = 2 * HG;                    // P^T columns: HG heads hi | HG heads lo
+    static constexpr int PN = P_IN_ROPE ? HG : 2 * HG;   // P^T columns: HG heads hi | HG heads lo (or one part)
     static constexpr int GN = SAME_D ? HG : PN;          // GEMM2 MMA N
     static constexpr int P_ROWGRP = PN * 16;             // bytes per 8-row group of P^T
     static constexpr int P_BYTES = TILE * PN * 2;
@@ -151,7 +156,8 @@ struct Cfg {
     static constexpr int OSEG = SAME_D ? 1 : 2;          // accumulator segments per d-block (hi, lo)
     static constexpr uint32_t TMEM_COLS = (TCOL_O + 4 * OBLK) <= 256 ? 256 : 512;
     static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
-    static_assert(NSLOT % 2 == 0 && (NSLOT == 16 || (NSLOT >= 18 && NSLOT <= 27)), "ring must hold two tiles, even slots");
+    static_assert(NSLOT % 2 == 0 && NSLOT >= 18 && NSLOT <= 27, "ring must hold two tiles, even slots");
+    static_assert(!P_IN_ROPE || (NSLOT == 18 && P_BYTES == SLOT_BYTES), "P part fills exactly the rope slot");
     static_assert(TCOL_O + 4 * OBLK <= 512, "TMEM budget");
     static_assert(HW % 16 == 0, "a warpgroup handles whole 16-column TMEM loads");
 };
@@ -219,13 +225,9 @@ __device__ __forceinline__ void issue_gemm2_block(uint32_t o_tmem, uint32_t slot
     const uint64_t a0 = ptx::smem_desc(slot_addr, SLOT_BYTES, 1024, ptx::LAYOUT_SW128);
     const uint64_t b0 = p_desc<C>(p_addr);
 #pragma unroll
-    for (int kk = 0; kk < TILE / 16; ++kk) {  // 16 KV rows = 2 row groups per MMA
+    for (int kk = 0; kk < TILE / 16; ++kk)  // 16 KV rows = 2 row groups per MMA
         ptx::umma_f16_elect(o_tmem, a0 + kk * (2048 >> 4), b0 + kk * ((2 * C::P_ROWGRP) >> 4),
                             idesc, (zero_init && kk == 0) ? 0u : 1u);
-        if constexpr (C::SAME_D)  // P_lo: columns [HG, 2HG) of the P^T tile, 8-column groups of 128 B
-            ptx::umma_f16_elect(o_tmem, a0 + kk * (2048 >> 4),
-                                b0 + kk * ((2 * C::P_ROWGRP) >> 4) + ((C::HG / 8 * 128) >> 4), idesc, 1u);
-    }
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo_elem, float hi_elem) {
@@ -254,6 +256,18 @@ __device__ __forceinline__ void write_p_hilo(uint8_t* p, int r, int half, const 
             make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
         *reinterpret_cast<uint4*>(row + (n_lo >> 3) * 128) =
             make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+    }
+}
+
+// One part (hi or lo, HH heads of KV row r as bf16 pairs) into row r of a P^T tile of PN = HG
+// columns (two-pass GEMM2, C::P_IN_ROPE).
+template <class C>
+__device__ __forceinline__ void write_p_part(uint8_t* p, int r, int half, const uint32_t (&v)[C::HH / 2], int hoff) {
+    uint8_t* row = p + (r >> 3) * C::P_ROWGRP + (r & 7) * 16;
+#pragma unroll
+    for (int c = 0; c < C::HH / 8; ++c) {  // 8 heads = one 16 B core-matrix row
+        const int n = hoff + half * C::HH + 8 * c;
+        *reinterpret_cast<uint4*>(row + (n >> 3) * 128) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     }
 }
 

@@ -69,10 +69,10 @@ def test_sizes_and_shape_validation():
     # partial O + LSE (16 heads per unit), then the FP8 path's per-CTA Q-term scratch (3 slots)
     assert ws.value == al((148 + 16) * 16 * (512 + 1) * 4) + 148 * 3 * 48 * 576
     # head groups: 32 heads per work unit when heads % 32 == 0, else 16
-    assert [mla.head_group(h) for h in (16, 32, 48, 64, 128)] == [16, 32, 16, 32, 32]
+    assert [mla.head_group(h) for h in (16, 32, 48, 64, 96, 128)] == [16, 32, 16, 64, 32, 64]
     assert L.etap_mla_sched_ints(4, 128, 148, C.byref(a), C.byref(b)) == _lib.ETAP_OK and b.value == 4 * 8 + 1
     assert L.etap_mla_workspace_bytes(4, 128, 148, C.byref(ws)) == _lib.ETAP_OK
-    assert ws.value == al((148 + 16) * 32 * (512 + 1) * 4) + 148 * 3 * 48 * 576
+    assert ws.value == al((148 + 4 * 2) * 64 * (512 + 1) * 4) + 148 * 3 * 48 * 576
     hg = C.c_int()
     assert L.etap_mla_head_group(24, C.byref(hg)) == _lib.ETAP_ERR_SHAPE
     # decode rejects q_tokens outside [1, 8], q_tokens * heads not a multiple of 16 and a bad
