@@ -370,6 +370,9 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
 
 // L2 prefetch depth before the grid dependency, in bytes of KV: 2 bf16 pages = 4 FP8 pages
 // (measured best for each kernel; deeper prefetch competes with the previous step's tail)
+#ifndef ETAP_HG64_PF_AHEAD
+#define ETAP_HG64_PF_AHEAD 0  // L2 prefetch of the next tile's page: measured slower (pf1 290.0 vs 281.9 us at 64 heads)
+#endif
 #ifndef ETAP_HINT_BYTES
 #define ETAP_HINT_BYTES (2 * 64 * 576 * 2)
 #endif
@@ -644,6 +647,15 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 if (gt == 0 && pro.late_wait) dep_wait_producer<kDebug>(prm);
                 // group A reuses slots of tile gt - A_LAG (all GEMM2 work of that tile done)
                 constexpr uint32_t A_LAG = C::P_IN_ROPE ? 2 : 3;
+                // two-tile ring (P_IN_ROPE): the page PF_AHEAD tiles ahead in this split is pulled
+                // into L2 now, so its TMA load (issued only once GEMM2 two tiles back released
+                // the slots) is an L2 hit instead of an HBM round trip on the tile chain
+                int page_ahead = -1;
+                if constexpr (C::P_IN_ROPE && ETAP_HG64_PF_AHEAD > 0) {
+                    const int ta = t + ETAP_HG64_PF_AHEAD;
+                    const int v = __shfl_sync(0xffffffffu, pg, min(ta - base, 31));
+                    page_ahead = (ta < sd.t1 && ta - base < 32) ? v : -1;
+                }
                 if (gt >= A_LAG) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - A_LAG) % NTB], ((gt - A_LAG) / NTB) & 1);
                 if (lane == 0) {
                     if (gt == 0) { ETAP_TRACE_G(prm, 9); ETAP_TRACE_CLK(prm, 15); }
@@ -655,6 +667,10 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                         ptx::tma_load_2d(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_A + tb],
                                          chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
                     }
+                    if (page_ahead >= 0 && page_ahead < prm.num_pages)
+                        ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) +
+                                                  static_cast<size_t>(page_ahead) * PAGE * D_QK * 2,
+                                              PAGE * D_QK * 2);
                 }
                 __syncwarp();
                 if (q_pending) {
