@@ -22,7 +22,7 @@ KEYS = [
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg", "launch__registers_per_thread",
     "launch__grid_size", "launch__block_size", "lts__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
-    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed",
 ]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "nsecond": 1e-9, "msecond": 1e-3,
          "us": 1e-6, "ns": 1e-9}
@@ -44,7 +44,10 @@ def raw(rep: str) -> dict:
 
 def main() -> None:
     fp8 = "--fp8" in sys.argv  # FP8 kernel capture: profiles/<tag>/ncu_fp8_kernel.md only
-    args = [a for a in sys.argv[1:] if a != "--fp8"]
+    heads = 16
+    if "--heads" in sys.argv:  # other head counts: profiles/<tag>/ncu_decode_kernel_h<H>.md only
+        heads = int(sys.argv[sys.argv.index("--heads") + 1])
+    args = [a for i, a in enumerate(sys.argv[1:], 1) if a not in ("--fp8", "--heads") and sys.argv[i - 1] != "--heads"]
     rep, launches, tag = args[0], args[1] if len(args) > 1 and args[1] != "-" else None, args[2] if len(args) > 2 else "r01"
     from paper_2506_01969_b200 import inputs
 
@@ -52,17 +55,21 @@ def main() -> None:
     rd = d["dram__bytes_read.sum"][0] * SCALE[d["dram__bytes_read.sum"][1]]
     wr = d["dram__bytes_write.sum"][0] * SCALE[d["dram__bytes_write.sum"][1]]
     dur = d["gpu__time_duration.sum"][0] * SCALE[d["gpu__time_duration.sum"][1]]
-    alg = inputs.algorithmic_bytes([65536] * 16, 16)
+    alg = inputs.algorithmic_bytes([65536] * 16, heads)
+    flops = inputs.flops([65536] * 16, heads)
     if fp8:  # the latent cache is one byte per element
         alg -= 65536 * 16 * 576
     summary = {
-        "workload": "mla_decode_b16_ctx64k_h16_per_gpu", "tag": tag, "source": rep,
+        "workload": "mla_decode_b16_ctx64k_h16_per_gpu" if heads == 16 else f"mla_decode_b16_ctx64k_h{heads}",
+        "tag": tag, "source": rep,
         "decode_kernel": {
             "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
             "algorithmic_bytes": alg, "traffic_over_algorithmic": (rd + wr) / alg,
             "duration_us_cold_serialised": dur * 1e6,
             "dram_throughput_pct_of_ncu_peak": d["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"][0],
             "tensor_pipe_active_pct": d["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"][0],
+            "tc_issue_pipe_active_pct": d.get("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed", (None,))[0],
+            "useful_tflops_at_capture": flops / dur / 1e12,
             "sm_throughput_pct": d["sm__throughput.avg.pct_of_peak_sustained_elapsed"][0],
             "sm_clock_ghz": d["sm__cycles_elapsed.avg"][0] / dur / 1e9,
             "registers_per_thread": d["launch__registers_per_thread"][0],
@@ -79,12 +86,12 @@ def main() -> None:
         tot = sum(sum(v) for v in ks.values())
         summary["launch_list"] = {k: {"launches": len(v), "avg_us": sum(v) / len(v) * 1e6,
                                       "share": sum(v) / tot} for k, v in ks.items()}
-    if not fp8:
+    if not fp8 and heads == 16:
         (ROOT / "profiles" / "ncu_summary.json").write_text(json.dumps(summary, indent=1) + "\n")
     tagdir = ROOT / "profiles" / tag
     tagdir.mkdir(parents=True, exist_ok=True)
     kname = "etap_mla_decode_fp8_kernel (K2-FP8, e4m3 latent cache)" if fp8 else "etap_mla_decode_kernel (K2)"
-    lines = [f"# ncu — {kname}, B=16 x 64K, 16 heads ({tag})", "",
+    lines = [f"# ncu — {kname}, B=16 x 64K, {heads} heads ({tag})", "",
              f"source: `{rep}` (`ncu --set full --clock-control none --import-source on`, one launch)", "",
              "| metric | value |", "|---|---|"]
     for k, v in summary["decode_kernel"].items():
@@ -94,7 +101,8 @@ def main() -> None:
                   "|---|---|---|---|"]
         for k, v in summary["launch_list"].items():
             lines.append(f"| {k} | {v['launches']} | {v['avg_us']:.2f} | {v['share']:.3f} |")
-    (tagdir / ("ncu_fp8_kernel.md" if fp8 else "ncu_decode_kernel.md")).write_text("\n".join(lines) + "\n")
+    fname = "ncu_fp8_kernel.md" if fp8 else ("ncu_decode_kernel.md" if heads == 16 else f"ncu_decode_kernel_h{heads}.md")
+    (tagdir / fname).write_text("\n".join(lines) + "\n")
     print(json.dumps(summary, indent=1))
 
 
