@@ -341,6 +341,10 @@ int etap_mla_umma_bench(int variant, int n, long long* out_dev, int grid);
  * (grid CTAs x pages_per_cta pages, ring of nslot 8 KB slots) — the attainable read rate. */
 int etap_mla_stream_bench(const void* kv_pool, int64_t num_pages, int pages_per_cta, int grid,
                           int nslot, void* stream);
+/* Debug: the same with clusters of two CTAs that stream the same pages, each issuing every
+ * other box as a cluster multicast into both (grid even; grid / 2 page ranges). */
+int etap_mla_stream_bench_mc(const void* kv_pool, int64_t num_pages, int pages_per_cta, int grid,
+                             int nslot, void* stream);
 
 /* Debug / tests: a one-CTA kernel launched with programmatic dependent launch that triggers
  * its dependents at entry, sleeps delay_ns, then copies n int32 from src to dst (device

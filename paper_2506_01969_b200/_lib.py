@@ -80,6 +80,7 @@ def _declare(lib: C.CDLL) -> None:
         "etap_mla_debug_trace_combine": (i32, [vp]),
         "etap_mla_umma_bench": (i32, [i32, i32, vp, i32]),
         "etap_mla_stream_bench": (i32, [vp, i64, i32, i32, i32, vp]),
+        "etap_mla_stream_bench_mc": (i32, [vp, i64, i32, i32, i32, vp]),
         "etap_mla_debug_pdl_write": (i32, [vp, vp, i32, i32, vp]),
     }
     for name, (res, args) in sig.items():

@@ -2859,6 +2859,74 @@ __global__ void __launch_bounds__(64, 1) etap_stream_bench_kernel(const __grid_c
 }
 }  // namespace
 
+namespace {
+// Cluster-of-two variant: both CTAs stream the same pages (as the two head-group lanes of a
+// 128-head decode do); each issues every other box with .multicast::cluster into both CTAs, so
+// every SM still receives whole pages but generates half the requests. A slot is reloaded once
+// both CTAs released it (remote arrive on the peer's `done`).
+__global__ void __launch_bounds__(64, 1) etap_stream_bench_mc_kernel(const __grid_constant__ CUtensorMap tm_kv,
+                                                                      int pages_per_cta, int nslot) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = ptx::align_smem_1024(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 200 * 1024);
+    uint64_t* done = full + NTB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_ctarank();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NTB; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&done[i], 2); }
+        ptx::fence_mbar_init();
+    }
+    ptx::cluster_sync_all();
+    const int p0 = (blockIdx.x >> 1) * pages_per_cta;
+    const uint32_t tiles_in_ring = (uint32_t)nslot / NCHUNK;
+    if (warp == 0) {
+        const uint64_t pol = ptx::policy_evict_first();
+        for (uint32_t gt = 0; gt < (uint32_t)pages_per_cta; ++gt) {
+            if (gt >= tiles_in_ring)
+                ptx::mbar_wait(&done[(gt - tiles_in_ring) % NTB], ((gt - tiles_in_ring) / NTB) & 1);
+            if (lane == 0) {
+                ptx::mbar_arrive_expect_tx(&full[gt % NTB], NCHUNK * SLOT_BYTES);
+                const uint32_t base = (gt % tiles_in_ring) * NCHUNK;
+                for (int c = static_cast<int>(rank); c < NCHUNK; c += 2)
+                    ptx::tma_load_2d_mc(smem + (base + c) * SLOT_BYTES, &tm_kv, &full[gt % NTB], c * 64,
+                                        (p0 + gt) * PAGE, 0x3, pol);
+            }
+            __syncwarp();
+        }
+    } else {
+        for (uint32_t gt = 0; gt < (uint32_t)pages_per_cta; ++gt) {
+            ptx::mbar_wait(&full[gt % NTB], (gt / NTB) & 1);
+            if (lane == 0) {
+                ptx::mbar_arrive(&done[gt % NTB]);
+                ptx::mbar_arrive_cluster(&done[gt % NTB], rank ^ 1u);
+            }
+            __syncwarp();
+        }
+    }
+    ptx::cluster_sync_all();  // no remote arrive may target an exited CTA
+}
+}  // namespace
+
+extern "C" int etap_mla_stream_bench_mc(const void* kv_pool, int64_t num_pages, int pages_per_cta,
+                                        int grid, int nslot, void* stream) {
+    if (nslot < NCHUNK || nslot * SLOT_BYTES > 200 * 1024 || grid % 2) return fail(ETAP_ERR_SHAPE, "bad nslot/grid");
+    CUtensorMap tm;
+    if (int rc = make_map(&tm, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, PAGE)) return rc;
+    cudaFuncSetAttribute(etap_stream_bench_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 202 * 1024);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(64);
+    cfg.dynamicSmemBytes = 202 * 1024;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_stream_bench_mc_kernel, tm, pages_per_cta, nslot));
+    return ETAP_OK;
+}
+
 extern "C" int etap_mla_stream_bench(const void* kv_pool, int64_t num_pages, int pages_per_cta,
                                      int grid, int nslot, void* stream) {
     if (nslot < NCHUNK || nslot * SLOT_BYTES > 200 * 1024) return fail(ETAP_ERR_SHAPE, "bad nslot");
