@@ -345,6 +345,10 @@ int etap_mla_stream_bench(const void* kv_pool, int64_t num_pages, int pages_per_
  * other box as a cluster multicast into both (grid even; grid / 2 page ranges). */
 int etap_mla_stream_bench_mc(const void* kv_pool, int64_t num_pages, int pages_per_cta, int grid,
                              int nslot, void* stream);
+/* Debug: the same with 3-D TMA boxes of box_chunks chunks (1, 3 or 9: one box per page)
+ * instead of nine 2-D chunk boxes. */
+int etap_mla_stream_bench_page(const void* kv_pool, int64_t num_pages, int pages_per_cta, int grid,
+                               int nslot, int box_chunks, void* stream);
 
 /* Debug / tests: a one-CTA kernel launched with programmatic dependent launch that triggers
  * its dependents at entry, sleeps delay_ns, then copies n int32 from src to dst (device

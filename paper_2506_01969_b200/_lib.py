@@ -37,7 +37,7 @@ class EtapShapeError(ValueError):
     """Shape / argument rejected (the reference raises std::invalid_argument there)."""
 
 
-def _declare(lib: C.CDLL) -> None:
+def _declare(lib: C.CDLL, variant: bool = False) -> None:
     vp, i32, i64, u32, f32, f64, sz = C.c_void_p, C.c_int, C.c_int64, C.c_uint, C.c_float, C.c_double, C.c_size_t
     P = C.POINTER
     sig = {
@@ -81,9 +81,12 @@ def _declare(lib: C.CDLL) -> None:
         "etap_mla_umma_bench": (i32, [i32, i32, vp, i32]),
         "etap_mla_stream_bench": (i32, [vp, i64, i32, i32, i32, vp]),
         "etap_mla_stream_bench_mc": (i32, [vp, i64, i32, i32, i32, vp]),
+        "etap_mla_stream_bench_page": (i32, [vp, i64, i32, i32, i32, i32, vp]),
         "etap_mla_debug_pdl_write": (i32, [vp, vp, i32, i32, vp]),
     }
     for name, (res, args) in sig.items():
+        if "_bench" in name and variant and not hasattr(lib, name):
+            continue  # an older A/B variant build without a later debug microbenchmark
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
@@ -101,7 +104,7 @@ def lib() -> C.CDLL:
     if not LIB_PATH.exists():
         raise EtapError(f"{LIB_PATH} is missing and could not be built")
     handle = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
-    _declare(handle)
+    _declare(handle, variant=bool(os.environ.get("ETAP_LIB_VARIANT")))
     _lib = handle
     return _lib
 

@@ -842,15 +842,23 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
             SplitDesc sd;
             if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
             float m_own[HH];    // running max of this thread's heads (log2 units)
+            // derived from m_own, refreshed only when it moves (the lazy-rescale branch), so the
+            // per-tile path spends one compare and one subtraction per element on them:
+            float m_thr[HH];    // m_own + thresh: the vote threshold
+            float mu[HH];       // exp2 offset: m_own, or 0 while a causal column has seen no row
             float l_part[HH];   // partial column sums of this thread's rows, own heads
             float dbg_l = 0.f;  // debug state dump: running column sum of head `lane`
             int row_lim[HH];    // causal multi-token decode: rows visible to each column
+            int row_all = sd.seqlen;  // rows below this are visible to every column of the thread
 #pragma unroll
             for (int j = 0; j < HH; ++j) {
                 m_own[j] = -INFINITY;
+                m_thr[j] = -INFINITY;
+                mu[j] = mtp ? 0.f : -INFINITY;
                 l_part[j] = 0.f;
                 const int tok = (sd.g * HG + hoff + half * HH + j) / prm.heads_per_token;
                 row_lim[j] = sd.seqlen - (prm.causal ? prm.q_tokens - 1 - tok : 0);
+                row_all = min(row_all, row_lim[j]);
                 // a split whose first tile shows no row to any column skips the max exchange
                 // (bar.red.or is false), so s_m must already read -inf for the epilogue
                 // (the previous split's epilogue released s_m with its final barrier)
@@ -867,20 +875,27 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 ptx::tmem_wait_ld();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&bars[BAR_S_FREE + buf]);
+                if (tracer) ETAP_TRACE(prm, gt, 12);  // (tile rows: slots 10-15 are the epilogue's on a split's last tile)
 
                 const int grow = t * TILE + row;
                 float x[HH];
+                if (grow < row_all) {  // every row of a split but its last tile's tail
+#pragma unroll
+                    for (int j = 0; j < HH; ++j) x[j] = __uint_as_float(sr[j]) * prm.scale_log2;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < HH; ++j)
+                        x[j] = grow < row_lim[j] ? __uint_as_float(sr[j]) * prm.scale_log2 : -INFINITY;
+                }
                 bool exceed = false;
 #pragma unroll
-                for (int j = 0; j < HH; ++j) {
-                    x[j] = grow < row_lim[j] ? __uint_as_float(sr[j]) * prm.scale_log2 : -INFINITY;
-                    exceed |= x[j] > m_own[j] + thresh;
-                }
+                for (int j = 0; j < HH; ++j) exceed |= x[j] > m_thr[j];
                 const bool first = (t == sd.t0);
                 const bool debug = kDebug && prm.state != nullptr && t < prm.state_tiles;
                 const float dbg_m_old = (debug && lane_head && !first) ? s_m[hoff + lane] : -INFINITY;
                 // one barrier decides, CTA-uniformly, whether any running max must move
                 const bool any = ptx::bar_red_or(bar_a, 128, exceed || (negate && !first));
+                if (tracer) ETAP_TRACE(prm, gt, 13);
                 bool need_rescale = false;
                 float alpha_own[HH];
 #pragma unroll
@@ -915,14 +930,18 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                             s_alpha[hoff + half * HH + j] = alpha_own[j];
                         }
                     }
+#pragma unroll
+                    for (int j = 0; j < HH; ++j) {
+                        m_thr[j] = m_own[j] + thresh;
+                        // a column may have no visible row yet (multi-token causal mask): m = -inf
+                        mu[j] = (mtp && m_own[j] == -INFINITY) ? 0.f : m_own[j];
+                    }
                 }
                 float pv[HH];
 #pragma unroll
                 for (int j = 0; j < HH; ++j) {
-                    // a column may have no visible row yet (multi-token causal mask): m = -inf
-                    const float mu = (mtp && m_own[j] == -INFINITY) ? 0.f : m_own[j];
-                    pv[j] = ptx::exp2_ftz(x[j] - mu);
-                    l_part[j] = first ? pv[j] : fmaf(l_part[j], alpha_own[j], pv[j]);
+                    pv[j] = ptx::exp2_ftz(x[j] - mu[j]);
+                    l_part[j] = fmaf(l_part[j], alpha_own[j], pv[j]);  // first tile: alpha = 0, l = 0
                 }
                 if (debug) {
                     // BlockHook replay: column sums of this tile's P, running l, m, rescale in
@@ -1428,13 +1447,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             SplitDesc sd;
             if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
             float m_own[HH], l_part[HH];
+            float m_thr[HH], mu[HH];  // m_own + thresh, exp2 offset (refreshed when m_own moves)
             int row_lim[HH];
+            int row_all = sd.seqlen;  // rows below this are visible to every column of the thread
 #pragma unroll
             for (int j = 0; j < HH; ++j) {
                 m_own[j] = -INFINITY;
+                m_thr[j] = -INFINITY;
+                mu[j] = mtp ? 0.f : -INFINITY;
                 l_part[j] = 0.f;
                 const int tok = (sd.g * HG + half * HH + j) / prm.heads_per_token;
                 row_lim[j] = sd.seqlen - (prm.causal ? prm.q_tokens - 1 - tok : 0);
+                row_all = min(row_all, row_lim[j]);
                 if (head_owner) s_m[half * HH + j] = -INFINITY;
             }
             for (int t = sd.t0; t < sd.t1; ++t) {
@@ -1452,15 +1476,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
                 const int grow = t * TILE + row;
                 float x[HH];
+#pragma unroll
+                for (int j = 0; j < HH; ++j)  // S = S_q0 + S_q1 / 16 + S_q2 / 256 (the three fp8 terms of Q)
+                    x[j] = (__uint_as_float(s0[j]) +
+                            (__uint_as_float(s1[j]) * 0.0625f + __uint_as_float(s2[j]) * 0.00390625f)) * prm.scale_log2;
+                if (grow >= row_all) {  // a split's last tile: rows past the (per-token) context
+#pragma unroll
+                    for (int j = 0; j < HH; ++j) x[j] = grow < row_lim[j] ? x[j] : -INFINITY;
+                }
                 bool exceed = false;
 #pragma unroll
-                for (int j = 0; j < HH; ++j) {
-                    // S = S_q0 + S_q1 / 16 + S_q2 / 256 (the three fp8 terms of Q)
-                    const float sv = __uint_as_float(s0[j]) +
-                                     (__uint_as_float(s1[j]) * 0.0625f + __uint_as_float(s2[j]) * 0.00390625f);
-                    x[j] = grow < row_lim[j] ? sv * prm.scale_log2 : -INFINITY;
-                    exceed |= x[j] > m_own[j] + thresh;
-                }
+                for (int j = 0; j < HH; ++j) exceed |= x[j] > m_thr[j];
                 const bool first = (t == sd.t0);
                 const bool any = ptx::bar_red_or(1, 128, exceed);
                 bool need_rescale = false;
@@ -1496,13 +1522,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             s_alpha[half * HH + j] = alpha_own[j];
                         }
                     }
+#pragma unroll
+                    for (int j = 0; j < HH; ++j) {
+                        m_thr[j] = m_own[j] + thresh;
+                        mu[j] = (mtp && m_own[j] == -INFINITY) ? 0.f : m_own[j];
+                    }
                 }
                 float pv[HH];
 #pragma unroll
                 for (int j = 0; j < HH; ++j) {
-                    const float mu = (mtp && m_own[j] == -INFINITY) ? 0.f : m_own[j];
-                    pv[j] = ptx::exp2_ftz(x[j] - mu);
-                    l_part[j] = first ? pv[j] : fmaf(l_part[j], alpha_own[j], pv[j]);
+                    pv[j] = ptx::exp2_ftz(x[j] - mu[j]);
+                    l_part[j] = fmaf(l_part[j], alpha_own[j], pv[j]);  // first tile: alpha = 0, l = 0
                 }
                 // the P buffer is reused every other tile: GEMM2(gt-2) must have read it
                 if (tracer) ETAP_TRACE(prm, gt, 8);
@@ -1953,6 +1983,26 @@ int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_row
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return ETAP_OK;
+}
+
+// 3-D view of the same pool for whole-page boxes: {64 cols of a chunk, rows, chunk}, strides
+// 1152 B (row) and 128 B (chunk), so a box {64, 64, nchunk} lands chunks c0.. c0+nchunk-1 of one
+// page as consecutive 8 KB SW128 slots ([chunk][row][128 B]) with one TMA instruction.
+int make_map_page3d(CUtensorMap* map, const void* base, uint64_t rows, uint32_t nchunk) {
+    auto enc = get_encode_fn();
+    if (!enc) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver)");
+    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
+        return fail(ETAP_ERR_SHAPE, "tensor base address must be 16-byte aligned");
+    cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(NCHUNK)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(D_QK) * 2, 128};
+    cuuint32_t box[3] = {64, PAGE, nchunk};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled (page box) failed: " + std::to_string(r));
     return ETAP_OK;
 }
 
@@ -2924,6 +2974,58 @@ extern "C" int etap_mla_stream_bench_mc(const void* kv_pool, int64_t num_pages, 
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_stream_bench_mc_kernel, tm, pages_per_cta, nslot));
+    return ETAP_OK;
+}
+
+namespace {
+// Whole-page boxes: one 3-D TMA instruction per page instead of nine 2-D chunk boxes.
+__global__ void __launch_bounds__(64, 1) etap_stream_bench_page_kernel(const __grid_constant__ CUtensorMap tm_pg,
+                                                                        int pages_per_cta, int nslot, int box_chunks) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = ptx::align_smem_1024(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 200 * 1024);
+    uint64_t* done = full + NTB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NTB; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&done[i], 1); }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    const int p0 = blockIdx.x * pages_per_cta;
+    const uint32_t tiles_in_ring = (uint32_t)nslot / NCHUNK;
+    if (warp == 0) {
+        const uint64_t pol = ptx::policy_evict_first();
+        for (uint32_t gt = 0; gt < (uint32_t)pages_per_cta; ++gt) {
+            if (gt >= tiles_in_ring)
+                ptx::mbar_wait(&done[(gt - tiles_in_ring) % NTB], ((gt - tiles_in_ring) / NTB) & 1);
+            if (lane == 0) {
+                ptx::mbar_arrive_expect_tx(&full[gt % NTB], NCHUNK * SLOT_BYTES);
+                const uint32_t base = (gt % tiles_in_ring) * NCHUNK;
+                for (int c = 0; c < NCHUNK; c += box_chunks)
+                    ptx::tma_load_3d(smem + (base + c) * SLOT_BYTES, &tm_pg, &full[gt % NTB], 0, (p0 + gt) * PAGE, c, pol);
+            }
+            __syncwarp();
+        }
+    } else {
+        for (uint32_t gt = 0; gt < (uint32_t)pages_per_cta; ++gt) {
+            ptx::mbar_wait(&full[gt % NTB], (gt / NTB) & 1);
+            if (lane == 0) ptx::mbar_arrive(&done[gt % NTB]);
+            __syncwarp();
+        }
+    }
+}
+}  // namespace
+
+extern "C" int etap_mla_stream_bench_page(const void* kv_pool, int64_t num_pages, int pages_per_cta,
+                                          int grid, int nslot, int box_chunks, void* stream) {
+    if (nslot < NCHUNK || nslot * SLOT_BYTES > 200 * 1024 || box_chunks < 1 || NCHUNK % box_chunks)
+        return fail(ETAP_ERR_SHAPE, "bad nslot / box_chunks");
+    CUtensorMap tm;
+    if (int rc = make_map_page3d(&tm, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, box_chunks)) return rc;
+    cudaFuncSetAttribute(etap_stream_bench_page_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 202 * 1024);
+    etap_stream_bench_page_kernel<<<grid, 64, 202 * 1024, static_cast<cudaStream_t>(stream)>>>(tm, pages_per_cta, nslot,
+                                                                                                   box_chunks);
+    ETAP_CUDA(cudaGetLastError());
     return ETAP_OK;
 }
 

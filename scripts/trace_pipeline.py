@@ -81,11 +81,14 @@ def main() -> None:
                 nxt[0] - e[7],          # GEMM2(g) commit -> producer issues first chunk of g+1
                 nxt[1] - e[7],          # GEMM2(g) commit -> producer issued last chunk of g+1
                 nxt[4] - e[5],          # softmax idle: P(g) written -> sees S(g+1)
+                e[12] - e[4],           # softmax: TMEM load of S (bf16 kernel)
+                e[13] - e[12],          # softmax: lazy-rescale vote (bar.red.or) wait
+                e[8] - e[13],           # softmax: max exchange (if any) + exp
             ])
-    r = np.array(rows) if rows else np.zeros((0, 13))
+    r = np.array(rows) if rows else np.zeros((0, 16))
     labels = ["lat_tile(last issue->seen)", "issue_span", "g1_issue", "s_ready_wait", "softmax_exp",
               "softmax_pbuf_wait", "softmax_pwrite", "p_to_mma", "g2_issue", "PERIOD", "g2->next_first_issue",
-              "g2->next_last_issue", "softmax_idle"]
+              "g2->next_last_issue", "softmax_idle", "  s_tmem_ld", "  vote_wait", "  exp"]
     print(f"{len(rows)} steady-state tiles over {nparts} CTAs (ns): median / p10 / p90")
     for i, lab in enumerate(labels):
         if not len(r):
