@@ -548,6 +548,23 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
     return r;
 }
 
+// A softmax warpgroup's wait on an mbarrier: one warp polls it, the other three block on the
+// warpgroup's named barrier (no issue slots while blocked), so four warps instead of sixteen
+// re-issue the try_wait loop next to the softmax arithmetic. The named barrier is the thread
+// synchronisation after which every warp's tcgen05.fence::after_thread_sync orders its TMEM /
+// smem reads behind the observed phase.
+#ifndef ETAP_WG_POLL
+#define ETAP_WG_POLL 1
+#endif
+__device__ __forceinline__ void wg_wait(uint64_t* bar, uint32_t parity, uint32_t wg_bar, int wq) {
+#if ETAP_WG_POLL
+    if (wq == 0) ptx::mbar_wait(bar, parity);
+    ptx::named_bar_sync(wg_bar, 128);
+#else
+    ptx::mbar_wait(bar, parity);
+#endif
+}
+
 template <int HG_, bool DBG>
 __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
     etap_mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv,
@@ -867,7 +884,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
 
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
-                ptx::mbar_wait(&bars[BAR_S_FULL + buf], (gt >> 1) & 1);
+                wg_wait(&bars[BAR_S_FULL + buf], (gt >> 1) & 1, bar_a, wq);
                 ptx::tc_fence_after();
                 if (tracer) ETAP_TRACE(prm, gt, 4);
                 uint32_t sr[HH];
@@ -967,7 +984,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 // the P buffer is reused every P_BUFS tiles: GEMM2(gt - P_BUFS) must have read it (P in
                 // the tile's own rope slot: free since GEMM1 of this tile completed)
                 if (C::P_BUFS > 0 && gt >= C::P_BUFS)
-                    ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - C::P_BUFS) % NTB], ((gt - C::P_BUFS) / NTB) & 1);
+                    wg_wait(&bars[BAR_G2_DONE + (gt - C::P_BUFS) % NTB], ((gt - C::P_BUFS) / NTB) & 1, bar_a, wq);
                 if (tracer) ETAP_TRACE(prm, gt, 9);
                 if (need_rescale) {
                     // O^T must contain GEMM2(gt-1) before it is rescaled; s_alpha written above
@@ -1030,7 +1047,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 ptx::mbar_arrive(&bars[BAR_P_FULL + buf]);
                 if constexpr (C::P_IN_ROPE) {
                     // P_lo replaces P_hi once GEMM2 pass 1 of this tile has read it
-                    ptx::mbar_wait(&bars[BAR_G2_P1 + gt % NTB], (gt / NTB) & 1);
+                    wg_wait(&bars[BAR_G2_P1 + gt % NTB], (gt / NTB) & 1, bar_a, wq);
                     ptx::tc_fence_after();
                     write_p_part<C>(p_rope, row, half, p_lo, hoff);
                     ptx::fence_proxy_async_smem();

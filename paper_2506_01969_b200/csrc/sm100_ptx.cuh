@@ -63,8 +63,24 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
+// try_wait suspends the thread until the phase completes or a time limit expires; without a
+// hint the limit is short and a waiting warp re-issues the probe loop, stealing issue slots
+// from the softmax warps on its SM sub-partition (ncu at 128 heads: ~8k spin instructions per
+// tile against ~1.5k of softmax arithmetic). ETAP_WAIT_HINT_NS sets the suspend time limit.
+#ifndef ETAP_WAIT_HINT_NS
+#define ETAP_WAIT_HINT_NS 0
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar_addr, uint32_t parity) {
     uint32_t ok;
+#if ETAP_WAIT_HINT_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar_addr), "r"(parity), "n"(ETAP_WAIT_HINT_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -72,6 +88,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar_addr, uint32_t parity
         : "=r"(ok)
         : "r"(bar_addr), "r"(parity)
         : "memory");
+#endif
     return ok != 0;
 }
 
