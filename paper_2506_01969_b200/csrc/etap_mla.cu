@@ -574,6 +574,10 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
     constexpr int HG = C::HG, HH = C::HH;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = ptx::align_smem_1024(smem_raw);
+    // no alignment slack allocated (P_LO_BUF): the dynamic smem base must already be 1024-aligned
+    if constexpr (C::SMEM_ALLOC == C::SMEM_USED) {
+        if (smem != smem_raw) asm volatile("trap;");
+    }
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
     const int warp = threadIdx.x >> 5;
@@ -673,16 +677,20 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     const int v = __shfl_sync(0xffffffffu, pg, min(ta - base, 31));
                     page_ahead = (ta < sd.t1 && ta - base < 32) ? v : -1;
                 }
-                if (gt >= A_LAG) ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - A_LAG) % NTB], ((gt - A_LAG) / NTB) & 1);
+                if constexpr (C::P_LO_BUF) {  // V0-V1 of gt-2: free after its GEMM2 d-block 0
+                    if (gt >= 2) ptx::mbar_wait(&bars[BAR_G2_Q1 + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+                } else if (gt >= A_LAG) {
+                    ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - A_LAG) % NTB], ((gt - A_LAG) / NTB) & 1);
+                }
                 if (lane == 0) {
                     if (gt == 0) { ETAP_TRACE_G(prm, 9); ETAP_TRACE_CLK(prm, 15); }
                     ETAP_TRACE(prm, gt, 0);
                     ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_A + tb], C::SPLIT_POS * SLOT_BYTES);
 #pragma unroll 1
                     for (int pos = 0; pos < C::SPLIT_POS; ++pos) {
-                        const uint32_t s = (pos0 + pos) % C::NSLOT;
+                        const uint32_t s = (pos0 + item_pos<C>(pos, gt)) % C::NSLOT;
                         ptx::tma_load_2d(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_A + tb],
-                                         chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
+                                         item_chunk<C>(pos, gt) * 64, page * PAGE, pol_kv);
                     }
                     if (page_ahead >= 0 && page_ahead < prm.num_pages)
                         ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) +
@@ -709,14 +717,16 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 // positions [SPLIT_POS, SPLIT_POS2) reuse tile gt-2's first four positions: free
                 // once GEMM2 d-blocks 0-1 of gt-2 completed (16-slot ring: tile gt-1's first two
                 // positions, free once GEMM2 d-block 0 of gt-1 completed)
+                // (P_LO_BUF: V2-V5 of gt-2, free after its GEMM2 d-blocks 0-2)
                 if (!C::P_IN_ROPE && gt >= 2) ptx::mbar_wait(&bars[BAR_G2_HALF + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+                if (C::P_LO_BUF && gt >= 2) ptx::mbar_wait(&bars[BAR_G2_3Q + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
                 if (lane == 0) {
                     ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_B + tb], (C::SPLIT_POS2 - C::SPLIT_POS) * SLOT_BYTES);
 #pragma unroll 1
                     for (int pos = C::SPLIT_POS; pos < C::SPLIT_POS2; ++pos) {
-                        const uint32_t s = (pos0 + pos) % C::NSLOT;
+                        const uint32_t s = (pos0 + item_pos<C>(pos, gt)) % C::NSLOT;
                         ptx::tma_load_2d(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_B + tb],
-                                         chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
+                                         item_chunk<C>(pos, gt) * 64, page * PAGE, pol_kv);
                     }
                     if (!C::THIRD_GROUP) ETAP_TRACE(prm, gt, 1);
                 }
@@ -724,16 +734,20 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     // the rest reuse gt-2's positions [4, 9 - SPLIT_POS): free after GEMM2 d-blocks
                     // 0-2 of gt-2 (22-slot ring) or the whole GEMM2
                     __syncwarp();
+                    // (P_LO_BUF: V6, V7 and the rope slot, whose P_hi GEMM2 reads in every d-block,
+                    // free after the whole GEMM2 of gt-2)
                     if (!C::P_IN_ROPE && gt >= 2)
                         ptx::mbar_wait(&bars[(C::G3_AFTER_3Q ? BAR_G2_3Q : BAR_G2_DONE) + (gt - 2) % NTB],
                                        ((gt - 2) / NTB) & 1);
+                    if (C::P_LO_BUF && gt >= 2)
+                        ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
                     if (lane == 0) {
                         ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_C + tb], (NCHUNK - C::SPLIT_POS2) * SLOT_BYTES);
 #pragma unroll 1
                         for (int pos = C::SPLIT_POS2; pos < NCHUNK; ++pos) {
-                            const uint32_t s = (pos0 + pos) % C::NSLOT;
+                            const uint32_t s = (pos0 + item_pos<C>(pos, gt)) % C::NSLOT;
                             ptx::tma_load_2d(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_C + tb],
-                                             chunk_at(pos, gt) * 64, page * PAGE, pol_kv);
+                                             item_chunk<C>(pos, gt) * 64, page * PAGE, pol_kv);
                         }
                         ETAP_TRACE(prm, gt, 1);
                     }
@@ -791,7 +805,22 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 ptx::tc_fence_after();
                 ETAP_TRACE(prm, gt, 6);
                 const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
-                if constexpr (C::P_IN_ROPE) {
+                if constexpr (C::P_LO_BUF) {
+                    // per d-block: O^T += V^T P_hi^T (P_hi in the tile's rope slot) then
+                    // O^T += V^T P_lo^T (the P_lo buffer), one accumulator; a commit after d-block 0
+                    // and after d-block 2 releases V0-V1 / V2-V5 to the next tile of this ring half
+                    const uint32_t pa = ring_addr + ((pos0 + pos_of_chunk(8, gt)) % C::NSLOT) * SLOT_BYTES;
+#pragma unroll
+                    for (int blk = 0; blk < 4; ++blk) {
+                        uint32_t sa = pos0 + pos_of_chunk(2 * blk, gt);
+                        sa = sa >= C::NSLOT ? sa - C::NSLOT : sa;
+                        const uint32_t ot = tmem_base + C::TCOL_O + C::OBLK * blk;
+                        issue_gemm2_block<C>(ot, ring_addr + sa * SLOT_BYTES, pa, t == sd.t0);
+                        issue_gemm2_block<C>(ot, ring_addr + sa * SLOT_BYTES, p_addr, false);
+                        if (blk == 0) ptx::umma_commit_elect(&bars[BAR_G2_Q1 + gt % NTB]);
+                        if (blk == 2) ptx::umma_commit_elect(&bars[BAR_G2_3Q + gt % NTB]);
+                    }
+                } else if constexpr (C::P_IN_ROPE) {
                     // pass 1: O^T += V^T P_hi^T (P in the tile's rope slot), then the softmax
                     // replaces P_hi by P_lo in the same slot; pass 2: O^T += V^T P_lo^T
                     const uint32_t pa = ring_addr + ((pos0 + pos_of_chunk(8, gt)) % C::NSLOT) * SLOT_BYTES;
@@ -840,11 +869,17 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
         const int half = lane >> 4;
         const int row = s_row_of(wq, lane);    // KV row in the tile
         const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
-        float* red_max = reinterpret_cast<float*>(smem + C::OFF_RED);  // [2][4][HG]
-        float* red_sum = red_max + 8 * HG;                               // [4][HG]
-        float* s_m = red_sum + 4 * HG;         // [HG] running max per head (log2 units)
+        float* red_max = reinterpret_cast<float*>(smem + C::OFF_RED);  // [RED_MAX_BUFS][4][HG]
+        // [4][HG] column sums (epilogue; BlockHook dump): aliases red_max with P_LO_BUF (every use
+        // lies between a vote and the next max exchange of the warpgroup's own heads)
+        float* red_sum = C::P_LO_BUF ? red_max : red_max + 8 * HG;
+        float* s_m = red_max + C::RED_MAX_BUFS * 4 * HG + (C::P_LO_BUF ? 0 : 4 * HG);  // [HG] running max (log2)
         float* s_alpha = s_m + HG;             // [HG] rescale factors of the current tile
-        int* s_row = reinterpret_cast<int*>(s_alpha + HG);  // [HG] output row of each head (epilogue)
+        // [HG] output row of each head (epilogue): with P_LO_BUF in the warpgroup's own 256 B
+        // column stripe of row group 0 of the P_lo buffer (idle from the split's last GEMM2 until
+        // this warpgroup writes the next P_lo)
+        int* s_row = C::P_LO_BUF ? reinterpret_cast<int*>(smem + C::OFF_P + wg * 256) - hoff
+                                 : reinterpret_cast<int*>(s_alpha + HG);
         const bool negate = prm.flags & FLAG_NEGATE_RESCALE;
         const bool eager = negate || (prm.flags & FLAG_EAGER_RESCALE);
         const float thresh = eager ? 0.f : LAZY_RESCALE_LOG2;
@@ -919,7 +954,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 for (int j = 0; j < HH; ++j) alpha_own[j] = first ? 0.f : 1.f;
                 if (any) {
                     const float wm = halfwarp_reduce<true, HH>(x, lane);
-                    float* rm = red_max + (gt & 1) * 4 * HG;
+                    float* rm = red_max + (C::RED_MAX_BUFS == 2 ? (gt & 1) : 0) * 4 * HG;
                     if (rwriter) rm[wq * HG + hoff + half * HH + rhead] = wm;
                     ptx::named_bar_sync(bar_b, 128);
                     bool upd = false;
@@ -985,6 +1020,8 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 // the tile's own rope slot: free since GEMM1 of this tile completed)
                 if (C::P_BUFS > 0 && gt >= C::P_BUFS)
                     wg_wait(&bars[BAR_G2_DONE + (gt - C::P_BUFS) % NTB], ((gt - C::P_BUFS) / NTB) & 1, bar_a, wq);
+                if (C::P_LO_BUF && gt >= 1)  // the P_lo buffer: GEMM2(gt - 1) must have read it
+                    wg_wait(&bars[BAR_G2_DONE + (gt - 1) % NTB], ((gt - 1) / NTB) & 1, bar_a, wq);
                 if (tracer) ETAP_TRACE(prm, gt, 9);
                 if (need_rescale) {
                     // O^T must contain GEMM2(gt-1) before it is rescaled; s_alpha written above
@@ -1025,6 +1062,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
                     p_rope = smem + C::OFF_RING + ((pos0 + pos_of_chunk(8, gt)) % C::NSLOT) * SLOT_BYTES;
                     write_p_part<C>(p_rope, row, half, p_hi, hoff);
+                    if constexpr (C::P_LO_BUF) write_p_part<C>(smem + C::OFF_P, row, half, p_lo, hoff);
                 } else {
                     write_p_hilo<C>(smem + C::OFF_P + (buf % C::P_BUFS) * C::P_BYTES, row, half, pv, hoff);
                 }
@@ -1045,7 +1083,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 ptx::tc_fence_before();
                 if (tracer) ETAP_TRACE(prm, gt, 5);
                 ptx::mbar_arrive(&bars[BAR_P_FULL + buf]);
-                if constexpr (C::P_IN_ROPE) {
+                if constexpr (C::P_IN_ROPE && !C::P_LO_BUF) {
                     // P_lo replaces P_hi once GEMM2 pass 1 of this tile has read it
                     wg_wait(&bars[BAR_G2_P1 + gt % NTB], (gt / NTB) & 1, bar_a, wq);
                     ptx::tc_fence_after();
@@ -1079,7 +1117,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
             // in every thread costs ~1.6k cycles); 1/l is broadcast through red_max, which no
             // one reads between tiles
             float L_own = 0.f;
-            float* s_inv = red_max;
+            float* s_inv = C::P_LO_BUF ? s_alpha : red_max;  // (P_LO_BUF: red_max holds red_sum)
             if (lane_head) {
                 const int h = hoff + lane;
                 const float l = red_sum[h] + red_sum[HG + h] + red_sum[2 * HG + h] + red_sum[3 * HG + h];
@@ -2476,7 +2514,7 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     prm.split_off_out = const_cast<int32_t*>(split_off);
     prm.lanes_on = lanes_enabled() ? 1 : 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
-    const int max_vb = MAX_FUSED_VB;
+    const int max_vb = hg == 64 ? Cfg<64>::MAX_VB : (hg == 32 ? Cfg<32>::MAX_VB : Cfg<16>::MAX_VB);
     prm.inkernel_sched = (ls.line_n <= max_vb && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
     prm.early_meta = (early_meta_enabled() && (flags & ETAP_FLAG_EARLY_METADATA)) ? 1 : 0;
     prm.fixed_cost = META_FIXED_COST;

@@ -39,7 +39,7 @@ constexpr int NBAR = 8 * NTB + 10;
 // kernel computes itself (the block-wide scan takes one line entry per thread of the >= 256-
 // thread CTA); longer lines run K1 first.
 constexpr int MAX_FUSED_VB = 256;
-constexpr int sched_smem_ints(int max_vb) { return 3 * max_vb + 2 + 8 + 16; }  // pref, soff, len, sched, wt (<= 16 warps)
+constexpr int sched_smem_ints(int max_vb) { return 3 * max_vb + 2 + 8 + 32; }  // pref, soff, len, sched, wt (<= 32 warps)
 
 // warp 0 TMA producer, warp 1 GEMM1 issuer (+TMEM alloc), warp 2 GEMM2 issuer, warp 3 idle,
 // warps 4..7 softmax / epilogue (warp % 4 = TMEM lane quadrant)
@@ -79,8 +79,8 @@ constexpr int BAR_G2_HALF = 3 * NTB;    // [NTB] GEMM2 d-blocks 0-1 of tile gt c
 constexpr int BAR_FULL_C = 4 * NTB + 8;  // [NTB] ring positions [SPLIT_POS2, 9) of tile gt landed
 constexpr int BAR_G2_3Q = 5 * NTB + 8;   // [NTB] GEMM2 d-blocks 0-2 of tile gt complete (V0..V5 free)
 constexpr int BAR_G2_Q1 = 6 * NTB + 8;   // [NTB] GEMM2 d-block 0 of tile gt complete (its first two positions free)
-constexpr int BAR_G2_P1 = 7 * NTB + 8;   // [NTB] GEMM2 pass 1 (P_hi) of tile gt complete (two-pass GEMM2)
-constexpr int BAR_P2_FULL = 8 * NTB + 8; // [2] P_lo written (two-pass GEMM2), count 128 * NWG
+constexpr int BAR_G2_P1 = 7 * NTB + 8;   // [NTB] GEMM2 pass 1 (P_hi) of tile gt complete (two-pass GEMM2, !P_LO_BUF)
+constexpr int BAR_P2_FULL = 8 * NTB + 8; // [2] P_lo written (two-pass GEMM2, !P_LO_BUF), count 128 * NWG
 constexpr int BAR_Q_FULL = 4 * NTB + 0;
 constexpr int BAR_Q_EMPTY = 4 * NTB + 1;
 constexpr int BAR_S_FULL = 4 * NTB + 2;  // [2]
@@ -118,6 +118,18 @@ struct Cfg {
     static constexpr bool P_IN_ROPE = HG == 64;
     static constexpr bool SAME_D = P_IN_ROPE;
     static constexpr int P_BUFS = P_IN_ROPE ? 0 : ((HG == 16 || (HG == 32 && NSLOT <= 20)) ? 2 : 1);
+    // P_LO_BUF (HG = 64, round 2): P_lo gets its own 8 KB buffer, so GEMM2 issues each d-block's
+    // hi and lo MMAs back to back and commits per d-block; the next tile of the ring half then
+    // lands in three groups in the order GEMM2 frees the slots (V0-V1 after d-block 0, V2-V5
+    // after d-block 2, V6-V7 + rope after the whole GEMM2) instead of after the whole two-pass
+    // GEMM2. The 8 KB come from a 64-entry fused-schedule line, a single-buffered max exchange,
+    // the epilogue's sums and output rows aliased into buffers it does not use, and no 1 KB
+    // alignment slack (the dynamic smem base is 1024-aligned; the kernel traps if it is not).
+#ifndef ETAP_HG64_PLO
+#define ETAP_HG64_PLO 1
+#endif
+    static constexpr bool P_LO_BUF = P_IN_ROPE && ETAP_HG64_PLO;
+    static constexpr int RED_MAX_BUFS = P_LO_BUF ? 1 : 2;  // the per-tile vote separates consecutive uses
     // >= 20 slots: tile gt's ring positions [0, SPLIT_POS) reuse tile gt-3's last slots (free
     // after its GEMM2), positions p >= SPLIT_POS reuse tile gt-2's position p - SPLIT_POS. Of
     // those, gt-2's positions [0, 4) hold {V0..V3} or {rope, V0..V2}: free once GEMM2 d-blocks
@@ -125,7 +137,10 @@ struct Cfg {
     // then and only [SPLIT_POS2, 9) wait for the whole GEMM2 of gt-2 (an empty group for HG = 16).
     // 18 slots (P_IN_ROPE): tile gt reuses tile gt-2's slots, all free after GEMM2(gt-2); the
     // three landing groups only let GEMM1 start on the first chunks while the rest stream in.
-    static constexpr int SPLIT_POS = P_IN_ROPE ? 3 : NSLOT - 18;
+    // Landing groups are ranges of "items" [0, SPLIT_POS), [SPLIT_POS, SPLIT_POS2), [SPLIT_POS2, 9):
+    // ring positions (chunk = chunk_at(pos)), or with P_LO_BUF chunks (pos = pos_of_chunk(chunk)):
+    // V0-V1 | V2-V5 | V6, V7, rope, the order GEMM2 of the tile two back frees their slots.
+    static constexpr int SPLIT_POS = P_LO_BUF ? 2 : (P_IN_ROPE ? 3 : NSLOT - 18);
     static constexpr int SPLIT_POS2 = P_IN_ROPE ? 6 : (SPLIT_POS + 4 < NCHUNK ? SPLIT_POS + 4 : NCHUNK);
     static constexpr bool THIRD_GROUP = SPLIT_POS2 < NCHUNK;
     // the third group reuses gt-2's positions [4, 9 - SPLIT_POS): V chunks up to V(8 - SPLIT_POS),
@@ -139,15 +154,19 @@ struct Cfg {
     static constexpr int P_BYTES = TILE * PN * 2;
     static constexpr int OFF_RING = 0;
     static constexpr int OFF_Q = OFF_RING + NSLOT * SLOT_BYTES;
-    static constexpr int OFF_P = OFF_Q + Q_BYTES;        // P_BUFS buffers
-    static constexpr int OFF_RED = OFF_P + P_BUFS * P_BYTES;  // red_max[2][4][HG], red_sum[4][HG], m[HG], alpha[HG], row[HG]
-    static constexpr int RED_FLOATS = 2 * 4 * HG + 4 * HG + HG + HG + HG;  // + output row per head
+    static constexpr int OFF_P = OFF_Q + Q_BYTES;        // P_BUFS buffers, or the P_lo buffer
+    static constexpr int P_TOTAL = P_LO_BUF ? P_BYTES : P_BUFS * P_BYTES;
+    // red_max[RED_MAX_BUFS][4][HG], then (without P_LO_BUF) red_sum[4][HG], m[HG], alpha[HG],
+    // row[HG]; with P_LO_BUF the epilogue's red_sum aliases red_max, 1/l aliases alpha and the
+    // output rows sit in the warpgroup's own column stripe of the (then idle) P_lo buffer
+    static constexpr int OFF_RED = OFF_P + P_TOTAL;
+    static constexpr int RED_FLOATS = RED_MAX_BUFS * 4 * HG + (P_LO_BUF ? 0 : 4 * HG) + HG + HG + (P_LO_BUF ? 0 : HG);
     static constexpr int OFF_BAR = align_up(OFF_RED + RED_FLOATS * 4, 16);
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr int OFF_SCHED = OFF_TMEM + 16;
-    static constexpr int MAX_VB = MAX_FUSED_VB;  // fused-schedule line limit
+    static constexpr int MAX_VB = P_LO_BUF ? 64 : MAX_FUSED_VB;  // fused-schedule line limit (longer lines: K1)
     static constexpr int SMEM_USED = OFF_SCHED + sched_smem_ints(MAX_VB) * 4;
-    static constexpr int SMEM_ALLOC = SMEM_USED + 1024;  // slack for manual 1024 B alignment
+    static constexpr int SMEM_ALLOC = SMEM_USED + (P_LO_BUF ? 0 : 1024);  // slack for manual 1024 B alignment
     // TMEM columns (128 lanes x 32 bit): S^T double buffer [0, 2HG) (M=64 lane layout), then
     // four O^T d-blocks of GN columns (HG hi | HG lo, or HG summed for SAME_D)
     static constexpr uint32_t TCOL_S = 0;
@@ -158,6 +177,8 @@ struct Cfg {
     static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
     static_assert(NSLOT % 2 == 0 && NSLOT >= 18 && NSLOT <= 27, "ring must hold two tiles, even slots");
     static_assert(!P_IN_ROPE || (NSLOT == 18 && P_BYTES == SLOT_BYTES), "P part fills exactly the rope slot");
+    static_assert(!P_LO_BUF || (OFF_P % 1024 == 0 && P_BYTES == 8 * 1024 && HW * 16 == 256),
+                  "P_lo buffer: 8 row groups of 1024 B, a warpgroup's heads are one 256 B stripe per row group");
     static_assert(TCOL_O + 4 * OBLK <= 512, "TMEM budget");
     static_assert(HW % 16 == 0, "a warpgroup handles whole 16-column TMEM loads");
 };
@@ -191,9 +212,15 @@ __device__ __forceinline__ int pos_of_chunk(int chunk, uint32_t gt) {
     return chunk;
 }
 
+// Landing-group item i of tile gt: its ring position and its latent column chunk (Cfg::SPLIT_POS)
+template <class C>
+__device__ __forceinline__ int item_pos(int i, uint32_t gt) { return C::P_LO_BUF ? pos_of_chunk(i, gt) : i; }
+template <class C>
+__device__ __forceinline__ int item_chunk(int i, uint32_t gt) { return C::P_LO_BUF ? i : chunk_at(i, gt); }
+
 // GEMM1 of one tile: S^T[64 x HG] = K[64 x 576] . Q^T[576 x HG], 9 chunks x 4 MMAs (K=16),
-// ring positions [POS_BEGIN, POS_END). Whole-warp call (elect inside). pos0 = ring slot of
-// the tile's first position.
+// landing-group items [POS_BEGIN, POS_END). Whole-warp call (elect inside). pos0 = ring slot of
+// the tile's first position. The tile's first MMA (item 0) zero-initialises S^T.
 template <class C, int POS_BEGIN, int POS_END>
 __device__ __forceinline__ void issue_gemm1_tile(uint32_t s_tmem, uint32_t ring_addr,
                                                  uint32_t q_addr, uint32_t pos0, uint32_t gt) {
@@ -202,9 +229,9 @@ __device__ __forceinline__ void issue_gemm1_tile(uint32_t s_tmem, uint32_t ring_
     const uint64_t b_q = ptx::smem_desc(q_addr, 16, 1024, ptx::LAYOUT_SW128);
 #pragma unroll
     for (int pos = POS_BEGIN; pos < POS_END; ++pos) {
-        uint32_t s = pos0 + pos;
+        uint32_t s = pos0 + item_pos<C>(pos, gt);
         s = s >= C::NSLOT ? s - C::NSLOT : s;
-        const int chunk = chunk_at(pos, gt);
+        const int chunk = item_chunk<C>(pos, gt);
         const uint64_t a0 = a_ring + static_cast<uint64_t>(s * (SLOT_BYTES >> 4));
         const uint64_t b0 = b_q + static_cast<uint64_t>(chunk * (C::Q_CHUNK_BYTES >> 4));
 #pragma unroll
