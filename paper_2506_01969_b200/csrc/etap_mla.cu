@@ -1016,8 +1016,23 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     ptx::named_bar_sync(bar_b, 128);
                 }
                 if (tracer) ETAP_TRACE(prm, gt, 8);
-                // the P buffer is reused every P_BUFS tiles: GEMM2(gt - P_BUFS) must have read it (P in
-                // the tile's own rope slot: free since GEMM1 of this tile completed)
+                // head group 64: P_hi goes to the tile's own rope slot (free since GEMM1 of this tile
+                // completed) before the wait for the P_lo buffer below
+                uint32_t p_lo[HH / 2];  // two-pass GEMM2: written after pass 1
+                uint8_t* p_rope = nullptr;
+                if constexpr (C::P_IN_ROPE) {
+                    uint32_t p_hi[HH / 2];
+#pragma unroll
+                    for (int i = 0; i < HH / 2; ++i) {
+                        p_hi[i] = pack_bf16x2(pv[2 * i], pv[2 * i + 1]);
+                        p_lo[i] = pack_bf16x2(pv[2 * i] - __uint_as_float(p_hi[i] << 16),
+                                              pv[2 * i + 1] - __uint_as_float(p_hi[i] & 0xffff0000u));
+                    }
+                    const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
+                    p_rope = smem + C::OFF_RING + ((pos0 + pos_of_chunk(8, gt)) % C::NSLOT) * SLOT_BYTES;
+                    write_p_part<C>(p_rope, row, half, p_hi, hoff);
+                }
+                // the P buffer is reused every P_BUFS tiles: GEMM2(gt - P_BUFS) must have read it
                 if (C::P_BUFS > 0 && gt >= C::P_BUFS)
                     wg_wait(&bars[BAR_G2_DONE + (gt - C::P_BUFS) % NTB], ((gt - C::P_BUFS) / NTB) & 1, bar_a, wq);
                 if (C::P_LO_BUF && gt >= 1)  // the P_lo buffer: GEMM2(gt - 1) must have read it
@@ -1049,19 +1064,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     }
                     ptx::tmem_wait_st();
                 }
-                uint32_t p_lo[HH / 2];  // two-pass GEMM2: written after pass 1
-                uint8_t* p_rope = nullptr;
                 if constexpr (C::P_IN_ROPE) {
-                    uint32_t p_hi[HH / 2];
-#pragma unroll
-                    for (int i = 0; i < HH / 2; ++i) {
-                        p_hi[i] = pack_bf16x2(pv[2 * i], pv[2 * i + 1]);
-                        p_lo[i] = pack_bf16x2(pv[2 * i] - __uint_as_float(p_hi[i] << 16),
-                                              pv[2 * i + 1] - __uint_as_float(p_hi[i] & 0xffff0000u));
-                    }
-                    const uint32_t pos0 = (gt * NCHUNK) % C::NSLOT;
-                    p_rope = smem + C::OFF_RING + ((pos0 + pos_of_chunk(8, gt)) % C::NSLOT) * SLOT_BYTES;
-                    write_p_part<C>(p_rope, row, half, p_hi, hoff);
                     if constexpr (C::P_LO_BUF) write_p_part<C>(smem + C::OFF_P, row, half, p_lo, hoff);
                 } else {
                     write_p_hilo<C>(smem + C::OFF_P + (buf % C::P_BUFS) * C::P_BYTES, row, half, pv, hoff);
