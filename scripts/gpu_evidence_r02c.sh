@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 evidence session on one B200: sanitizer, streaming bound, launch lists + ncu of the
 # 16-head K2, the FP8 K2 and the 64/128-head K2, the reference harness, sweeps, bench lines.
-TAG=${1:-r02c}
+TAG=${1:-r02d}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 bash scripts/gpu_call_sanitize.sh
