@@ -350,6 +350,11 @@ int etap_mla_stream_bench_mc(const void* kv_pool, int64_t num_pages, int pages_p
 int etap_mla_stream_bench_page(const void* kv_pool, int64_t num_pages, int pages_per_cta, int grid,
                                int nslot, int box_chunks, void* stream);
 
+/* Debug / tests (host only): the binary64 -> bfloat16 round-to-nearest-even that
+ * etap_mla_run_etap_f64 applies to AttentionProblem operands, as the bit-level fast form or
+ * (reference_form != 0) the frexp / nearbyint form it must equal. out: n bf16 bit patterns. */
+int etap_mla_debug_bf16_rne(const double* x, int64_t n, uint16_t* out, int reference_form);
+
 /* Debug / tests: a one-CTA kernel launched with programmatic dependent launch that triggers
  * its dependents at entry, sleeps delay_ns, then copies n int32 from src to dst (device
  * pointers) — a PDL producer writing seqlens or block_table right before a decode. */

@@ -83,6 +83,7 @@ def _declare(lib: C.CDLL, variant: bool = False) -> None:
         "etap_mla_stream_bench_mc": (i32, [vp, i64, i32, i32, i32, vp]),
         "etap_mla_stream_bench_page": (i32, [vp, i64, i32, i32, i32, i32, vp]),
         "etap_mla_debug_pdl_write": (i32, [vp, vp, i32, i32, vp]),
+        "etap_mla_debug_bf16_rne": (i32, [vp, i64, vp, i32]),
     }
     for name, (res, args) in sig.items():
         if "_bench" in name and variant and not hasattr(lib, name):

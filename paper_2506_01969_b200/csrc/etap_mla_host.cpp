@@ -11,7 +11,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/etap_mla.h"
@@ -39,8 +41,9 @@ struct DevBuf {
 };
 
 // Round a binary64 value to the nearest bfloat16 (ties to even) directly, without the
-// double -> float -> bf16 double rounding; returns the 16-bit pattern.
-uint16_t bf16_bits_rne(double x) {
+// double -> float -> bf16 double rounding; returns the 16-bit pattern. Reference form, used for
+// the bf16 subnormal range only (frexp / nearbyint / ldexp cost ~40 ns per element).
+uint16_t bf16_bits_rne_slow(double x) {
     if (std::isnan(x)) return 0x7FC0;
     const double ax = std::fabs(x);
     float f;
@@ -60,6 +63,42 @@ uint16_t bf16_bits_rne(double x) {
     uint32_t u;
     std::memcpy(&u, &f, 4);
     return static_cast<uint16_t>(u >> 16);
+}
+
+// The same rounding on the bit pattern: for |x| >= 2^-126 (bf16 normal range) rebias the
+// exponent, add the ties-to-even increment at bit 45 and shift; a carry out of the mantissa
+// bumps the exponent (to infinity past the largest finite bf16). Bit-identical to the reference
+// form (CPU test against it over random, boundary and tie values).
+inline uint16_t bf16_bits_rne(double x) {
+    uint64_t u;
+    std::memcpy(&u, &x, 8);
+    const uint16_t sign = static_cast<uint16_t>((u >> 48) & 0x8000u);
+    const uint64_t m = u & 0x7FFFFFFFFFFFFFFFull;
+    if (m > 0x7FF0000000000000ull) return 0x7FC0;  // NaN
+    const int64_t e = static_cast<int64_t>(m >> 52) - 1023;
+    if (e < -126) return bf16_bits_rne_slow(x);    // zero and the bf16 subnormal range
+    if (e > 127) return sign | 0x7F80;             // overflow and infinity
+    uint64_t t = m - (static_cast<uint64_t>(1023 - 127) << 52);
+    t += (1ull << 44) - 1 + ((t >> 45) & 1);
+    const uint64_t r = t >> 45;
+    return sign | static_cast<uint16_t>(r >= 0x7F80 ? 0x7F80 : r);
+}
+
+// for (i in [0, n)) f(i) over up to 16 host threads (large problems only)
+template <class F>
+void parallel_for(int64_t n, const F& f) {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int64_t nt = n < (1 << 16) ? 1 : static_cast<int64_t>(hw);
+    if (nt <= 1) {
+        for (int64_t i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int64_t t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            for (int64_t i = n * t / nt; i < n * (t + 1) / nt; ++i) f(i);
+        });
+    for (auto& x : th) x.join();
 }
 
 // Device address of page-locked (cudaHostAlloc / cudaHostRegister) host memory, or nullptr
@@ -247,9 +286,10 @@ static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int6
         return host_fail(ETAP_ERR_SHAPE, "scale must be finite and >= 0");
     if (n_kv > (int64_t)1 << 30) return host_fail(ETAP_ERR_SHAPE, "n_kv too large");
     // MLA aliasing: V must be the first 512 columns of the latent KV rows
-    for (int64_t i = 0; i < n_kv; ++i)
-        if (std::memcmp(v + i * d_v, k + i * d_qk, sizeof(double) * d_v) != 0)
-            return host_fail(ETAP_ERR_SHAPE, "V must be the first 512 columns of K (MLA aliasing)");
+    std::vector<uint8_t> v_ok(static_cast<size_t>(n_kv));
+    parallel_for(n_kv, [&](int64_t i) { v_ok[i] = std::memcmp(v + i * d_v, k + i * d_qk, sizeof(double) * d_v) == 0; });
+    if (std::find(v_ok.begin(), v_ok.end(), uint8_t{0}) != v_ok.end())
+        return host_fail(ETAP_ERR_SHAPE, "V must be the first 512 columns of K (MLA aliasing)");
 
     const int heads = static_cast<int>((n_q + ETAP_MLA_HEAD_GROUP - 1) / ETAP_MLA_HEAD_GROUP) *
                       ETAP_MLA_HEAD_GROUP;
@@ -267,7 +307,9 @@ static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int6
     for (int64_t i = 0; i < n_q * d_qk; ++i) qb[i] = bf16_bits_rne(q[i]);
     for (int64_t b = 1; b < batch; ++b)
         std::memcpy(qb.data() + b * heads * d_qk, qb.data(), sizeof(uint16_t) * heads * d_qk);
-    for (int64_t i = 0; i < n_kv * d_qk; ++i) kvb[i] = bf16_bits_rne(k[i]);
+    parallel_for(n_kv, [&](int64_t r) {
+        for (int64_t c = 0; c < d_qk; ++c) kvb[r * d_qk + c] = bf16_bits_rne(k[r * d_qk + c]);
+    });
     std::vector<int32_t> bt(static_cast<size_t>(batch) * pages), sl(batch);
     for (int64_t b = 0; b < batch; ++b) {
         for (int64_t i = 0; i < pages; ++i) bt[b * pages + i] = static_cast<int32_t>(i);
@@ -275,23 +317,41 @@ static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int6
     }
     std::vector<float> of(static_cast<size_t>(batch) * heads * d_v), lf(static_cast<size_t>(batch) * heads);
 
-    etap_mla_host_ctx* ctx = nullptr;
-    int rc = etap_mla_host_ctx_create(static_cast<int>(batch), heads, pages, static_cast<int>(pages), &ctx);
-    if (rc) return rc;
+    // one cached context per host thread and device, rebuilt when the shape changes: a
+    // reference harness calls run_etap once per problem, and per-call cudaMalloc / cudaFree /
+    // stream creation would dominate a decode that takes microseconds
+    thread_local struct CtxCache {
+        etap_mla_host_ctx* ctx = nullptr;
+        int dev = -1, batch = 0, heads = 0;
+        int64_t pages = 0;
+        ~CtxCache() { etap_mla_host_ctx_destroy(ctx); }
+    } cache;
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return host_fail(ETAP_ERR_CUDA, "no CUDA device");
+    int rc = ETAP_OK;
+    if (!cache.ctx || cache.dev != dev || cache.batch != batch || cache.heads != heads || cache.pages != pages) {
+        etap_mla_host_ctx_destroy(cache.ctx);
+        cache.ctx = nullptr;
+        rc = etap_mla_host_ctx_create(static_cast<int>(batch), heads, pages, static_cast<int>(pages), &cache.ctx);
+        if (rc) return rc;
+        cache.dev = dev;
+        cache.batch = static_cast<int>(batch);
+        cache.heads = heads;
+        cache.pages = pages;
+    }
+    etap_mla_host_ctx* ctx = cache.ctx;
+    int full_parts = 0;
+    if (int e = etap_mla_num_sm_parts(dev, &full_parts)) return e;
+    ctx->num_sm_parts = full_parts;
     float* st_dev = nullptr;
     int hg = ETAP_MLA_HEAD_GROUP;
-    if (int e = etap_mla_head_group(heads, &hg)) {
-        etap_mla_host_ctx_destroy(ctx);
-        return e;
-    }
+    if (int e = etap_mla_head_group(heads, &hg)) return e;
     const int groups = heads / hg;
     const size_t st_n = static_cast<size_t>(groups) * batch * pages * 4 * hg;
     if (state) {
         ctx->num_sm_parts = 1;  // one split per sequence: the reference's serial chain of KV blocks
-        if (cudaMalloc(&st_dev, st_n * sizeof(float)) != cudaSuccess) {
-            etap_mla_host_ctx_destroy(ctx);
+        if (cudaMalloc(&st_dev, st_n * sizeof(float)) != cudaSuccess)
             return host_fail(ETAP_ERR_CUDA, "state buffer allocation failed");
-        }
         cudaMemset(st_dev, 0, st_n * sizeof(float));
         etap_mla_debug_state(st_dev, static_cast<int>(pages));
     }
@@ -332,12 +392,18 @@ static int run_etap_f64_impl(const double* q, int64_t n_q, const double* k, int6
                 }
             }
     }
-    etap_mla_host_ctx_destroy(ctx);
+    ctx->num_sm_parts = full_parts;
     if (rc) return rc;
     // the full problem is the last prefix sequence
     const size_t last = static_cast<size_t>(batch - 1) * heads;
     for (int64_t i = 0; i < n_q * d_v; ++i) o[i] = static_cast<double>(of[last * d_v + i]);
     for (int64_t i = 0; i < n_q; ++i) l[i] = static_cast<double>(lf[last + i]);
+    return ETAP_OK;
+}
+
+int etap_mla_debug_bf16_rne(const double* x, int64_t n, uint16_t* out, int reference_form) {
+    if ((!x || !out) && n > 0) return host_fail(ETAP_ERR_SHAPE, "NULL buffer");
+    for (int64_t i = 0; i < n; ++i) out[i] = reference_form ? bf16_bits_rne_slow(x[i]) : bf16_bits_rne(x[i]);
     return ETAP_OK;
 }
 

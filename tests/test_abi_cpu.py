@@ -185,3 +185,34 @@ def test_peer_gather_descriptor_and_validation():
     assert L.etap_mla_decode_peer(*args, C.byref(d), 0, 0, None) == _lib.ETAP_ERR_SHAPE
     assert "epoch" in _lib.last_error()
     assert L.etap_mla_decode_peer(*args, None, 1, 0, None) == _lib.ETAP_ERR_SHAPE
+
+
+def test_bf16_rounding_of_binary64_operands_is_bit_exact():
+    """etap_mla_run_etap_f64 rounds the reference's binary64 AttentionProblem storage to bf16
+    (ties to even, single rounding) with a bit-level fast path; it must equal the frexp /
+    nearbyint reference form on random values, ties, carries into the exponent, the bf16
+    subnormal range, overflow and non-finite values."""
+    rng = np.random.default_rng(7)
+    parts = [
+        rng.standard_normal(200000) * 10.0 ** rng.integers(-45, 40, 200000),
+        rng.standard_normal(20000),
+        # exact ties and near-ties at bf16 resolution: 1 + k/256 (+- 1 ulp of binary64)
+        (1 + np.arange(512) / 256.0) * 2.0 ** rng.integers(-130, 128, 512),
+        np.nextafter(1 + np.arange(512) / 256.0, 2), np.nextafter(1 + np.arange(512) / 256.0, 0),
+        (2 - 2.0 ** -9) * 2.0 ** np.arange(-130, 128),  # rounds up into the next binade
+        np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 3.3895313892515355e38, 3.3961e38, 3.4e38, 1e300,
+                  -1e300, 2.0 ** -126, 2.0 ** -127, 2.0 ** -133, 2.0 ** -134, 1.5 * 2.0 ** -134, 5e-324,
+                  np.nextafter(2.0 ** -126, 0)]),
+    ]
+    x = np.ascontiguousarray(np.concatenate(parts), dtype=np.float64)
+    fast = np.empty(x.size, dtype=np.uint16)
+    ref = np.empty(x.size, dtype=np.uint16)
+    L = _lib.lib()
+    assert L.etap_mla_debug_bf16_rne(x.ctypes.data, x.size, fast.ctypes.data, 0) == 0
+    assert L.etap_mla_debug_bf16_rne(x.ctypes.data, x.size, ref.ctypes.data, 1) == 0
+    bad = np.nonzero(fast != ref)[0]
+    assert bad.size == 0, [(x[i], hex(fast[i]), hex(ref[i])) for i in bad[:5]]
+    # and both agree with torch's own RNE on everything that is not a float32 double-rounding case
+    t = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    same32 = x.astype(np.float32).astype(np.float64) == x
+    assert (fast[same32] == t[same32]).all()
