@@ -547,22 +547,25 @@ def e2e_serving_host(inp, steps: int, dev) -> dict:
 
 
 def cpu_baseline(heads: int, args) -> dict | None:
-    """The reference's CPU path on this box's host cores: one full step (all 16 sequences x 64K
-    rows) of run_etap exact64 after one warm-up step, on the same operands as the GPU arm."""
+    """The reference's CPU path on this box's host cores: full steps (all 16 sequences x 64K
+    rows) of run_etap exact64 after one warm-up step, on the same operands as the GPU arm; the
+    median of 3 steps at 16 heads (one step above: 128 heads take ~4 s per step)."""
     try:
         import oracle
 
         if not oracle.ref_available():
             return None
         threads = cpu_threads()
-        times, gen = reference_full_step(heads, args.cpu_ctx, 1, 1, threads)
+        nsteps = 3 if heads <= 16 else 1
+        times, gen = reference_full_step(heads, args.cpu_ctx, nsteps, 1, threads)
         scale_up = CTX / args.cpu_ctx
-        us = times[0] * 1e6 * scale_up
+        med = sorted(times)[len(times) // 2]
+        us = med * 1e6 * scale_up
         return {"value": us, "unit": "us/step", "cores": threads, "kind": "reference",
                 "sample": (f"reference run_etap exact64 (oracle/_ref, etaplab compiled from source) on {BATCH} "
                            f"sequences x {args.cpu_ctx} rows x {heads} heads, the GPU arm's operands (reference "
                            f"generator, bf16-rounded, V = KV[:, :512]; {gen:.1f} s generation untimed), {threads} "
-                           f"threads, one step after one warm-up step, {times[0]:.2f} s wall"
+                           f"threads, median of {nsteps} step(s) after one warm-up step, {med:.2f} s wall"
                            + (f", scaled x{scale_up:g}" if args.cpu_ctx != CTX else " (full workload, not scaled)"))}
     except Exception as e:  # pragma: no cover
         log(f"[bench] cpu baseline failed: {e}")
