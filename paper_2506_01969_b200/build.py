@@ -24,7 +24,7 @@ MODEL = LIBDIR / "etap_model"
 
 SOURCES = [CSRC / "etap_mla.cu", CSRC / "etap_peer.cu", CSRC / "etap_proj.cu", CSRC / "etap_fp8.cu",
            CSRC / "etap_mla_host.cpp"]
-DEPS = SOURCES + [CSRC / "etap_bench.cpp", CSRC / "sm100_ptx.cuh", CSRC / "etap_mla_kernels.cuh", CSRC / "etap_fp8.cuh", ROOT / "include" / "etap_mla.h"]
+DEPS = SOURCES + [CSRC / "etap_bench.cpp", CSRC / "sm100_ptx.cuh", CSRC / "etap_mla_kernels.cuh", CSRC / "etap_mla_pair.cuh", CSRC / "etap_fp8.cuh", ROOT / "include" / "etap_mla.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -221,7 +221,8 @@ __device__ void schedule_own_range(const DecodeParams& prm, const LineShape& ls,
                                    const int* s_soff, const int* s_len, int* s_sched, int total, int T,
                                    bool publish) {
     const int n = ls.line_n;
-    const int lane = blockIdx.x / ls.p_line, k = blockIdx.x - lane * ls.p_line;
+    const int part = sched_part(prm);
+    const int lane = part / ls.p_line, k = part - lane * ls.p_line;
     auto map = [&](int x, int& vb, int& t) {
         int lo = 0, hi = n - 1;
         while (lo < hi) {
@@ -245,7 +246,7 @@ __device__ void schedule_own_range(const DecodeParams& prm, const LineShape& ls,
     s_sched[6] = min(lane, ls.lanes - 1) * s_soff[n];  // partial-index offset of the lane
     s_sched[7] = 0;
     if (!publish) return;
-    int32_t* g = prm.sched_out + blockIdx.x * SCHED_INTS;
+    int32_t* g = prm.sched_out + sched_part(prm) * SCHED_INTS;
     for (int i = 0; i < SCHED_INTS; ++i) g[i] = s_sched[i];
 }
 
@@ -292,7 +293,8 @@ __device__ void inkernel_schedule_warp(const DecodeParams& prm, const LineShape&
     const int ns_line = __shfl_sync(0xffffffffu, so, 31);
     // this CTA's cost interval [x0, x1) -> (entry, tile) at both ends: the largest live entry
     // whose prefix is <= x (zero-cost entries sharing the prefix resolve to the last one)
-    const int cl = blockIdx.x / ls.p_line, k = blockIdx.x - cl * ls.p_line;
+    const int part = sched_part(prm);
+    const int cl = part / ls.p_line, k = part - cl * ls.p_line;
     const int x0 = k * T, x1 = min(total, (k + 1) * T);
     const int b0 = 31 - __clz(__ballot_sync(0xffffffffu, live && pref <= x0) | 1u);
     const int b1m = 31 - __clz(__ballot_sync(0xffffffffu, live && pref <= x1) | 1u);
@@ -323,16 +325,16 @@ __device__ void inkernel_schedule_warp(const DecodeParams& prm, const LineShape&
     __syncwarp();
     // published for the combine kernel and external readers (not read back by this CTA)
     if (!publish) return;
-    if (lane < SCHED_INTS) prm.sched_out[blockIdx.x * SCHED_INTS + lane] = s_sched[lane];
-    if (blockIdx.x == 0) publish_split_off(prm, ls, s_soff, lane, 32);
+    if (lane < SCHED_INTS) prm.sched_out[sched_part(prm) * SCHED_INTS + lane] = s_sched[lane];
+    if (sched_part(prm) == 0) publish_split_off(prm, ls, s_soff, lane, 32);
 }
 
 // The schedule computed before the grid dependency (DecodeParams::early_meta) is published
 // only after it: the previous step's combine may still read split_off until then.
 __device__ __forceinline__ void publish_schedule(const DecodeParams& prm, const LineShape& ls, const int* s_soff,
                                                  const int* s_sched, int tid, int nthreads) {
-    if (tid < SCHED_INTS) prm.sched_out[blockIdx.x * SCHED_INTS + tid] = s_sched[tid];
-    if (blockIdx.x == 0) publish_split_off(prm, ls, s_soff, tid, nthreads);
+    if (tid < SCHED_INTS) prm.sched_out[sched_part(prm) * SCHED_INTS + tid] = s_sched[tid];
+    if (sched_part(prm) == 0) publish_split_off(prm, ls, s_soff, tid, nthreads);
 }
 
 __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, int* s_pref, int* s_soff,
@@ -364,7 +366,7 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
     if (tid == 0) s_soff[n] = nsplits;
     __syncthreads();
     if (tid == 0) schedule_own_range(prm, ls, s_pref, s_soff, s_len, s_sched, total, T, publish);
-    if (publish && blockIdx.x == 0) publish_split_off(prm, ls, s_soff, tid, blockDim.x);
+    if (publish && sched_part(prm) == 0) publish_split_off(prm, ls, s_soff, tid, blockDim.x);
     __syncthreads();
 }
 
@@ -386,7 +388,7 @@ __device__ __forceinline__ void prev_range_hint(const DecodeParams& prm, int hg,
 #ifndef ETAP_NO_PREFETCH_HINT
     if (!prm.inkernel_sched) return;
     if (lane == 0) {
-        const int32_t* prev = prm.sched_out + blockIdx.x * SCHED_INTS;
+        const int32_t* prev = prm.sched_out + sched_part(prm) * SCHED_INTS;
         const int p0 = prev[0], tb = prev[1], p1 = prev[2], off = prev[5];
         const int vb = off + p0, nvb = prm.batch * prm.groups;
         if (p1 >= p0 && p0 >= 0 && vb >= 0 && vb < nvb && tb >= 0 && tb < prm.max_pages) {
@@ -472,7 +474,7 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
     r.s_len = s_len;
     r.hint_b = -1;
     LineShape ls{};
-    if (fused) ls = line_shape(prm.batch, prm.groups, gridDim.x, prm.lanes_on != 0);
+    if (fused) ls = line_shape(prm.batch, prm.groups, sched_parts(prm), prm.lanes_on != 0);
     auto schedule = [&](bool publish) {
         if (ls.line_n <= 32) {
             if (warp == 0) inkernel_schedule_warp(prm, ls, s_soff, s_len, s_sched, publish);
@@ -532,15 +534,15 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
     if (threadIdx.x == 0 && !early) { span_stamp(prm, 0); ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
     if (fused) {
         if (early) {
-            if (warp == 3) publish_schedule(prm, ls, s_soff, s_sched, lane, 32);
+            if (warp == 3 && sched_publisher(prm)) publish_schedule(prm, ls, s_soff, s_sched, lane, 32);
         } else {
-            schedule(true);
+            schedule(sched_publisher(prm));
         }
         r.sch = s_sched;
         r.soff = s_soff;  // line-local split offsets
         r.idx_off = s_sched[6];
     } else {
-        r.sch = prm.sched + blockIdx.x * SCHED_INTS;
+        r.sch = prm.sched + sched_part(prm) * SCHED_INTS;
         r.soff = prm.split_off + r.sch[5];  // indexed by line position like the fused copy
         r.idx_off = 0;
     }
@@ -1206,6 +1208,8 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
         ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
     }
 }
+
+#include "etap_mla_pair.cuh"
 
 // =============================================================================================
 // K2-FP8: the transposed pipeline on an FP8 (e4m3) latent cache (etap_fp8.cuh for the operand
@@ -2171,6 +2175,19 @@ int head_group_of(int heads) {
 
 bool heads_ok(int heads) { return heads >= 16 && heads % 16 == 0; }
 
+// The CTA-pair kernel (etap_mla_pair.cuh) takes 128-head work units when the head count allows
+// it. ETAP_PAIR=0 or a forced ETAP_HEAD_GROUP in the environment keeps the single-CTA kernels
+// (A/B runs); the debug instantiations (trace / BlockHook state dump) are single-CTA only, and so
+// are external schedules and separate combines (their layouts follow etap_mla_head_group).
+bool pair_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("ETAP_PAIR");
+        const char* f = std::getenv("ETAP_HEAD_GROUP");
+        return !(e && e[0] == '0') && !(f && f[0] != '\0');
+    }();
+    return on;
+}
+
 // Head-group lanes of the split schedule (line_shape); ETAP_GROUP_LANES=0 disables them (A/B).
 bool lanes_enabled() {
     static const bool on = [] {
@@ -2437,9 +2454,11 @@ OutMap local_outmap(int heads, float* out, float* lse) {
 // hg_unit: heads per work unit of the decode that wrote the partials (the FP8 kernel uses 16
 // whatever the head count); the partial / LSE areas keep the allocation layout of
 // etap_mla_workspace_bytes either way
+// sched_parts: parts of the decode's split schedule when they differ from the allocation's
+// num_sm_parts (the CTA-pair kernel schedules pairs)
 int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_parts, void* workspace,
                  const OutMap& om, void* stream, const int32_t* seqlens = nullptr, int hg_unit = 0,
-                 int fixed_cost = META_FIXED_COST) {
+                 int fixed_cost = META_FIXED_COST, int sched_parts = 0) {
     const int hg_alloc = head_group_of(heads);
     const int hg = hg_unit > 0 ? hg_unit : hg_alloc;
     const int groups = heads / hg;
@@ -2458,8 +2477,99 @@ int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_part
     cfg2.numAttrs = pdl_attrs();
     ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, static_cast<const float*>(ws_o),
                                  static_cast<const float*>(ws_lse), split_off, hg, batch, om,
-                                 static_cast<unsigned long long*>(g_combine_trace_buf), seqlens, num_sm_parts,
-                                 lanes_enabled() ? 1 : 0, fixed_cost));
+                                 static_cast<unsigned long long*>(g_combine_trace_buf), seqlens,
+                                 sched_parts > 0 ? sched_parts : num_sm_parts, lanes_enabled() ? 1 : 0, fixed_cost));
+    return ETAP_OK;
+}
+
+// CTA pairs co-resident at once for the pair kernel (clusters of two must share a TPC; with
+// 1 CTA per SM at most num_sms / 2), cached per device.
+int pair_capacity(int* pairs) {
+    int dev = 0;
+    ETAP_CUDA(cudaGetDevice(&dev));
+    static int cached[64] = {0};
+    if (dev < 0 || dev >= 64) return fail(ETAP_ERR_CUDA, "device index out of range");
+    if (cached[dev] == 0) {
+        auto kern = etap_mla_decode_pair_kernel<false>;
+        if (int rc = ensure_smem_attr(kern, pairk::SMEM)) return rc;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2);
+        cfg.blockDim = dim3(pairk::THREADS);
+        cfg.dynamicSmemBytes = pairk::SMEM;
+        int n = 0;
+        ETAP_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+        cached[dev] = n > 0 ? n : -1;
+    }
+    *pairs = cached[dev];
+    return ETAP_OK;
+}
+
+// K2-pair (+ K3): 128-head work units on CTA pairs. Same contract as decode_impl; the split
+// schedule is over pairs (num_sm_parts / 2, capped by the pairs that fit at once), partials are
+// 128 heads wide inside the allocation layout of etap_mla_workspace_bytes.
+int decode_pair(const void* q, const void* kv_pool, int64_t num_pages, const int32_t* block_table,
+                int max_pages_per_seq, const int32_t* seqlens, int batch, int q_tokens, int heads_per_token,
+                float scale, int causal, int32_t* sched, int32_t* split_off, int pairs, void* workspace,
+                size_t ws_lse_off, const OutMap& om, unsigned flags, void* stream) {
+    const int heads = q_tokens * heads_per_token;
+    CUtensorMap tm_kv, tm_kv32, tm_q;
+    if (int rc = cached_map(&tm_kv, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, PAGE)) return rc;
+    if (int rc = cached_map(&tm_kv32, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, 32)) return rc;
+    if (int rc = cached_map(&tm_q, q, static_cast<uint64_t>(batch) * heads, pairk::HPC)) return rc;
+    const int groups = heads / pairk::UNIT;
+    DecodeParams prm;
+    prm.block_table = block_table;
+    prm.seqlens = seqlens;
+    prm.sched = sched;
+    prm.split_off = split_off;
+    prm.om = om;
+    prm.ws_o = static_cast<float*>(workspace);
+    prm.ws_lse = prm.ws_o + ws_lse_off;
+    prm.kv_pool = kv_pool;
+    prm.q = q;
+    prm.num_pages = num_pages;
+    prm.max_pages = max_pages_per_seq;
+    prm.batch = batch;
+    prm.heads = heads;
+    prm.groups = groups;
+    prm.q_tokens = q_tokens;
+    prm.heads_per_token = heads_per_token;
+    prm.causal = causal ? 1 : 0;
+    prm.sched_out = sched;
+    prm.split_off_out = split_off;
+    prm.lanes_on = lanes_enabled() ? 1 : 0;
+    prm.pair = 1;
+    const LineShape ls = line_shape(batch, groups, pairs, prm.lanes_on != 0);
+    prm.inkernel_sched = ls.line_n <= pairk::MAX_VB ? 1 : 0;
+    prm.early_meta = (early_meta_enabled() && (flags & ETAP_FLAG_EARLY_METADATA)) ? 1 : 0;
+    prm.fixed_cost = META_FIXED_COST;
+    if (!prm.inkernel_sched) {
+        if (int rc = metadata_launch(seqlens, batch, groups, pairs, sched, split_off, stream)) return rc;
+    }
+    prm.scale_log2 = scale * 1.4426950408889634f;
+    prm.flags = flags;
+    prm.trace = static_cast<unsigned long long*>(g_trace_buf);
+    prm.span = static_cast<unsigned long long*>(g_span_buf);
+    prm.state = nullptr;
+    prm.state_tiles = 0;
+
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(pairk::THREADS);
+    cfg.dynamicSmemBytes = pairk::SMEM;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_attrs();
+    if (prm.trace != nullptr) {
+        static int attr_rc = ensure_smem_attr(etap_mla_decode_pair_kernel<true>, pairk::SMEM);
+        if (attr_rc) return attr_rc;
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_pair_kernel<true>, tm_kv, tm_kv32, tm_q, prm));
+    } else {
+        ETAP_CUDA(cudaLaunchKernelEx(&cfg, etap_mla_decode_pair_kernel<false>, tm_kv, tm_kv32, tm_q, prm));
+    }
     return ETAP_OK;
 }
 
@@ -2487,6 +2597,25 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
         return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
     if (int rc = check_device()) return rc;
+
+    if (heads % pairk::UNIT == 0 && pair_enabled() && g_state_buf == nullptr &&
+        !(flags & (ETAP_FLAG_EXTERNAL_SCHEDULE | ETAP_FLAG_SKIP_COMBINE)) && num_sm_parts >= 2) {
+        int cap = 0;
+        if (int rc = pair_capacity(&cap)) return rc;
+        const int pairs = std::min(num_sm_parts / 2, cap);
+        if (pairs >= 1) {
+            // partial LSEs sit where the allocation layout (head_group_of units) puts them
+            const size_t ws_lse_off = max_partials(batch, heads, num_sm_parts) * head_group_of(heads) * D_V;
+            if (int rc = decode_pair(q, kv_pool, num_pages, block_table, max_pages_per_seq, seqlens, batch, q_tokens,
+                                     heads_per_token, scale, causal, const_cast<int32_t*>(sched),
+                                     const_cast<int32_t*>(split_off), pairs, workspace, ws_lse_off, om, flags, stream))
+                return rc;
+            const bool closed_form = batch * (heads / pairk::UNIT) <= 32 &&
+                                     line_shape(batch, heads / pairk::UNIT, pairs, lanes_enabled()).line_n <= 32;
+            return combine_impl(split_off, batch, heads, num_sm_parts, workspace, om, stream,
+                                closed_form ? seqlens : nullptr, pairk::UNIT, META_FIXED_COST, pairs);
+        }
+    }
 
     CUtensorMap tm_kv, tm_q;
     if (int rc = cached_map(&tm_kv, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, PAGE)) return rc;
@@ -2516,6 +2645,7 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     prm.sched_out = const_cast<int32_t*>(sched);
     prm.split_off_out = const_cast<int32_t*>(split_off);
     prm.lanes_on = lanes_enabled() ? 1 : 0;
+    prm.pair = 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
     const int max_vb = hg == 64 ? Cfg<64>::MAX_VB : (hg == 32 ? Cfg<32>::MAX_VB : Cfg<16>::MAX_VB);
     prm.inkernel_sched = (ls.line_n <= max_vb && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
@@ -2648,6 +2778,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     prm.sched_out = const_cast<int32_t*>(sched);
     prm.split_off_out = const_cast<int32_t*>(split_off);
     prm.lanes_on = lanes_enabled() ? 1 : 0;
+    prm.pair = 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
     prm.inkernel_sched = ls.line_n <= MAX_FUSED_VB ? 1 : 0;
     prm.early_meta = (early_meta_enabled() && (flags & ETAP_FLAG_EARLY_METADATA)) ? 1 : 0;

@@ -400,6 +400,7 @@ struct DecodeParams {
     int early_meta;      // 1: read seqlens / block_table before the grid dependency (decode_prologue)
     int fixed_cost;      // per-split overhead in tile units of the split schedule
     int lanes_on;        // head-group lanes enabled (line_shape)
+    int pair;            // 1: CTA-pair kernel, a schedule part is a pair of CTAs (part = blockIdx.x >> 1)
     float scale_log2;
     unsigned flags;
     unsigned long long* trace;  // debug: [cta][TRACE_TILES][TRACE_SLOTS] stamps (ETAP_TRACE), or null
@@ -407,6 +408,12 @@ struct DecodeParams {
     float* state;               // debug: per-tile softmax state [vb][state_tiles][4][16], or null
     int state_tiles;
 };
+
+// Split-schedule part of this CTA, number of parts, and whether this CTA publishes the part's
+// schedule row (the CTA-pair kernel schedules pairs: both CTAs compute the same range).
+__device__ __forceinline__ int sched_part(const DecodeParams& prm) { return static_cast<int>(blockIdx.x) >> prm.pair; }
+__device__ __forceinline__ int sched_parts(const DecodeParams& prm) { return static_cast<int>(gridDim.x) >> prm.pair; }
+__device__ __forceinline__ bool sched_publisher(const DecodeParams& prm) { return (blockIdx.x & prm.pair) == 0; }
 
 // Debug stamps and the softmax-state dump are compiled into the DBG instantiations of the
 // decode kernels only (selected at launch when a debug buffer is registered): in the product
