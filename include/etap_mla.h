@@ -101,6 +101,15 @@ const char* etap_mla_version(void);
  * 16). Sizes below, the split_off layout and the debug state dump follow it. */
 int etap_mla_head_group(int heads, int* head_group);
 
+/* Work unit of the split schedule for `heads` query rows and num_sm_parts: what the entries of
+ * sched / split_off refer to. 128 heads per unit over num_sm_parts / 2 CTA pairs when the
+ * CTA-pair kernel runs the head count (heads a multiple of 128, num_sm_parts >= 2; ETAP_PAIR=0 or
+ * a forced ETAP_HEAD_GROUP in the environment turns it off), else etap_mla_head_group units over
+ * num_sm_parts CTAs. K1, etap_mla_metadata_host, the decode and etap_mla_combine follow it; the
+ * buffer sizes below (head_group units) bound either layout.
+ * Replaces nothing in the reference: its run_etap is one serial loop (etap.cpp:122-129). */
+int etap_mla_schedule_unit(int heads, int num_sm_parts, int* unit_heads, int* parts);
+
 /* Number of persistent CTAs the decode kernel uses on `device` (= its SM count). */
 int etap_mla_num_sm_parts(int device, int* num_sm_parts);
 

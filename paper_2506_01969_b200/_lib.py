@@ -45,6 +45,7 @@ def _declare(lib: C.CDLL, variant: bool = False) -> None:
         "etap_mla_version": (C.c_char_p, []),
         "etap_mla_num_sm_parts": (i32, [i32, P(i32)]),
         "etap_mla_head_group": (i32, [i32, P(i32)]),
+        "etap_mla_schedule_unit": (i32, [i32, i32, P(i32), P(i32)]),
         "etap_mla_sched_ints": (i32, [i32, i32, i32, P(sz), P(sz)]),
         "etap_mla_workspace_bytes": (i32, [i32, i32, i32, P(sz)]),
         "etap_mla_metadata": (i32, [vp, i32, i32, i32, vp, vp, vp]),

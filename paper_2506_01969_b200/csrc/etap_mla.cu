@@ -2188,6 +2188,18 @@ bool pair_enabled() {
     return on;
 }
 
+// Work-unit layout of the split schedule, i.e. what sched / split_off entries mean: 128-head units
+// over num_sm_parts / 2 CTA pairs when the pair kernel runs the head count, else head_group_of
+// units over num_sm_parts CTAs. K1, the host restatement, the decode and the combine agree on it.
+bool pair_used(int heads, int num_sm_parts) {
+    return heads % pairk::UNIT == 0 && pair_enabled() && num_sm_parts >= 2;
+}
+void sched_layout(int heads, int num_sm_parts, int* unit, int* parts) {
+    const bool p = pair_used(heads, num_sm_parts);
+    *unit = p ? pairk::UNIT : head_group_of(heads);
+    *parts = p ? num_sm_parts / 2 : num_sm_parts;
+}
+
 // Head-group lanes of the split schedule (line_shape); ETAP_GROUP_LANES=0 disables them (A/B).
 bool lanes_enabled() {
     static const bool on = [] {
@@ -2306,6 +2318,15 @@ int etap_mla_head_group(int heads, int* head_group) {
     return ETAP_OK;
 }
 
+int etap_mla_schedule_unit(int heads, int num_sm_parts, int* unit_heads, int* parts) {
+    if (!unit_heads || !parts) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
+    if (!heads_ok(heads)) return fail(ETAP_ERR_SHAPE, "heads must be a positive multiple of 16");
+    if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
+        return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
+    sched_layout(heads, num_sm_parts, unit_heads, parts);
+    return ETAP_OK;
+}
+
 int etap_mla_num_sm_parts(int device, int* num_sm_parts) {
     if (!num_sm_parts) return fail(ETAP_ERR_SHAPE, "num_sm_parts is NULL");
     int n = 0;
@@ -2338,12 +2359,14 @@ int etap_mla_metadata_host(const int32_t* seqlens, int batch, int heads, int num
     if (!seqlens || !sched || !split_off) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
     if (batch < 1 || !heads_ok(heads))
         return fail(ETAP_ERR_SHAPE, "batch >= 1 and heads a multiple of 16 required");
-    const int groups = heads / head_group_of(heads);
-    const int nvb = batch * groups;
-    if (nvb > META_MAX_VB) return fail(ETAP_ERR_SHAPE, "batch * head groups too large");
     if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
         return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
-    const LineShape ls = line_shape(batch, groups, num_sm_parts, lanes_enabled());
+    int unit = 0, parts = 0;
+    sched_layout(heads, num_sm_parts, &unit, &parts);
+    const int groups = heads / unit;
+    const int nvb = batch * groups;
+    if (nvb > META_MAX_VB) return fail(ETAP_ERR_SHAPE, "batch * head groups too large");
+    const LineShape ls = line_shape(batch, groups, parts, lanes_enabled());
     const int n = ls.line_n;
     std::vector<int> tiles(n), pref(n + 1, 0), ns(n, 0), first(n, 0x7fffffff), soff(n + 1, 0);
     for (int i = 0; i < n; ++i) {
@@ -2382,7 +2405,7 @@ int etap_mla_metadata_host(const int32_t* seqlens, int batch, int heads, int num
     for (int i = 0; i < n; ++i) soff[i + 1] = soff[i] + ns[i];
     const int ns_line = soff[n];
     for (int v = 0; v <= nvb; ++v) split_off[v] = (v / n) * ns_line + soff[v % n];
-    for (int kk = 0; kk < num_sm_parts; ++kk) {
+    for (int kk = 0; kk < parts; ++kk) {
         const int lane = kk / ls.p_line, k = kk - lane * ls.p_line;
         int32_t* s = sched + kk * SCHED_INTS;
         const int lo = std::min(lane, ls.lanes - 1);
@@ -2406,7 +2429,11 @@ int etap_mla_metadata(const int32_t* seqlens, int batch, int heads, int num_sm_p
     if (!seqlens || !sched || !split_off) return fail(ETAP_ERR_SHAPE, "NULL pointer argument");
     if (batch < 1 || !heads_ok(heads))
         return fail(ETAP_ERR_SHAPE, "batch >= 1 and heads a multiple of 16 required");
-    return metadata_launch(seqlens, batch, heads / head_group_of(heads), num_sm_parts, sched, split_off, stream);
+    if (num_sm_parts < 1 || num_sm_parts > META_THREADS)
+        return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
+    int unit = 0, parts = 0;
+    sched_layout(heads, num_sm_parts, &unit, &parts);
+    return metadata_launch(seqlens, batch, heads / unit, parts, sched, split_off, stream);
 }
 
 int metadata_launch(const int32_t* seqlens, int batch, int groups, int num_sm_parts, int32_t* sched,
@@ -2540,10 +2567,11 @@ int decode_pair(const void* q, const void* kv_pool, int64_t num_pages, const int
     prm.lanes_on = lanes_enabled() ? 1 : 0;
     prm.pair = 1;
     const LineShape ls = line_shape(batch, groups, pairs, prm.lanes_on != 0);
-    prm.inkernel_sched = ls.line_n <= pairk::MAX_VB ? 1 : 0;
+    const bool external = flags & ETAP_FLAG_EXTERNAL_SCHEDULE;
+    prm.inkernel_sched = (ls.line_n <= pairk::MAX_VB && !external) ? 1 : 0;
     prm.early_meta = (early_meta_enabled() && (flags & ETAP_FLAG_EARLY_METADATA)) ? 1 : 0;
     prm.fixed_cost = META_FIXED_COST;
-    if (!prm.inkernel_sched) {
+    if (!prm.inkernel_sched && !external) {
         if (int rc = metadata_launch(seqlens, batch, groups, pairs, sched, split_off, stream)) return rc;
     }
     prm.scale_log2 = scale * 1.4426950408889634f;
@@ -2598,19 +2626,22 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
         return fail(ETAP_ERR_SHAPE, "num_sm_parts must be in [1, 1024]");
     if (int rc = check_device()) return rc;
 
-    if (heads % pairk::UNIT == 0 && pair_enabled() && g_state_buf == nullptr &&
-        !(flags & (ETAP_FLAG_EXTERNAL_SCHEDULE | ETAP_FLAG_SKIP_COMBINE)) && num_sm_parts >= 2) {
+    if (pair_used(heads, num_sm_parts) && g_state_buf == nullptr) {
         int cap = 0;
         if (int rc = pair_capacity(&cap)) return rc;
-        const int pairs = std::min(num_sm_parts / 2, cap);
-        if (pairs >= 1) {
+        const int pairs = num_sm_parts / 2;
+        if (cap < pairs && (flags & ETAP_FLAG_EXTERNAL_SCHEDULE))
+            return fail(ETAP_ERR_SHAPE, "external schedule for " + std::to_string(pairs) + " CTA pairs, but only " +
+                                            std::to_string(cap) + " fit on the device at once");
+        if (cap >= pairs) {  // (else: the single-CTA kernels with their own schedule)
             // partial LSEs sit where the allocation layout (head_group_of units) puts them
             const size_t ws_lse_off = max_partials(batch, heads, num_sm_parts) * head_group_of(heads) * D_V;
             if (int rc = decode_pair(q, kv_pool, num_pages, block_table, max_pages_per_seq, seqlens, batch, q_tokens,
                                      heads_per_token, scale, causal, const_cast<int32_t*>(sched),
                                      const_cast<int32_t*>(split_off), pairs, workspace, ws_lse_off, om, flags, stream))
                 return rc;
-            const bool closed_form = batch * (heads / pairk::UNIT) <= 32 &&
+            if (flags & ETAP_FLAG_SKIP_COMBINE) return ETAP_OK;
+            const bool closed_form = !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE) &&
                                      line_shape(batch, heads / pairk::UNIT, pairs, lanes_enabled()).line_n <= 32;
             return combine_impl(split_off, batch, heads, num_sm_parts, workspace, om, stream,
                                 closed_form ? seqlens : nullptr, pairk::UNIT, META_FIXED_COST, pairs);
@@ -2653,8 +2684,8 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     prm.fixed_cost = META_FIXED_COST;
     if (!prm.inkernel_sched && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) {
         // too many virtual sequences for the fused prologue: run K1 first on the same stream
-        if (int rc = etap_mla_metadata(seqlens, batch, heads, num_sm_parts, const_cast<int32_t*>(sched),
-                                       const_cast<int32_t*>(split_off), stream))
+        if (int rc = metadata_launch(seqlens, batch, groups, num_sm_parts, const_cast<int32_t*>(sched),
+                                     const_cast<int32_t*>(split_off), stream))
             return rc;
     }
     prm.scale_log2 = scale * 1.4426950408889634f;
@@ -2909,7 +2940,10 @@ int etap_mla_combine(const int32_t* split_off, int batch, int heads, int num_sm_
     if (!aligned16(out) || !aligned16(workspace)) return fail(ETAP_ERR_SHAPE, "out / workspace must be 16-byte aligned");
     if (batch < 1 || !heads_ok(heads) || num_sm_parts < 1)
         return fail(ETAP_ERR_SHAPE, "batch >= 1, heads a multiple of 16, num_sm_parts >= 1 required");
-    return combine_impl(split_off, batch, heads, num_sm_parts, workspace, local_outmap(heads, out, lse), stream);
+    int unit = 0, parts = 0;
+    sched_layout(heads, num_sm_parts, &unit, &parts);
+    return combine_impl(split_off, batch, heads, num_sm_parts, workspace, local_outmap(heads, out, lse), stream,
+                        nullptr, unit, META_FIXED_COST, parts);
 }
 
 int etap_mla_debug_state(void* device_buf, int max_tiles) {

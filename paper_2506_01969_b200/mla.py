@@ -24,10 +24,20 @@ SCHED_INTS = 8
 
 
 def head_group(heads: int) -> int:
-    """Heads per CTA work unit the library uses (32 when heads % 32 == 0, else 16)."""
+    """Heads per CTA work unit of the single-CTA kernels (64 / 32 / 16 as the head count allows),
+    the unit the buffer sizes follow; see schedule_unit() for the CTA-pair kernel's 128."""
     out = C.c_int(0)
     check(_lib.lib().etap_mla_head_group(heads, C.byref(out)), "etap_mla_head_group")
     return out.value
+
+
+def schedule_unit(heads: int, num_parts: int) -> tuple[int, int]:
+    """(heads per schedule unit, schedule parts): 128-head units over num_parts / 2 CTA pairs when
+    the pair kernel runs the head count, else (head_group(heads), num_parts)."""
+    unit, parts = C.c_int(0), C.c_int(0)
+    check(_lib.lib().etap_mla_schedule_unit(heads, num_parts, C.byref(unit), C.byref(parts)),
+          "etap_mla_schedule_unit")
+    return unit.value, parts.value
 
 
 def _dev_index(device: torch.device | str | int | None) -> int:

@@ -70,6 +70,9 @@ def test_sizes_and_shape_validation():
     assert ws.value == al((148 + 16) * 16 * (512 + 1) * 4) + 148 * 3 * 48 * 576
     # head groups: 32 heads per work unit when heads % 32 == 0, else 16
     assert [mla.head_group(h) for h in (16, 32, 48, 64, 96, 128)] == [16, 32, 16, 64, 32, 64]
+    # the schedule unit: 128-head units over CTA pairs for multiples of 128 (num_sm_parts >= 2)
+    assert [mla.schedule_unit(h, 148) for h in (16, 64, 128, 256)] == [(16, 148), (64, 148), (128, 74), (128, 74)]
+    assert mla.schedule_unit(128, 1) == (64, 1) and mla.schedule_unit(128, 7) == (128, 3)
     assert L.etap_mla_sched_ints(4, 128, 148, C.byref(a), C.byref(b)) == _lib.ETAP_OK and b.value == 4 * 8 + 1
     assert L.etap_mla_workspace_bytes(4, 128, 148, C.byref(ws)) == _lib.ETAP_OK
     assert ws.value == al((148 + 4 * 2) * 64 * (512 + 1) * 4) + 148 * 3 * 48 * 576
@@ -124,12 +127,13 @@ def test_host_metadata_partition_invariants():
              ([100], 16, 3), ([1024], 16, 148), ([10**6], 128, 148), ([7] * 300, 16, 148),
              ([65536] * 16, 128, 148), ([4096] * 64, 128, 148), ([100, 3000], 64, 3), ([5000], 128, 2),
              ([0, 0, 900], 96, 148)]
-    for seqlens, heads, parts in cases:
-        B, G = len(seqlens), heads // mla.head_group(heads)
-        sched = np.zeros(parts * 8, np.int32)
+    for seqlens, heads, nparts in cases:
+        unit, parts = mla.schedule_unit(heads, nparts)  # 128-head units over CTA pairs when they run it
+        B, G = len(seqlens), heads // unit
+        sched = np.zeros(nparts * 8, np.int32)
         so = np.zeros(B * G + 1, np.int32)
         sl = np.array(seqlens, np.int32)
-        assert L.etap_mla_metadata_host(sl.ctypes.data_as(C.c_void_p), B, heads, parts,
+        assert L.etap_mla_metadata_host(sl.ctypes.data_as(C.c_void_p), B, heads, nparts,
                                         sched.ctypes.data_as(C.c_void_p), so.ctypes.data_as(C.c_void_p)) == 0
         lanes = G if (G > 1 and parts >= G) else 1
         p_line = parts // lanes
