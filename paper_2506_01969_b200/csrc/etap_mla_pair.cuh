@@ -43,7 +43,7 @@ constexpr int OFF_X = OFF_Q + Q_BYTES;         // P exchange [2 wg][128 lanes][1
 constexpr int X_BYTES = 2 * 128 * 64;
 constexpr int OFF_RED = OFF_X + X_BYTES;       // [4][64] floats: per-(row quarter) head max / sum
 constexpr int OFF_BAR = OFF_RED + 4 * HPC * 4;
-constexpr int NB = 18;
+constexpr int NB = 20;
 constexpr int OFF_TMEM = OFF_BAR + NB * 8;
 constexpr int OFF_SCHED = OFF_TMEM + 16;
 constexpr int MAX_VB = 64;                     // fused-schedule line limit (longer lines: K1)
@@ -51,9 +51,15 @@ constexpr int SMEM = OFF_SCHED + sched_smem_ints(MAX_VB) * 4;
 constexpr int THREADS = 384;                   // warps 0-3 roles, 4-11 two softmax warpgroups
 constexpr int SM_WARP0 = 4;
 // TMEM columns (512 allocated per CTA): O [0, 256): N block n at 128n (lane h: head h, d 256n +
-// c; lane 64+h: head h, d 256n + 128 + c); S [256, 320) two pages; P [320, 448) two pages of
-// (32 hi | 32 lo) columns, k-step j of a page at column 8j (bf16 pairs along the rows).
+// c; lane 64+h: head h, d 256n + 128 + c); S [256, 320) two pages; P [320, 512) three pages of
+// 64 columns, k-step j of a page at [16j, 16j + 8) (hi) and [16j + 8, 16j + 16) (lo), bf16 pairs
+// along the KV rows. Three P buffers: the softmax writes P of page gp while GEMM2 of gp-1 and
+// gp-2 may still be queued on the tensor pipe.
 constexpr uint32_t TC_O = 0, TC_S = 256, TC_P = 320, TMEM_COLS = 512;
+constexpr int NPB = 3;   // P buffers (tensor memory)
+constexpr int P_TILE = HPC * 128;  // P in shared memory: one [64 heads][64 rows] bf16 tile (hi, then lo)
+constexpr int NG2 = 4;   // GEMM2-done barriers (waits reach back three pages: a ring of four keeps
+                         // every waited phase the newest or the one before on its barrier)
 // barriers (same offsets in both CTAs); "L" = only the leader's copy is used
 enum : int {
     B_FULL_G1 = 0,   // [2] L: both CTAs' GEMM1 halves of the page landed (tx from both)
@@ -62,9 +68,9 @@ enum : int {
     B_V_READY = 5,   // [2] L: both CTAs' V chunks landed and tail rows zeroed (2 arrivals)
     B_S_FULL = 7,    // [2] both: GEMM1 of the page complete (S ready, GEMM1 halves free)
     B_Q_EMPTY = 9,   // both: GEMM1 of the split's last page complete (Q buffer free)
-    B_G2_DONE = 10,  // [2] both: GEMM2 of the page complete (V chunks, P columns free; O final)
-    B_S_FREE = 12,   // [2] L: both CTAs' softmax read S of the page (16 warp arrivals)
-    B_P_FULL = 14,   // [2] L: both CTAs' P of the page in TMEM, O rescaled (16 warp arrivals)
+    B_G2_DONE = 10,  // [NG2] both: GEMM2 of the page complete (V chunks, P columns free; O final)
+    B_S_FREE = 14,   // [2] L: both CTAs' softmax read S of the page (16 warp arrivals)
+    B_P_FULL = 16,   // [2] L: both CTAs' P of the page in TMEM, O rescaled (16 warp arrivals)
 };
 static_assert(SMEM <= 232448, "shared memory budget");
 // timing experiments only (wrong results): fewer GEMM1 chunks / GEMM2 MMAs, no P stores
@@ -77,6 +83,12 @@ static_assert(SMEM <= 232448, "shared memory budget");
 #ifndef ETAP_PAIR_P_STORE
 #define ETAP_PAIR_P_STORE 1
 #endif
+// GEMM2's A operand: 0 = P in tensor memory (TS UMMA, duplicated lanes: an exchange between the
+// two row halves of each head through shared memory), 1 = P in shared memory (SS UMMA, K-major
+// SW128 [64 heads][64 rows] hi and lo tiles in the exchange buffer's 16 KB, single-buffered)
+#ifndef ETAP_PAIR_P_SMEM
+#define ETAP_PAIR_P_SMEM 1
+#endif
 // Arrivals on the leader's barriers: 0 = every CTA arrives through the cluster window with
 // release.cluster, 1 = the leader's own warps arrive locally (release.cta), 2 = as 1 and the
 // partner arrives relaxed.cluster. A cluster-scope release costs ~1k cycles per arrival on B200
@@ -88,7 +100,8 @@ static_assert(SMEM <= 232448, "shared memory budget");
 #define ETAP_PAIR_ARRIVE 2
 #endif
 static_assert(OFF_Q % 1024 == 0 && STAGE % 1024 == 0 && STAGE_G1 % 1024 == 0, "SW128 alignment");
-static_assert(B_P_FULL + 2 <= NB, "barrier count");
+static_assert(B_P_FULL + 2 <= NB && B_G2_DONE + NG2 <= B_S_FREE, "barrier count");
+static_assert(TC_P + NPB * 64 <= TMEM_COLS, "TMEM budget");
 // V chunk i (0..3) of CTA r: N block i/2, 64-column atom i%2
 __host__ __device__ constexpr int v_chunk(int r, int i) { return 2 * r + (i & 1) + 4 * (i >> 1); }
 }  // namespace pairk
@@ -135,10 +148,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
             ptx::mbar_init(&bars[B_V_LAND + i], 1);
             ptx::mbar_init(&bars[B_V_READY + i], 2);
             ptx::mbar_init(&bars[B_S_FULL + i], 1);
-            ptx::mbar_init(&bars[B_G2_DONE + i], 1);
             ptx::mbar_init(&bars[B_S_FREE + i], 16);
             ptx::mbar_init(&bars[B_P_FULL + i], 16);
         }
+        for (int i = 0; i < NG2; ++i) ptx::mbar_init(&bars[B_G2_DONE + i], 1);
         ptx::mbar_init(&bars[B_FULL_Q], 1);
         ptx::mbar_init(&bars[B_Q_EMPTY], 1);
         ptx::fence_mbar_init();
@@ -277,7 +290,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
                     ptx::tc_fence_after();
                     if (lane == 0) ETAP_TRACE(prm, gp, 10);
                     const uint32_t v0 = stage_addr + buf * STAGE + STAGE_G1;
-                    const uint32_t p0 = tmem_base + TC_P + 64 * buf;
+                    const uint32_t p0 = tmem_base + TC_P + 64 * (gp % NPB);
+                    const uint64_t p_desc = ptx::smem_desc(ptx::smem_u32(smem + OFF_X), 16, 1024, ptx::LAYOUT_SW128);
 #pragma unroll
                     for (int n = 0; n < 2; ++n) {
                         // MN-major SW128 B: LBO = the next 64-column atom (chunk), SBO = 8-row group
@@ -285,12 +299,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
 #pragma unroll
                         for (int j = 0; j < ETAP_PAIR_G2_KSTEPS; ++j)
 #pragma unroll
-                            for (int part = 0; part < 2; ++part)
-                                ptx::umma_pair_ts(tmem_base + TC_O + 128 * n, p0 + 32 * part + 8 * j,
-                                                  v_desc + j * (2048 >> 4), idesc,
-                                                  (t == sd.t0 && j == 0 && part == 0) ? 0u : 1u);
+                            for (int part = 0; part < 2; ++part) {
+                                const uint32_t acc = (t == sd.t0 && j == 0 && part == 0) ? 0u : 1u;
+                                if (ETAP_PAIR_P_SMEM)  // K-major SW128 A: +32 B per 16 rows of K
+                                    ptx::umma_pair_ss(tmem_base + TC_O + 128 * n,
+                                                      p_desc + part * (P_TILE >> 4) + 2 * j, v_desc + j * (2048 >> 4),
+                                                      idesc, acc);
+                                else
+                                    ptx::umma_pair_ts(tmem_base + TC_O + 128 * n, p0 + 16 * j + 8 * part,
+                                                      v_desc + j * (2048 >> 4), idesc, acc);
+                            }
                     }
-                    ptx::umma_commit_pair(&bars[B_G2_DONE + buf]);
+                    ptx::umma_commit_pair(&bars[B_G2_DONE + (gp % NG2)]);
                     if (lane == 0) ETAP_TRACE(prm, gp, 11);
                     ++gp;
                 }
@@ -316,7 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
                 const int page = __shfl_sync(0xffffffffu, pg, t - base);
                 const uint32_t buf = gp & 1;
                 // V chunks of page gp-2 are free once its GEMM2 completed
-                if (gp >= 2) ptx::mbar_wait(&bars[B_G2_DONE + buf], ((gp - 2) >> 1) & 1);
+                if (gp >= 2) ptx::mbar_wait(&bars[B_G2_DONE + (gp - 2) % NG2], ((gp - 2) / NG2) & 1);
                 if (lane == 0) {
                     ETAP_TRACE(prm, gp, 1);
                     ptx::mbar_arrive_expect_tx(&bars[B_V_LAND + buf], 4 * V_BYTES);
@@ -436,16 +456,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
                 // this thread's k-step goes to its own lane and, via shared memory, to the
                 // duplicate lane L ^ 64 of the 2-SM A layout (warp q ^ 2 of the same warpgroup)
                 if (tracer) ETAP_TRACE(prm, gp, 6);
+                if constexpr (ETAP_PAIR_P_SMEM) {
+                    // GEMM2 of page gp-1 must have read the single P tile (and O must hold it
+                    // before a rescale): one wait covers both
+                    if (gp >= 1) wg_wait(&bars[B_G2_DONE + (gp - 1) % NG2], ((gp - 1) / NG2) & 1, wg_bar, q);
+                    if (tracer) ETAP_TRACE(prm, gp, 7);
+                    const bool resc = __any_sync(0xffffffffu, upd) || (negate && !first);
+                    if (resc) {
+                        ptx::tc_fence_after();
+                        const float a = negate ? -alpha : alpha;
+#pragma unroll 1
+                        for (int c = 0; c < 4; ++c) {
+                            uint32_t o[32];
+                            const uint32_t ta = t_lane + TC_O + 128 * wg + 32 * c;
+                            ptx::tmem_ld32(ta, o);
+                            ptx::tmem_wait_ld();
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
+                            ptx::tmem_st32(ta, o);
+                        }
+                        ptx::tmem_wait_st();
+                    }
+                    // row h of the K-major SW128 tiles: rows 32r + 16wg + [0, 16) are 32 B = two
+                    // 16 B chunks at chunk index 4r + 2wg (+1), XOR-swizzled with h % 8
+                    uint8_t* prow = smem + OFF_X + (h >> 3) * 1024 + (h & 7) * 128;
+                    const int c0 = 4 * r + 2 * wg;
+#pragma unroll
+                    for (int part = 0; part < 2; ++part) {
+#pragma unroll
+                        for (int k = 0; k < 2; ++k) {
+                            const int i0 = part * 8 + 4 * k;
+                            *reinterpret_cast<uint4*>(prow + part * P_TILE + (((c0 + k) ^ (h & 7)) << 4)) =
+                                make_uint4(pk[i0], pk[i0 + 1], pk[i0 + 2], pk[i0 + 3]);
+                        }
+                    }
+                    ptx::fence_proxy_async_smem();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (tracer) ETAP_TRACE(prm, gp, 15);
+                    if (lane == 0) pair_arrive(&bars[B_P_FULL + buf], leader);
+                    if (tracer) ETAP_TRACE(prm, gp, 8);
+                    ++gp;
+                    continue;
+                }
                 uint4* mine = xb + (wg * 128 + L) * 4;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) mine[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-                // P columns of this buffer: GEMM2 of page gp-2 must have read them
-                if (gp >= 2) wg_wait(&bars[B_G2_DONE + buf], ((gp - 2) >> 1) & 1, wg_bar, q);
+                // P columns of this buffer: GEMM2 of page gp-NPB must have read them
+                if (gp >= NPB) wg_wait(&bars[B_G2_DONE + (gp - NPB) % NG2], ((gp - NPB) / NG2) & 1, wg_bar, q);
                 if (tracer) ETAP_TRACE(prm, gp, 7);
                 const bool resc = __any_sync(0xffffffffu, upd) || (negate && !first);
                 if (resc) {
                     // O must contain GEMM2 of page gp-1 before it is rescaled
-                    ptx::mbar_wait(&bars[B_G2_DONE + ((gp - 1) & 1)], ((gp - 1) >> 1) & 1);
+                    ptx::mbar_wait(&bars[B_G2_DONE + (gp - 1) % NG2], ((gp - 1) / NG2) & 1);
                     ptx::tc_fence_after();
                     const float a = negate ? -alpha : alpha;
 #pragma unroll 1
@@ -472,12 +535,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
                 }
 #pragma unroll
                 for (int i = 0; i < 8; ++i) { ph[i] = pk[i]; pl[i] = pk[8 + i]; }
-                const uint32_t pcol = t_lane + TC_P + 64 * buf;
+                const uint32_t pcol = t_lane + TC_P + 64 * (gp % NPB);
                 if (ETAP_PAIR_P_STORE) {
-                    ptx::tmem_st8(pcol + 8 * kstep, ph);
-                    ptx::tmem_st8(pcol + 32 + 8 * kstep, pl);
-                    ptx::tmem_st8(pcol + 8 * (kstep ^ 2), oh);
-                    ptx::tmem_st8(pcol + 32 + 8 * (kstep ^ 2), ol);
+                    uint32_t mine16[16], theirs16[16];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        mine16[i] = ph[i]; mine16[8 + i] = pl[i];
+                        theirs16[i] = oh[i]; theirs16[8 + i] = ol[i];
+                    }
+                    ptx::tmem_st16(pcol + 16 * kstep, mine16);
+                    ptx::tmem_st16(pcol + 16 * (kstep ^ 2), theirs16);
                     ptx::tmem_wait_st();
                 }
                 if (tracer) ETAP_TRACE(prm, gp, 15);
@@ -495,7 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
             const float l = red[h] + red[HPC + h] + red[2 * HPC + h] + red[3 * HPC + h];
             const float inv = l > 0.f ? 1.f / l : 0.f;  // l = 0: the row saw no KV row (O = 0, L = -inf)
             const uint32_t last = gp - 1;
-            wg_wait(&bars[B_G2_DONE + (last & 1)], (last >> 1) & 1, wg_bar, q);
+            wg_wait(&bars[B_G2_DONE + last % NG2], (last / NG2) & 1, wg_bar, q);
             ptx::tc_fence_after();
             const int ns = soff[vb + 1] - soff[vb];
             const bool direct = ns == 1;
