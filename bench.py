@@ -330,6 +330,8 @@ def run_ours(args) -> None:
     k2_us = (sp[:, :, 1].max(axis=1) - sp[:, :, 0].min(axis=1)) / 1e3  # per launch
     k2_avg_us = float(k2_us.mean())
 
+    unit_heads, _parts = mla.schedule_unit(heads, plan.num_sm_parts)
+    pair = unit_heads == 128
     nbytes = inputs.algorithmic_bytes(seqlens, heads)
     nflops = inputs.flops(seqlens, heads)
     peak, peak_kind = peaks()
@@ -371,7 +373,8 @@ def run_ours(args) -> None:
                     "frac": achieved_tf / tpeak, "peak_kind": tpeak_kind, "hbm_frac": achieved / peak,
                     "note": "useful FLOPs 2*H*ctx*(576+512); the bf16 hi+lo split of P doubles the issued GEMM2 "
                             "FLOPs (1.47x useful) and is not credited"}
-        roof.update({"traffic": traffic, "kernel": "etap_mla_decode_kernel (K2)", "kernel_avg_us": k2_avg_us,
+        roof.update({"traffic": traffic, "kernel": ("etap_mla_decode_pair_kernel (K2, CTA pairs)" if pair
+                                                    else "etap_mla_decode_kernel (K2)"), "kernel_avg_us": k2_avg_us,
                      "kernel_min_us": float(k2_us.min()), "kernel_max_us": float(k2_us.max()),
                      "timing": (f"per-CTA %globaltimer span of the product K2 over the {args.steps} timed steps "
                                 "(max exit - min grid-dependency resolution per launch, etap_mla_debug_span), "
@@ -382,7 +385,9 @@ def run_ours(args) -> None:
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": name, "batch": BATCH, "ctx": CTX, "heads_per_gpu": heads,
                        "total_heads": total_heads, "dist_backend": backend if world > 1 else None, "d_qk": 576,
-                       "d_v": 512, "page_rows": 64, "head_group": mla.head_group(heads),
+                       "d_v": 512, "page_rows": 64, "head_group": unit_heads,
+                       "work_unit": (f"{unit_heads} heads on a CTA pair (tcgen05 cta_group::2)" if pair
+                                     else f"{unit_heads} heads on one CTA"),
                        "kv_bytes_per_gpu": inp.kv_bytes(), "l2": "inputs (1.2 GB KV) > 126 MB L2, no flush",
                        "parallelism": (f"head-shard tp{world} (KV replicated, all-gather of O fused into K2/K3 "
                                        "over NVLink peer memory)" if gather == "peer" else
