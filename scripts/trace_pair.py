@@ -55,6 +55,15 @@ def main() -> None:
     g0 = ent[used].min()
     print(f"entry spread {(ent[used].max() - g0) / 1e3:.2f} us, exit min/median/max "
           f"{(ext[used].min() - g0) / 1e3:.1f} / {(np.median(ext[used]) - g0) / 1e3:.1f} / {(ext[used].max() - g0) / 1e3:.1f} us")
+    # per pair: exit of the later CTA, pages streamed (stamped tile rows), sorted by exit
+    pe = []
+    for c in range(0, nparts, 2):
+        if used[c]:
+            n = int((raw[c, :TT - 1, 0] > 0).sum())
+            pe.append(((max(ext[c], ext[c + 1]) - g0) / 1e3, n))
+    pe.sort()
+    print("pair exits (us, pages) fastest 5:", [(round(a, 1), b) for a, b in pe[:5]],
+          "slowest 5:", [(round(a, 1), b) for a, b in pe[-5:]])
     ghz = (raw[:, TT - 1, 6] - raw[:, TT - 1, 5]) / np.maximum(1, ext - ent)
     print(f"SM clock {np.median(ghz[used]):.3f} GHz")
     for role, ctas in (("leader", [c for c in range(0, nparts, 2) if used[c]]),
