@@ -17,6 +17,7 @@ from paper_2506_01969_b200 import inputs, mla
 def run() -> None:
     cases = [([300, 1, 0, 129], 16, 1, 148), ([700, 65], 32, 1, 7), ([200, 90], 16, 2, 148), ([5000], 64, 1, 148),
              ([3000, 64, 1, 777], 128, 1, 9), ([900, 4100], 96, 1, 148), ([640, 70], 64, 2, 5),
+             ([1000, 300], 256, 1, 148), ([2000, 65], 128, 1, 148),  # CTA-pair kernel (128-head units)
              ([70 * (i % 5 + 1) for i in range(20)], 16, 1, 3)]  # FP8: > 4 splits per CTA (warp-3 Q terms)
     for seqlens, heads, t, parts in cases:
         inp = inputs.make_mla_inputs(seqlens, heads=heads, seed=3, pad_value=float("nan"), q_tokens=t)
