@@ -1789,8 +1789,12 @@ __global__ void __launch_bounds__(72)
 #endif
 constexpr int COMBINE_HPB = ETAP_COMBINE_HPB;  // heads per CTA (128 threads each)
 constexpr int COMBINE_THREADS = 128 * COMBINE_HPB;
-constexpr int COMBINE_BATCH = 16;  // partial float4 loads in flight per thread
+// Partial float4 loads in flight per thread (template COMBINE_BATCH): 16 for head groups of up to
+// 64 (one round trip for up to 16 splits per sequence), 8 for the CTA-pair kernel's 128-head
+// units: 2048 rows at B = 16 with ~6 splits each, where 114 registers per thread (batch 16) allow
+// four CTAs per SM and the merge runs in 3.5 waves.
 
+template <int COMBINE_BATCH>
 __global__ void __launch_bounds__(COMBINE_THREADS)
     etap_mla_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
                             const int32_t* __restrict__ split_off, int hg, int batch,
@@ -2502,7 +2506,8 @@ int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_part
     cfg2.stream = static_cast<cudaStream_t>(stream);
     cfg2.attrs = attr;
     cfg2.numAttrs = pdl_attrs();
-    ETAP_CUDA(cudaLaunchKernelEx(&cfg2, etap_mla_combine_kernel, static_cast<const float*>(ws_o),
+    ETAP_CUDA(cudaLaunchKernelEx(&cfg2, hg >= 128 ? etap_mla_combine_kernel<8> : etap_mla_combine_kernel<16>,
+                                 static_cast<const float*>(ws_o),
                                  static_cast<const float*>(ws_lse), split_off, hg, batch, om,
                                  static_cast<unsigned long long*>(g_combine_trace_buf), seqlens,
                                  sched_parts > 0 ? sched_parts : num_sm_parts, lanes_enabled() ? 1 : 0, fixed_cost));

@@ -6,12 +6,12 @@ import numpy as np
 import torch
 from paper_2506_01969_b200 import _lib, inputs, mla
 
-B, CTX = int(os.environ.get("B", 16)), int(os.environ.get("CTX", 1024))
-inp = inputs.make_mla_inputs([CTX] * B, heads=16, pad_value=0.0)
-plan = mla.MlaDecodePlan.create(B, 16, "cuda")
+B, CTX, H = int(os.environ.get("B", 16)), int(os.environ.get("CTX", 1024)), int(os.environ.get("HEADS", 16))
+inp = inputs.make_mla_inputs([CTX] * B, heads=H, pad_value=0.0)
+plan = mla.MlaDecodePlan.create(B, H, "cuda")
 n, TT, STEPS = plan.num_sm_parts, 256, 4
 k2 = [torch.zeros(n * TT * 16, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
-k3 = [torch.zeros(B * 16 * 4, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
+k3 = [torch.zeros(B * H * 4, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
 L = _lib.lib()
 f = lambda: plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
 if os.environ.get("FP8"):  # FP8 (e4m3) latent cache
