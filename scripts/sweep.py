@@ -212,15 +212,14 @@ if __name__ == "__main__":
         sys.exit(0)
     if "--heads" in sys.argv:  # head-count sweep at the headline context (head group per ETAP_HEAD_GROUP)
         hg = os.environ.get("ETAP_HEAD_GROUP", "auto")
-        for h in (16, 32, 64, 128):
-            measure([65536] * 16, h, f"B=16 ctx=64K H={h} head_group={mla.head_group(h) if hg == 'auto' else hg}",
-                    iters=20)
-        measure([4096] * 64, 128, f"B=64 ctx=4K H=128 head_group={mla.head_group(128) if hg == 'auto' else hg}",
-                iters=20)
+        unit = lambda h: mla.schedule_unit(h, mla.num_sm_parts())[0] if hg == "auto" else hg  # 128: CTA pairs
+        for h in (16, 32, 64, 128, 256):
+            measure([65536] * 16, h, f"B=16 ctx=64K H={h} work_unit={unit(h)}", iters=20 if h <= 128 else 10)
+        measure([4096] * 64, 128, f"B=64 ctx=4K H=128 work_unit={unit(128)}", iters=20)
         sys.exit(0)
     measure([1024], 16, "config1 B=1 H=16 ctx=1K")
     for ctx in (1024, 2048, 4096, 8192, 16384, 32768, 65536):
         measure([ctx] * 16, 16, f"config3 B=16 H=16 ctx={ctx}")
     measure(inputs.varlen_seqlens(32), 16, "config4 B=32 varlen 4K-128K")
     if "--no-config5" not in sys.argv:
-        measure([65536] * 16, 128, "config5 single-GPU B=16 H=128 ctx=64K (4 head groups of 32)", iters=10)
+        measure([65536] * 16, 128, "config5 single-GPU B=16 H=128 ctx=64K (128-head units on CTA pairs)", iters=10)
