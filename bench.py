@@ -233,6 +233,11 @@ def run_ours(args) -> None:
             dist.init_process_group(backend)
 
     name, heads, total_heads = workload(args.scaling, args.total_heads, world)
+    fp8 = args.kv == "fp8"
+    if fp8:
+        if world > 1:
+            raise SystemExit("--kv fp8 runs on one GPU (the fused peer gather is bf16-only)")
+        name += "_fp8kv"
     seqlens = [CTX] * BATCH
     h0, _ = sharding.head_shard(total_heads, world, rank)
     inp = inputs.make_mla_inputs(seqlens, heads=heads, seed=SEED, device=dev, pad_value=0.0,
@@ -283,8 +288,14 @@ def run_ours(args) -> None:
     # opt-in early metadata read (etap_mla.h ETAP_FLAG_EARLY_METADATA): nothing in this loop
     # writes seqlens / block_table, so K2 may read them before its grid dependency resolves
     dflags = mla.FLAG_EARLY_METADATA
+    KV_SCALE = 0.125  # dequantised value = KV_SCALE * e4m3 (the scale the GPU tests and sweeps use)
+    kv8 = (inp.kv_pool.float() / KV_SCALE).to(torch.float8_e4m3fn) if fp8 else None
 
     def step():
+        if fp8:  # K2-FP8 (kind::f8f6f4 UMMAs straight from the fp8 pages) + K3
+            plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, KV_SCALE, out=out, lse=lse,
+                            flags=dflags)
+            return out, lse
         # K2 computes the split schedule in its prologue (same partition as K1, which is the
         # per-step metadata call of the API and is off the critical path here) + K3 combine
         if gather == "peer":  # K2 + K3 store every rank's copy, K4 = arrival flags
@@ -333,6 +344,8 @@ def run_ours(args) -> None:
     unit_heads, _parts = mla.schedule_unit(heads, plan.num_sm_parts)
     pair = unit_heads == 128
     nbytes = inputs.algorithmic_bytes(seqlens, heads)
+    if fp8:  # the latent cache is one byte per element
+        nbytes -= sum(seqlens) * 576
     nflops = inputs.flops(seqlens, heads)
     peak, peak_kind = peaks()
     tpeak, tpeak_kind = tensor_peak()
@@ -358,10 +371,12 @@ def run_ours(args) -> None:
         clocks = clk.summary()
         # e2e: the reference-facing C-ABI call with HOST buffers (H2D + K1/K2/K3 + D2H per step)
         e2e, e2e_serving = e2e_multi, None
-        if world == 1 and args.e2e_steps > 0:
+        if world == 1 and args.e2e_steps > 0 and fp8:
+            e2e = e2e_fp8(inp, kv8, KV_SCALE, plan, args.e2e_steps, dev)
+        elif world == 1 and args.e2e_steps > 0:
             e2e = e2e_host(inp, args.e2e_steps, dev)
             # serving-style step (cache resident in HBM): reported beside e2e, not instead
-            e2e_serving = e2e_serving_host(inp, 50, dev)
+            e2e_serving = None if fp8 else e2e_serving_host(inp, 50, dev)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(heads, args)
@@ -373,8 +388,9 @@ def run_ours(args) -> None:
                     "frac": achieved_tf / tpeak, "peak_kind": tpeak_kind, "hbm_frac": achieved / peak,
                     "note": "useful FLOPs 2*H*ctx*(576+512); the bf16 hi+lo split of P doubles the issued GEMM2 "
                             "FLOPs (1.47x useful) and is not credited"}
-        roof.update({"traffic": traffic, "kernel": ("etap_mla_decode_pair_kernel (K2, CTA pairs)" if pair
-                                                    else "etap_mla_decode_kernel (K2)"), "kernel_avg_us": k2_avg_us,
+        kname = ("etap_mla_decode_fp8_kernel (K2-FP8)" if fp8 else
+                 "etap_mla_decode_pair_kernel (K2, CTA pairs)" if pair else "etap_mla_decode_kernel (K2)")
+        roof.update({"traffic": traffic, "kernel": kname, "kernel_avg_us": k2_avg_us,
                      "kernel_min_us": float(k2_us.min()), "kernel_max_us": float(k2_us.max()),
                      "timing": (f"per-CTA %globaltimer span of the product K2 over the {args.steps} timed steps "
                                 "(max exit - min grid-dependency resolution per launch, etap_mla_debug_span), "
@@ -382,7 +398,8 @@ def run_ours(args) -> None:
         result = {
             "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": args.scaling,
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "vs_baseline": None, "dtype": "e4m3 latent cache, fp32 accumulate" if fp8 else "bf16",
+            "data": "synthetic",
             "config": {"workload": name, "batch": BATCH, "ctx": CTX, "heads_per_gpu": heads,
                        "total_heads": total_heads, "dist_backend": backend if world > 1 else None, "d_qk": 576,
                        "d_v": 512, "page_rows": 64, "head_group": unit_heads,
@@ -460,6 +477,37 @@ def e2e_host(inp, steps: int, dev) -> dict:
             "api": "etap_mla_host_decode (C-ABI, pinned host buffers, synchronous)", "steps": steps,
             "bound": {"kind": "pcie_h2d", "measured_h2d_gbs": h2d_gbs,
                       "bound_us": (h2d + d2h) / h2d_gbs / 1e3, "frac": (h2d + d2h) / h2d_gbs / 1e3 / (dt * 1e6)}}
+
+
+def e2e_fp8(inp, kv8, kv_scale: float, plan, steps: int, dev) -> dict:
+    """FP8 cache, end to end through the Python API (decode_fp8 has no host-buffer C-ABI entry):
+    per step the Q, the fp8 latent cache, the block table and seqlens are copied from pinned host
+    memory, the step runs, O / LSE are read back into pinned host memory; wall clock."""
+    import torch
+
+    host = [t.cpu().pin_memory() for t in (inp.q, kv8, inp.block_table, inp.seqlens)]
+    devb = [torch.empty_like(t) for t in (inp.q, kv8, inp.block_table, inp.seqlens)]
+    out_h = torch.empty((inp.batch, 1, inp.heads, 512), dtype=torch.float32).pin_memory()
+    lse_h = torch.empty((inp.batch, 1, inp.heads), dtype=torch.float32).pin_memory()
+
+    def call():
+        for d, h in zip(devb, host):
+            d.copy_(h, non_blocking=True)
+        o, l = plan.decode_fp8(devb[0], devb[1], devb[2], devb[3], inp.scale, kv_scale)
+        out_h.copy_(o, non_blocking=True)
+        lse_h.copy_(l, non_blocking=True)
+        torch.cuda.synchronize(dev)
+
+    call()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    dt = (time.perf_counter() - t0) / steps
+    h2d = sum(t.numel() * t.element_size() for t in host)
+    d2h = out_h.numel() * 4 + lse_h.numel() * 4
+    return {"value": dt * 1e6, "unit": "us/step", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "api": "MlaDecodePlan.decode_fp8 (Python API over the C-ABI, pinned host buffers, synchronous)",
+            "steps": steps}
 
 
 def e2e_ranks(inp, steps: int, dev, run_step, barrier, world: int) -> dict:
@@ -590,6 +638,8 @@ def main() -> None:
     ap.add_argument("--cpu-ctx", type=int, default=CTX, help="KV rows per sequence of the CPU baseline step")
     ap.add_argument("--ref-ctx", type=int, default=CTX, help="KV rows per sequence of each reference-arm step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kv", choices=["bf16", "fp8"], default="bf16",
+                    help="latent cache format: bf16 (the headline) or fp8 e4m3 (K2-FP8, single GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (contract minimum)")
