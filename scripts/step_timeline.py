@@ -13,10 +13,11 @@ n, TT, STEPS = plan.num_sm_parts, 256, 4
 k2 = [torch.zeros(n * TT * 16, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
 k3 = [torch.zeros(B * H * 4, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
 L = _lib.lib()
-f = lambda: plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
+FL = mla.FLAG_EARLY_METADATA if os.environ.get("EARLY") else 0  # the bench's opt-in early schedule
+f = lambda: plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, flags=FL)
 if os.environ.get("FP8"):  # FP8 (e4m3) latent cache
     kv8 = (inp.kv_pool.float() / 0.125).to(torch.float8_e4m3fn)
-    f = lambda: plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 0.125)
+    f = lambda: plan.decode_fp8(inp.q, kv8, inp.block_table, inp.seqlens, inp.scale, 0.125, flags=FL)
 for _ in range(5): f()
 torch.cuda.synchronize()
 for i in range(STEPS):  # back to back, a different trace buffer per step
