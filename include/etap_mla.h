@@ -89,6 +89,15 @@ extern "C" {
                                        and triggers its dependents early does not). Without
                                        the flag (default) both are read after the dependency
                                        resolves, which is safe whoever wrote them. */
+#define ETAP_FLAG_INDEPENDENT_INPUTS 64u /* opt-in, implies EARLY_METADATA: the kernel launched
+                                       immediately before the decode on the stream writes none
+                                       of its inputs (q, kv_pool, block_table, seqlens) and is
+                                       not a decode launched with SKIP_COMBINE. The decode then
+                                       streams KV and Q while that kernel still runs and waits
+                                       for it only before its first global write (schedule
+                                       publish, split partials, outputs): back-to-back decode
+                                       steps overlap the next step's start with the previous
+                                       step's combine. Ignored with ETAP_FLAG_SKIP_COMBINE. */
 
 /* Thread-local description of the last error. Never NULL. */
 const char* etap_mla_last_error(void);

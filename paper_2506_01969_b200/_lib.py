@@ -25,6 +25,7 @@ FLAG_EXTERNAL_SCHEDULE = 8
 FLAG_DEP_METADATA = 16  # no-op since round 2: seqlens / block_table are read after the grid dependency by default
 PRECISION_EXACT64 = 0  # etaplab::Precision (matrix.hpp:22); fp32 = 1 / fp16emu = 2 are rejected
 FLAG_EARLY_METADATA = 32  # opt-in: read seqlens / block_table before the grid dependency (etap_mla.h)
+FLAG_INDEPENDENT_INPUTS = 64  # opt-in: the preceding kernel writes none of the inputs; wait only before writes
 
 _lib = None
 

@@ -456,9 +456,19 @@ __device__ __forceinline__ void span_stamp(const DecodeParams& prm, int slot) {
 
 template <bool kDebug>
 __device__ __forceinline__ void dep_wait_producer(const DecodeParams& prm) {
-    ptx::grid_dep_wait();
-    ptx::grid_dep_launch();
+    if (!prm.defer_dep) {
+        ptx::grid_dep_wait();
+        ptx::grid_dep_launch();
+    }
+    // (deferred dependency: the first moment the kernel touches KV is its first TMA)
     if (threadIdx.x == 0) { span_stamp(prm, 0); ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
+}
+
+// Before a warp's first global write under a deferred grid dependency (ETAP_FLAG_INDEPENDENT_
+// INPUTS): the kernel before this one (the previous step's combine) may still read the split
+// partials / split_off this kernel is about to write. Immediate once the dependency resolved.
+__device__ __forceinline__ void dep_wait_before_write(const DecodeParams& prm) {
+    if (prm.defer_dep) ptx::grid_dep_wait();
 }
 
 template <bool kDebug, int MAXVB>
@@ -521,7 +531,12 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
     // it waits for the dependency itself, right before issuing it (dep_wait_producer), with
     // the issue path already fetched and its page ids in registers.
     r.late_wait = early;
-    if (!(early && warp == 0)) {
+    if (early && prm.defer_dep) {
+        // ETAP_FLAG_INDEPENDENT_INPUTS: the caller guarantees that the kernel before this one
+        // writes none of the inputs, so the loads need not wait for it; every global write does
+        // (dep_wait_before_write). The combine may be scheduled right away.
+        ptx::grid_dep_launch();
+    } else if (!(early && warp == 0)) {
         ptx::grid_dep_wait();     // KV / Q and the outputs of earlier kernels in the stream
         ptx::grid_dep_launch();   // let the combine kernel get scheduled
     }
@@ -534,7 +549,10 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
     if (threadIdx.x == 0 && !early) { span_stamp(prm, 0); ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
     if (fused) {
         if (early) {
-            if (warp == 3 && sched_publisher(prm)) publish_schedule(prm, ls, s_soff, s_sched, lane, 32);
+            if (warp == 3 && sched_publisher(prm)) {
+                dep_wait_before_write(prm);  // the previous step's combine may still read split_off
+                publish_schedule(prm, ls, s_soff, s_sched, lane, 32);
+            }
         } else {
             schedule(sched_publisher(prm));
         }
@@ -1104,6 +1122,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
             // (the single transpose of etap.cpp:140 is the TMEM lane -> d mapping),
             // L = m + log l (etap.cpp:144)
             const uint32_t last = gt - 1;
+            dep_wait_before_write(prm);
             ptx::mbar_wait(&bars[BAR_G2_DONE + last % NTB], (last / NTB) & 1);
             ptx::tc_fence_after();
             if (tracer) ETAP_TRACE_G(prm, 10);
@@ -1651,6 +1670,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
             // ---- epilogue: O = kv_scale * (O_0 + O_1/16 + O_2/256) / l, L = m + log l
             const uint32_t last = gt - 1;
+            dep_wait_before_write(prm);
             ptx::mbar_wait(&bars[BAR_G2D + last % NTB8], (last / NTB8) & 1);
             ptx::tc_fence_after();
             if (tracer) { ETAP_TRACE_G(prm, 10); ETAP_TRACE(prm, last, 10); }
@@ -1784,26 +1804,35 @@ __global__ void __launch_bounds__(72)
 // non-goal; the math is pinned by L = m + log l, etap.cpp:144, and partition
 // invariance, acceptance.cpp:209-229). Grid: one CTA of 128 threads per (vb, head).
 // =============================================================================================
-#ifndef ETAP_COMBINE_HPB
-#define ETAP_COMBINE_HPB 1
+// Heads per CTA (template HPB, 128 threads each) and partial float4 loads in flight per thread
+// (template COMBINE_BATCH, any value gives the same bits):
+//   * 16-head units (the headline): HPB 2, batch 8 -> 128 CTAs of 72 registers, so one combine
+//     CTA fits on an SM beside the decode CTA (43k registers, 224 KB): every combine CTA is
+//     resident before the decode ends, and the next step's decode CTAs can launch beside the
+//     running combine (with ETAP_FLAG_INDEPENDENT_INPUTS they then stream at once); two round
+//     trips for the ~10 splits of a sequence instead of one;
+//   * 32 / 64-head units: HPB 1, batch 16 (one round trip for up to 16 splits per sequence);
+//   * the CTA-pair kernel's 128-head units: HPB 1, batch 8 (2048 rows at B = 16 with ~6 splits
+//     each: 72 instead of 114 registers, two waves instead of 3.5).
+constexpr int COMBINE_GROUP = 16;  // splits merged per rescale of the running sums
+// K3 lets the next kernel launch before its own grid dependency (1) or after it (0). Early: the
+// next step's decode CTAs take SMs as this step's decode CTAs exit (during its tail), and with
+// ETAP_FLAG_INDEPENDENT_INPUTS they stream right away; without that flag they wait for this
+// combine in their prologue as before. Either way every global write of the next decode is
+// ordered after this combine (its grid dependency covers this grid's completion).
+#ifndef ETAP_K3_EARLY_TRIGGER
+#define ETAP_K3_EARLY_TRIGGER 1
 #endif
-constexpr int COMBINE_HPB = ETAP_COMBINE_HPB;  // heads per CTA (128 threads each)
-constexpr int COMBINE_THREADS = 128 * COMBINE_HPB;
-// Partial float4 loads in flight per thread (template COMBINE_BATCH): 16 for head groups of up to
-// 64 (one round trip for up to 16 splits per sequence), 8 for the CTA-pair kernel's 128-head
-// units: 2048 rows at B = 16 with ~6 splits each, where 114 registers per thread (batch 16) allow
-// four CTAs per SM and the merge runs in 3.5 waves.
-
-template <int COMBINE_BATCH>
-__global__ void __launch_bounds__(COMBINE_THREADS)
-    etap_mla_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
-                            const int32_t* __restrict__ split_off, int hg, int batch,
-                            const __grid_constant__ OutMap om, unsigned long long* trace,
-                            const int32_t* __restrict__ seqlens, int parts, int lanes_on, int fixed_cost) {
+template <int COMBINE_BATCH, int HPB>
+__device__ __forceinline__ void combine_body(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
+                                             const int32_t* __restrict__ split_off, int hg, int batch,
+                                             const OutMap& om, unsigned long long* trace,
+                                             const int32_t* __restrict__ seqlens, int parts, int lanes_on,
+                                             int fixed_cost) {
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 0] = ptx::global_timer_ns();
-    const int units = hg / COMBINE_HPB;           // CTAs per virtual sequence
+    const int units = hg / HPB;                   // CTAs per virtual sequence
     const int vb = blockIdx.x / units;
-    const int h = (blockIdx.x - vb * units) * COMBINE_HPB + threadIdx.x / 128;
+    const int h = (blockIdx.x - vb * units) * HPB + threadIdx.x / 128;
     const int t = threadIdx.x % 128;              // float4 of the 512-wide O row
     const int g = vb / batch, b = vb - g * batch;  // head-group-major virtual sequences
     int s0, ns;
@@ -1847,11 +1876,13 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
         __syncthreads();
         s0 = s_info[0];
         ns = s_info[1];
+        if (ETAP_K3_EARLY_TRIGGER) ptx::grid_dep_launch();
         ptx::grid_dep_wait();
-        ptx::grid_dep_launch();  // the next decode step's prologue may overlap this combine
+        if (!ETAP_K3_EARLY_TRIGGER) ptx::grid_dep_launch();  // the next decode step's prologue may overlap this combine
     } else {
+        if (ETAP_K3_EARLY_TRIGGER) ptx::grid_dep_launch();
         ptx::grid_dep_wait();
-        ptx::grid_dep_launch();
+        if (!ETAP_K3_EARLY_TRIGGER) ptx::grid_dep_launch();
         s0 = __ldg(split_off + vb);
         ns = __ldg(split_off + vb + 1) - s0;
     }
@@ -1868,42 +1899,50 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
         }
         return;
     }
-    // One round trip after split_off: every thread issues all of its partial loads (one float4
-    // per split, up to COMBINE_BATCH in flight) together with the split LSEs, then merges.
+    // Splits merge in groups of COMBINE_GROUP (the group's LSEs first: its max rescales the running
+    // sums once), each group's partial float4s loaded COMBINE_BATCH at a time (registers): the
+    // arithmetic, and so every output bit, is the same for every COMBINE_BATCH.
     const float* l_base = ws_lse + static_cast<size_t>(s0) * hg + h;
     const float4* p4 = reinterpret_cast<const float4*>(ws_o + (static_cast<size_t>(s0) * hg + h) * D_V) + t;
     const size_t stride4 = static_cast<size_t>(hg) * D_V / 4;
     float mx = -INFINITY, sum = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < ns; s += COMBINE_BATCH) {
-        const int n = min(COMBINE_BATCH, ns - s);
+    for (int s = 0; s < ns; s += COMBINE_GROUP) {
+        const int n = min(COMBINE_GROUP, ns - s);
+        float l[COMBINE_GROUP];
         float4 v[COMBINE_BATCH];
-        float l[COMBINE_BATCH];
 #pragma unroll
-        for (int j = 0; j < COMBINE_BATCH; ++j) {
-            if (j < n) {
-                v[j] = __ldg(p4 + (s + j) * stride4);
-                l[j] = __ldg(l_base + static_cast<size_t>(s + j) * hg);
-            }
-        }
-        // online merge of this batch (same algebra as L = m + log l, etap.cpp:144)
+        for (int j = 0; j < COMBINE_GROUP; ++j)
+            if (j < n) l[j] = __ldg(l_base + static_cast<size_t>(s + j) * hg);
+#pragma unroll
+        for (int j = 0; j < COMBINE_BATCH; ++j)  // the first loads go out with the LSEs
+            if (j < n) v[j] = __ldg(p4 + (s + j) * stride4);
+        // online merge of this group (same algebra as L = m + log l, etap.cpp:144)
         float bm = mx;
 #pragma unroll
-        for (int j = 0; j < COMBINE_BATCH; ++j)
+        for (int j = 0; j < COMBINE_GROUP; ++j)
             if (j < n) bm = fmaxf(bm, l[j]);
         const float bs = bm == -INFINITY ? 0.f : bm;  // all partials empty so far (causal MTP)
-        const float corr = __expf(mx - bs);  // 0 on the first batch (mx = -inf)
+        const float corr = __expf(mx - bs);  // 0 on the first group (mx = -inf)
         sum *= corr;
         acc.x *= corr; acc.y *= corr; acc.z *= corr; acc.w *= corr;
 #pragma unroll
-        for (int j = 0; j < COMBINE_BATCH; ++j) {
-            if (j < n) {
-                const float w = __expf(l[j] - bs);
-                sum += w;
-                acc.x = fmaf(w, v[j].x, acc.x);
-                acc.y = fmaf(w, v[j].y, acc.y);
-                acc.z = fmaf(w, v[j].z, acc.z);
-                acc.w = fmaf(w, v[j].w, acc.w);
+        for (int j0 = 0; j0 < COMBINE_GROUP; j0 += COMBINE_BATCH) {
+            if (j0 > 0) {
+#pragma unroll
+                for (int j = 0; j < COMBINE_BATCH; ++j)
+                    if (j0 + j < n) v[j] = __ldg(p4 + (s + j0 + j) * stride4);
+            }
+#pragma unroll
+            for (int j = 0; j < COMBINE_BATCH; ++j) {
+                if (j0 + j < n) {
+                    const float w = __expf(l[j0 + j] - bs);
+                    sum += w;
+                    acc.x = fmaf(w, v[j].x, acc.x);
+                    acc.y = fmaf(w, v[j].y, acc.y);
+                    acc.z = fmaf(w, v[j].z, acc.z);
+                    acc.w = fmaf(w, v[j].w, acc.w);
+                }
             }
         }
         mx = bm;
@@ -1915,6 +1954,23 @@ __global__ void __launch_bounds__(COMBINE_THREADS)
         reinterpret_cast<float4*>(om.out[r] + orow * D_V)[t] = acc;
     }
     if (trace && threadIdx.x == 0) trace[blockIdx.x * 4 + 2] = ptx::global_timer_ns();
+}
+
+template <int COMBINE_BATCH>
+__global__ void __launch_bounds__(128)
+    etap_mla_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
+                            const int32_t* __restrict__ split_off, int hg, int batch,
+                            const __grid_constant__ OutMap om, unsigned long long* trace,
+                            const int32_t* __restrict__ seqlens, int parts, int lanes_on, int fixed_cost) {
+    combine_body<COMBINE_BATCH, 1>(ws_o, ws_lse, split_off, hg, batch, om, trace, seqlens, parts, lanes_on, fixed_cost);
+}
+// two heads per CTA, at most 80 registers: one CTA beside a 16-head decode CTA (43k registers)
+__global__ void __launch_bounds__(256, 3)
+    etap_mla_combine2_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
+                             const int32_t* __restrict__ split_off, int hg, int batch,
+                             const __grid_constant__ OutMap om, unsigned long long* trace,
+                             const int32_t* __restrict__ seqlens, int parts, int lanes_on, int fixed_cost) {
+    combine_body<8, 2>(ws_o, ws_lse, split_off, hg, batch, om, trace, seqlens, parts, lanes_on, fixed_cost);
 }
 
 // =============================================================================================
@@ -2223,6 +2279,18 @@ unsigned pdl_attrs() {
     return n;
 }
 
+// ETAP_FLAG_INDEPENDENT_INPUTS (implies the early metadata read): the decode kernels wait for the
+// grid dependency only before their first global write. Never with SKIP_COMBINE (K2 would then
+// be the predecessor of the next call's K2, which writes the same workspace / FP8 Q scratch);
+// ETAP_DEFER_DEP=0 in the environment ignores the flag (A/B runs).
+int defer_dep_of(unsigned flags, int early_meta) {
+    static const bool on = [] {
+        const char* e = std::getenv("ETAP_DEFER_DEP");
+        return !(e && e[0] == '0');
+    }();
+    return (on && early_meta && (flags & ETAP_FLAG_INDEPENDENT_INPUTS) && !(flags & ETAP_FLAG_SKIP_COMBINE)) ? 1 : 0;
+}
+
 // Schedule before the grid dependency (DecodeParams::early_meta, opt-in per call with
 // ETAP_FLAG_EARLY_METADATA); ETAP_EARLY_META=0 in the environment ignores that flag (A/B runs).
 bool early_meta_enabled() {
@@ -2500,13 +2568,21 @@ int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_part
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg2 = {};
-    cfg2.gridDim = dim3(batch * groups * hg / COMBINE_HPB);
-    cfg2.blockDim = dim3(COMBINE_THREADS);
+    // (ETAP_COMBINE_NARROW=0 in the environment: HPB 1 / batch 16 for 16-head units too, A/B)
+    static const bool narrow2 = [] {
+        const char* e = std::getenv("ETAP_COMBINE_NARROW");
+        return !(e && e[0] == '0');
+    }();
+    const int hpb = (hg == 16 && narrow2) ? 2 : 1;
+    cfg2.gridDim = dim3(batch * groups * hg / hpb);
+    cfg2.blockDim = dim3(128 * hpb);
     cfg2.dynamicSmemBytes = 0;
     cfg2.stream = static_cast<cudaStream_t>(stream);
     cfg2.attrs = attr;
     cfg2.numAttrs = pdl_attrs();
-    ETAP_CUDA(cudaLaunchKernelEx(&cfg2, hg >= 128 ? etap_mla_combine_kernel<8> : etap_mla_combine_kernel<16>,
+    auto kern = hpb == 2 ? etap_mla_combine2_kernel
+                         : (hg >= 128 ? etap_mla_combine_kernel<8> : etap_mla_combine_kernel<16>);
+    ETAP_CUDA(cudaLaunchKernelEx(&cfg2, kern,
                                  static_cast<const float*>(ws_o),
                                  static_cast<const float*>(ws_lse), split_off, hg, batch, om,
                                  static_cast<unsigned long long*>(g_combine_trace_buf), seqlens,
@@ -2574,7 +2650,8 @@ int decode_pair(const void* q, const void* kv_pool, int64_t num_pages, const int
     const LineShape ls = line_shape(batch, groups, pairs, prm.lanes_on != 0);
     const bool external = flags & ETAP_FLAG_EXTERNAL_SCHEDULE;
     prm.inkernel_sched = (ls.line_n <= pairk::MAX_VB && !external) ? 1 : 0;
-    prm.early_meta = (early_meta_enabled() && (flags & ETAP_FLAG_EARLY_METADATA)) ? 1 : 0;
+    prm.early_meta = (early_meta_enabled() && (flags & (ETAP_FLAG_EARLY_METADATA | ETAP_FLAG_INDEPENDENT_INPUTS))) ? 1 : 0;
+    prm.defer_dep = defer_dep_of(flags, prm.early_meta);
     prm.fixed_cost = META_FIXED_COST;
     if (!prm.inkernel_sched && !external) {
         if (int rc = metadata_launch(seqlens, batch, groups, pairs, sched, split_off, stream)) return rc;
@@ -2685,7 +2762,8 @@ int decode_impl(const void* q, const void* kv_pool, int64_t num_pages, const int
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
     const int max_vb = hg == 64 ? Cfg<64>::MAX_VB : (hg == 32 ? Cfg<32>::MAX_VB : Cfg<16>::MAX_VB);
     prm.inkernel_sched = (ls.line_n <= max_vb && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) ? 1 : 0;
-    prm.early_meta = (early_meta_enabled() && (flags & ETAP_FLAG_EARLY_METADATA)) ? 1 : 0;
+    prm.early_meta = (early_meta_enabled() && (flags & (ETAP_FLAG_EARLY_METADATA | ETAP_FLAG_INDEPENDENT_INPUTS))) ? 1 : 0;
+    prm.defer_dep = defer_dep_of(flags, prm.early_meta);
     prm.fixed_cost = META_FIXED_COST;
     if (!prm.inkernel_sched && !(flags & ETAP_FLAG_EXTERNAL_SCHEDULE)) {
         // too many virtual sequences for the fused prologue: run K1 first on the same stream
@@ -2817,7 +2895,10 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     prm.pair = 0;
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
     prm.inkernel_sched = ls.line_n <= MAX_FUSED_VB ? 1 : 0;
-    prm.early_meta = (early_meta_enabled() && (flags & ETAP_FLAG_EARLY_METADATA)) ? 1 : 0;
+    prm.early_meta = (early_meta_enabled() && (flags & (ETAP_FLAG_EARLY_METADATA | ETAP_FLAG_INDEPENDENT_INPUTS))) ? 1 : 0;
+    // never deferred: the prologue writes the per-CTA Q-term scratch, which the previous call's
+    // K2-FP8 CTAs may still read once the combine lets this kernel launch early
+    prm.defer_dep = 0;
     prm.fixed_cost = FP8_FIXED_COST;
     prm.scale_log2 = scale * kv_scale * 1.4426950408889634f;
     prm.flags = flags;

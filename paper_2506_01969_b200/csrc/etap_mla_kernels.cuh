@@ -401,6 +401,8 @@ struct DecodeParams {
     int fixed_cost;      // per-split overhead in tile units of the split schedule
     int lanes_on;        // head-group lanes enabled (line_shape)
     int pair;            // 1: CTA-pair kernel, a schedule part is a pair of CTAs (part = blockIdx.x >> 1)
+    int defer_dep;       // 1 (ETAP_FLAG_INDEPENDENT_INPUTS): the grid dependency is waited for only before
+                         // the first global write (schedule publish, epilogue), not before the loads
     float scale_log2;
     unsigned flags;
     unsigned long long* trace;  // debug: [cta][TRACE_TILES][TRACE_SLOTS] stamps (ETAP_TRACE), or null

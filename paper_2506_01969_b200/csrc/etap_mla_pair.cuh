@@ -471,6 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
             }
 
             // ---- epilogue: l over the four row quarters, O = O / l, L = m + log l (etap.cpp:140-144)
+            dep_wait_before_write(prm);
             ptx::named_bar_sync(2, 256);  // every thread is past its last read of red
             red[quarter * HPC + h] = l_part;
             ptx::named_bar_sync(2, 256);

@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from ._lib import (FLAG_DEP_METADATA, FLAG_EAGER_RESCALE, FLAG_EARLY_METADATA,  # noqa: F401
-                   FLAG_EXTERNAL_SCHEDULE, FLAG_NEGATE_RESCALE, FLAG_SKIP_COMBINE, check)
+                   FLAG_EXTERNAL_SCHEDULE, FLAG_INDEPENDENT_INPUTS, FLAG_NEGATE_RESCALE, FLAG_SKIP_COMBINE, check)
 
 D_QK = 576
 D_V = 512

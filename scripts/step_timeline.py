@@ -13,7 +13,9 @@ n, TT, STEPS = plan.num_sm_parts, 256, 4
 k2 = [torch.zeros(n * TT * 16, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
 k3 = [torch.zeros(B * H * 4, dtype=torch.int64, device="cuda") for _ in range(STEPS)]
 L = _lib.lib()
-FL = mla.FLAG_EARLY_METADATA if os.environ.get("EARLY") else 0  # the bench's opt-in early schedule
+# EARLY=1: the opt-in early schedule; INDEP=1: the bench's flags (independent inputs, implies early)
+FL = (mla.FLAG_INDEPENDENT_INPUTS if os.environ.get("INDEP") else
+      mla.FLAG_EARLY_METADATA if os.environ.get("EARLY") else 0)
 f = lambda: plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale, flags=FL)
 if os.environ.get("FP8"):  # FP8 (e4m3) latent cache
     kv8 = (inp.kv_pool.float() / 0.125).to(torch.float8_e4m3fn)
