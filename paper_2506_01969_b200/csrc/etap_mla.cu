@@ -1357,9 +1357,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
         }
+        // the first split's terms go to shared memory at once; the scratch slots are global
+        // writes, after the grid dependency under ETAP_FLAG_INDEPENDENT_INPUTS (the previous
+        // call's CTAs may still read them until then)
 #pragma unroll
         for (int j = 0; j < 1 + NSCR; ++j) {
             if (j >= nq) break;
+            if (j == 1) {
+                ptx::fence_proxy_async_smem();
+                ptx::named_bar_sync(5, QPRO_THREADS);
+                if (pt == 0) ptx::mbar_arrive(&bars[BAR_QF]);
+                dep_wait_before_write(prm);
+            }
 #pragma unroll
             for (int i = 0; i < QPRO_VEC; ++i) {
                 const int vi = pt + QPRO_THREADS * i, h = vi / (D_QK / 8), cv = vi - h * (D_QK / 8);
@@ -1374,11 +1383,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
         }
-        ptx::fence_proxy_async_smem();
-        ptx::fence_proxy_async_global();
+        if (nq == 1) ptx::fence_proxy_async_smem();
+        else ptx::fence_proxy_async_global();
         ptx::named_bar_sync(5, QPRO_THREADS);
         if (pt == 0) {
-            if (nq > 0) ptx::mbar_arrive(&bars[BAR_QF]);
+            if (nq == 1) ptx::mbar_arrive(&bars[BAR_QF]);
             for (int j = 1; j < nq; ++j) ptx::mbar_arrive(&bars[BAR_SCF + j - 1]);
         }
     }
@@ -1498,6 +1507,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (j > NSCR) {
                 const uint32_t slot_q = (j - 1) % NSCR, u = (j - 1) / NSCR;
                 ptx::mbar_wait(&bars[BAR_SCE + slot_q], (u - 1) & 1);
+                dep_wait_before_write(prm);
                 fp8::quant_q_global_warp(q_rows(sd), scratch(slot_q), lane);
                 ptx::fence_proxy_async_global();
                 __syncwarp();
@@ -2896,9 +2906,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     const LineShape ls = line_shape(batch, groups, num_sm_parts, prm.lanes_on != 0);
     prm.inkernel_sched = ls.line_n <= MAX_FUSED_VB ? 1 : 0;
     prm.early_meta = (early_meta_enabled() && (flags & (ETAP_FLAG_EARLY_METADATA | ETAP_FLAG_INDEPENDENT_INPUTS))) ? 1 : 0;
-    // never deferred: the prologue writes the per-CTA Q-term scratch, which the previous call's
-    // K2-FP8 CTAs may still read once the combine lets this kernel launch early
-    prm.defer_dep = 0;
+    prm.defer_dep = defer_dep_of(flags, prm.early_meta);
     prm.fixed_cost = FP8_FIXED_COST;
     prm.scale_log2 = scale * kv_scale * 1.4426950408889634f;
     prm.flags = flags;
