@@ -375,6 +375,9 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
 #ifndef ETAP_HG64_PF_AHEAD
 #define ETAP_HG64_PF_AHEAD 0  // L2 prefetch of the next tile's page: measured slower (pf1 290.0 vs 281.9 us at 64 heads)
 #endif
+#ifndef ETAP_HINT_PAGES
+#define ETAP_HINT_PAGES 1  // the producer takes its first page ids from the prologue's hint (A/B: 0)
+#endif
 #ifndef ETAP_HINT_BYTES
 #define ETAP_HINT_BYTES (2 * 64 * 576 * 2)
 #endif
@@ -384,33 +387,43 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
 // a page), and return that guess (b, first tile). Hints only: every byte used is loaded after
 // the grid dependency, and a wrong or stale guess merely wastes a prefetch. Whole warp.
 __device__ __forceinline__ void prev_range_hint(const DecodeParams& prm, int hg, uint32_t page_bytes, bool q_rows,
-                                                int lane, int& hint_b, int& hint_t0) {
+                                                int lane, int& hint_b, int& hint_t0, int* s_hint = nullptr) {
 #ifndef ETAP_NO_PREFETCH_HINT
     if (!prm.inkernel_sched) return;
-    if (lane == 0) {
-        const int32_t* prev = prm.sched_out + sched_part(prm) * SCHED_INTS;
-        const int p0 = prev[0], tb = prev[1], p1 = prev[2], off = prev[5];
-        const int vb = off + p0, nvb = prm.batch * prm.groups;
-        if (p1 >= p0 && p0 >= 0 && vb >= 0 && vb < nvb && tb >= 0 && tb < prm.max_pages) {
-            const int g = vb / prm.batch, b = vb - g * prm.batch;
-            hint_b = b;
-            hint_t0 = tb;
-            const int32_t* bt = prm.block_table + static_cast<size_t>(b) * prm.max_pages;
-#pragma unroll 1
-            for (int k = 0; k < static_cast<int>(ETAP_HINT_BYTES / page_bytes) && tb + k < prm.max_pages; ++k) {
-                const int page = bt[tb + k];
-                if (page >= 0 && page < prm.num_pages)
-                    ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) + static_cast<size_t>(page) * page_bytes,
-                                          page_bytes);
-            }
-            if (q_rows)
-                ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.q) +
-                                          (static_cast<size_t>(b) * prm.heads + g * hg) * D_QK * 2,
-                                      hg * D_QK * 2);
+    // one dependent load (the previous range), then the page ids on parallel lanes: the
+    // schedule's __syncthreads waits for this warp, so no serial chain of block_table reads
+    const int32_t* prev = prm.sched_out + sched_part(prm) * SCHED_INTS;
+    int p0 = 0, tb = -1, p1 = -1, off = -1;
+    if (lane == 0) { p0 = prev[0]; tb = prev[1]; p1 = prev[2]; off = prev[5]; }
+    p0 = __shfl_sync(0xffffffffu, p0, 0);
+    tb = __shfl_sync(0xffffffffu, tb, 0);
+    p1 = __shfl_sync(0xffffffffu, p1, 0);
+    off = __shfl_sync(0xffffffffu, off, 0);
+    const int vb = off + p0, nvb = prm.batch * prm.groups;
+    if (s_hint != nullptr && lane == 0) s_hint[0] = -1;
+    if (p1 >= p0 && p0 >= 0 && vb >= 0 && vb < nvb && tb >= 0 && tb < prm.max_pages) {
+        const int g = vb / prm.batch, b = vb - g * prm.batch;
+        hint_b = b;
+        hint_t0 = tb;
+        const int32_t* bt = prm.block_table + static_cast<size_t>(b) * prm.max_pages;
+        const int page = (s_hint != nullptr || lane < static_cast<int>(ETAP_HINT_BYTES / page_bytes)) &&
+                                 tb + lane < prm.max_pages
+                             ? bt[tb + lane]
+                             : 0;
+        if (lane < static_cast<int>(ETAP_HINT_BYTES / page_bytes) && page >= 0 && page < prm.num_pages)
+            ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) + static_cast<size_t>(page) * page_bytes,
+                                  page_bytes);
+        if (s_hint != nullptr) {
+            // the 32 page ids from (b, tb) for the producer: its first TMA needs no block_table
+            // read of its own when this call's range starts where the previous one did
+            s_hint[2 + lane] = page;
+            if (lane == 0) { s_hint[0] = b; s_hint[1] = tb; }
         }
+        if (q_rows && lane == 0)
+            ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.q) +
+                                      (static_cast<size_t>(b) * prm.heads + g * hg) * D_QK * 2,
+                                  hg * D_QK * 2);
     }
-    hint_b = __shfl_sync(0xffffffffu, hint_b, 0);
-    hint_t0 = __shfl_sync(0xffffffffu, hint_t0, 0);
 #endif
 }
 
@@ -497,17 +510,32 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
         // warp 2 (idle until the first tile) warms L2 with the previous call's first pages while
         // warp 0 computes this call's schedule (matters when nothing overlaps the prologue,
         // e.g. the first node of a CUDA graph replay)
+        // (line <= 32 entries: the warp schedule leaves s_pref unused, and warp 2 leaves there the
+        // page ids it read, s_hint = {b, t0, 32 ids})
+#ifdef ETAP_NO_PREFETCH_HINT
+        int* s_hint = nullptr;
+#else
+        int* s_hint = (ls.line_n <= 32 && ETAP_HINT_PAGES) ? s_pref : nullptr;
+#endif
         if (warp == 2) {
             int gb = -1, gt0 = 0;
-            prev_range_hint(prm, hg, page_bytes, q_rows, lane, gb, gt0);
+            prev_range_hint(prm, hg, page_bytes, q_rows, lane, gb, gt0, s_hint);
+            if (lane == 0) ETAP_TRACE_PRO(prm, 0);
         }
         schedule(false);
+        if (warp == 0 && lane == 0) ETAP_TRACE_PRO(prm, 1);
         if (warp == 0) {
             for (int vb = s_sched[0]; vb <= s_sched[2]; ++vb) {
                 SplitDesc sd;
                 if (!split_at(s_sched, s_len[vb], prm.batch, vb, sd)) continue;
                 r.hint_b = sd.b;
                 r.hint_t0 = sd.t0;
+                if (s_hint != nullptr && s_hint[0] == sd.b && s_hint[1] == sd.t0) {
+                    // the previous call's range starts here too: warp 2 read these page ids from
+                    // this call's block_table and prefetched the first pages and Q already
+                    r.hint_pg = (sd.t0 + lane < sd.t1) ? s_hint[2 + lane] : 0;
+                    break;
+                }
                 r.hint_pg = (sd.t0 + lane < sd.t1) ? __ldg(prm.block_table + static_cast<size_t>(sd.b) * prm.max_pages +
                                                            sd.t0 + lane) : 0;
 #ifndef ETAP_NO_PREFETCH_HINT
@@ -522,6 +550,10 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
                                           hg * D_QK * 2);
 #endif
                 break;
+            }
+            if (kDebug && prm.trace != nullptr) {  // page ids in registers (waits for their load)
+                const int pg0 = __shfl_sync(0xffffffffu, r.hint_pg, 0);
+                if (lane == 0 && pg0 != (-2147483647 - 1)) ETAP_TRACE_PRO(prm, 2);
             }
         }
     } else if (warp == 0) {
@@ -605,6 +637,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
     if (threadIdx.x == 0) {
         ETAP_TRACE_G(prm, 0);
         ETAP_TRACE_CLK(prm, 5);
+        ETAP_TRACE_SMID(prm);
     }
 
     // ---- prologue (overlaps the previous kernel under programmatic dependent launch)
@@ -1271,8 +1304,13 @@ static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
 static_assert(OFF_Q % 1024 == 0 && OFF_P % 1024 == 0, "alignment");
 }  // namespace kfp8
 
+#ifdef ETAP_FP8_MAXNREG
+#define ETAP_FP8_BOUNDS __maxnreg__(ETAP_FP8_MAXNREG)
+#else
+#define ETAP_FP8_BOUNDS __launch_bounds__(NUM_THREADS, 1)
+#endif
 template <bool DBG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void ETAP_FP8_BOUNDS
     etap_mla_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_kv128, const __grid_constant__ CUtensorMap tm_kv64,
                                const __grid_constant__ CUtensorMap tm_q128, const __grid_constant__ CUtensorMap tm_q64,
                                const DecodeParams prm, float kv_scale, uint8_t* __restrict__ q3s) {
@@ -1288,6 +1326,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (threadIdx.x == 0) {
         ETAP_TRACE_G(prm, 0);
         ETAP_TRACE_CLK(prm, 5);
+        ETAP_TRACE_SMID(prm);
     }
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tm_kv128);
@@ -1394,9 +1433,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     if (warp == 0) {
         // ===================================================== TMA producer
+        if (lane == 0) ETAP_TRACE_PRO(prm, 3);
         const bool kv_shared = line_shape(B, prm.groups, gridDim.x, prm.lanes_on != 0).lanes > 1;
         const uint64_t pol_kv = kv_shared ? ptx::policy_evict_normal() : ptx::policy_evict_first();
         const uint64_t pol_q = ptx::policy_evict_first();
+        if (lane == 0) ETAP_TRACE_PRO(prm, 4);
         uint32_t gt = 0, nsplit = 0;
         for (int vb = vb_begin; vb <= vb_end; ++vb) {
             SplitDesc sd;
@@ -1406,6 +1447,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int pg;
             if (nsplit == 0 && sd.b == hint_b && sd.t0 == hint_t0) pg = hint_pg;  // loaded already
             else pg = (base + lane < sd.t1) ? __ldg(bt + base + lane) : 0;
+            if (nsplit == 0 && lane == 0) ETAP_TRACE_PRO(prm, 5);
             bool q_pending = nsplit > 0;  // the first split's Q terms come from the prologue
             for (int t = sd.t0; t < sd.t1; ++t) {
                 if (t - base >= 32) {
@@ -1975,7 +2017,12 @@ __global__ void __launch_bounds__(128)
     combine_body<COMBINE_BATCH, 1>(ws_o, ws_lse, split_off, hg, batch, om, trace, seqlens, parts, lanes_on, fixed_cost);
 }
 // two heads per CTA, at most 80 registers: one CTA beside a 16-head decode CTA (43k registers)
-__global__ void __launch_bounds__(256, 3)
+#ifdef ETAP_COMBINE2_MAXNREG
+#define ETAP_COMBINE2_BOUNDS __maxnreg__(ETAP_COMBINE2_MAXNREG)
+#else
+#define ETAP_COMBINE2_BOUNDS __launch_bounds__(256, 3)
+#endif
+__global__ void ETAP_COMBINE2_BOUNDS
     etap_mla_combine2_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
                              const int32_t* __restrict__ split_off, int hg, int batch,
                              const __grid_constant__ OutMap om, unsigned long long* trace,

@@ -440,6 +440,23 @@ constexpr int TRACE_SLOTS = 16;
             (prm).trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + TRACE_TILES - 1) * TRACE_SLOTS + \
                         (slot)] = ptx::global_timer_ns();                                           \
     } while (0)
+// Prologue clock64 stamps in the second-to-last trace row (debug instantiation; that row is a
+// tile row only for CTAs with more than 254 tiles): slots 0-7, see decode_prologue
+#define ETAP_TRACE_PRO(prm, slot)                                                                   \
+    do {                                                                                            \
+        if (kDebug && (prm).trace != nullptr)                                                       \
+            (prm).trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + TRACE_TILES - 2) * TRACE_SLOTS + \
+                        (slot)] = clock64();                                                        \
+    } while (0)
+// SM id of the CTA in global slot 3 (debug instantiation): per-SM gaps between launches
+#define ETAP_TRACE_SMID(prm)                                                                        \
+    do {                                                                                            \
+        if (kDebug && (prm).trace != nullptr) {                                                     \
+            uint32_t smid_;                                                                         \
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                                      \
+            (prm).trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + TRACE_TILES - 1) * TRACE_SLOTS + 3] = smid_; \
+        }                                                                                           \
+    } while (0)
 #define ETAP_TRACE_CLK(prm, slot)                                                                   \
     do {                                                                                            \
         if (kDebug && (prm).trace != nullptr)                                                       \
