@@ -484,9 +484,13 @@ __device__ __forceinline__ void dep_wait_before_write(const DecodeParams& prm) {
     if (prm.defer_dep) ptx::grid_dep_wait();
 }
 
+// defer_publish: under the early schedule the kernel publishes this CTA's schedule itself, later,
+// with publish_after_prologue (warp 3 waits for the grid dependency first; a kernel whose
+// prologue holds warp 3 in a named barrier with others must not let that wait stall them)
 template <bool kDebug, int MAXVB>
 __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uint8_t* sched_smem, int hg,
-                                                    uint32_t page_bytes, bool q_rows, int warp, int lane) {
+                                                    uint32_t page_bytes, bool q_rows, int warp, int lane,
+                                                    bool defer_publish = false) {
     int* s_pref = reinterpret_cast<int*>(sched_smem);
     int* s_soff = s_pref + MAXVB + 1;
     int* s_len = s_soff + MAXVB + 1;
@@ -581,7 +585,7 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
     if (threadIdx.x == 0 && !early) { span_stamp(prm, 0); ETAP_TRACE_G(prm, 7); ETAP_TRACE_CLK(prm, 12); }
     if (fused) {
         if (early) {
-            if (warp == 3 && sched_publisher(prm)) {
+            if (warp == 3 && sched_publisher(prm) && !defer_publish) {
                 dep_wait_before_write(prm);  // the previous step's combine may still read split_off
                 publish_schedule(prm, ls, s_soff, s_sched, lane, 32);
             }
@@ -598,6 +602,15 @@ __device__ __forceinline__ Prologue decode_prologue(const DecodeParams& prm, uin
     }
     if (threadIdx.x == 0) { ETAP_TRACE_G(prm, 1); ETAP_TRACE_CLK(prm, 14); }
     return r;
+}
+
+// The early schedule's publish that decode_prologue(defer_publish = true) left out (warp 3).
+__device__ __forceinline__ void publish_after_prologue(const DecodeParams& prm, const Prologue& pro, int lane) {
+    if (prm.inkernel_sched != 0 && prm.early_meta != 0 && sched_publisher(prm)) {
+        dep_wait_before_write(prm);  // the previous step's combine may still read split_off
+        const LineShape ls = line_shape(prm.batch, prm.groups, sched_parts(prm), prm.lanes_on != 0);
+        publish_schedule(prm, ls, pro.soff, pro.sch, lane, 32);
+    }
 }
 
 // A softmax warpgroup's wait on an mbarrier: one warp polls it, the other three block on the
@@ -1272,6 +1285,23 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
 //     8 MMAs per tile of V^T against three fp8 terms of P (N = 48), both straight from the
 //     fp8 page: no dequantising pass; the KV scale folds into the softmax scale and 1/l.
 // =============================================================================================
+#ifndef ETAP_FP8_PAGE3D
+#define ETAP_FP8_PAGE3D 1  // FP8 page = one 3-D box (V chunks) + the rope box; 0: five 2-D boxes (A/B)
+#endif
+// One FP8 page (64 rows x 576 B) into a ring slot: V chunks 0-3 as [chunk][row][128 B] SW128,
+// the rope chunk as [row][64 B] SW64, all completing one mbarrier (lane 0 of the producer).
+__device__ __forceinline__ void fp8_page_load(uint8_t* slot, const CUtensorMap* kv128, const CUtensorMap* kv64,
+                                              uint64_t* full, int page, uint64_t pol) {
+#if ETAP_FP8_PAGE3D
+    ptx::tma_load_3d(slot, kv128, full, 0, page * PAGE, 0, pol);
+#else
+#pragma unroll 1
+    for (int c = 0; c < fp8::VCH; ++c)
+        ptx::tma_load_2d(slot + c * fp8::VCH_BYTES, kv128, full, c * 128, page * PAGE, pol);
+#endif
+    ptx::tma_load_2d(slot + fp8::ROPE_OFF, kv64, full, 512, page * PAGE, pol);
+}
+
 namespace kfp8 {
 constexpr int NPS = 5;                               // page slots in the ring
 constexpr int NTB8 = 8;                              // tile-barrier ring depth (>= NPS + 1)
@@ -1304,7 +1334,14 @@ static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
 static_assert(OFF_Q % 1024 == 0 && OFF_P % 1024 == 0, "alignment");
 }  // namespace kfp8
 
-#ifdef ETAP_FP8_MAXNREG
+// At most 176 registers (256 threads: 45056 of the SM's 65536): one 80-register combine CTA
+// (256 threads) fits beside the decode CTA, so the next step's decode CTA takes each SM the
+// moment this step's leaves it instead of waiting behind combine CTAs that hold the SM until
+// the whole decode grid is done (DESIGN §3 "step overlap"; 0: the compiler's 241, A/B)
+#ifndef ETAP_FP8_MAXNREG
+#define ETAP_FP8_MAXNREG 176
+#endif
+#if ETAP_FP8_MAXNREG > 0
 #define ETAP_FP8_BOUNDS __maxnreg__(ETAP_FP8_MAXNREG)
 #else
 #define ETAP_FP8_BOUNDS __launch_bounds__(NUM_THREADS, 1)
@@ -1355,7 +1392,11 @@ __global__ void ETAP_FP8_BOUNDS
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const Prologue pro = decode_prologue<kDebug, MAX_FUSED_VB>(prm, smem + OFF_SCHED, HG, PAGE * D_QK, false, warp, lane);
+    // (the schedule publish waits for the grid dependency: warp 3 does it after the Q prologue,
+    // whose named barrier it shares with warps 2 and 4-7, so the first split's Q terms do not
+    // wait for the previous step's combine under a deferred dependency)
+    const Prologue pro = decode_prologue<kDebug, MAX_FUSED_VB>(prm, smem + OFF_SCHED, HG, PAGE * D_QK, false, warp, lane,
+                                                               true);
     const int32_t* sch = pro.sch;
     const int32_t* soff = pro.soff;
     const int idx_off = pro.idx_off;
@@ -1463,10 +1504,7 @@ __global__ void ETAP_FP8_BOUNDS
                     uint8_t* slot = smem + OFF_RING + (gt % NPS) * fp8::TILE_BYTES;
                     uint64_t* full = &bars[BAR_FULL + gt % NTB8];
                     ptx::mbar_arrive_expect_tx(full, fp8::TILE_BYTES);
-#pragma unroll 1
-                    for (int c = 0; c < fp8::VCH; ++c)
-                        ptx::tma_load_2d(slot + c * fp8::VCH_BYTES, &tm_kv128, full, c * 128, page * PAGE, pol_kv);
-                    ptx::tma_load_2d(slot + fp8::ROPE_OFF, &tm_kv64, full, 512, page * PAGE, pol_kv);
+                    fp8_page_load(slot, &tm_kv128, &tm_kv64, full, page, pol_kv);
                     ETAP_TRACE(prm, gt, 1);
                 }
                 __syncwarp();
@@ -1500,6 +1538,7 @@ __global__ void ETAP_FP8_BOUNDS
             SplitDesc sd;
             if (!split_at(sch, seqlen_of(vb), B, vb, sd)) continue;
             ptx::mbar_wait(&bars[BAR_QF], nsplit & 1);
+            if (nsplit == 0 && lane == 0) ETAP_TRACE_PRO(prm, 6);  // first split's Q terms in shared memory
             if (nsplit > 0 && lane == 0) ptx::mbar_arrive(&bars[BAR_SCE + (nsplit - 1) % NSCR]);  // slot read
             for (int t = sd.t0; t < sd.t1; ++t) {
                 const uint32_t buf = gt & 1;
@@ -1539,6 +1578,7 @@ __global__ void ETAP_FP8_BOUNDS
             }
         }
     } else if (warp == 3) {
+        publish_after_prologue(prm, pro, lane);
         // ===================================================== Q terms of splits past 1 + NSCR
         // (many short sequences per CTA): into scratch slot (j-1) % NSCR once GEMM1 saw the Q
         // that slot held land in shared memory
@@ -2241,17 +2281,23 @@ int cached_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_r
 
 // 2-D uint8 tensor map over a row-major [rows][576] byte matrix (FP8 pool / three-term Q),
 // box {box_cols, box_rows}, SW128 (box_cols 128) or SW64 (box_cols 64); cached
-int cached_map_u8(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_cols, uint32_t box_rows) {
+// box_chunks > 0: a 3-D view {128 B of a chunk, rows, chunk} (strides 576 B, 128 B) whose box
+// {128, box_rows, box_chunks} lands box_chunks consecutive 128-column chunks of the rows as
+// [chunk][row][128 B] SW128 tiles with ONE TMA instruction (each instruction costs the
+// issuing thread ~115 cycles, so a page in two boxes instead of five shortens every tile's
+// load chain and the start-of-step ring fill)
+int cached_map_u8(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_cols, uint32_t box_rows,
+                  uint32_t box_chunks = 0) {
     struct Entry {
         const void* base = nullptr;
         uint64_t rows = 0;
-        uint32_t bc = 0, br = 0;
+        uint32_t bc = 0, br = 0, bk = 0;
         CUtensorMap map;
     };
     thread_local Entry cache[8];
     thread_local unsigned next = 0;
     for (auto& e : cache)
-        if (e.base == base && e.rows == rows && e.bc == box_cols && e.br == box_rows) {
+        if (e.base == base && e.rows == rows && e.bc == box_cols && e.br == box_rows && e.bk == box_chunks) {
             *map = e.map;
             return ETAP_OK;
         }
@@ -2259,20 +2305,32 @@ int cached_map_u8(CUtensorMap* map, const void* base, uint64_t rows, uint32_t bo
     if (!enc) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver)");
     if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
         return fail(ETAP_ERR_SHAPE, "tensor base address must be 16-byte aligned");
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(D_QK), rows};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(D_QK)};
-    cuuint32_t box[2] = {box_cols, box_rows};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     box_cols == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r;
+    if (box_chunks > 0) {
+        cuuint64_t dims[3] = {128, rows, static_cast<cuuint64_t>(D_V / 128)};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(D_QK), 128};
+        cuuint32_t box[3] = {128, box_rows, box_chunks};
+        cuuint32_t estr[3] = {1, 1, 1};
+        r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(D_QK), rows};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(D_QK)};
+        cuuint32_t box[2] = {box_cols, box_rows};
+        cuuint32_t estr[2] = {1, 1};
+        r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE,
+                box_cols == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     if (r != CUDA_SUCCESS) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled (u8) failed: " + std::to_string(r));
     Entry& e = cache[next++ % 8];
     e.base = base;
     e.rows = rows;
     e.bc = box_cols;
     e.br = box_rows;
+    e.bk = box_chunks;
     e.map = *map;
     return ETAP_OK;
 }
@@ -2923,7 +2981,7 @@ int decode_impl_fp8(const void* q, const void* kv_pool8, float kv_scale, int64_t
     CUtensorMap tm_kv128, tm_kv64, tm_q128, tm_q64;
     const uint64_t pool_rows = static_cast<uint64_t>(num_pages) * PAGE;
     const uint64_t q3_rows = static_cast<uint64_t>(num_sm_parts) * kfp8::NSCR * fp8::NQ;
-    if (int rc = cached_map_u8(&tm_kv128, kv_pool8, pool_rows, 128, PAGE)) return rc;
+    if (int rc = cached_map_u8(&tm_kv128, kv_pool8, pool_rows, 128, PAGE, ETAP_FP8_PAGE3D ? fp8::VCH : 0)) return rc;
     if (int rc = cached_map_u8(&tm_kv64, kv_pool8, pool_rows, 64, PAGE)) return rc;
     if (int rc = cached_map_u8(&tm_q128, q3, q3_rows, 128, fp8::NQ)) return rc;
     if (int rc = cached_map_u8(&tm_q64, q3, q3_rows, 64, fp8::NQ)) return rc;

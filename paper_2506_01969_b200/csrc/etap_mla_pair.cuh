@@ -147,7 +147,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const Prologue pro = decode_prologue<kDebug, MAX_VB>(prm, smem + OFF_SCHED, UNIT, PAGE * D_QK * 2, true, warp, lane);
+    // (the leader's warp 3 streams V: the schedule publish, which waits for the grid
+    // dependency, comes after its last page instead of before its first)
+    const Prologue pro = decode_prologue<kDebug, MAX_VB>(prm, smem + OFF_SCHED, UNIT, PAGE * D_QK * 2, true, warp, lane,
+                                                         true);
     const int32_t* sch = pro.sch;
     const int32_t* soff = pro.soff;
     const int idx_off = pro.idx_off;
@@ -344,6 +347,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
                 ++gp;
             }
         }
+        publish_after_prologue(prm, pro, lane);
     } else {
         // ===================================================== softmax + epilogue (both CTAs)
         // thread = TMEM lane L of its quadrant (head h = L % 64, row half r = L / 64) x the 16

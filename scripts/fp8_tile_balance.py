@@ -45,6 +45,7 @@ for c in range(n):
         continue
     for g in range(8, nt - 8):
         rows["period"].append(t[g + 1, 0] - t[g, 0])
+        rows.setdefault("TMA issue (5 boxes)", []).append(t[g, 1] - t[g, 0])
         rows["latency"].append(t[g, 2] - t[g, 0])
         rows["g1_after_prev_g1"].append(t[g, 2] - t[g - 1, 2])
         if NPS:
@@ -58,6 +59,8 @@ for c in range(n):
             rows.setdefault("P written->G2 sees P", []).append(t[g, 6] - t[g, 5])
             rows.setdefault("G2 sees->G2 commit", []).append(t[g, 7] - t[g, 6])
             rows.setdefault("G1sees->G2commit (residency)", []).append(t[g, 7] - t[g, 2])
+t = raw[:, :5]
+print("first five tiles, TMA issue cycles (median over CTAs):", [int(np.median(t[:, j, 1] - t[:, j, 0])) for j in range(5)])
 print(f"{'bf16' if bf16 else 'fp8'}: SM clock {np.median(ghz):.3f} GHz, CTAs {n}")
 for k, v in rows.items():
     if v:

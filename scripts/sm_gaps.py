@@ -61,9 +61,12 @@ clk0 = g[i, :, 5].astype(np.int64)
 ghz = (g[i, :, 6] - g[i, :, 5]).astype(np.float64) / np.maximum(1, (g[i, :, 2] - g[i, :, 0]).astype(np.float64))
 marks = {"seqlens in + scan (warp 0)": g[i, :, 13], "prev range + page ids (warp 2)": prol[i, :, 0],
          "schedule barrier passed": prol[i, :, 1], "first page ids in registers": prol[i, :, 2],
+         "FP8 first Q terms in smem (GEMM1 issuer)": prol[i, :, 6],
          "FP8 producer entered": prol[i, :, 3], "FP8 producer policies made": prol[i, :, 4],
          "FP8 producer first split found": prol[i, :, 5],
          "producer at its first TMA": g[i, :, 12], "first TMA issued": g[i, :, 15]}
+t0seen = np.stack([k.view(n, TT, 16).cpu().numpy()[:, 0, 2] for k in k2])[i].astype(np.int64)
+marks["tile 0 seen by GEMM1"] = t0seen
 print(f"prologue, step {i} (SM clock {np.median(ghz):.3f} GHz), us after entry:")
 for k, v in marks.items():
     v = v.astype(np.int64)
