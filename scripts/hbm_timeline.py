@@ -14,7 +14,7 @@ import torch
 
 from paper_2506_01969_b200 import _lib, inputs, mla
 
-B, CTX, H = 16, 65536, 16
+B, CTX, H = 16, 65536, int(os.environ.get("HEADS", 16))
 BIN = float(os.environ.get("BIN", 2))
 inp = inputs.make_mla_inputs([CTX] * B, heads=H, pad_value=0.0)
 plan = mla.MlaDecodePlan.create(B, H, "cuda")
