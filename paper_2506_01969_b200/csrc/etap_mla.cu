@@ -2056,6 +2056,14 @@ __global__ void __launch_bounds__(128)
                             const int32_t* __restrict__ seqlens, int parts, int lanes_on, int fixed_cost) {
     combine_body<COMBINE_BATCH, 1>(ws_o, ws_lse, split_off, hg, batch, om, trace, seqlens, parts, lanes_on, fixed_cost);
 }
+// at most 64 registers (8 CTAs of 128 threads per SM): the CTAs of one combine pack onto few SMs
+__global__ void __launch_bounds__(128, 8)
+    etap_mla_combine_dense_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
+                                  const int32_t* __restrict__ split_off, int hg, int batch,
+                                  const __grid_constant__ OutMap om, unsigned long long* trace,
+                                  const int32_t* __restrict__ seqlens, int parts, int lanes_on, int fixed_cost) {
+    combine_body<4, 1>(ws_o, ws_lse, split_off, hg, batch, om, trace, seqlens, parts, lanes_on, fixed_cost);
+}
 // two heads per CTA, at most 80 registers: one CTA beside a 16-head decode CTA (43k registers)
 #ifdef ETAP_COMBINE2_MAXNREG
 #define ETAP_COMBINE2_BOUNDS __maxnreg__(ETAP_COMBINE2_MAXNREG)
@@ -2695,8 +2703,19 @@ int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_part
     cfg2.stream = static_cast<cudaStream_t>(stream);
     cfg2.attrs = attr;
     cfg2.numAttrs = pdl_attrs();
+// 32 / 64-head units: the dense combine (64 registers, 8 CTAs per SM). Its CTAs take SMs as
+// decode CTAs leave and hold them until the decode grid is done, and the next decode launches
+// only once all of them are resident: packed 8 per SM they block 64 SMs at B = 16 x 32 heads
+// instead of every SM (3 per SM at 139 registers); 0.5-1% per step at 32 / 64 heads, outputs
+// bitwise unchanged (A/B: 0 batch 16, 1 batch 8)
+#ifndef ETAP_COMBINE_WIDE
+#define ETAP_COMBINE_WIDE 2
+#endif
     auto kern = hpb == 2 ? etap_mla_combine2_kernel
-                         : (hg >= 128 ? etap_mla_combine_kernel<8> : etap_mla_combine_kernel<16>);
+                         : (hg >= 128 ? etap_mla_combine_kernel<8>
+                                      : (hg >= 32 && ETAP_COMBINE_WIDE == 1 ? etap_mla_combine_kernel<8>
+                                         : (hg >= 32 && ETAP_COMBINE_WIDE == 2 ? etap_mla_combine_dense_kernel
+                                                                               : etap_mla_combine_kernel<16>)));
     ETAP_CUDA(cudaLaunchKernelEx(&cfg2, kern,
                                  static_cast<const float*>(ws_o),
                                  static_cast<const float*>(ws_lse), split_off, hg, batch, om,
