@@ -117,14 +117,19 @@ def peaks() -> tuple[float, str]:
     return 6650.0, "fallback"
 
 
-def ncu_traffic() -> float | None:
-    """DRAM read+write bytes per K2 launch at this workload from the committed ncu capture."""
+def ncu_traffic(name: str = WORKLOAD, world: int = 1) -> float | None:
+    """DRAM read+write bytes per K2 launch at this workload from the committed ncu capture
+    (profiles/ncu_summary.json: the headline K2, plus the FP8 and the 128-head single-GPU K2
+    under "others", which match only the one-GPU run of those workloads)."""
     f = ROOT / "profiles" / "ncu_summary.json"
     if not f.exists():
         return None
     try:
         d = json.loads(f.read_text())
-        return float(d["decode_kernel"]["dram_bytes_per_launch"]) if d.get("workload") == WORKLOAD else None
+        if name == WORKLOAD and d.get("workload") == WORKLOAD:
+            return float(d["decode_kernel"]["dram_bytes_per_launch"])
+        o = d.get("others", {}).get(name)
+        return float(o["decode_kernel"]["dram_bytes_per_launch"]) if o and world == 1 else None
     except Exception:
         return None
 
@@ -378,7 +383,7 @@ def run_ours(args) -> None:
     # arithmetic intensity vs the ridge: 16 heads (30 FLOP/B) are HBM-bound, 128 heads (242) sit
     # at the ridge (peak TF/s / peak GB/s ~ 251)
     bound = "hbm" if nflops / nbytes < tpeak * 1e12 / (peak * 1e9) else "tensor"
-    traffic = ncu_traffic() if name == WORKLOAD else None
+    traffic = ncu_traffic(name, world)
 
     # N > 1 e2e: every rank, through the Python API, with host buffers (all ranks take part)
     e2e_multi = None

@@ -86,8 +86,18 @@ def main() -> None:
         tot = sum(sum(v) for v in ks.values())
         summary["launch_list"] = {k: {"launches": len(v), "avg_us": sum(v) / len(v) * 1e6,
                                       "share": sum(v) / tot} for k, v in ks.items()}
+    # profiles/ncu_summary.json: the headline K2 at top level (bench.py roofline.traffic), the
+    # FP8 and other-head-count captures under "others", keyed by bench.py's config.workload
+    f = ROOT / "profiles" / "ncu_summary.json"
+    old = json.loads(f.read_text()) if f.exists() else {}
+    others = old.get("others", {})
     if not fp8 and heads == 16:
-        (ROOT / "profiles" / "ncu_summary.json").write_text(json.dumps(summary, indent=1) + "\n")
+        out = dict(summary, others=others)
+    else:
+        key = "mla_decode_b16_ctx64k_h16_per_gpu_fp8kv" if fp8 else f"mla_decode_b16_ctx64k_h{heads}_strong"
+        others[key] = {"tag": tag, "source": rep, "decode_kernel": summary["decode_kernel"]}
+        out = dict(old, others=others)
+    f.write_text(json.dumps(out, indent=1) + "\n")
     tagdir = ROOT / "profiles" / tag
     tagdir.mkdir(parents=True, exist_ok=True)
     kname = "etap_mla_decode_fp8_kernel (K2-FP8, e4m3 latent cache)" if fp8 else "etap_mla_decode_kernel (K2)"
