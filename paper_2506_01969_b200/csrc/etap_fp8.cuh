@@ -53,6 +53,26 @@ __device__ __forceinline__ void umma_f8_elect(uint32_t d_tmem, uint64_t a_desc, 
         : "memory");
 }
 
+#ifndef ETAP_FP8_UMMA_X4
+#define ETAP_FP8_UMMA_X4 0  // four-MMA issue blocks in GEMM1: 0.5% slower here (A/B), unlike the bf16 kernels
+#endif
+// four MMAs along K in one warp-uniform block (see ptx::umma_f16_x4_elect)
+__device__ __forceinline__ void umma_f8_x4_elect(uint32_t d_tmem, uint64_t a0, uint64_t a_step, uint64_t b0,
+                                                 uint64_t b_step, uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "add.s64 a1, %1, %2;\n\tadd.s64 a2, a1, %2;\n\tadd.s64 a3, a2, %2;\n\t"
+        "add.s64 b1, %3, %4;\n\tadd.s64 b2, b1, %4;\n\tadd.s64 b3, b2, %4;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a1, b1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a2, b2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a3, b3, %5, 1;\n\t}" ::"r"(d_tmem),
+        "l"(a0), "l"(a_step), "l"(b0), "l"(b_step), "r"(idesc), "r"(acc0)
+        : "memory");
+}
+
 // byte offset of (row, byte b) in a swizzled K-major / MN-major block with 128 B rows (SW128)
 // or 64 B rows (SW64): 16-byte units XOR-permuted within 1024 B / 512 B atoms
 __host__ __device__ inline uint32_t sw128_off(uint32_t row, uint32_t b) {
@@ -73,9 +93,13 @@ __device__ __forceinline__ void issue_gemm1(uint32_t s_tmem, uint32_t tile, uint
     for (int c = 0; c < VCH; ++c) {
         const uint64_t a0 = ptx::smem_desc(tile + c * VCH_BYTES, 16, 1024, ptx::LAYOUT_SW128);
         const uint64_t b0 = ptx::smem_desc(q + c * Q_VBLK, 16, 1024, ptx::LAYOUT_SW128);
+#if ETAP_FP8_UMMA_X4
+        umma_f8_x4_elect(s_tmem, a0, 2, b0, 2, idesc, c == 0 ? 0u : 1u);  // +32 B (32 fp8) along K per MMA
+#else
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // +32 B (32 fp8) along K inside the 128 B row
             umma_f8_elect(s_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, (c == 0 && kk == 0) ? 0u : 1u);
+#endif
     }
     const uint64_t a0 = ptx::smem_desc(tile + ROPE_OFF, 16, 512, ptx::LAYOUT_SW64);
     const uint64_t b0 = ptx::smem_desc(q + VCH * Q_VBLK, 16, 512, ptx::LAYOUT_SW64);

@@ -218,6 +218,9 @@ __device__ __forceinline__ int item_pos(int i, uint32_t gt) { return C::P_LO_BUF
 template <class C>
 __device__ __forceinline__ int item_chunk(int i, uint32_t gt) { return C::P_LO_BUF ? i : chunk_at(i, gt); }
 
+#ifndef ETAP_UMMA_X4
+#define ETAP_UMMA_X4 1  // four K-steps per issue block (ptx::umma_f16_x4_elect); 0: one MMA per block (A/B)
+#endif
 // GEMM1 of one tile: S^T[64 x HG] = K[64 x 576] . Q^T[576 x HG], 9 chunks x 4 MMAs (K=16),
 // landing-group items [POS_BEGIN, POS_END). Whole-warp call (elect inside). pos0 = ring slot of
 // the tile's first position. The tile's first MMA (item 0) zero-initialises S^T.
@@ -234,10 +237,14 @@ __device__ __forceinline__ void issue_gemm1_tile(uint32_t s_tmem, uint32_t ring_
         const int chunk = item_chunk<C>(pos, gt);
         const uint64_t a0 = a_ring + static_cast<uint64_t>(s * (SLOT_BYTES >> 4));
         const uint64_t b0 = b_q + static_cast<uint64_t>(chunk * (C::Q_CHUNK_BYTES >> 4));
+#if ETAP_UMMA_X4
+        ptx::umma_f16_x4_elect(s_tmem, a0, 2, b0, 2, idesc, pos == 0 ? 0u : 1u);  // +32 B along K per MMA
+#else
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // +32 B along K inside the 128 B swizzle row
             ptx::umma_f16_elect(s_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc,
                                 (pos == 0 && kk == 0) ? 0u : 1u);
+#endif
     }
 }
 
@@ -251,10 +258,15 @@ __device__ __forceinline__ void issue_gemm2_block(uint32_t o_tmem, uint32_t slot
     // MN-major SW128: LBO = stride between 64-wide MN atoms (next slot), SBO = 8-row group
     const uint64_t a0 = ptx::smem_desc(slot_addr, SLOT_BYTES, 1024, ptx::LAYOUT_SW128);
     const uint64_t b0 = p_desc<C>(p_addr);
+#if ETAP_UMMA_X4
+    static_assert(TILE / 16 == 4, "four MMAs per d-block");
+    ptx::umma_f16_x4_elect(o_tmem, a0, 2048 >> 4, b0, (2 * C::P_ROWGRP) >> 4, idesc, zero_init ? 0u : 1u);
+#else
 #pragma unroll
     for (int kk = 0; kk < TILE / 16; ++kk)  // 16 KV rows = 2 row groups per MMA
         ptx::umma_f16_elect(o_tmem, a0 + kk * (2048 >> 4), b0 + kk * ((2 * C::P_ROWGRP) >> 4),
                             idesc, (zero_init && kk == 0) ? 0u : 1u);
+#endif
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo_elem, float hi_elem) {

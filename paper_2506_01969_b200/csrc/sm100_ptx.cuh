@@ -373,6 +373,26 @@ __device__ __forceinline__ void umma_f16_elect(uint32_t d_tmem, uint64_t a_desc,
         : "memory");
 }
 
+// Four MMAs along K in one warp-uniform block: descriptors a0 + i*a_step, b0 + i*b_step
+// (i = 0..3), accumulate flag acc0 for the first and 1 for the rest. One elect.sync and one
+// move of each base descriptor into uniform registers for the four (the per-MMA form pays an
+// ELECT, a VOTEU and four R2UR per instruction: ~50 issue cycles each).
+__device__ __forceinline__ void umma_f16_x4_elect(uint32_t d_tmem, uint64_t a0, uint64_t a_step, uint64_t b0,
+                                                  uint64_t b_step, uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "add.s64 a1, %1, %2;\n\tadd.s64 a2, a1, %2;\n\tadd.s64 a3, a2, %2;\n\t"
+        "add.s64 b1, %3, %4;\n\tadd.s64 b2, b1, %4;\n\tadd.s64 b3, b2, %4;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %5, 1;\n\t}" ::"r"(d_tmem),
+        "l"(a0), "l"(a_step), "l"(b0), "l"(b_step), "r"(idesc), "r"(acc0)
+        : "memory");
+}
+
 __device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
