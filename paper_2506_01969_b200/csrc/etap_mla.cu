@@ -375,6 +375,9 @@ __device__ void inkernel_schedule(const DecodeParams& prm, const LineShape& ls, 
 #ifndef ETAP_HG64_PF_AHEAD
 #define ETAP_HG64_PF_AHEAD 0  // L2 prefetch of the next tile's page: measured slower (pf1 290.0 vs 281.9 us at 64 heads)
 #endif
+#ifndef ETAP_TMA_ELECT
+#define ETAP_TMA_ELECT 1  // the producer issues a landing group's boxes warp-uniformly (A/B: 0)
+#endif
 #ifndef ETAP_HINT_PAGES
 #define ETAP_HINT_PAGES 1  // the producer takes its first page ids from the prologue's hint (A/B: 0)
 #endif
@@ -748,6 +751,23 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 } else if (gt >= A_LAG) {
                     ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - A_LAG) % NTB], ((gt - A_LAG) / NTB) & 1);
                 }
+#if ETAP_TMA_ELECT
+                // (the group's boxes are issued warp-uniformly: one elect inside each TMA)
+                if (lane == 0) {
+                    if (gt == 0) { ETAP_TRACE_G(prm, 9); ETAP_TRACE_CLK(prm, 15); }
+                    ETAP_TRACE(prm, gt, 0);
+                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_A + tb], C::SPLIT_POS * SLOT_BYTES);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int pos = 0; pos < C::SPLIT_POS; ++pos) {
+                    uint32_t s = pos0 + item_pos<C>(pos, gt);
+                    s = s >= C::NSLOT ? s - C::NSLOT : s;
+                    ptx::tma_load_2d_elect(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_A + tb],
+                                           item_chunk<C>(pos, gt) * 64, page * PAGE, pol_kv);
+                }
+                if (lane == 0) {
+#else
                 if (lane == 0) {
                     if (gt == 0) { ETAP_TRACE_G(prm, 9); ETAP_TRACE_CLK(prm, 15); }
                     ETAP_TRACE(prm, gt, 0);
@@ -758,6 +778,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                         ptx::tma_load_2d(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_A + tb],
                                          item_chunk<C>(pos, gt) * 64, page * PAGE, pol_kv);
                     }
+#endif
                     if (page_ahead >= 0 && page_ahead < prm.num_pages)
                         ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(prm.kv_pool) +
                                                   static_cast<size_t>(page_ahead) * PAGE * D_QK * 2,
@@ -786,6 +807,19 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                 // (P_LO_BUF: V2-V5 of gt-2, free after its GEMM2 d-blocks 0-2)
                 if (!C::P_IN_ROPE && gt >= 2) ptx::mbar_wait(&bars[BAR_G2_HALF + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
                 if (C::P_LO_BUF && gt >= 2) ptx::mbar_wait(&bars[BAR_G2_3Q + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+#if ETAP_TMA_ELECT
+                if (lane == 0)
+                    ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_B + tb], (C::SPLIT_POS2 - C::SPLIT_POS) * SLOT_BYTES);
+                __syncwarp();
+#pragma unroll
+                for (int pos = C::SPLIT_POS; pos < C::SPLIT_POS2; ++pos) {
+                    uint32_t s = pos0 + item_pos<C>(pos, gt);
+                    s = s >= C::NSLOT ? s - C::NSLOT : s;
+                    ptx::tma_load_2d_elect(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_B + tb],
+                                           item_chunk<C>(pos, gt) * 64, page * PAGE, pol_kv);
+                }
+                if (lane == 0 && !C::THIRD_GROUP) ETAP_TRACE(prm, gt, 1);
+#else
                 if (lane == 0) {
                     ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_B + tb], (C::SPLIT_POS2 - C::SPLIT_POS) * SLOT_BYTES);
 #pragma unroll 1
@@ -796,6 +830,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                     }
                     if (!C::THIRD_GROUP) ETAP_TRACE(prm, gt, 1);
                 }
+#endif
                 if constexpr (C::THIRD_GROUP) {
                     // the rest reuse gt-2's positions [4, 9 - SPLIT_POS): free after GEMM2 d-blocks
                     // 0-2 of gt-2 (22-slot ring) or the whole GEMM2
@@ -807,6 +842,19 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                                        ((gt - 2) / NTB) & 1);
                     if (C::P_LO_BUF && gt >= 2)
                         ptx::mbar_wait(&bars[BAR_G2_DONE + (gt - 2) % NTB], ((gt - 2) / NTB) & 1);
+#if ETAP_TMA_ELECT
+                    if (lane == 0)
+                        ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_C + tb], (NCHUNK - C::SPLIT_POS2) * SLOT_BYTES);
+                    __syncwarp();
+#pragma unroll
+                    for (int pos = C::SPLIT_POS2; pos < NCHUNK; ++pos) {
+                        uint32_t s = pos0 + item_pos<C>(pos, gt);
+                        s = s >= C::NSLOT ? s - C::NSLOT : s;
+                        ptx::tma_load_2d_elect(smem + C::OFF_RING + s * SLOT_BYTES, &tm_kv, &bars[BAR_FULL_C + tb],
+                                               item_chunk<C>(pos, gt) * 64, page * PAGE, pol_kv);
+                    }
+                    if (lane == 0) ETAP_TRACE(prm, gt, 1);
+#else
                     if (lane == 0) {
                         ptx::mbar_arrive_expect_tx(&bars[BAR_FULL_C + tb], (NCHUNK - C::SPLIT_POS2) * SLOT_BYTES);
 #pragma unroll 1
@@ -817,6 +865,7 @@ __global__ void __launch_bounds__(Cfg<HG_>::THREADS, 1)
                         }
                         ETAP_TRACE(prm, gt, 1);
                     }
+#endif
                 }
                 __syncwarp();
                 ++gt;

@@ -17,8 +17,9 @@ from paper_2506_01969_b200 import _lib, inputs, mla
 
 TT = 256
 bf16 = "--bf16" in sys.argv
-inp = inputs.make_mla_inputs([65536] * 16, heads=16, pad_value=0.0)
-plan = mla.MlaDecodePlan.create(16, 16, "cuda")
+H = int(os.environ.get("HEADS", 16))  # bf16 head-group kernels: HEADS=32 -> head group 32
+inp = inputs.make_mla_inputs([65536] * 16, heads=H, pad_value=0.0)
+plan = mla.MlaDecodePlan.create(16, H, "cuda")
 if bf16:
     f = lambda: plan.decode(inp.q, inp.kv_pool, inp.block_table, inp.seqlens, inp.scale)
 else:
@@ -50,6 +51,7 @@ for c in range(n):
         rows["g1_after_prev_g1"].append(t[g, 2] - t[g - 1, 2])
         if NPS:
             rows["g2commit_to_issue"].append(t[g, 0] - t[g - NPS, 7])
+        if True:
             # the tile's compute residency in its ring slot, stage by stage
             rows.setdefault("G1sees->Scommit", []).append(t[g, 3] - t[g, 2])
             rows.setdefault("Scommit->softmax sees S", []).append(t[g, 4] - t[g, 3])
