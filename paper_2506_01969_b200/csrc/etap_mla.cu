@@ -2265,14 +2265,14 @@ int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_row
 // 3-D view of the same pool for whole-page boxes: {64 cols of a chunk, rows, chunk}, strides
 // 1152 B (row) and 128 B (chunk), so a box {64, 64, nchunk} lands chunks c0.. c0+nchunk-1 of one
 // page as consecutive 8 KB SW128 slots ([chunk][row][128 B]) with one TMA instruction.
-int make_map_page3d(CUtensorMap* map, const void* base, uint64_t rows, uint32_t nchunk) {
+int make_map_page3d(CUtensorMap* map, const void* base, uint64_t rows, uint32_t nchunk, uint32_t box_rows = PAGE) {
     auto enc = get_encode_fn();
     if (!enc) return fail(ETAP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver)");
     if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
         return fail(ETAP_ERR_SHAPE, "tensor base address must be 16-byte aligned");
     cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(NCHUNK)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(D_QK) * 2, 128};
-    cuuint32_t box[3] = {64, PAGE, nchunk};
+    cuuint32_t box[3] = {64, box_rows, nchunk};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -2316,22 +2316,29 @@ struct MapCacheEntry {
     const void* base = nullptr;
     uint64_t rows = 0;
     uint32_t box_rows = 0;
+    uint32_t box_chunks = 0;
     CUtensorMap map;
 };
 
-int cached_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_rows) {
+// box_chunks > 0: the 3-D page view (make_map_page3d), box {64, box_rows, box_chunks}
+int cached_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_rows, uint32_t box_chunks = 0) {
     thread_local MapCacheEntry cache[8];
     thread_local unsigned next = 0;
     for (auto& e : cache)
-        if (e.base == base && e.rows == rows && e.box_rows == box_rows) {
+        if (e.base == base && e.rows == rows && e.box_rows == box_rows && e.box_chunks == box_chunks) {
             *map = e.map;
             return ETAP_OK;
         }
-    if (int rc = make_map(map, base, rows, box_rows)) return rc;
+    if (box_chunks > 0) {
+        if (int rc = make_map_page3d(map, base, rows, box_chunks, box_rows)) return rc;
+    } else if (int rc = make_map(map, base, rows, box_rows)) {
+        return rc;
+    }
     MapCacheEntry& e = cache[next++ % 8];
     e.base = base;
     e.rows = rows;
     e.box_rows = box_rows;
+    e.box_chunks = box_chunks;
     e.map = *map;
     return ETAP_OK;
 }
@@ -2804,8 +2811,12 @@ int decode_pair(const void* q, const void* kv_pool, int64_t num_pages, const int
                 size_t ws_lse_off, const OutMap& om, unsigned flags, void* stream) {
     const int heads = q_tokens * heads_per_token;
     CUtensorMap tm_kv, tm_kv32, tm_q;
-    if (int rc = cached_map(&tm_kv, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, PAGE)) return rc;
-    if (int rc = cached_map(&tm_kv32, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, 32)) return rc;
+    // (ETAP_PAIR_BOX3D: 3-D page views, one box per GEMM1 half-page and per V chunk pair)
+    if (int rc = cached_map(&tm_kv, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, PAGE, ETAP_PAIR_BOX3D ? 2 : 0))
+        return rc;
+    if (int rc = cached_map(&tm_kv32, kv_pool, static_cast<uint64_t>(num_pages) * PAGE, 32,
+                            ETAP_PAIR_BOX3D ? NCHUNK : 0))
+        return rc;
     if (int rc = cached_map(&tm_q, q, static_cast<uint64_t>(batch) * heads, pairk::HPC)) return rc;
     const int groups = heads / pairk::UNIT;
     DecodeParams prm;

@@ -34,6 +34,9 @@
 // buffered and their load latency sets the period: 422 vs 371 us).
 #pragma once
 
+#ifndef ETAP_PAIR_BOX3D
+#define ETAP_PAIR_BOX3D 1  // 3-D page boxes: 1 TMA per GEMM1 half-page (was 9), 2 per V half (was 4); A/B: 0
+#endif
 namespace pairk {
 constexpr int HPC = 64;                        // heads per CTA
 constexpr int UNIT = 2 * HPC;                  // heads per pair work unit
@@ -194,10 +197,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
                 if (lane == 0) {
                     ETAP_TRACE(prm, gp, 0);
                     if (leader) ptx::mbar_arrive_expect_tx(&bars[B_FULL_G1 + buf], 2 * STAGE_G1);
+#if ETAP_PAIR_BOX3D
+                    // this CTA's 32 rows of the page, all nine chunks, as [chunk][row][128 B]
+                    ptx::tma_load_3d_pair(stage, &tm_kv32, bar_g1[buf], 0, page * PAGE + 32 * static_cast<int>(rank), 0,
+                                          pol_kv);
+#else
 #pragma unroll 1
                     for (int c = 0; c < NCHUNK; ++c)
                         ptx::tma_load_2d_pair(stage + c * G1_BYTES, &tm_kv32, bar_g1[buf], c * 64,
                                               page * PAGE + 32 * static_cast<int>(rank), pol_kv);
+#endif
                 }
                 __syncwarp();
                 if (q_pending) {
@@ -321,11 +330,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pairk::THREADS, 1)
                 if (lane == 0) {
                     ETAP_TRACE(prm, gp, 1);
                     ptx::mbar_arrive_expect_tx(&bars[B_V_LAND + buf], 4 * V_BYTES);
+#if ETAP_PAIR_BOX3D
+                    // V chunks {2r, 2r+1} and {2r+4, 2r+5}: two boxes of two consecutive chunks
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        ptx::tma_load_3d(smem + OFF_STAGE + buf * STAGE + STAGE_G1 + 2 * h * V_BYTES, &tm_kv,
+                                         &bars[B_V_LAND + buf], 0, page * PAGE, v_chunk(static_cast<int>(rank), 2 * h),
+                                         pol_kv);
+#else
 #pragma unroll 1
                     for (int i = 0; i < 4; ++i)
                         ptx::tma_load_2d(smem + OFF_STAGE + buf * STAGE + STAGE_G1 + i * V_BYTES, &tm_kv,
                                          &bars[B_V_LAND + buf], v_chunk(static_cast<int>(rank), i) * 64, page * PAGE,
                                          pol_kv);
+#endif
                 }
                 __syncwarp();
                 ptx::mbar_wait(&bars[B_V_LAND + buf], (gp >> 1) & 1);
