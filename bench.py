@@ -342,7 +342,7 @@ def run_ours(args) -> None:
     # The same K steps without the overlap of consecutive steps (ETAP_FLAG_EARLY_METADATA only:
     # every decode waits for the previous step's combine before its loads), reported beside
     ms_dep = None
-    if not fp8 and world == 1 and gather is None:
+    if world == 1 and gather is None:
         dflags_run = dflags
         dflags = mla.FLAG_EARLY_METADATA
         for _ in range(3):
