@@ -385,11 +385,16 @@ def run_ours(args) -> None:
     # ETAP_FLAG_INDEPENDENT_INPUTS consecutive launches overlap (the next step's CTAs start on SMs
     # this step's CTAs leave, during its tail), so first-start -> last-exit of one launch is not
     # its duration; every CTA streams its 1/148 share of the bytes within its own span.
-    # The launch's duration is taken as its slowest CTA's span (the mean CTA span undercounts:
-    # L2 prefetches issued before a CTA's first stamp and the next step's early start both move
-    # bytes outside the spans, and read that way the FP8 kernel would pass the read-only stream).
+    # A launch's duration: first CTA start -> last CTA exit, but counting time it overlaps the
+    # previous launch only once, i.e. min(that span, last exit - the previous launch's last
+    # exit). Without the step overlap this is the launch span; with it, the exit-to-exit period
+    # of consecutive launches. (The mean CTA busy span undercounts: L2 prefetches issued before
+    # a CTA's first stamp and the next step's early start move bytes outside the spans; the
+    # slowest CTA's span overcounts: it includes the time it ran beside the previous launch.)
     cta_us = (sp[:, :, 1] - sp[:, :, 0]) / 1e3
-    k2_us = cta_us.max(axis=1)
+    first, last = sp[:, :, 0].min(axis=1), sp[:, :, 1].max(axis=1)
+    k2_us = (last - first) / 1e3
+    k2_us[1:] = np.minimum(k2_us[1:], (last[1:] - last[:-1]) / 1e3)
     k2_avg_us = float(k2_us.mean())
     k2_mean_cta_us = float(cta_us.mean())
     launch_span_us = float(((sp[:, :, 1].max(axis=1) - sp[:, :, 0].min(axis=1)) / 1e3).mean())
@@ -454,9 +459,9 @@ def run_ours(args) -> None:
                      "launch_span_us": launch_span_us,
                      "timing": (f"%globaltimer stamps of the product K2 over the {args.steps} timed steps "
                                 "(etap_mla_debug_span: per CTA, first KV load and exit), programmatic launch "
-                                "intact; kernel_avg_us = mean over launches of the slowest CTA's busy span (consecutive "
-                                "launches overlap: launch_span_us, first start to last exit of one launch, "
-                                "includes the previous launch's tail)")})
+                                "intact; kernel_avg_us = mean over launches of min(first CTA start -> last CTA exit, last exit - "
+                                "the previous launch's last exit): consecutive launches overlap, and the overlap "
+                                "is counted once; launch_span_us = first start -> last exit, overlap included)")})
         result = {
             "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": args.scaling,

@@ -100,7 +100,8 @@ def main() -> None:
     f.write_text(json.dumps(out, indent=1) + "\n")
     tagdir = ROOT / "profiles" / tag
     tagdir.mkdir(parents=True, exist_ok=True)
-    kname = "etap_mla_decode_fp8_kernel (K2-FP8, e4m3 latent cache)" if fp8 else "etap_mla_decode_kernel (K2)"
+    kname = ("etap_mla_decode_fp8_kernel (K2-FP8, e4m3 latent cache)" if fp8 else
+             "etap_mla_decode_pair_kernel (K2, CTA pairs)" if heads % 128 == 0 else "etap_mla_decode_kernel (K2)")
     lines = [f"# ncu — {kname}, B=16 x 64K, {heads} heads ({tag})", "",
              f"source: `{rep}` (`ncu --set full --clock-control none --import-source on`, one launch)", "",
              "| metric | value |", "|---|---|"]
