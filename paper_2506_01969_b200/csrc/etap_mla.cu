@@ -1953,8 +1953,9 @@ __global__ void __launch_bounds__(72)
 //     running combine (with ETAP_FLAG_INDEPENDENT_INPUTS they then stream at once); two round
 //     trips for the ~10 splits of a sequence instead of one;
 //   * 32 / 64-head units: HPB 1, batch 16 (one round trip for up to 16 splits per sequence);
-//   * the CTA-pair kernel's 128-head units: HPB 1, batch 8 (2048 rows at B = 16 with ~6 splits
-//     each: 72 instead of 114 registers, two waves instead of 3.5).
+//   * the CTA-pair kernel's 128-head units: the dense combine, HPB 1, batch 4 (2048 rows at
+//     B = 16 with ~6 splits each: 64 registers, 8 CTAs per SM; batch 8 at 72 registers measured
+//     0.4% slower, batch 16 at 114 registers 1.2%).
 constexpr int COMBINE_GROUP = 16;  // splits merged per rescale of the running sums
 // K3 lets the next kernel launch before its own grid dependency (1) or after it (0). Early: the
 // next step's decode CTAs take SMs as this step's decode CTAs exit (during its tail), and with
@@ -2767,8 +2768,16 @@ int combine_impl(const int32_t* split_off, int batch, int heads, int num_sm_part
 #ifndef ETAP_COMBINE_WIDE
 #define ETAP_COMBINE_WIDE 2
 #endif
+// 128-head (CTA-pair) units: 1 = the dense combine (64 registers, 8 CTAs per SM; 360.2 vs 361.6 us
+// at 128 heads, same box, three interleaved repetitions, scripts/ab_combine_pair.sh), 0 = batch 8
+// (72 registers), 2 = batch 16 (365.9 us)
+#ifndef ETAP_COMBINE_PAIR
+#define ETAP_COMBINE_PAIR 1
+#endif
     auto kern = hpb == 2 ? etap_mla_combine2_kernel
-                         : (hg >= 128 ? etap_mla_combine_kernel<8>
+                         : (hg >= 128 ? (ETAP_COMBINE_PAIR == 1 ? etap_mla_combine_dense_kernel
+                                         : ETAP_COMBINE_PAIR == 2 ? etap_mla_combine_kernel<16>
+                                                                  : etap_mla_combine_kernel<8>)
                                       : (hg >= 32 && ETAP_COMBINE_WIDE == 1 ? etap_mla_combine_kernel<8>
                                          : (hg >= 32 && ETAP_COMBINE_WIDE == 2 ? etap_mla_combine_dense_kernel
                                                                                : etap_mla_combine_kernel<16>)));
